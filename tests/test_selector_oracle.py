@@ -1,0 +1,124 @@
+"""Pins of the selector and partition oracles (oracle/selector.py, oracle/partition.py)."""
+import itertools
+import random
+
+import pytest
+
+from oracle import selector as so
+from oracle.partition import partition_rows
+
+
+def run_stream(sel, key, eligible, cost, n_runs):
+    """Drive the oracle with synthetic costs (virtual clock): returns the (v, mode) trace."""
+    trace = []
+    for _ in range(n_runs):
+        v, mode = sel.decide(key, eligible)
+        warm = sel.commit(v, key, mode)
+        sel.harvest(v, key, mode, warm, cost(v))
+        trace.append((v, mode))
+    return trace
+
+
+def test_spec_s369_alternation():
+    """2 variants, unseen key, K=3 -> the first 6 executions alternate (3 each)."""
+    sel = so.SelectorOracle(2, calib_warmup=0, calib_k=3)
+    trace = run_stream(sel, "k", [0, 1], lambda v: 100 + v, 6)
+    assert [v for v, _ in trace] == [0, 1, 0, 1, 0, 1]
+    assert all(m == so.MODE_CALIB for _, m in trace)
+    v, m = sel.decide("k", [0, 1])
+    assert m == so.MODE_MODEL and v == 0
+
+
+def test_config1_calibration_plan():
+    """3 variants x (1 warm-up + 3 timed) = 12 calibration runs in order 0,1,2,... then model."""
+    sel = so.SelectorOracle(3)
+    trace = run_stream(sel, "k", [0, 1, 2], lambda v: [30, 10, 20][v], 13)
+    assert [v for v, _ in trace[:12]] == [0, 1, 2] * 4
+    assert [m for _, m in trace[:3]] == [so.MODE_WARMUP] * 3
+    assert all(m == so.MODE_CALIB for _, m in trace[3:12])
+    assert trace[12] == (1, so.MODE_MODEL)
+
+
+def test_spec_s370_closed_form_crossover(golden):
+    """cost0 = 0.1n, cost1 = 50 + 0.01n -> n=256 -> 0, n=4096 -> 1."""
+    g = golden("selector_crossover.txt")
+    expect = {256: 0, 4096: 1}
+    for n, want in expect.items():
+        sel = so.SelectorOracle(2)
+        costs = [round(0.1 * n * 1000), round((50 + 0.01 * n) * 1000)]   # ns
+        run_stream(sel, ("n", n), [0, 1], lambda v: costs[v], 8)
+        assert sel.decide(("n", n), [0, 1]) == (want, so.MODE_MODEL)
+    assert float(g["crossover"]) == pytest.approx(50 / 0.09)
+
+
+def test_omniscient_accuracy_is_one():
+    """a truthful model picks the argmin at every size (accuracy 1.0)."""
+    sel = so.SelectorOracle(2)
+    for n in [64, 128, 256, 512, 555, 556, 600, 1024, 4096]:
+        c = [round(100 * n), round(50000 + 10 * n)]
+        run_stream(sel, n, [0, 1], lambda v: c[v], 8)
+        v, _ = sel.decide(n, [0, 1])
+        assert v == min((0, 1), key=lambda t: (c[t], t))
+
+
+def test_tie_goes_to_lowest_index_and_eligibility_order():
+    sel = so.SelectorOracle(3)
+    run_stream(sel, "k", [0, 1, 2], lambda v: 500, 12)
+    assert sel.decide("k", [0, 1, 2]) == (0, so.MODE_MODEL)
+    assert sel.decide("k", [1, 2]) == (1, so.MODE_MODEL)
+
+
+def test_permutation_invariance_of_samples():
+    """Integer sums: harvest order does not change the model decision (exact here)."""
+    samples = [(0, 1003), (0, 997), (0, 1000), (1, 999), (1, 1001), (1, 1000)]
+    decisions = set()
+    for perm in itertools.permutations(samples):
+        sel = so.SelectorOracle(2, calib_warmup=0)
+        for v, _ in [(0, 0), (1, 0)] * 3:
+            sel.commit(v, "k", so.MODE_CALIB)
+        for v, ns in perm:
+            sel.harvest(v, "k", so.MODE_CALIB, False, ns)
+        decisions.add(sel.decide("k", [0, 1]))
+    assert decisions == {(0, so.MODE_MODEL)}          # exact tie 3000 vs 3000 -> index 0
+
+
+def test_eager_and_no_variant():
+    sel = so.SelectorOracle(3, eager=True)
+    assert sel.decide("k", [2, 1]) == (2, so.MODE_EAGER)
+    with pytest.raises(LookupError):
+        sel.decide("k", [])
+
+
+def test_admits_table():
+    """§8(b) eligibility: strict FP32 -> SIMT, TMA; TF32 -> + TC_TF32; BF16 -> TC_BF16 only."""
+    f32, bf16 = so.F32, so.BF16
+    el = lambda d, c: [t for t in range(4) if so.admits(t, d, c)]
+    assert el(f32, so.COMPUTE_F32_STRICT) == [0, 1]
+    assert el(f32, so.COMPUTE_TF32) == [0, 1, 2]
+    assert el(bf16, so.COMPUTE_BF16) == [3]
+    assert el(bf16, so.COMPUTE_TF32) == []
+    assert so.tma_ok(4, [0, 256], [64, 8]) and not so.tma_ok(4, [4], [64]) and not so.tma_ok(2, [0], [9])
+
+
+@pytest.mark.parametrize("m,p,expect", [
+    (32768, 8, [0, 4096, 8192, 12288, 16384, 20480, 24576, 28672, 32768]),
+    (32768, 2, [0, 16384, 32768]),
+    (1000, 3, [0, 384, 768, 1000]),
+    (100, 4, [0, 100, 100, 100, 100]),
+    (0, 2, [0, 0, 0]),
+    (64, 1, [0, 64]),
+])
+def test_partition_hand_cases(m, p, expect):
+    assert partition_rows(m, p) == expect
+
+
+def test_partition_invariants():
+    rnd = random.Random(1)
+    for _ in range(500):
+        m, p = rnd.randint(0, 100000), rnd.randint(1, 8)
+        o = partition_rows(m, p)
+        assert o[0] == 0 and o[-1] == m and len(o) == p + 1
+        assert all(a <= b for a, b in zip(o, o[1:]))
+        assert all(x % 128 == 0 for x in o[:-1] if x < m)       # panel starts are tile-aligned
+        sizes = [b - a for a, b in zip(o, o[1:])]
+        assert max(sizes) - min(s for s in sizes if s > 0 or m == 0) <= 128 * p if m else True
