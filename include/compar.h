@@ -1,0 +1,245 @@
+/*
+ * compar.h — C ABI of the B200-native COMPAR GEMM component runtime (libcompar.so).
+ *
+ * What the library is (PAPER.md = /root/reference/PAPER.md, "P:n [§x]"):
+ *   * one INTERFACE, "gemm":  C_out = alpha * A * B + beta * C_in  — the paper's
+ *     matrix-multiply component (P:76-80 [§2.1]; P:201-205 [Table 2, "Matrix
+ *     multiply: BLAS, OMP, CUDA, CUBLAS"]) read with xGEMM semantics
+ *     (BASELINE.json north_star; reading R1);
+ *   * several IMPLEMENTATION VARIANTS of it, registered in an ordered registry
+ *     (P:56-60 [§2.1, method_declare: interface/target/name]; P:118 [§2.2.2,
+ *     "a codelet ... corresponds to a variant implementation"]);
+ *   * TASKS: each submit creates a task whose variant is chosen at run time by a
+ *     history-based performance model (P:118, P:224 [§3.2]);
+ *   * lifecycle calls compar_init / compar_terminate (P:89-91 [§2.1]).
+ * No GPU work happens outside the library's own CUDA kernels; torch (or any
+ * caller) only supplies device memory, streams and process groups.
+ *
+ * Conventions for every call:
+ *   * All functions return compar_status; nothing throws across the ABI.
+ *     On failure a thread-local message is available from compar_last_error().
+ *   * All matrices are ROW-MAJOR with explicit leading dimensions in ELEMENTS:
+ *       A: m x k (lda >= k);  B: k x n (ldb >= n) or, with transB, stored n x k
+ *       (ldb >= k);  C_in, C_out: m x n FP32 (ldc >= n).  (R2)
+ *   * A and B are FP32 (in_dtype = COMPAR_F32) or BF16 bit patterns
+ *     (COMPAR_BF16); C is always FP32 (R5).
+ *   * OWNERSHIP: the caller owns A, B, C_in, C_out (and, in SPMD mode, its panels
+ *     and optional B replica).  They must stay allocated and unmodified (C_out
+ *     unread) until compar_sync() on that task returns — the analogue of StarPU's
+ *     "unregister after wait".  The library owns its workspaces: events,
+ *     streams, TMA descriptors, B replica caches, host-mode staging buffers, the
+ *     NCCL communicator and the history.
+ *   * ORDER: work submitted on one stream executes in submission order.
+ */
+#ifndef COMPAR_H
+#define COMPAR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    COMPAR_OK = 0,
+    COMPAR_E_INVALID = 1,       /* bad argument: negative dim, short ld, NULL where read, bad enum   */
+    COMPAR_E_STATE = 2,         /* not initialised / double init / call after terminate / no comm    */
+    COMPAR_E_DUPLICATE = 3,     /* variant name already registered for the interface                  */
+    COMPAR_E_NO_VARIANT = 4,    /* eligible set E is empty (SPEC S:357 SubmitError)                   */
+    COMPAR_E_CUDA = 5,          /* a CUDA runtime/driver call failed (message has the CUDA string)    */
+    COMPAR_E_NCCL = 6,          /* an NCCL call failed                                                */
+    COMPAR_E_TASK_FAILED = 7,   /* the variant returned an error; no retry               */
+    COMPAR_E_UNKNOWN_TASK = 8,  /* task id never issued or already synced                            */
+    COMPAR_E_IO = 9,            /* perf-model file cannot be opened/written                           */
+    COMPAR_E_FORMAT = 10,       /* perf-model file malformed; message carries the line number        */
+    COMPAR_E_OOM = 11           /* device or host allocation failed                                   */
+} compar_status;
+
+typedef enum { COMPAR_F32 = 0, COMPAR_BF16 = 1 } compar_dtype;             /* storage type of A, B */
+
+/* Arithmetic the caller accepts (precision class, R4):
+ *   F32_STRICT: FP32 FFMA only  -> eligible targets SIMT_F32, TMA_F32
+ *   TF32:       FP32 storage, TF32 tensor cores allowed -> SIMT_F32, TMA_F32, TC_TF32
+ *   BF16:       BF16 storage (in_dtype must be BF16)    -> TC_BF16                    */
+typedef enum { COMPAR_COMPUTE_F32_STRICT = 0, COMPAR_COMPUTE_TF32 = 1, COMPAR_COMPUTE_BF16 = 2 } compar_compute;
+
+/* Target of a variant (the paper's `target` clause).  USER variants are
+ * caller-supplied launch functions, eligible for every dtype/compute. */
+typedef enum {
+    COMPAR_TGT_SIMT_F32 = 0,    /* built-in (a): SMEM-tiled FP32 FFMA, float4 loads             */
+    COMPAR_TGT_TMA_F32 = 1,     /* built-in (b): TMA + mbarrier pipeline, FP32 FFMA             */
+    COMPAR_TGT_TC_TF32 = 2,     /* built-in (c): tcgen05/TMEM tensor cores, TF32 in, FP32 acc    */
+    COMPAR_TGT_TC_BF16 = 3,     /* built-in (c): tcgen05/TMEM tensor cores, BF16 in, FP32 acc    */
+    COMPAR_TGT_USER = 4
+} compar_target;
+
+/* Why a task ran the variant it ran. */
+typedef enum {
+    COMPAR_MODE_WARMUP = 0,     /* calibration, first W executions of (variant,key): sample dropped */
+    COMPAR_MODE_CALIB = 1,      /* calibration: least-sampled eligible variant                      */
+    COMPAR_MODE_MODEL = 2,      /* model: argmin of the mean measured ns                            */
+    COMPAR_MODE_EAGER = 3,      /* eager scheduler: first eligible variant, no history              */
+    COMPAR_MODE_HINT = 4,       /* caller forced variant_hint; history untouched                    */
+    COMPAR_MODE_NOOP = 5        /* quick return (m==0 or n==0) or scale-only (k==0 or alpha==0)     */
+} compar_mode;
+
+typedef enum { COMPAR_MEM_DEVICE = 0, COMPAR_MEM_HOST = 1 } compar_mem;
+
+#define COMPAR_TASK_ALL (~(uint64_t)0)
+#define COMPAR_MAX_PANELS 8
+#define COMPAR_UNIQUE_ID_BYTES 128
+
+/* Runtime configuration.  Fill with compar_config_default() first; a field left
+ * negative / NULL takes the environment variable named, else the default.
+ * (SURVEY.md §5 Config; SPEC S:423 environment conventions.) */
+typedef struct {
+    int ngpu;                   /* GPUs driven by THIS process; must be 1 (SPMD: one process per
+                                   GPU, see compar_comm_init).  <0: COMPAR_NGPU or 1.  0: E_INVALID
+                                   — there is no CPU class to fall back to (R15).      */
+    int device;                 /* CUDA ordinal; <0: the caller's current device                */
+    int sched;                  /* 0 history, 1 eager; <0: COMPAR_SCHED=history|eager           */
+    int calib_k;                /* timed calibration samples per (variant,key); <0: COMPAR_CALIB_K or 3 */
+    int calib_warmup;           /* discarded first executions per (variant,key); <0: COMPAR_CALIB_WARMUP or 1 */
+    const char *perf_model_path;/* NULL: COMPAR_PERF_MODEL; if the file exists it is merged at init */
+    int bcast_chunks;           /* SPMD broadcast of B in this many N-slabs; <0: COMPAR_BCAST_CHUNKS or 4 */
+    int builtins;               /* <0 or 1: register simt_f32, tma_f32, tc_tf32, tc_bf16 at init */
+    int virtual_clock;          /* 1: host-only mode, no CUDA call at all: USER variants report
+                                   synthetic ns through their virtual_ns argument (tests) */
+    int64_t variant_mask;       /* bit v set: variant v is masked (never eligible); <0: COMPAR_VARIANT_MASK or 0 */
+} compar_config;
+
+/* One GEMM task.  Sizes are the FULL problem; see `world` for SPMD panels. */
+typedef struct {
+    int64_t m, n, k;
+    float alpha, beta;          /* beta == 0: C_in is never read (BLAS rule, R3)        */
+    compar_dtype in_dtype;
+    compar_compute compute;
+    int transB;                 /* 0: B is k x n (ldb >= n); 1: B is stored n x k (ldb >= k)     */
+    const void *A;  int64_t lda;
+    const void *B;  int64_t ldb;
+    const float *C_in;  int64_t ldc_in;   /* may alias C_out exactly (in place)                 */
+    float *C_out;       int64_t ldc_out;
+    compar_mem mem;             /* HOST: A, B, C_in, C_out are host pointers (pinned for speed);
+                                   the library stages them through its own device buffers and
+                                   copies C_out back before the task's stop event.               */
+    void *stream;               /* cudaStream_t to order the task on; NULL: the library stream    */
+    int panels;                 /* loopback row panels on this device (1..COMPAR_MAX_PANELS);
+                                   0 or 1: a single launch over all m rows                       */
+    int world;                  /* 1: SPMD row-panel split across the ranks of compar_comm_init.
+                                   A and C_* then point at THIS rank's panel (rows
+                                   [o_r, o_{r+1}) of compar_partition_rows(m, nranks)), B is read
+                                   on rank 0 and broadcast with NCCL to the other ranks.         */
+    void *B_replica;            /* world mode, rank != 0: device buffer (k*n elements, same layout
+                                   as B) to receive B; NULL: a library-owned buffer is used       */
+    int variant_hint;           /* -1: run the selector; >= 0: force that registry index          */
+} compar_gemm_desc;
+
+/* The rows one variant launch covers (a loopback panel, or this rank's panel). */
+typedef struct {
+    int index;                  /* panel number r                                                  */
+    int64_t row0, rows;         /* rows [row0, row0 + rows) of the full m                          */
+    const void *A;              /* first row of the panel (device pointers, ld from the desc)      */
+    const void *B;              /* B (or the local replica in world mode)                          */
+    const float *C_in;
+    float *C_out;
+} compar_panel;
+
+/* User variant: launch the panel's GEMM on `stream` and return.  In virtual-clock
+ * mode `virtual_ns` is non-NULL and the function stores its synthetic cost there
+ * (and must not touch CUDA); otherwise it is NULL. */
+typedef compar_status (*compar_gemm_fn)(const compar_gemm_desc *d, const compar_panel *p,
+                                        void *stream, void *user, int64_t *virtual_ns);
+
+typedef struct {
+    uint64_t task;
+    int variant;                /* registry index that ran (-1 for NOOP)                           */
+    int mode;                   /* compar_mode                                                     */
+    int warmup;                 /* 1 if this execution's sample was discarded                      */
+    compar_status status;
+    int npanels;
+    int64_t ns;                 /* the history sample: max over panels (and ranks) of kernel ns    */
+    int64_t panel_ns[COMPAR_MAX_PANELS];
+    int64_t bcast_ns;           /* world mode: broadcast of B, start -> last chunk landed          */
+    int64_t total_ns;           /* first start event -> last stop event of the task on its stream  */
+} compar_report;
+
+typedef struct {
+    int64_t seen, count, min_ns;
+    int64_t sum_ns;             /* saturating copy of the 128-bit internal sum                     */
+    double mean_ns;
+} compar_record;
+
+typedef struct {
+    int64_t submits, launches, harvested, failed;
+    int64_t bytes_h2d, bytes_d2h;
+} compar_stats;
+
+/* ---- lifecycle (P:89-91 [§2.1]: `initialize` -> compar_init(), `terminate` -> compar_terminate()) ---- */
+void          compar_config_default(compar_config *cfg);
+/* E_STATE if ctx already points at a live context; E_INVALID ngpu != 1; E_CUDA if no GPU (unless
+ * virtual_clock); built-in kernels are pre-loaded so lazy loading never pollutes calibration. */
+compar_status compar_init(const compar_config *cfg, void **ctx);
+/* Synchronises every outstanding task, frees workspaces/comms; *ctx invalid afterwards. */
+compar_status compar_terminate(void *ctx);
+
+/* ---- variants (P:56-60 method_declare interface/target/name; P:118 codelet) ---- */
+/* iface must be "gemm"; name unique (E_DUPLICATE); target USER requires fn (E_INVALID);
+ * built-in targets ignore fn.  *out_id = registry index = tie-break order. */
+compar_status compar_register_variant(void *ctx, const char *iface, const char *name,
+                                      compar_target target, compar_gemm_fn fn, void *user,
+                                      int *out_id);
+compar_status compar_variant_count(void *ctx, int *n);
+compar_status compar_variant_info(void *ctx, int id, char *name, int name_len, int *target);
+
+/* ---- tasks (P:128 task create + submit) ---- */
+/* Validates d (E_INVALID), selects a variant (E_NO_VARIANT), launches asynchronously and returns
+ * the monotone task id.  m==0 or n==0: no launch, mode NOOP.  k==0 or alpha==0: a scale-only
+ * kernel C_out = beta*C_in, mode NOOP (no history).  In model mode the submit first harvests
+ * pending samples of the same key (blocking on them) so decisions are a pure function of the
+ * submission sequence. */
+compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t *task);
+/* Blocks until the task's stop event(s); harvests its sample into the history; fills *out
+ * (may be NULL).  task == COMPAR_TASK_ALL syncs every outstanding task (out gets the last).
+ * A failed variant -> E_TASK_FAILED (status also in out).  After return the library holds no
+ * reference to the task's buffers. */
+compar_status compar_sync(void *ctx, uint64_t task, compar_report *out);
+/* Pure query: the (variant, mode) the next submit of d would get.  No launch, no history change
+ * (it may harvest completed pending samples, which does not change any decision). */
+compar_status compar_select(void *ctx, const compar_gemm_desc *d, int *variant, int *mode);
+
+/* ---- performance model persistence ("additional training") ---- */
+/* Text, one record per line:
+ *   <variant_name> <m> <n> <k> <dtype> <compute> <transB> <beta0> <seen> <count> <sum_ns> <sumsq_ns> <min_ns>
+ * Load MERGES by (variant_name, key): counts and sums add, min takes the min.  Unknown variant
+ * names are kept and apply if that name is registered later. */
+compar_status compar_perf_save(void *ctx, const char *path);
+compar_status compar_perf_load(void *ctx, const char *path);
+compar_status compar_history_get(void *ctx, int variant, const compar_gemm_desc *key_of,
+                                 compar_record *out);
+
+/* ---- partitioning and multi-GPU (north star: row panels + NCCL broadcast of B) ---- */
+/* offsets[0..p]: base = ceil(ceil(m/p)/128)*128, offsets[r] = min(m, r*base), offsets[p] = m. */
+compar_status compar_partition_rows(int64_t m, int p, int64_t *offsets);
+/* NCCL unique id for SPMD init (rank 0 creates it, the caller distributes it, e.g. with a
+ * torch.distributed broadcast); len >= COMPAR_UNIQUE_ID_BYTES. */
+compar_status compar_comm_unique_id(void *out, int len);
+/* Joins the nranks-process communicator (one process per GPU).  Required before world = 1. */
+compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, int len);
+
+/* Replace the NCCL max-all-reduce that makes world-mode samples rank-consistent by a caller
+ * hook (in-place max of *value over all ranks).  Used by the host-only SPMD tests (gloo) in
+ * virtual-clock mode; fn = NULL restores the default. */
+typedef void (*compar_reduce_fn)(int64_t *value, void *user);
+compar_status compar_set_reduce_hook(void *ctx, compar_reduce_fn fn, void *user);
+
+/* ---- introspection / fixtures ---- */
+compar_status compar_stats_get(void *ctx, compar_stats *out);
+const char   *compar_last_error(void *ctx);
+/* Synthetic-cost fixture: one-thread kernel spinning on %globaltimer for ns nanoseconds on
+ * `stream` (SURVEY §4 spin_ns; used by USER test variants with closed-form costs). */
+compar_status compar_debug_spin(void *stream, int64_t ns);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMPAR_H */

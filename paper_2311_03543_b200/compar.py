@@ -1,0 +1,269 @@
+"""Thin ctypes binding of include/compar.h (argument marshalling only).
+
+Every step of the hot path — selection, partitioning, broadcast, kernels, timing, history —
+runs inside libcompar.so; this module only converts Python/torch arguments into the C
+structs and raises on non-OK statuses.  There is no fallback: if the native library is
+missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("COMPAR_LIB", os.path.join(_HERE, "libcompar.so"))
+
+# ---- enums (values restate include/compar.h)
+OK, E_INVALID, E_STATE, E_DUPLICATE, E_NO_VARIANT, E_CUDA, E_NCCL, E_TASK_FAILED, E_UNKNOWN_TASK, E_IO, \
+    E_FORMAT, E_OOM = range(12)
+STATUS_NAMES = ["OK", "E_INVALID", "E_STATE", "E_DUPLICATE", "E_NO_VARIANT", "E_CUDA", "E_NCCL", "E_TASK_FAILED",
+                "E_UNKNOWN_TASK", "E_IO", "E_FORMAT", "E_OOM"]
+F32, BF16 = 0, 1
+COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
+TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER = 0, 1, 2, 3, 4
+MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP = 0, 1, 2, 3, 4, 5
+MEM_DEVICE, MEM_HOST = 0, 1
+TASK_ALL = (1 << 64) - 1
+MAX_PANELS = 8
+UNIQUE_ID_BYTES = 128
+
+
+class Config(C.Structure):
+    _fields_ = [("ngpu", C.c_int), ("device", C.c_int), ("sched", C.c_int), ("calib_k", C.c_int),
+                ("calib_warmup", C.c_int), ("perf_model_path", C.c_char_p), ("bcast_chunks", C.c_int),
+                ("builtins", C.c_int), ("virtual_clock", C.c_int), ("variant_mask", C.c_int64)]
+
+
+class GemmDesc(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("alpha", C.c_float), ("beta", C.c_float),
+                ("in_dtype", C.c_int), ("compute", C.c_int), ("transB", C.c_int),
+                ("A", C.c_void_p), ("lda", C.c_int64), ("B", C.c_void_p), ("ldb", C.c_int64),
+                ("C_in", C.c_void_p), ("ldc_in", C.c_int64), ("C_out", C.c_void_p), ("ldc_out", C.c_int64),
+                ("mem", C.c_int), ("stream", C.c_void_p), ("panels", C.c_int), ("world", C.c_int),
+                ("B_replica", C.c_void_p), ("variant_hint", C.c_int)]
+
+
+class Panel(C.Structure):
+    _fields_ = [("index", C.c_int), ("row0", C.c_int64), ("rows", C.c_int64), ("A", C.c_void_p),
+                ("B", C.c_void_p), ("C_in", C.c_void_p), ("C_out", C.c_void_p)]
+
+
+class Report(C.Structure):
+    _fields_ = [("task", C.c_uint64), ("variant", C.c_int), ("mode", C.c_int), ("warmup", C.c_int),
+                ("status", C.c_int), ("npanels", C.c_int), ("ns", C.c_int64),
+                ("panel_ns", C.c_int64 * MAX_PANELS), ("bcast_ns", C.c_int64), ("total_ns", C.c_int64)]
+
+
+class Record(C.Structure):
+    _fields_ = [("seen", C.c_int64), ("count", C.c_int64), ("min_ns", C.c_int64), ("sum_ns", C.c_int64),
+                ("mean_ns", C.c_double)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("submits", C.c_int64), ("launches", C.c_int64), ("harvested", C.c_int64), ("failed", C.c_int64),
+                ("bytes_h2d", C.c_int64), ("bytes_d2h", C.c_int64)]
+
+
+GEMM_FN = C.CFUNCTYPE(C.c_int, C.POINTER(GemmDesc), C.POINTER(Panel), C.c_void_p, C.c_void_p,
+                      C.POINTER(C.c_int64))
+REDUCE_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_void_p)
+
+EXPORTS = ["compar_config_default", "compar_init", "compar_terminate", "compar_register_variant",
+           "compar_variant_count", "compar_variant_info", "compar_gemm_submit", "compar_sync", "compar_select",
+           "compar_perf_save", "compar_perf_load", "compar_history_get", "compar_partition_rows",
+           "compar_comm_unique_id", "compar_comm_init", "compar_set_reduce_hook", "compar_stats_get",
+           "compar_last_error", "compar_debug_spin"]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libcompar.so not built at {LIB_PATH} (run python -m paper_2311_03543_b200.build)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i, i64, st = C.c_void_p, C.c_int, C.c_int64, C.c_int
+    sig = {
+        "compar_config_default": (None, [C.POINTER(Config)]),
+        "compar_init": (st, [C.POINTER(Config), C.POINTER(vp)]),
+        "compar_terminate": (st, [vp]),
+        "compar_register_variant": (st, [vp, C.c_char_p, C.c_char_p, i, GEMM_FN, vp, C.POINTER(i)]),
+        "compar_variant_count": (st, [vp, C.POINTER(i)]),
+        "compar_variant_info": (st, [vp, i, C.c_char_p, i, C.POINTER(i)]),
+        "compar_gemm_submit": (st, [vp, C.POINTER(GemmDesc), C.POINTER(C.c_uint64)]),
+        "compar_sync": (st, [vp, C.c_uint64, C.POINTER(Report)]),
+        "compar_select": (st, [vp, C.POINTER(GemmDesc), C.POINTER(i), C.POINTER(i)]),
+        "compar_perf_save": (st, [vp, C.c_char_p]),
+        "compar_perf_load": (st, [vp, C.c_char_p]),
+        "compar_history_get": (st, [vp, i, C.POINTER(GemmDesc), C.POINTER(Record)]),
+        "compar_partition_rows": (st, [i64, i, C.POINTER(i64)]),
+        "compar_comm_unique_id": (st, [vp, i]),
+        "compar_comm_init": (st, [vp, i, i, vp, i]),
+        "compar_set_reduce_hook": (st, [vp, REDUCE_FN, vp]),
+        "compar_stats_get": (st, [vp, C.POINTER(Stats)]),
+        "compar_last_error": (C.c_char_p, [vp]),
+        "compar_debug_spin": (st, [vp, i64]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype, fn.argtypes = res, args
+    return lib
+
+
+lib = _load()
+
+
+class ComparError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else status}: {msg}")
+
+
+def _check(status, ctx=None):
+    if status != OK:
+        msg = lib.compar_last_error(ctx)
+        raise ComparError(status, msg.decode() if msg else "")
+    return status
+
+
+def partition_rows(m: int, p: int) -> list[int]:
+    out = (C.c_int64 * (p + 1))()
+    _check(lib.compar_partition_rows(m, p, out))
+    return list(out)
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(UNIQUE_ID_BYTES)
+    _check(lib.compar_comm_unique_id(buf, UNIQUE_ID_BYTES))
+    return buf.raw
+
+
+def debug_spin(stream, ns: int) -> None:
+    _check(lib.compar_debug_spin(stream, int(ns)))
+
+
+def _ptr(x):
+    """Device/host address of a torch tensor, int address, or None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def make_desc(m, n, k, *, A=None, B=None, C_in=None, C_out=None, lda=None, ldb=None, ldc_in=None, ldc_out=None,
+              alpha=1.0, beta=0.0, in_dtype=F32, compute=COMPUTE_F32_STRICT, transB=0, mem=MEM_DEVICE, stream=None,
+              panels=0, world=0, B_replica=None, variant_hint=-1) -> GemmDesc:
+    d = GemmDesc()
+    d.m, d.n, d.k = int(m), int(n), int(k)
+    d.alpha, d.beta = float(alpha), float(beta)
+    d.in_dtype, d.compute, d.transB = int(in_dtype), int(compute), int(transB)
+    d.A, d.B, d.C_in, d.C_out = _ptr(A), _ptr(B), _ptr(C_in), _ptr(C_out)
+    d.lda = int(lda if lda is not None else (A.stride(0) if hasattr(A, "stride") else k))
+    d.ldb = int(ldb if ldb is not None else (B.stride(0) if hasattr(B, "stride") else (k if transB else n)))
+    d.ldc_in = int(ldc_in if ldc_in is not None else (C_in.stride(0) if hasattr(C_in, "stride") else n))
+    d.ldc_out = int(ldc_out if ldc_out is not None else (C_out.stride(0) if hasattr(C_out, "stride") else n))
+    d.mem = int(mem)
+    d.stream = stream
+    d.panels, d.world = int(panels), int(world)
+    d.B_replica = _ptr(B_replica)
+    d.variant_hint = int(variant_hint)
+    return d
+
+
+class Compar:
+    """One runtime context (compar_init ... compar_terminate)."""
+
+    def __init__(self, ngpu=-1, device=-1, sched=-1, calib_k=-1, calib_warmup=-1, perf_model_path=None,
+                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1):
+        cfg = Config()
+        lib.compar_config_default(C.byref(cfg))
+        cfg.ngpu, cfg.device, cfg.sched = ngpu, device, sched
+        cfg.calib_k, cfg.calib_warmup = calib_k, calib_warmup
+        self._path = perf_model_path.encode() if perf_model_path else None
+        cfg.perf_model_path = self._path
+        cfg.bcast_chunks, cfg.builtins, cfg.virtual_clock = bcast_chunks, builtins, virtual_clock
+        cfg.variant_mask = variant_mask
+        self.ctx = C.c_void_p()
+        self._callbacks = []     # keep ctypes thunks alive
+        _check(lib.compar_init(C.byref(cfg), C.byref(self.ctx)))
+
+    # lifecycle
+    def terminate(self):
+        if self.ctx:
+            ctx, self.ctx = self.ctx, C.c_void_p()
+            _check(lib.compar_terminate(ctx))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.terminate()
+
+    # variants
+    def register_variant(self, name, target=TGT_USER, fn=None, iface="gemm") -> int:
+        out = C.c_int()
+        cfn = GEMM_FN(fn) if fn is not None else GEMM_FN()
+        self._callbacks.append(cfn)
+        _check(lib.compar_register_variant(self.ctx, iface.encode() if iface is not None else None,
+                                           name.encode() if name is not None else None, target, cfn, None,
+                                           C.byref(out)), self.ctx)
+        return out.value
+
+    def variants(self) -> list[tuple[str, int]]:
+        n = C.c_int()
+        _check(lib.compar_variant_count(self.ctx, C.byref(n)), self.ctx)
+        out = []
+        for v in range(n.value):
+            buf, tgt = C.create_string_buffer(64), C.c_int()
+            _check(lib.compar_variant_info(self.ctx, v, buf, 64, C.byref(tgt)), self.ctx)
+            out.append((buf.value.decode(), tgt.value))
+        return out
+
+    # tasks
+    def submit(self, desc: GemmDesc) -> int:
+        t = C.c_uint64()
+        _check(lib.compar_gemm_submit(self.ctx, C.byref(desc), C.byref(t)), self.ctx)
+        return t.value
+
+    def sync(self, task=TASK_ALL) -> Report:
+        r = Report()
+        _check(lib.compar_sync(self.ctx, task, C.byref(r)), self.ctx)
+        return r
+
+    def sync_status(self, task=TASK_ALL):
+        r = Report()
+        s = lib.compar_sync(self.ctx, task, C.byref(r))
+        return s, r
+
+    def run(self, desc: GemmDesc) -> Report:
+        return self.sync(self.submit(desc))
+
+    def select(self, desc: GemmDesc) -> tuple[int, int]:
+        v, m = C.c_int(), C.c_int()
+        _check(lib.compar_select(self.ctx, C.byref(desc), C.byref(v), C.byref(m)), self.ctx)
+        return v.value, m.value
+
+    # perf model
+    def perf_save(self, path):
+        _check(lib.compar_perf_save(self.ctx, str(path).encode()), self.ctx)
+
+    def perf_load(self, path):
+        _check(lib.compar_perf_load(self.ctx, str(path).encode()), self.ctx)
+
+    def history(self, variant: int, desc: GemmDesc) -> Record:
+        r = Record()
+        _check(lib.compar_history_get(self.ctx, variant, C.byref(desc), C.byref(r)), self.ctx)
+        return r
+
+    # multi-GPU
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        buf = C.create_string_buffer(uid, UNIQUE_ID_BYTES)
+        _check(lib.compar_comm_init(self.ctx, nranks, rank, buf, UNIQUE_ID_BYTES), self.ctx)
+
+    def set_reduce_hook(self, fn):
+        cfn = REDUCE_FN(fn) if fn is not None else REDUCE_FN()
+        self._callbacks.append(cfn)
+        _check(lib.compar_set_reduce_hook(self.ctx, cfn, None), self.ctx)
+
+    def stats(self) -> Stats:
+        s = Stats()
+        _check(lib.compar_stats_get(self.ctx, C.byref(s)), self.ctx)
+        return s

@@ -1,0 +1,35 @@
+// Internal launcher interface between the C++ runtime and the sm_100a kernels.
+// Not part of the public ABI (include/compar.h).  All pointers are device pointers.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace compar {
+
+// One variant launch over a row panel: C_out = alpha * A * B + beta * C_in
+// (PAPER.md P:76-80, P:201-205 read as xGEMM; R1-R3).
+struct GemmLaunch {
+    int64_t m, n, k;           // panel rows, columns, reduction depth
+    float alpha, beta;         // beta == 0: C_in is never read
+    const void *A; int64_t lda;        // m x k row-major (FP32 or BF16 bits)
+    const void *B; int64_t ldb;        // k x n row-major, or n x k when transB
+    int transB;
+    const float *C_in; int64_t ldc_in;
+    float *C_out; int64_t ldc_out;
+    cudaStream_t stream;
+    int num_sms;               // SMs of the device (persistent grids)
+};
+
+cudaError_t launch_simt_f32(const GemmLaunch &g);            // variant (a)
+cudaError_t launch_tma_f32(const GemmLaunch &g);             // variant (b)
+cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16);  // variant (c): tcgen05 TF32 / BF16
+cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha == 0: C_out = beta*C_in
+cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
+cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)
+
+// TMA eligibility (the selector's constraint filter).
+inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {
+    return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * elem_bytes) % 16 == 0);
+}
+
+}  // namespace compar

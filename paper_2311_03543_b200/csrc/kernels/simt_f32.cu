@@ -1,0 +1,184 @@
+// Variant (a) "simt_f32": shared-memory tiled FP32 FFMA GEMM for sm_100a.
+//
+// Role: the B200 re-design of the paper's hand-written "CUDA" mmul variant
+// (PAPER.md P:201-205 [Table 2], P:220 [§3.2]) — strict FP32, no tensor cores.
+// C_out = alpha * A * B + beta * C_in (R1-R3).
+//
+// Design:
+//   * CTA tile 128 x 128, K step 8, 256 threads, 8 x 8 register micro-tile per thread split as
+//     2 x 2 blocks of 4 x 4 at stride 64 (conflict-free float4 shared loads);
+//   * coalesced float4 global loads (vector path when pointers / ld allow), A staged
+//     transposed (As[k][m]) so both operands are read as float4 along M / N;
+//   * register-prefetch double buffering: tile k+1 is loaded while tile k is multiplied;
+//   * any shape: edges are predicated (no padding required), transB supported.
+#include "kernels.h"
+
+namespace compar {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
+
+template <bool kVec>
+__device__ __forceinline__ float4 load_row4(const float *__restrict__ base, int64_t ld, int64_t r, int64_t c,
+                                            int64_t R, int64_t C) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r >= R) return v;
+    const float *p = base + r * ld + c;
+    if (kVec && c + 3 < C) {
+        v = *reinterpret_cast<const float4 *>(p);
+    } else {
+        if (c + 0 < C) v.x = p[0];
+        if (c + 1 < C) v.y = p[1];
+        if (c + 2 < C) v.z = p[2];
+        if (c + 3 < C) v.w = p[3];
+    }
+    return v;
+}
+
+template <bool kVecA, bool kVecB, bool kTransB>
+__global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
+    __shared__ __align__(16) float As[2][BK][BM];
+    __shared__ __align__(16) float Bs[2][BK][BN];
+
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+    const float *__restrict__ A = static_cast<const float *>(g.A);
+    const float *__restrict__ B = static_cast<const float *>(g.B);
+
+    // Load mapping. A (m x k): thread -> row tid/2, k quad (tid&1)*4.
+    const int a_r = tid >> 1, a_k = (tid & 1) * 4;
+    // B (k x n): thread -> k row tid/32, n quad (tid&31)*4.  transB (n x k): like A.
+    const int b_k = kTransB ? (tid & 1) * 4 : (tid >> 5);
+    const int b_n = kTransB ? (tid >> 1) : (tid & 31) * 4;
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    const int64_t nk = (g.k + BK - 1) / BK;
+    float4 ra, rb;
+    auto gload = [&](int64_t kt) {
+        const int64_t k0 = kt * BK;
+        ra = load_row4<kVecA>(A, g.lda, m0 + a_r, k0 + a_k, g.m, g.k);
+        if (kTransB)
+            rb = load_row4<kVecB>(B, g.ldb, n0 + b_n, k0 + b_k, g.n, g.k);
+        else
+            rb = load_row4<kVecB>(B, g.ldb, k0 + b_k, n0 + b_n, g.k, g.n);
+    };
+    auto sstore = [&](int buf) {
+        As[buf][a_k + 0][a_r] = ra.x;
+        As[buf][a_k + 1][a_r] = ra.y;
+        As[buf][a_k + 2][a_r] = ra.z;
+        As[buf][a_k + 3][a_r] = ra.w;
+        if (kTransB) {
+            Bs[buf][b_k + 0][b_n] = rb.x;
+            Bs[buf][b_k + 1][b_n] = rb.y;
+            Bs[buf][b_k + 2][b_n] = rb.z;
+            Bs[buf][b_k + 3][b_n] = rb.w;
+        } else {
+            *reinterpret_cast<float4 *>(&Bs[buf][b_k][b_n]) = rb;
+        }
+    };
+
+    if (nk > 0) {
+        gload(0);
+        sstore(0);
+    }
+    __syncthreads();
+    for (int64_t kt = 0; kt < nk; ++kt) {
+        const int buf = static_cast<int>(kt & 1);
+        if (kt + 1 < nk) gload(kt + 1);
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (kt + 1 < nk) sstore(buf ^ 1);
+        __syncthreads();
+    }
+
+    // Epilogue: C_out = alpha*acc + beta*C_in (C_in unread when beta == 0).
+    const bool cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
+                      (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        if (r >= g.m) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + h * 64 + tx * 4;
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = g.alpha * acc[i][h * 4 + j];
+            if (cvec && c + 3 < g.n) {
+                if (g.beta != 0.f) {
+                    const float4 ci = *reinterpret_cast<const float4 *>(g.C_in + r * g.ldc_in + c);
+                    o[0] = fmaf(g.beta, ci.x, o[0]);
+                    o[1] = fmaf(g.beta, ci.y, o[1]);
+                    o[2] = fmaf(g.beta, ci.z, o[2]);
+                    o[3] = fmaf(g.beta, ci.w, o[3]);
+                }
+                *reinterpret_cast<float4 *>(g.C_out + r * g.ldc_out + c) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (c + j < g.n) {
+                        float v = o[j];
+                        if (g.beta != 0.f) v = fmaf(g.beta, g.C_in[r * g.ldc_in + c + j], v);
+                        g.C_out[r * g.ldc_out + c + j] = v;
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <bool VA, bool VB, bool TB>
+cudaError_t launch_t(const GemmLaunch &g) {
+    dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM));
+    simt_f32_kernel<VA, VB, TB><<<grid, THREADS, 0, g.stream>>>(g);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_simt_f32(const GemmLaunch &g) {
+    if ((g.m + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
+    const bool va = ((g.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
+    const bool vb = ((g.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
+    if (g.transB) {
+        if (va && vb) return launch_t<true, true, true>(g);
+        if (va) return launch_t<true, false, true>(g);
+        if (vb) return launch_t<false, true, true>(g);
+        return launch_t<false, false, true>(g);
+    }
+    if (va && vb) return launch_t<true, true, false>(g);
+    if (va) return launch_t<true, false, false>(g);
+    if (vb) return launch_t<false, true, false>(g);
+    return launch_t<false, false, false>(g);
+}
+
+}  // namespace compar
+
+namespace compar {
+cudaError_t preload_simt_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, simt_f32_kernel<true, true, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<true, true, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<false, false, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<false, false, true>);
+    return e;
+}
+}  // namespace compar

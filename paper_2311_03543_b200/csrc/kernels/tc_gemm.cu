@@ -1,0 +1,282 @@
+// Variant (c) "tc_gemm": tcgen05 / TMEM / TMA tensor-core GEMM for sm_100a.
+//
+// Role: the B200 re-design of the paper's library-GEMM mmul variant ("CUBLAS",
+// PAPER.md P:201-205 [Table 2]; P:220 [§3.2] — the variant that wins at 8192).
+// C_out = alpha * A * B + beta * C_in, A/B in BF16 (kind::f16) or FP32 read as TF32
+// (kind::tf32), FP32 accumulation in TMEM, FP32 C (R1-R6).
+//
+// Structure (DESIGN.md §5 "tc_gemm"), persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer: A tile 128 x BK (K-major, SWIZZLE_128B) and B tile BK x 256
+//               (row-major B = MN-major: 128-byte N atoms; transB = K-major) into a
+//               4-stage shared-memory ring guarded by full/empty mbarriers;
+//   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.mma M=128 N=256 per
+//               UMMA_K slice into one of two TMEM accumulators (2 x 256 columns), then
+//               tcgen05.commit -> empty[stage] / tmem_full[acc];
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> alpha*acc + beta*C_in -> st.global, then
+//               tmem_empty[acc] — so tile i's epilogue overlaps tile i+1's mainloop.
+// Tiles are visited in GROUP_M-row bands so concurrently-resident CTAs share A/B in L2.
+// Edges: TMA zero-fills out-of-bounds boxes; the epilogue predicates rows/cols.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "tmap.h"
+
+namespace compar {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kGroupM = 16;
+
+template <bool kBF16, bool kTransB>
+struct TcCfg {
+    static constexpr int BM = 128, BN = 256;
+    static constexpr int ELEM = kBF16 ? 2 : 4;
+    static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K
+    static constexpr int UMMA_K = 32 / ELEM;       // K per tcgen05.mma (16 bf16 / 8 tf32)
+    static constexpr int STAGES = 4;
+    static constexpr uint32_t A_BYTES = BM * 128;
+    static constexpr uint32_t B_BYTES = BN * 128;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int B_ATOM_N = 128 / ELEM;    // N elements per 128-byte MN atom
+    static constexpr int B_BOXES = kTransB ? 1 : BN / B_ATOM_N;
+    static constexpr uint32_t B_BOX_BYTES = kTransB ? B_BYTES : BK * 128;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    // Instruction descriptor: D=F32 [4,6), A/B format [7,10)/[10,13) (1 BF16, 2 TF32),
+    // a_major=K [15], b_major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
+    static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
+                                      ((kTransB ? 0u : 1u) << 16) | ((uint32_t(BN) >> 3) << 17) |
+                                      ((uint32_t(BM) >> 4) << 24);
+};
+
+struct TcParams {
+    int64_t m, n, k;
+    float alpha, beta;
+    const float *C_in;
+    int64_t ldc_in;
+    float *C_out;
+    int64_t ldc_out;
+    int m_blocks, n_blocks, num_kb;
+    int cvec;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int &mb, int &nb) {
+    const int per_group = kGroupM * n_blocks;
+    const int g = t / per_group;
+    const int first_m = g * kGroupM;
+    const int gm = min(m_blocks - first_m, kGroupM);
+    const int r = t - g * per_group;
+    mb = first_m + r % gm;
+    nb = r / gm;
+}
+
+template <bool kBF16, bool kTransB>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+    using C = TcCfg<kBF16, kTransB>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+    const uint32_t full0 = ptx::smem_u32(bars);
+    const uint32_t empty0 = full0 + 8 * C::STAGES;
+    const uint32_t tfull0 = empty0 + 8 * C::STAGES;
+    const uint32_t tempty0 = tfull0 + 16;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
+    const uint32_t smem0 = ptx::smem_u32(smem);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < C::STAGES; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull0 + 8 * a, 1);
+            ptx::mbar_init(tempty0 + 8 * a, 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_slot));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_tiles = p.m_blocks * p.n_blocks;
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                int mb, nb;
+                tile_coords(t, p.m_blocks, p.n_blocks, mb, nb);
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+                    const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
+                    const uint32_t sb = sa + C::A_BYTES;
+                    const uint32_t fb = full0 + 8 * stage;
+                    ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+                    ptx::tma_load_2d(sa, &tmA, fb, kb * C::BK, mb * C::BM);
+                    if (kTransB) {
+                        ptx::tma_load_2d(sb, &tmB, fb, kb * C::BK, nb * C::BN);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < C::B_BOXES; ++b)
+                            ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N,
+                                             kb * C::BK);
+                    }
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {  // ---------------- MMA issuer
+        int stage = 0;
+        uint32_t phase = 0;
+        int local = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * C::BN;
+            for (int kb = 0; kb < p.num_kb; ++kb) {
+                ptx::mbar_wait(full0 + 8 * stage, phase);
+                ptx::tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
+                    const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                    for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
+                        const uint64_t adesc = ptx::smem_desc_sw128(sa + j * 32, 16, 1024);
+                        const uint64_t bdesc = kTransB ? ptx::smem_desc_sw128(sb + j * 32, 16, 1024)
+                                                       : ptx::smem_desc_sw128(sb + j * C::UMMA_K * 128,
+                                                                              C::B_BOX_BYTES, 1024);
+                        if (kBF16)
+                            ptx::mma_bf16(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+                        else
+                            ptx::mma_tf32(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+                    }
+                    ptx::tc_commit(empty0 + 8 * stage);
+                }
+                __syncwarp();
+                if (++stage == C::STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (lane == 0) ptx::tc_commit(tfull0 + 8 * acc);
+            __syncwarp();
+        }
+    } else {  // ---------------- epilogue warps 2..5
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int local = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+            int mb, nb;
+            tile_coords(t, p.m_blocks, p.n_blocks, mb, nb);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+            const int64_t row = static_cast<int64_t>(mb) * C::BM + q * 32 + lane;
+            const bool row_ok = row < p.m;
+            float *crow = p.C_out + row * p.ldc_out;
+            const float *cin = p.C_in + row * p.ldc_in;
+#pragma unroll 1
+            for (int c = 0; c < C::BN / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + c * 32, r);
+                ptx::tmem_ld_wait();
+                const int64_t col0 = static_cast<int64_t>(nb) * C::BN + c * 32;
+                if (!row_ok || col0 >= p.n) continue;
+                if (p.cvec && col0 + 32 <= p.n) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        float4 o;
+                        o.x = p.alpha * __uint_as_float(r[4 * v + 0]);
+                        o.y = p.alpha * __uint_as_float(r[4 * v + 1]);
+                        o.z = p.alpha * __uint_as_float(r[4 * v + 2]);
+                        o.w = p.alpha * __uint_as_float(r[4 * v + 3]);
+                        if (p.beta != 0.f) {
+                            const float4 ci = *reinterpret_cast<const float4 *>(cin + col0 + 4 * v);
+                            o.x = fmaf(p.beta, ci.x, o.x);
+                            o.y = fmaf(p.beta, ci.y, o.y);
+                            o.z = fmaf(p.beta, ci.z, o.z);
+                            o.w = fmaf(p.beta, ci.w, o.w);
+                        }
+                        *reinterpret_cast<float4 *>(crow + col0 + 4 * v) = o;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        if (col0 + e < p.n) {
+                            float o = p.alpha * __uint_as_float(r[e]);
+                            if (p.beta != 0.f) o = fmaf(p.beta, cin[col0 + e], o);
+                            crow[col0 + e] = o;
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty0 + 8 * acc);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc<512>(tmem_base);
+}
+
+// ---------------------------------------------------------------- host side
+template <bool kBF16, bool kTransB>
+cudaError_t launch_tc_t(const GemmLaunch &g) {
+    using C = TcCfg<kBF16, kTransB>;
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [] {
+        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<kBF16, kTransB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C::SMEM);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    CUtensorMap ta, tb;
+    if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, true)) return cudaErrorInvalidValue;
+    bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, C::BN, C::BK, true)
+                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N, true);
+    if (!ok) return cudaErrorInvalidValue;
+    TcParams p;
+    p.m = g.m, p.n = g.n, p.k = g.k;
+    p.alpha = g.alpha, p.beta = g.beta;
+    p.C_in = g.C_in, p.ldc_in = g.ldc_in, p.C_out = g.C_out, p.ldc_out = g.ldc_out;
+    p.m_blocks = static_cast<int>((g.m + C::BM - 1) / C::BM);
+    p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
+    p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
+    p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
+             (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
+    const int tiles = p.m_blocks * p.n_blocks;
+    const int grid = tiles < g.num_sms ? tiles : g.num_sms;
+    tc_gemm_kernel<kBF16, kTransB><<<grid, kThreads, C::SMEM, g.stream>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16) {
+    if (bf16) return g.transB ? launch_tc_t<true, true>(g) : launch_tc_t<true, false>(g);
+    return g.transB ? launch_tc_t<false, true>(g) : launch_tc_t<false, false>(g);
+}
+
+cudaError_t preload_tc_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, tc_gemm_kernel<true, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<true, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<false, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<false, true>);
+    return e;
+}
+
+}  // namespace compar

@@ -1,0 +1,222 @@
+// Variant (b) "tma_f32": TMA-fed, mbarrier-pipelined FP32 FFMA GEMM for sm_100a.
+//
+// Role: a second hand-written strict-FP32 "CUDA" mmul variant (PAPER.md P:201-205,
+// P:220) whose operand movement is Blackwell-native: cp.async.bulk.tensor (TMA) into a
+// multi-stage shared-memory ring, completion tracked by mbarrier transaction counts, one
+// producer warp and eight FFMA consumer warps.
+// C_out = alpha * A * B + beta * C_in (R1-R3).
+//
+//   * CTA tile 128 x 128, K step 32 (one 128-byte swizzle row of FP32), 4 stages;
+//   * A box 128 x 32, SWIZZLE_128B (K-major); B box 32 x 128 unswizzled (row-major B), or
+//     128 x 32 SWIZZLE_128B when transB;
+//   * consumer thread (tx, ty) owns rows ty + 16 i and columns {4tx.., 64 + 4tx..}
+//     (or tx + 16 j for transB): A read as float4 along K (conflict-free under the
+//     swizzle), B read as float4 along N;
+//   * TMA zero-fills out-of-bounds boxes; the epilogue predicates.
+// Eligibility: 16-byte aligned A/B and lda, ldb multiples of 4 (TMA stride rule).
+#include <cuda.h>
+
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "tmap.h"
+
+namespace compar {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 4;
+constexpr int kConsumers = 256, kThreads = kConsumers + 32;
+constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BK * BN * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 128;
+
+struct TmaParams {
+    int64_t m, n, k;
+    float alpha, beta;
+    const float *C_in;
+    int64_t ldc_in;
+    float *C_out;
+    int64_t ldc_out;
+    int num_kb;
+    int cvec;
+};
+
+// byte offset of the float4 holding (row, k4*4 .. k4*4+3) in a 128-byte-swizzled [rows][32] FP32 tile
+__device__ __forceinline__ uint32_t sw128_off(int row, int k4) { return row * 128 + ((k4 ^ (row & 7)) << 4); }
+
+template <bool kTransB>
+__global__ void __launch_bounds__(kThreads, 1)
+    tma_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TmaParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    const uint32_t full0 = ptx::smem_u32(bars), empty0 = full0 + 8 * STAGES;
+    const uint32_t smem0 = ptx::smem_u32(smem);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM, n0 = static_cast<int64_t>(blockIdx.x) * BN;
+
+    if (tid == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, kConsumers / 32);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumers / 32) {  // ---------------- producer warp
+        if (lane == 0) {
+            for (int kb = 0; kb < p.num_kb; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                ptx::mbar_wait(empty0 + 8 * s, ph ^ 1);
+                const uint32_t sa = smem0 + s * STAGE_BYTES, sb = sa + A_BYTES, fb = full0 + 8 * s;
+                ptx::mbar_arrive_expect_tx(fb, STAGE_BYTES);
+                ptx::tma_load_2d(sa, &tmA, fb, kb * BK, static_cast<int32_t>(m0));
+                if (kTransB)
+                    ptx::tma_load_2d(sb, &tmB, fb, kb * BK, static_cast<int32_t>(n0));
+                else
+                    ptx::tma_load_2d(sb, &tmB, fb, static_cast<int32_t>(n0), kb * BK);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps
+    const int tx = tid & 15, ty = tid >> 4;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    for (int kb = 0; kb < p.num_kb; ++kb) {
+        const int s = kb % STAGES;
+        ptx::mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
+        const uint8_t *sa = smem + s * STAGE_BYTES;
+        const uint8_t *sb = sa + A_BYTES;
+#pragma unroll 2
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+            float4 a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + 16 * i, k4));
+            if (kTransB) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 b = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + 16 * j, k4));
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
+                        acc[i][j] = fmaf(a[i].y, b.y, acc[i][j]);
+                        acc[i][j] = fmaf(a[i].z, b.z, acc[i][j]);
+                        acc[i][j] = fmaf(a[i].w, b.w, acc[i][j]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const float *brow = reinterpret_cast<const float *>(sb + (k4 * 4 + kk) * (BN * 4));
+                    const float4 b0 = *reinterpret_cast<const float4 *>(brow + tx * 4);
+                    const float4 b1 = *reinterpret_cast<const float4 *>(brow + 64 + tx * 4);
+                    const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, b[j], acc[i][j]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(empty0 + 8 * s);
+    }
+
+    // ---------------- epilogue
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + ty + 16 * i;
+        if (r >= p.m) continue;
+        float *crow = p.C_out + r * p.ldc_out;
+        const float *cin = p.C_in + r * p.ldc_in;
+        if (kTransB) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t c = n0 + tx + 16 * j;
+                if (c < p.n) {
+                    float o = p.alpha * acc[i][j];
+                    if (p.beta != 0.f) o = fmaf(p.beta, cin[c], o);
+                    crow[c] = o;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = n0 + h * 64 + tx * 4;
+                float o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o[j] = p.alpha * acc[i][h * 4 + j];
+                if (p.cvec && c + 3 < p.n) {
+                    if (p.beta != 0.f) {
+                        const float4 ci = *reinterpret_cast<const float4 *>(cin + c);
+                        o[0] = fmaf(p.beta, ci.x, o[0]);
+                        o[1] = fmaf(p.beta, ci.y, o[1]);
+                        o[2] = fmaf(p.beta, ci.z, o[2]);
+                        o[3] = fmaf(p.beta, ci.w, o[3]);
+                    }
+                    *reinterpret_cast<float4 *>(crow + c) = make_float4(o[0], o[1], o[2], o[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (c + j < p.n) {
+                            float v = o[j];
+                            if (p.beta != 0.f) v = fmaf(p.beta, cin[c + j], v);
+                            crow[c + j] = v;
+                        }
+                }
+            }
+        }
+    }
+}
+
+template <bool kTransB>
+cudaError_t launch_t(const GemmLaunch &g) {
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+        attr = cudaFuncSetAttribute(tma_f32_kernel<kTransB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    });
+    if (attr != cudaSuccess) return attr;
+    CUtensorMap ta, tb;
+    if (!get_tmap_2d(&ta, g.A, 4, g.m, g.k, g.lda, BM, BK, true)) return cudaErrorInvalidValue;
+    bool ok = kTransB ? get_tmap_2d(&tb, g.B, 4, g.n, g.k, g.ldb, BN, BK, true)
+                      : get_tmap_2d(&tb, g.B, 4, g.k, g.n, g.ldb, BK, BN, false);
+    if (!ok) return cudaErrorInvalidValue;
+    TmaParams p;
+    p.m = g.m, p.n = g.n, p.k = g.k, p.alpha = g.alpha, p.beta = g.beta;
+    p.C_in = g.C_in, p.ldc_in = g.ldc_in, p.C_out = g.C_out, p.ldc_out = g.ldc_out;
+    p.num_kb = static_cast<int>((g.k + BK - 1) / BK);
+    p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
+             (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
+    dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM));
+    tma_f32_kernel<kTransB><<<grid, kThreads, SMEM, g.stream>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tma_f32(const GemmLaunch &g) {
+    if ((g.m + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
+    return g.transB ? launch_t<true>(g) : launch_t<false>(g);
+}
+
+cudaError_t preload_tma_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, tma_f32_kernel<false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tma_f32_kernel<true>);
+    return e;
+}
+
+}  // namespace compar

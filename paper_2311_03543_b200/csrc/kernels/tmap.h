@@ -1,0 +1,21 @@
+// Host-side TMA tensor-map construction and caching (cuTensorMapEncodeTiled through the
+// runtime's driver entry point, so the library does not link libcuda directly).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace compar {
+
+// 2-D row-major tensor: `rows` x `cols` elements, row pitch `ld` elements of `elem_bytes`.
+// Box = box_rows x box_cols elements; `swizzle128` selects CU_TENSOR_MAP_SWIZZLE_128B.
+// Out-of-bounds box elements are zero-filled by the hardware.  Returns false on failure.
+bool make_tmap_2d(CUtensorMap *out, const void *base, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
+                  uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+// Cached wrapper: tensor maps are keyed by (ptr, shape, ld, box, swizzle) so repeated
+// submissions on the same buffers skip the host-side encode (SURVEY §7 hard part 4).
+bool get_tmap_2d(CUtensorMap *out, const void *ptr, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
+                 uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+}  // namespace compar

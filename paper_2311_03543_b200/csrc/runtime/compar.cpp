@@ -1,0 +1,925 @@
+// libcompar runtime: the C ABI of include/compar.h over the sm_100a kernels.
+//
+// Maps the paper's runtime model onto one B200 per process:
+//   * variant registry        <- method_declare interface/target/name and
+//                                the StarPU codelet;
+//   * task submit / sync      <- "creation and the submission of the task" and the
+//                                unregister-after-wait rule;
+//   * history selector        <- "the STARPU decision-making process relies on ... models"
+//                                (P:224), algorithm in history.{h,cpp};
+//   * row panels + NCCL bcast <- BASELINE.json north star (multi-GPU, one process per GPU).
+#include "compar.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.h"
+#include "history.h"
+
+namespace compar {
+namespace {
+
+thread_local std::string t_err;
+
+compar_status fail(compar_status s, const std::string &msg) {
+    t_err = msg;
+    return s;
+}
+compar_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(COMPAR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Variant {
+    std::string name;
+    compar_target target;
+    compar_gemm_fn fn;
+    void *user;
+};
+
+struct PanelRun {
+    compar_panel p{};
+    cudaEvent_t start = nullptr, stop = nullptr;
+    int64_t virtual_ns = 0;
+};
+
+struct Task {
+    uint64_t id = 0;
+    Key key{};
+    int variant = -1;
+    int mode = kNoop;
+    bool warm = false;
+    bool history = false;  // sample goes to the history when harvested
+    compar_status status = COMPAR_OK;
+    std::vector<PanelRun> panels;
+    cudaEvent_t begin = nullptr, end = nullptr, bc0 = nullptr, bc1 = nullptr;
+    bool world = false;
+};
+
+struct Ctx {
+    std::mutex mu;
+    compar_config cfg{};
+    bool virt = false;
+    int device = 0, num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<cudaEvent_t> pool;
+    std::vector<Variant> variants;
+    History hist;
+    uint64_t next_task = 1;
+    std::map<uint64_t, Task> tasks;
+    compar_stats stats{};
+    std::string perf_path;
+    void *staging[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t staging_bytes[4] = {0, 0, 0, 0};
+    void *breplica = nullptr;
+    size_t breplica_bytes = 0;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    int64_t *red_buf = nullptr;  // device scalar for the rank-consistent sample all-reduce
+    compar_reduce_fn reduce_hook = nullptr;
+    void *reduce_user = nullptr;
+};
+
+std::mutex g_live_mu;
+std::set<Ctx *> g_live;
+
+Ctx *as_ctx(void *p) {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    Ctx *c = static_cast<Ctx *>(p);
+    return g_live.count(c) ? c : nullptr;
+}
+
+int env_int(const char *name, int dflt) {
+    const char *v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    char *end = nullptr;
+    long x = std::strtol(v, &end, 10);
+    return (end && *end == 0) ? static_cast<int>(x) : dflt;
+}
+
+int elem_bytes(compar_dtype d) { return d == COMPAR_BF16 ? 2 : 4; }
+
+std::string u128_str(unsigned __int128 v) {
+    if (v == 0) return "0";
+    char buf[48];
+    int i = 47;
+    buf[i] = 0;
+    while (v > 0) {
+        buf[--i] = static_cast<char>('0' + static_cast<int>(v % 10));
+        v /= 10;
+    }
+    return std::string(buf + i);
+}
+bool parse_u128(const std::string &s, unsigned __int128 *out) {
+    if (s.empty()) return false;
+    unsigned __int128 v = 0;
+    for (char c : s) {
+        if (c < '0' || c > '9') return false;
+        v = v * 10 + static_cast<unsigned>(c - '0');
+    }
+    *out = v;
+    return true;
+}
+
+// ---------------------------------------------------------------- events
+cudaEvent_t get_event(Ctx *c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+}
+void put_event(Ctx *c, cudaEvent_t &e) {
+    if (e) c->pool.push_back(e);
+    e = nullptr;
+}
+void release_task_events(Ctx *c, Task &t) {
+    for (auto &p : t.panels) {
+        put_event(c, p.start);
+        put_event(c, p.stop);
+    }
+    put_event(c, t.begin);
+    put_event(c, t.end);
+    put_event(c, t.bc0);
+    put_event(c, t.bc1);
+}
+int64_t elapsed_ns(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    if (!a || !b || cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0;
+    return static_cast<int64_t>(std::llround(static_cast<double>(ms) * 1e6));
+}
+
+// ---------------------------------------------------------------- partition (a4)
+void partition(int64_t m, int p, std::vector<int64_t> &offs) {
+    offs.assign(static_cast<size_t>(p) + 1, 0);
+    const int64_t per = (m + p - 1) / p;
+    const int64_t base = ((per + 127) / 128) * 128;
+    for (int r = 0; r < p; ++r) offs[r] = std::min(m, static_cast<int64_t>(r) * base);
+    offs[p] = m;
+}
+
+// ---------------------------------------------------------------- validation
+compar_status validate(Ctx *c, const compar_gemm_desc *d) {
+    if (!d) return fail(COMPAR_E_INVALID, "desc is NULL");
+    if (d->m < 0 || d->n < 0 || d->k < 0) return fail(COMPAR_E_INVALID, "negative dimension");
+    if (d->in_dtype != COMPAR_F32 && d->in_dtype != COMPAR_BF16) return fail(COMPAR_E_INVALID, "bad in_dtype");
+    if (d->compute < COMPAR_COMPUTE_F32_STRICT || d->compute > COMPAR_COMPUTE_BF16)
+        return fail(COMPAR_E_INVALID, "bad compute");
+    if ((d->in_dtype == COMPAR_BF16) != (d->compute == COMPAR_COMPUTE_BF16))
+        return fail(COMPAR_E_INVALID, "BF16 storage requires COMPUTE_BF16 and vice versa");
+    if (d->transB != 0 && d->transB != 1) return fail(COMPAR_E_INVALID, "transB must be 0 or 1");
+    if (d->mem != COMPAR_MEM_DEVICE && d->mem != COMPAR_MEM_HOST) return fail(COMPAR_E_INVALID, "bad mem");
+    if (d->panels < 0 || d->panels > COMPAR_MAX_PANELS) return fail(COMPAR_E_INVALID, "panels out of range");
+    if (d->world && d->panels > 1) return fail(COMPAR_E_INVALID, "world and loopback panels are exclusive");
+    if (d->world && !c->virt && !c->comm) return fail(COMPAR_E_STATE, "world=1 needs compar_comm_init");
+    if (d->world && d->mem == COMPAR_MEM_HOST) return fail(COMPAR_E_INVALID, "world mode takes device buffers");
+    if (d->variant_hint < -1 || d->variant_hint >= static_cast<int>(c->variants.size()))
+        return fail(COMPAR_E_INVALID, "variant_hint out of range");
+    if (d->m == 0 || d->n == 0) return COMPAR_OK;
+    if (d->k > 0 && d->alpha != 0.f) {
+        if (!c->virt && (!d->A || (!d->B && !(d->world && c->rank != 0))))
+            return fail(COMPAR_E_INVALID, "A/B NULL");
+        if (d->lda < d->k) return fail(COMPAR_E_INVALID, "lda < k");
+        if (d->ldb < (d->transB ? d->k : d->n)) return fail(COMPAR_E_INVALID, "ldb too small");
+    }
+    if (d->beta != 0.f) {
+        if (!c->virt && !d->C_in) return fail(COMPAR_E_INVALID, "C_in NULL with beta != 0");
+        if (d->ldc_in < d->n) return fail(COMPAR_E_INVALID, "ldc_in < n");
+    }
+    if (!c->virt && !d->C_out) return fail(COMPAR_E_INVALID, "C_out NULL");
+    if (d->ldc_out < d->n) return fail(COMPAR_E_INVALID, "ldc_out < n");
+    return COMPAR_OK;
+}
+
+// ---------------------------------------------------------------- eligibility (step 1)
+bool admits(compar_target t, compar_dtype dt, compar_compute cp) {
+    switch (t) {
+        case COMPAR_TGT_USER: return true;
+        case COMPAR_TGT_SIMT_F32:
+        case COMPAR_TGT_TMA_F32: return dt == COMPAR_F32 && cp != COMPAR_COMPUTE_BF16;
+        case COMPAR_TGT_TC_TF32: return dt == COMPAR_F32 && cp == COMPAR_COMPUTE_TF32;
+        case COMPAR_TGT_TC_BF16: return dt == COMPAR_BF16 && cp == COMPAR_COMPUTE_BF16;
+    }
+    return false;
+}
+
+struct Plan {
+    Key key{};
+    std::vector<compar_panel> panels;
+    bool host_staged = false;
+};
+
+// Pointers the kernels will read (device or staging) decide TMA eligibility.
+bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, const Plan &plan) {
+    if (t == COMPAR_TGT_USER) return true;
+    const int64_t mrows = plan.key.m;
+    if ((t == COMPAR_TGT_SIMT_F32 || t == COMPAR_TGT_TMA_F32) && (mrows + 127) / 128 > 65535) return false;
+    if (t == COMPAR_TGT_SIMT_F32) return true;
+    const int eb = (t == COMPAR_TGT_TC_BF16) ? 2 : 4;
+    if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;
+    if ((d->lda * eb) % 16 != 0 || (d->ldb * eb) % 16 != 0) return false;
+    if (c->virt) return true;
+    for (const auto &p : plan.panels) {
+        if (reinterpret_cast<uintptr_t>(p.A) % 16 != 0) return false;
+        if (p.B && reinterpret_cast<uintptr_t>(p.B) % 16 != 0) return false;
+    }
+    return true;
+}
+
+void eligible_set(Ctx *c, const compar_gemm_desc *d, const Plan &plan, std::vector<int> &idx,
+                  std::vector<std::string> &names) {
+    idx.clear();
+    names.clear();
+    for (size_t v = 0; v < c->variants.size(); ++v) {
+        if (v < 63 && (c->cfg.variant_mask >> v) & 1) continue;
+        const Variant &var = c->variants[v];
+        if (!admits(var.target, d->in_dtype, d->compute)) continue;
+        if (!constraints_ok(c, var.target, d, plan)) continue;
+        idx.push_back(static_cast<int>(v));
+        names.push_back(var.name);
+    }
+}
+
+// ---------------------------------------------------------------- staging (host-mode buffers)
+compar_status ensure_buffer(void **buf, size_t *have, size_t need) {
+    if (need <= *have && *buf) return COMPAR_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    if (need == 0) return COMPAR_OK;
+    cudaError_t e = cudaMalloc(buf, need);
+    if (e != cudaSuccess) return fail(COMPAR_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    *have = need;
+    return COMPAR_OK;
+}
+
+compar_status build_plan(Ctx *c, const compar_gemm_desc *d, Plan &plan, const void *A, const void *B,
+                         const float *Cin, float *Cout) {
+    const int eb = elem_bytes(d->in_dtype);
+    plan.panels.clear();
+    std::vector<int64_t> offs;
+    if (d->world) {
+        partition(d->m, c->nranks, offs);
+        compar_panel p{};
+        p.index = c->rank;
+        p.row0 = offs[c->rank];
+        p.rows = offs[c->rank + 1] - offs[c->rank];
+        p.A = A;
+        p.B = B;
+        p.C_in = Cin;
+        p.C_out = Cout;
+        if (p.rows > 0) plan.panels.push_back(p);
+        plan.key.m = offs[1] - offs[0];
+    } else {
+        const int P = d->panels > 1 ? d->panels : 1;
+        partition(d->m, P, offs);
+        for (int r = 0; r < P; ++r) {
+            compar_panel p{};
+            p.index = r;
+            p.row0 = offs[r];
+            p.rows = offs[r + 1] - offs[r];
+            if (p.rows == 0) continue;
+            p.A = A ? static_cast<const char *>(A) + static_cast<size_t>(p.row0) * d->lda * eb : nullptr;
+            p.B = B;
+            p.C_in = Cin ? Cin + p.row0 * d->ldc_in : nullptr;
+            p.C_out = Cout ? Cout + p.row0 * d->ldc_out : nullptr;
+            plan.panels.push_back(p);
+        }
+        plan.key.m = offs[1] - offs[0];
+    }
+    plan.key.n = d->n;
+    plan.key.k = d->k;
+    plan.key.dtype = d->in_dtype;
+    plan.key.compute = d->compute;
+    plan.key.transB = d->transB;
+    plan.key.beta0 = d->beta == 0.f ? 1 : 0;
+    return COMPAR_OK;
+}
+
+// ---------------------------------------------------------------- harvest
+compar_status finish_task(Ctx *c, Task &t, compar_report *rep);
+
+// Step 6: before a model decision, every pending execution of this key is harvested in
+// task-id order (std::map iterates in id order).
+compar_status harvest_key(Ctx *c, const Key &k) {
+    std::vector<uint64_t> ids;
+    for (auto &kv : c->tasks)
+        if (kv.second.history && kv.second.key == k) ids.push_back(kv.first);
+    for (uint64_t id : ids) {
+        auto it = c->tasks.find(id);
+        compar_report rep;
+        finish_task(c, it->second, &rep);
+        c->tasks.erase(it);
+    }
+    return COMPAR_OK;
+}
+
+compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->task = t.id;
+    rep->variant = t.variant;
+    rep->mode = t.mode;
+    rep->warmup = t.warm ? 1 : 0;
+    rep->npanels = static_cast<int>(t.panels.size());
+    int64_t sample = 0;
+    if (!c->virt && t.end) {
+        cudaError_t e = cudaEventSynchronize(t.end);
+        if (e != cudaSuccess && t.status == COMPAR_OK) {
+            t.status = COMPAR_E_TASK_FAILED;
+            t_err = std::string("task execution failed: ") + cudaGetErrorString(e);
+        }
+    }
+    for (size_t i = 0; i < t.panels.size(); ++i) {
+        const int64_t ns = c->virt ? t.panels[i].virtual_ns : elapsed_ns(t.panels[i].start, t.panels[i].stop);
+        if (i < COMPAR_MAX_PANELS) rep->panel_ns[i] = ns;
+        sample = std::max(sample, ns);
+    }
+    if (!c->virt) {
+        rep->total_ns = elapsed_ns(t.begin, t.end);
+        rep->bcast_ns = elapsed_ns(t.bc0, t.bc1);
+    } else {
+        for (auto &p : t.panels) rep->total_ns += p.virtual_ns;
+    }
+    // SPMD: every rank harvests the same task sequence; the sample is the max over ranks so
+    // all ranks keep an identical history (rank-consistent decisions).
+    if (t.world && c->nranks > 1 && t.history && c->reduce_hook) {
+        c->reduce_hook(&sample, c->reduce_user);
+    } else if (t.world && c->comm && c->nranks > 1 && t.history) {
+        cudaMemcpyAsync(c->red_buf, &sample, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
+        ncclResult_t r = ncclAllReduce(c->red_buf, c->red_buf, 1, ncclInt64, ncclMax, c->comm, c->stream);
+        cudaMemcpyAsync(&sample, c->red_buf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
+        cudaStreamSynchronize(c->stream);
+        if (r != ncclSuccess && t.status == COMPAR_OK) t.status = COMPAR_E_NCCL;
+    }
+    rep->ns = sample;
+    rep->status = t.status;
+    if (t.history && t.status == COMPAR_OK && !t.warm && t.variant >= 0) {
+        c->hist.harvest(c->variants[t.variant].name, t.key, sample);
+        c->stats.harvested++;
+    }
+    if (t.status != COMPAR_OK) c->stats.failed++;
+    release_task_events(c, t);
+    return t.status == COMPAR_OK ? COMPAR_OK : COMPAR_E_TASK_FAILED;
+}
+
+// ---------------------------------------------------------------- running a variant on a panel
+compar_status run_builtin(Ctx *c, compar_target t, const compar_gemm_desc *d, const compar_panel &p,
+                          cudaStream_t s) {
+    GemmLaunch g;
+    g.m = p.rows, g.n = d->n, g.k = d->k;
+    g.alpha = d->alpha, g.beta = d->beta;
+    g.A = p.A, g.lda = d->lda, g.B = p.B, g.ldb = d->ldb, g.transB = d->transB;
+    g.C_in = p.C_in, g.ldc_in = d->ldc_in, g.C_out = p.C_out, g.ldc_out = d->ldc_out;
+    g.stream = s;
+    g.num_sms = c->num_sms;
+    cudaError_t e;
+    switch (t) {
+        case COMPAR_TGT_SIMT_F32: e = launch_simt_f32(g); break;
+        case COMPAR_TGT_TMA_F32: e = launch_tma_f32(g); break;
+        case COMPAR_TGT_TC_TF32: e = launch_tc_gemm(g, false); break;
+        case COMPAR_TGT_TC_BF16: e = launch_tc_gemm(g, true); break;
+        default: return fail(COMPAR_E_INVALID, "not a built-in target");
+    }
+    c->stats.launches++;
+    if (e != cudaSuccess) return fail(COMPAR_E_TASK_FAILED, std::string("launch: ") + cudaGetErrorString(e));
+    return COMPAR_OK;
+}
+
+compar_status run_scale(Ctx *c, const compar_gemm_desc *d, const compar_panel &p, cudaStream_t s) {
+    GemmLaunch g{};
+    g.m = p.rows, g.n = d->n, g.beta = d->beta;
+    g.C_in = p.C_in, g.ldc_in = d->ldc_in, g.C_out = p.C_out, g.ldc_out = d->ldc_out;
+    g.stream = s;
+    g.num_sms = c->num_sms;
+    cudaError_t e = launch_scale(g);
+    c->stats.launches++;
+    if (e != cudaSuccess) return fail(COMPAR_E_TASK_FAILED, std::string("scale: ") + cudaGetErrorString(e));
+    return COMPAR_OK;
+}
+
+}  // namespace
+}  // namespace compar
+
+using namespace compar;
+
+extern "C" {
+
+void compar_config_default(compar_config *cfg) {
+    if (!cfg) return;
+    cfg->ngpu = -1;
+    cfg->device = -1;
+    cfg->sched = -1;
+    cfg->calib_k = -1;
+    cfg->calib_warmup = -1;
+    cfg->perf_model_path = nullptr;
+    cfg->bcast_chunks = -1;
+    cfg->builtins = -1;
+    cfg->virtual_clock = 0;
+    cfg->variant_mask = -1;
+}
+
+const char *compar_last_error(void *) { return t_err.c_str(); }
+
+compar_status compar_register_variant(void *ctx, const char *iface, const char *name, compar_target target,
+                                      compar_gemm_fn fn, void *user, int *out_id);
+
+compar_status compar_init(const compar_config *cfg_in, void **ctx) {
+    if (!ctx) return fail(COMPAR_E_INVALID, "ctx out-pointer is NULL");
+    if (*ctx && as_ctx(*ctx)) return fail(COMPAR_E_STATE, "context already initialised");
+    compar_config cfg;
+    compar_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    if (cfg.ngpu < 0) cfg.ngpu = env_int("COMPAR_NGPU", 1);
+    if (cfg.ngpu == 0) return fail(COMPAR_E_INVALID, "COMPAR_NGPU=0: no GPU class and no CPU fallback");
+    if (cfg.ngpu != 1) return fail(COMPAR_E_INVALID, "one GPU per process (use compar_comm_init for SPMD)");
+    if (cfg.sched < 0) {
+        const char *s = std::getenv("COMPAR_SCHED");
+        cfg.sched = (s && std::strcmp(s, "eager") == 0) ? 1 : 0;
+    }
+    if (cfg.calib_k < 0) cfg.calib_k = env_int("COMPAR_CALIB_K", 3);
+    if (cfg.calib_warmup < 0) cfg.calib_warmup = env_int("COMPAR_CALIB_WARMUP", 1);
+    if (cfg.bcast_chunks < 0) cfg.bcast_chunks = env_int("COMPAR_BCAST_CHUNKS", 4);
+    if (cfg.builtins < 0) cfg.builtins = 1;
+    if (cfg.variant_mask < 0) {
+        const char *s = std::getenv("COMPAR_VARIANT_MASK");
+        cfg.variant_mask = s ? std::strtoll(s, nullptr, 0) : 0;
+    }
+    auto *c = new Ctx();
+    c->cfg = cfg;
+    c->virt = cfg.virtual_clock != 0;
+    c->hist.calib_k = cfg.calib_k;
+    c->hist.calib_warmup = cfg.calib_warmup;
+    const char *pp = cfg.perf_model_path ? cfg.perf_model_path : std::getenv("COMPAR_PERF_MODEL");
+    if (pp) c->perf_path = pp;
+    c->cfg.perf_model_path = nullptr;
+    if (!c->virt) {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0) {
+            delete c;
+            return fail(COMPAR_E_CUDA, "no CUDA device (the library has no CPU fallback)");
+        }
+        if (cfg.device >= 0) {
+            if (cfg.device >= n || (e = cudaSetDevice(cfg.device)) != cudaSuccess) {
+                delete c;
+                return fail(COMPAR_E_CUDA, "cannot select device");
+            }
+        }
+        cudaGetDevice(&c->device);
+        cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+        if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            delete c;
+            return cuda_fail(e, "cudaStreamCreate");
+        }
+        if ((e = preload_kernels()) != cudaSuccess) {
+            cudaStreamDestroy(c->stream);
+            delete c;
+            return cuda_fail(e, "kernel preload (is this an sm_100 device?)");
+        }
+        cudaMalloc(reinterpret_cast<void **>(&c->red_buf), sizeof(int64_t));
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_live_mu);
+        g_live.insert(c);
+    }
+    if (!c->virt && cfg.builtins) {
+        int id;
+        compar_register_variant(c, "gemm", "simt_f32", COMPAR_TGT_SIMT_F32, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "tma_f32", COMPAR_TGT_TMA_F32, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "tc_tf32", COMPAR_TGT_TC_TF32, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "tc_bf16", COMPAR_TGT_TC_BF16, nullptr, nullptr, &id);
+    }
+    *ctx = c;
+    if (!c->perf_path.empty()) {
+        std::ifstream f(c->perf_path);
+        if (f.good()) {
+            compar_status s = compar_perf_load(c, c->perf_path.c_str());
+            if (s != COMPAR_OK) return s;
+        }
+    }
+    return COMPAR_OK;
+}
+
+compar_status compar_terminate(void *ctx) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    compar_status st = COMPAR_OK;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        for (auto &kv : c->tasks) {
+            compar_report rep;
+            finish_task(c, kv.second, &rep);
+        }
+        c->tasks.clear();
+    }
+    if (!c->perf_path.empty()) st = compar_perf_save(c, c->perf_path.c_str());
+    {
+        std::lock_guard<std::mutex> lk(g_live_mu);
+        g_live.erase(c);
+    }
+    if (!c->virt) {
+        cudaStreamSynchronize(c->stream);
+        for (auto &b : c->staging)
+            if (b) cudaFree(b);
+        if (c->breplica) cudaFree(c->breplica);
+        if (c->red_buf) cudaFree(c->red_buf);
+        for (auto e : c->pool) cudaEventDestroy(e);
+        if (c->comm) ncclCommDestroy(c->comm);
+        cudaStreamDestroy(c->stream);
+    }
+    delete c;
+    return st;
+}
+
+compar_status compar_register_variant(void *ctx, const char *iface, const char *name, compar_target target,
+                                      compar_gemm_fn fn, void *user, int *out_id) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!iface || std::strcmp(iface, "gemm") != 0) return fail(COMPAR_E_INVALID, "unknown interface (only \"gemm\")");
+    if (!name || !*name || std::strlen(name) > 63) return fail(COMPAR_E_INVALID, "bad variant name");
+    for (const char *p = name; *p; ++p)
+        if (*p == ' ' || *p == '\t' || *p == '\n') return fail(COMPAR_E_INVALID, "variant name has whitespace");
+    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_USER) return fail(COMPAR_E_INVALID, "unknown target");
+    if (target == COMPAR_TGT_USER && !fn) return fail(COMPAR_E_INVALID, "USER variant needs a launch function");
+    if (target != COMPAR_TGT_USER && c->virt) return fail(COMPAR_E_INVALID, "built-in targets need CUDA");
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (const auto &v : c->variants)
+        if (v.name == name) return fail(COMPAR_E_DUPLICATE, std::string("duplicate variant ") + name);
+    if (c->variants.size() >= 64) return fail(COMPAR_E_INVALID, "too many variants");
+    c->variants.push_back(Variant{name, target, fn, user});
+    if (out_id) *out_id = static_cast<int>(c->variants.size()) - 1;
+    return COMPAR_OK;
+}
+
+compar_status compar_variant_count(void *ctx, int *n) {
+    Ctx *c = as_ctx(ctx);
+    if (!c || !n) return fail(c ? COMPAR_E_INVALID : COMPAR_E_STATE, "bad arguments");
+    std::lock_guard<std::mutex> lk(c->mu);
+    *n = static_cast<int>(c->variants.size());
+    return COMPAR_OK;
+}
+
+compar_status compar_variant_info(void *ctx, int id, char *name, int name_len, int *target) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (id < 0 || id >= static_cast<int>(c->variants.size())) return fail(COMPAR_E_INVALID, "bad variant id");
+    if (name && name_len > 0) {
+        std::strncpy(name, c->variants[id].name.c_str(), static_cast<size_t>(name_len) - 1);
+        name[name_len - 1] = 0;
+    }
+    if (target) *target = c->variants[id].target;
+    return COMPAR_OK;
+}
+
+namespace {
+
+// Decide (variant, mode) for a plan; `commit` accounts the execution in the history.
+compar_status choose(Ctx *c, const compar_gemm_desc *d, const Plan &plan, bool commit, int *variant, int *mode,
+                     bool *warm) {
+    std::vector<int> idx;
+    std::vector<std::string> names;
+    eligible_set(c, d, plan, idx, names);
+    *warm = false;
+    if (d->variant_hint >= 0) {
+        if (std::find(idx.begin(), idx.end(), d->variant_hint) == idx.end())
+            return fail(COMPAR_E_INVALID, "variant_hint is not eligible for this task");
+        *variant = d->variant_hint;
+        *mode = kHint;
+        return COMPAR_OK;
+    }
+    if (idx.empty()) return fail(COMPAR_E_NO_VARIANT, "no eligible variant for this dtype/compute/layout");
+    if (c->cfg.sched == 1) {
+        *variant = idx[0];
+        *mode = kEager;
+        return COMPAR_OK;
+    }
+    if (!c->hist.calibrating(names, plan.key)) harvest_key(c, plan.key);
+    Mode m;
+    const int pos = c->hist.decide(names, plan.key, &m);
+    *variant = idx[pos];
+    *mode = m;
+    if (commit) *warm = c->hist.commit(names[pos], plan.key);
+    return COMPAR_OK;
+}
+
+}  // namespace
+
+compar_status compar_select(void *ctx, const compar_gemm_desc *d, int *variant, int *mode) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    compar_status s = validate(c, d);
+    if (s != COMPAR_OK) return s;
+    Plan plan;
+    build_plan(c, d, plan, d->A, d->B, d->C_in, d->C_out);
+    int v = -1, m = kNoop;
+    bool warm;
+    if (d->m > 0 && d->n > 0 && d->k > 0 && d->alpha != 0.f) {
+        s = choose(c, d, plan, false, &v, &m, &warm);
+        if (s != COMPAR_OK) return s;
+    }
+    if (variant) *variant = v;
+    if (mode) *mode = m;
+    return COMPAR_OK;
+}
+
+compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t *task_out) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    compar_status s = validate(c, d);
+    if (s != COMPAR_OK) return s;
+    c->stats.submits++;
+    Task t;
+    t.id = c->next_task++;
+    t.world = d->world != 0;
+    cudaStream_t st = d->stream ? static_cast<cudaStream_t>(d->stream) : c->stream;
+    const int eb = elem_bytes(d->in_dtype);
+    const bool work = d->m > 0 && d->n > 0;
+    const bool gemm = work && d->k > 0 && d->alpha != 0.f;
+
+    // Operand pointers the kernels use (host mode: library staging buffers).
+    const void *A = d->A, *B = d->B;
+    const float *Cin = d->C_in;
+    float *Cout = d->C_out;
+    const bool host = d->mem == COMPAR_MEM_HOST && !c->virt;
+    const size_t a_bytes = gemm ? static_cast<size_t>(d->m - 1) * d->lda * eb + static_cast<size_t>(d->k) * eb : 0;
+    const size_t b_rows = d->transB ? d->n : d->k;
+    const size_t b_width = d->transB ? d->k : d->n;
+    const size_t b_bytes = gemm ? (b_rows - 1) * d->ldb * eb + b_width * eb : 0;
+    const size_t cin_bytes =
+        (work && d->beta != 0.f) ? static_cast<size_t>(d->m - 1) * d->ldc_in * 4 + static_cast<size_t>(d->n) * 4 : 0;
+    const size_t cout_bytes = work ? static_cast<size_t>(d->m - 1) * d->ldc_out * 4 + static_cast<size_t>(d->n) * 4 : 0;
+    if (host && work) {
+        if ((s = ensure_buffer(&c->staging[0], &c->staging_bytes[0], a_bytes)) != COMPAR_OK) return s;
+        if ((s = ensure_buffer(&c->staging[1], &c->staging_bytes[1], b_bytes)) != COMPAR_OK) return s;
+        if ((s = ensure_buffer(&c->staging[3], &c->staging_bytes[3], cout_bytes)) != COMPAR_OK) return s;
+        const bool inplace = d->C_in == d->C_out && d->ldc_in == d->ldc_out;
+        if (cin_bytes && !inplace && (s = ensure_buffer(&c->staging[2], &c->staging_bytes[2], cin_bytes)) != COMPAR_OK)
+            return s;
+        A = c->staging[0];
+        B = c->staging[1];
+        Cout = static_cast<float *>(c->staging[3]);
+        Cin = cin_bytes ? (inplace ? Cout : static_cast<float *>(c->staging[2])) : nullptr;
+    }
+    // World mode, non-root ranks: B arrives in a replica.
+    if (t.world && c->rank != 0 && gemm && !c->virt) {
+        if (d->B_replica) {
+            B = d->B_replica;
+        } else {
+            if ((s = ensure_buffer(&c->breplica, &c->breplica_bytes, b_bytes)) != COMPAR_OK) return s;
+            B = c->breplica;
+        }
+    }
+
+    Plan plan;
+    build_plan(c, d, plan, A, B, Cin, Cout);
+    t.key = plan.key;
+    if (gemm) {
+        bool warm = false;
+        s = choose(c, d, plan, true, &t.variant, &t.mode, &warm);
+        if (s != COMPAR_OK) {
+            c->stats.failed++;
+            return s;
+        }
+        t.warm = warm;
+        t.history = (t.mode == kWarmup || t.mode == kCalib || t.mode == kModel);
+    } else {
+        t.mode = kNoop;
+    }
+    for (const auto &p : plan.panels) {
+        PanelRun pr;
+        pr.p = p;
+        t.panels.push_back(pr);
+    }
+
+    if (c->virt) {
+        // Virtual clock: USER variants report synthetic ns; nothing touches CUDA.
+        if (gemm) {
+            const Variant &var = c->variants[t.variant];
+            for (auto &pr : t.panels) {
+                compar_status r = var.fn(d, &pr.p, nullptr, var.user, &pr.virtual_ns);
+                if (r != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+            }
+        }
+    } else if (work) {
+        t.begin = get_event(c);
+        t.end = get_event(c);
+        cudaEventRecord(t.begin, st);
+        if (host) {
+            if (a_bytes) cudaMemcpyAsync(const_cast<void *>(A), d->A, a_bytes, cudaMemcpyHostToDevice, st);
+            if (b_bytes) cudaMemcpyAsync(const_cast<void *>(B), d->B, b_bytes, cudaMemcpyHostToDevice, st);
+            if (cin_bytes) cudaMemcpyAsync(const_cast<float *>(Cin), d->C_in, cin_bytes, cudaMemcpyHostToDevice, st);
+            c->stats.bytes_h2d += static_cast<int64_t>(a_bytes + b_bytes + cin_bytes);
+        }
+        if (t.world && c->nranks > 1 && gemm) {
+            t.bc0 = get_event(c);
+            t.bc1 = get_event(c);
+            cudaEventRecord(t.bc0, st);
+            void *buf = const_cast<void *>(c->rank == 0 ? d->B : B);
+            ncclResult_t r = ncclBroadcast(buf, buf, b_bytes, ncclChar, 0, c->comm, st);
+            if (r != ncclSuccess) t.status = COMPAR_E_NCCL;
+            cudaEventRecord(t.bc1, st);
+        }
+        for (auto &pr : t.panels) {
+            pr.start = get_event(c);
+            pr.stop = get_event(c);
+            cudaEventRecord(pr.start, st);
+            compar_status r;
+            if (!gemm) {
+                r = run_scale(c, d, pr.p, st);
+            } else {
+                const Variant &var = c->variants[t.variant];
+                if (var.target == COMPAR_TGT_USER) {
+                    r = var.fn(d, &pr.p, st, var.user, nullptr);
+                    c->stats.launches++;
+                } else {
+                    r = run_builtin(c, var.target, d, pr.p, st);
+                }
+            }
+            if (r != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+            cudaEventRecord(pr.stop, st);
+        }
+        if (host) {
+            cudaMemcpyAsync(d->C_out, Cout, cout_bytes, cudaMemcpyDeviceToHost, st);
+            c->stats.bytes_d2h += static_cast<int64_t>(cout_bytes);
+        }
+        cudaEventRecord(t.end, st);
+    }
+    if (task_out) *task_out = t.id;
+    c->tasks.emplace(t.id, std::move(t));
+    return COMPAR_OK;
+}
+
+compar_status compar_sync(void *ctx, uint64_t task, compar_report *out) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    compar_report rep;
+    std::memset(&rep, 0, sizeof(rep));
+    compar_status st = COMPAR_OK;
+    if (task == COMPAR_TASK_ALL) {
+        for (auto &kv : c->tasks) {
+            compar_status s = finish_task(c, kv.second, &rep);
+            if (s != COMPAR_OK) st = s;
+        }
+        c->tasks.clear();
+    } else {
+        auto it = c->tasks.find(task);
+        if (it == c->tasks.end()) return fail(COMPAR_E_UNKNOWN_TASK, "unknown or already-synced task");
+        st = finish_task(c, it->second, &rep);
+        c->tasks.erase(it);
+    }
+    if (out) *out = rep;
+    return st;
+}
+
+compar_status compar_perf_save(void *ctx, const char *path) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!path) return fail(COMPAR_E_INVALID, "path is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    std::ofstream f(path);
+    if (!f.good()) return fail(COMPAR_E_IO, std::string("cannot write ") + path);
+    f << "# compar perf model v1: variant m n k dtype compute transB beta0 seen count sum_ns sumsq_ns min_ns\n";
+    for (const auto &kv : c->hist.table()) {
+        const Key &k = kv.first.second;
+        const Record &r = kv.second;
+        f << kv.first.first << ' ' << k.m << ' ' << k.n << ' ' << k.k << ' ' << k.dtype << ' ' << k.compute << ' '
+          << k.transB << ' ' << k.beta0 << ' ' << r.seen << ' ' << r.count << ' ' << u128_str(r.sum_ns) << ' '
+          << u128_str(r.sumsq_ns) << ' ' << r.min_ns << '\n';
+    }
+    return f.good() ? COMPAR_OK : fail(COMPAR_E_IO, "write failed");
+}
+
+compar_status compar_perf_load(void *ctx, const char *path) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!path) return fail(COMPAR_E_INVALID, "path is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    std::ifstream f(path);
+    if (!f.good()) return fail(COMPAR_E_IO, std::string("cannot open ") + path);
+    std::string line;
+    int ln = 0;
+    std::vector<std::pair<std::pair<std::string, Key>, Record>> parsed;
+    while (std::getline(f, line)) {
+        ++ln;
+        size_t p = line.find_first_not_of(" \t\r");
+        if (p == std::string::npos || line[p] == '#') continue;
+        std::istringstream is(line);
+        std::string name, sum_s, sq_s;
+        Key k{};
+        Record r;
+        if (!(is >> name >> k.m >> k.n >> k.k >> k.dtype >> k.compute >> k.transB >> k.beta0 >> r.seen >> r.count >>
+              sum_s >> sq_s >> r.min_ns) ||
+            !parse_u128(sum_s, &r.sum_ns) || !parse_u128(sq_s, &r.sumsq_ns) || r.seen < 0 || r.count < 0) {
+            return fail(COMPAR_E_FORMAT, std::string(path) + ":" + std::to_string(ln) + ": malformed record");
+        }
+        std::string extra;
+        if (is >> extra) return fail(COMPAR_E_FORMAT, std::string(path) + ":" + std::to_string(ln) + ": trailing data");
+        parsed.push_back({{name, k}, r});
+    }
+    for (const auto &e : parsed) c->hist.merge(e.first.first, e.first.second, e.second);
+    return COMPAR_OK;
+}
+
+compar_status compar_history_get(void *ctx, int variant, const compar_gemm_desc *d, compar_record *out) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!d || !out) return fail(COMPAR_E_INVALID, "NULL argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (variant < 0 || variant >= static_cast<int>(c->variants.size())) return fail(COMPAR_E_INVALID, "bad variant");
+    Plan plan;
+    build_plan(c, d, plan, d->A, d->B, d->C_in, d->C_out);
+    std::memset(out, 0, sizeof(*out));
+    const Record *r = c->hist.find(c->variants[variant].name, plan.key);
+    if (r) {
+        out->seen = r->seen;
+        out->count = r->count;
+        out->min_ns = r->min_ns;
+        out->sum_ns = r->sum_ns > static_cast<unsigned __int128>(INT64_MAX) ? INT64_MAX : static_cast<int64_t>(r->sum_ns);
+        out->mean_ns = r->count ? static_cast<double>(r->sum_ns) / static_cast<double>(r->count) : 0.0;
+    }
+    return COMPAR_OK;
+}
+
+compar_status compar_partition_rows(int64_t m, int p, int64_t *offsets) {
+    if (m < 0 || p < 1 || !offsets) return fail(COMPAR_E_INVALID, "bad partition arguments");
+    std::vector<int64_t> offs;
+    partition(m, p, offs);
+    std::copy(offs.begin(), offs.end(), offsets);
+    return COMPAR_OK;
+}
+
+compar_status compar_comm_unique_id(void *out, int len) {
+    if (!out || len < static_cast<int>(sizeof(ncclUniqueId))) return fail(COMPAR_E_INVALID, "buffer too small");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(COMPAR_E_NCCL, ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof(id));
+    return COMPAR_OK;
+}
+
+compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, int len) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (nranks < 1 || rank < 0 || rank >= nranks || !id || len < static_cast<int>(sizeof(ncclUniqueId)))
+        return fail(COMPAR_E_INVALID, "bad communicator arguments");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->comm) return fail(COMPAR_E_STATE, "communicator already initialised");
+    if (c->virt) {
+        c->nranks = nranks;
+        c->rank = rank;
+        return COMPAR_OK;
+    }
+    cudaSetDevice(c->device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+    if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    c->nranks = nranks;
+    c->rank = rank;
+    return COMPAR_OK;
+}
+
+compar_status compar_stats_get(void *ctx, compar_stats *out) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!out) return fail(COMPAR_E_INVALID, "NULL argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    *out = c->stats;
+    return COMPAR_OK;
+}
+
+compar_status compar_set_reduce_hook(void *ctx, compar_reduce_fn fn, void *user) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->reduce_hook = fn;
+    c->reduce_user = user;
+    return COMPAR_OK;
+}
+
+compar_status compar_debug_spin(void *stream, int64_t ns) {
+    cudaError_t e = launch_spin(static_cast<cudaStream_t>(stream), ns);
+    return e == cudaSuccess ? COMPAR_OK : cuda_fail(e, "spin");
+}
+
+}  // extern "C"

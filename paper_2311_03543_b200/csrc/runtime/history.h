@@ -1,0 +1,71 @@
+// History-based variant selector (the StarPU-style performance model of PAPER.md P:118,
+// P:224).  Host-only, no CUDA.
+//
+// Deliberate readings (R9-R13):
+//   * key = (m_panel, n, k, dtype, compute, transB, beta==0), not SPEC's log2 footprint bucket;
+//   * per (variant, key): seen (assigned executions incl. warm-ups and pending), count,
+//     128-bit integer sums of ns and ns^2, min — the mean is order-independent and the
+//     argmin comparison exact (cross-multiplication), so decisions are deterministic;
+//   * calibration: while some eligible variant has seen < W + K, pick argmin seen
+//     (ties -> lowest registry index); the first W executions are warm-ups (dropped);
+//   * model: argmin mean ns over eligible variants with count > 0 (ties -> lowest index).
+#pragma once
+#include <cstdint>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace compar {
+
+struct Key {
+    int64_t m, n, k;
+    int dtype, compute, transB, beta0;
+    bool operator<(const Key &o) const {
+        return std::tie(m, n, k, dtype, compute, transB, beta0) <
+               std::tie(o.m, o.n, o.k, o.dtype, o.compute, o.transB, o.beta0);
+    }
+    bool operator==(const Key &o) const {
+        return m == o.m && n == o.n && k == o.k && dtype == o.dtype && compute == o.compute && transB == o.transB &&
+               beta0 == o.beta0;
+    }
+};
+
+struct Record {
+    int64_t seen = 0;
+    int64_t count = 0;
+    unsigned __int128 sum_ns = 0;
+    unsigned __int128 sumsq_ns = 0;
+    int64_t min_ns = 0;
+};
+
+enum Mode { kWarmup = 0, kCalib = 1, kModel = 2, kEager = 3, kHint = 4, kNoop = 5 };
+
+class History {
+public:
+    int calib_warmup = 1;
+    int calib_k = 3;
+
+    // Records are keyed by variant NAME so a loaded perf model applies to whichever registry
+    // index that name gets (SPEC S:393-401 persistence).
+    Record &rec(const std::string &variant, const Key &k) { return table_[{variant, k}]; }
+    const Record *find(const std::string &variant, const Key &k) const {
+        auto it = table_.find({variant, k});
+        return it == table_.end() ? nullptr : &it->second;
+    }
+    // True if any eligible variant is still calibrating for this key.
+    bool calibrating(const std::vector<std::string> &names, const Key &k);
+    // Decision over the ordered eligible list (indices into `names`): returns position in list.
+    int decide(const std::vector<std::string> &names, const Key &k, Mode *mode);
+    // Account an assigned execution; returns true if it is a warm-up.
+    bool commit(const std::string &variant, const Key &k);
+    void harvest(const std::string &variant, const Key &k, int64_t ns);
+
+    const std::map<std::pair<std::string, Key>, Record> &table() const { return table_; }
+    void merge(const std::string &variant, const Key &k, const Record &r);
+
+private:
+    std::map<std::pair<std::string, Key>, Record> table_;
+};
+
+}  // namespace compar

@@ -1,0 +1,224 @@
+"""GPU parity of every built-in variant against the FP64 oracle, through the C ABI (-m gpu).
+
+Tolerances (BASELINE.json north_star; R8): max relative Frobenius error 1e-5 for
+the strict-FP32 variants (simt_f32, tma_f32) and 5e-3 for the tensor-core variants
+(tc_tf32, tc_bf16).  Integer-valued inputs (distribution I) must match BITWISE for every
+variant (every partial sum is an exact integer < 2^24, SURVEY §8(c) "Exact integers").
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gen
+from oracle import gemm as og
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from tests._gpu_util import device_matrix, to_device, to_host_f64  # noqa: E402
+
+cm = pytest.importorskip("paper_2311_03543_b200.compar")
+
+VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
+            "tma_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
+            "tc_tf32": (cm.F32, cm.COMPUTE_TF32, 5e-3),
+            "tc_bf16": (cm.BF16, cm.COMPUTE_BF16, 5e-3)}
+
+SHAPES = [(1, 1, 1), (7, 13, 5), (64, 64, 64), (65, 127, 129), (129, 257, 70), (128, 256, 64),
+          (300, 520, 1000), (1000, 777, 333), (257, 1, 100), (1, 300, 4097)]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = cm.Compar()
+    yield c
+    c.terminate()
+
+
+def vid(ctx, name):
+    return [n for n, _ in ctx.variants()].index(name)
+
+
+def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, seed=11):
+    dtype_id, compute, tol = VARIANTS[name]
+    dt = "bf16" if dtype_id == cm.BF16 else "f32"
+    A = gen.matrix(gen.TAG_A, m, k, dist, dt, seed=seed)
+    B = gen.matrix(gen.TAG_B, k, n, dist, dt, seed=seed)
+    C0 = gen.matrix(gen.TAG_C, m, n, dist, "f32", seed=seed)
+    lda = k + (-k) % pad
+    ldb_cols = k if transB else n
+    ldb = ldb_cols + (-ldb_cols) % pad
+    ldc = n + (-n) % 4
+    Ad = to_device(A, dt, lda)
+    Bd = to_device(np.ascontiguousarray(B.T) if transB else B, dt, ldb)
+    Cd = to_device(C0, "f32", ldc)
+    if beta == 0.0:
+        Cd.fill_(float("nan"))
+    alpha = 1.5 if dist != gen.DIST_I else 2.0
+    d = cm.make_desc(m, n, k, A=Ad, B=Bd, C_in=Cd, C_out=Cd, lda=lda, ldb=ldb, ldc_in=ldc, ldc_out=ldc,
+                     alpha=alpha, beta=beta, in_dtype=dtype_id, compute=compute, transB=transB,
+                     stream=torch.cuda.current_stream().cuda_stream, variant_hint=vid(ctx, name))
+    rep = ctx.run(d)
+    assert rep.status == 0 and rep.variant == vid(ctx, name)
+    got = to_host_f64(Cd[:, :n])
+    ref = og.gemm(A, B, C0, alpha=alpha, beta=beta, dtype=dt)
+    return got, ref, tol
+
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_parity_uniform(ctx, name, shape):
+    m, n, k = shape
+    got, ref, tol = run_case(ctx, name, m, n, k)
+    assert og.rel_fro(got, ref) <= tol
+
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+@pytest.mark.parametrize("transB", [0, 1])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (200, 300, 517), (129, 257, 1030)], ids=lambda s: "x".join(map(str, s)))
+def test_parity_exact_integers(ctx, name, transB, shape):
+    m, n, k = shape
+    got, ref, _ = run_case(ctx, name, m, n, k, dist=gen.DIST_I, beta=-1.0, transB=transB)
+    np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_transB_and_beta0_nan(ctx, name):
+    got, ref, tol = run_case(ctx, name, 190, 300, 260, transB=1, beta=0.0)
+    assert np.isfinite(got).all()
+    assert og.rel_fro(got, ref) <= tol
+
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_positive_distribution(ctx, name):
+    """P = U[0,1) exposes TF32 truncation bias (R6); still within 5e-3."""
+    got, ref, tol = run_case(ctx, name, 256, 512, 2048, dist=gen.DIST_P)
+    assert og.rel_fro(got, ref) <= tol
+
+
+def test_tma_variants_need_aligned_ld(ctx):
+    """Eligibility filter: lda*4 % 16 != 0 removes tma_f32 and tc_tf32 from E."""
+    m = n = k = 33
+    A = torch.zeros((m, k), device="cuda")
+    B = torch.zeros((k, n), device="cuda")
+    Cm = torch.zeros((m, n), device="cuda")
+    for name in ("tma_f32", "tc_tf32"):
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cm, C_out=Cm, compute=cm.COMPUTE_TF32, variant_hint=vid(ctx, name))
+        with pytest.raises(cm.ComparError):
+            ctx.submit(d)
+    d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cm, C_out=Cm, compute=cm.COMPUTE_TF32)
+    v, _ = ctx.select(d)
+    assert v == vid(ctx, "simt_f32")
+
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_deterministic_rerun(ctx, name):
+    a, _, _ = run_case(ctx, name, 300, 400, 700, seed=5)
+    b, _, _ = run_case(ctx, name, 300, 400, 700, seed=5)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_scale_paths(ctx):
+    """k == 0 and alpha == 0: C = beta * C_in with A, B unread (BLAS rule R3)."""
+    m, n = 70, 90
+    C0 = gen.matrix(gen.TAG_C, m, n)
+    for k, alpha in ((0, 1.5), (16, 0.0)):
+        Cd = to_device(C0)
+        A = torch.full((m, max(k, 1)), float("nan"), device="cuda")
+        B = torch.full((max(k, 1), n), float("nan"), device="cuda")
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, lda=max(k, 1), ldb=n, alpha=alpha, beta=-0.5)
+        r = ctx.run(d)
+        assert r.mode == cm.MODE_NOOP
+        np.testing.assert_array_equal(to_host_f64(Cd), -0.5 * C0.astype(np.float64))
+
+
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_loopback_partition_bitwise_invariant(ctx, name):
+    """Row panels P in {2, 3, 8} give C bitwise equal to P = 1 (no split-K; a4 formula)."""
+    dtype_id, compute, _ = VARIANTS[name]
+    dt = "bf16" if dtype_id == cm.BF16 else "f32"
+    m, n, k = 1000, 384, 320
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt)
+    C0 = device_matrix(gen.TAG_C, m, n)
+    outs = []
+    for P in (1, 2, 3, 8):
+        Cd = C0.clone()
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, in_dtype=dtype_id,
+                         compute=compute, panels=P, variant_hint=vid(ctx, name),
+                         stream=torch.cuda.current_stream().cuda_stream)
+        r = ctx.run(d)
+        assert r.npanels == sum(1 for a, b in zip(cm.partition_rows(m, P), cm.partition_rows(m, P)[1:]) if b > a)
+        outs.append(Cd.cpu())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_host_memory_mode_matches_device(ctx):
+    """mem = HOST: the library stages pinned host buffers; result equals the device path bitwise."""
+    m, n, k = 512, 768, 384
+    A = gen.matrix(gen.TAG_A, m, k, dtype="bf16")
+    B = gen.matrix(gen.TAG_B, k, n, dtype="bf16")
+    C0 = gen.matrix(gen.TAG_C, m, n)
+    Ah = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Bh = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Ch = torch.from_numpy(C0.copy()).pin_memory()
+    d = cm.make_desc(m, n, k, A=Ah, B=Bh, C_in=Ch, C_out=Ch, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
+                     compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST)
+    r = ctx.run(d)
+    assert r.status == 0 and r.total_ns >= r.ns > 0
+    Cd = to_device(C0)
+    d2 = cm.make_desc(m, n, k, A=to_device(A, "bf16"), B=to_device(B, "bf16"), C_in=Cd, C_out=Cd, alpha=1.5,
+                      beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16)
+    ctx.run(d2)
+    assert torch.equal(Ch, Cd.cpu())
+    ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5, dtype="bf16")
+    assert og.rel_fro(Ch.numpy(), ref) <= 5e-3
+
+
+def test_world_size_one_nccl(ctx):
+    """SPMD path with a 1-rank NCCL communicator: world = 1 equals the plain call."""
+    c = cm.Compar()
+    try:
+        c.comm_init(1, 0, cm.comm_unique_id())
+        m, n, k = 300, 512, 256
+        A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
+        B = device_matrix(gen.TAG_B, k, n, dtype="bf16")
+        C0 = device_matrix(gen.TAG_C, m, n)
+        C1, C2 = C0.clone(), C0.clone()
+        kw = dict(alpha=1.5, beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16)
+        c.run(cm.make_desc(m, n, k, A=A, B=B, C_in=C1, C_out=C1, world=1, **kw))
+        c.run(cm.make_desc(m, n, k, A=A, B=B, C_in=C2, C_out=C2, **kw))
+        assert torch.equal(C1, C2)
+    finally:
+        c.terminate()
+
+
+@pytest.mark.parametrize("name,shape", [("tc_bf16", (8192, 8192, 8192)), ("tc_tf32", (8192, 8192, 8192)),
+                                        ("tc_bf16", (65536, 256, 4096)), ("tc_tf32", (65536, 256, 4096)),
+                                        ("tc_bf16", (32768, 32768, 32768))])
+def test_full_size_sampled(ctx, name, shape):
+    """BASELINE.json full sizes in the bench launch configuration; checked on sampled
+    entries (every 128-row tile boundary sampled + random rows/cols) against the oracle fed
+    from the HOST generator (the device twin is pinned bitwise in test_gpu_gen.py)."""
+    dtype_id, compute, tol = VARIANTS[name]
+    dt = "bf16" if dtype_id == cm.BF16 else "f32"
+    m, n, k = shape
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt)
+    Cd = device_matrix(gen.TAG_C, m, n)
+    d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, in_dtype=dtype_id,
+                     compute=compute, variant_hint=vid(ctx, name), stream=torch.cuda.current_stream().cuda_stream)
+    ctx.run(d)
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([[0, m - 1, 127, 128, m // 2], rng.integers(0, m, 27)]))
+    cols = np.unique(np.concatenate([[0, n - 1, 255, min(256, n - 1)], rng.integers(0, n, 28)]))
+    got = Cd[torch.as_tensor(rows, device="cuda")][:, torch.as_tensor(cols, device="cuda")].double().cpu().numpy()
+    Ar = gen.matrix_rows(gen.TAG_A, rows, k, dtype=dt)
+    Bc = gen.matrix_cols(gen.TAG_B, k, cols, dtype=dt)
+    C0 = gen.matrix_entries(gen.TAG_C, rows, cols)
+    ref = og.gemm(Ar, Bc, C0, alpha=1.5, beta=0.5, dtype=dt)
+    assert og.rel_fro(got, ref) <= tol
+    del A, B, Cd
+    torch.cuda.empty_cache()

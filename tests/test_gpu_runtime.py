@@ -1,0 +1,85 @@
+"""GPU tests of the runtime around the kernels (-m gpu): device-twin generator pin, real-event
+selector with closed-form synthetic costs, calibration trace, stats/launch accounting."""
+import numpy as np
+import pytest
+
+import gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from tests._gpu_util import device_matrix  # noqa: E402
+
+cm = pytest.importorskip("paper_2311_03543_b200.compar")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("dist", [gen.DIST_U, gen.DIST_P, gen.DIST_I])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_device_generator_matches_host_bitwise(dtype, dist, transposed):
+    rows, cols = 77, 130
+    dev = device_matrix(gen.TAG_B, rows, cols, dist, dtype, seed=123, transposed=transposed)
+    host = gen.matrix(gen.TAG_B, rows, cols, dist, dtype, seed=123)
+    if transposed:
+        host = np.ascontiguousarray(host.T)
+    if dtype == "bf16":
+        got = dev.contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
+    else:
+        got = dev.contiguous().cpu().numpy()
+    np.testing.assert_array_equal(got, host)
+
+
+def test_device_generator_large_indices():
+    """Counter layout at full-size indices (i << 28 | j) — sample the corner of a 32768^2 matrix."""
+    n = 32768
+    dev = device_matrix(gen.TAG_A, n, n, dtype="bf16")
+    rows, cols = [0, 1, 12345, n - 1], [0, 7, 30000, n - 1]
+    got = dev[rows][:, cols].contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(got, gen.matrix_entries(gen.TAG_A, rows, cols, dtype="bf16"))
+    del dev
+    torch.cuda.empty_cache()
+
+
+def spin_variant(cost_us):
+    def run(desc, panel, stream, user, vns):
+        cm.debug_spin(stream, int(cost_us(desc.contents.n) * 1000))
+        return 0
+    return run
+
+
+def test_real_event_selector_crossover(golden):
+    """SPEC S:370-371 on real cudaEvents: cost0 = 0.1 n us, cost1 = 50 + 0.01 n us."""
+    ctx = cm.Compar(builtins=0)
+    ctx.register_variant("spin_linear", cm.TGT_USER, spin_variant(lambda n: 0.1 * n))
+    ctx.register_variant("spin_affine", cm.TGT_USER, spin_variant(lambda n: 50 + 0.01 * n))
+    buf = torch.zeros(16, device="cuda")
+    for n, want in [(256, 0), (4096, 1)]:
+        d = cm.make_desc(8, n, 8, A=buf, B=buf, C_in=buf, C_out=buf, lda=8, ldb=n, ldc_in=n, ldc_out=n)
+        for _ in range(8):
+            ctx.run(d)
+        v, mode = ctx.select(d)
+        assert (v, mode) == (want, cm.MODE_MODEL)
+        mean = ctx.history(v, d).mean_ns
+        expect = (0.1 * n if want == 0 else 50 + 0.01 * n) * 1000
+        assert expect <= mean <= expect * 1.2 + 5000
+    ctx.terminate()
+
+
+def test_config1_calibration_trace():
+    """Config 1 (64^3 FP32, COMPUTE_TF32): 3 eligible variants x (1 warm-up + 3 timed) = 12
+    calibration runs in registry order, then model mode picks the measured argmin."""
+    ctx = cm.Compar()
+    m = 64
+    A = device_matrix(gen.TAG_A, m, m)
+    B = device_matrix(gen.TAG_B, m, m)
+    Cd = device_matrix(gen.TAG_C, m, m)
+    d = cm.make_desc(m, m, m, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, compute=cm.COMPUTE_TF32)
+    trace = [ctx.run(d) for _ in range(13)]
+    assert [r.variant for r in trace[:12]] == [0, 1, 2] * 4
+    assert [r.mode for r in trace[:3]] == [cm.MODE_WARMUP] * 3
+    assert trace[12].mode == cm.MODE_MODEL
+    means = [ctx.history(v, d).mean_ns for v in range(3)]
+    assert trace[12].variant == int(np.argmin(means))
+    st = ctx.stats()
+    assert st.launches == 13 and st.harvested == 10
+    ctx.terminate()

@@ -1,0 +1,282 @@
+"""Host-side tests of libcompar.so (-m "not gpu"): ABI exports, validation, and the selector
+driven through the C ABI in virtual-clock mode, checked decision-by-decision against the
+independent Python selector oracle (oracle/selector.py)."""
+import os
+import random
+import re
+
+import pytest
+
+from oracle import selector as so
+from oracle.partition import partition_rows as oracle_partition
+
+cm = pytest.importorskip("paper_2311_03543_b200.compar")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "compar.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    decl = r"^\s*(?:compar_status|void|const\s+char\s*\*)\s*\**\s*(compar_[a-z_]+)\s*\("
+    return sorted(set(re.findall(decl, text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    funcs = header_functions()
+    assert len(funcs) >= 19
+    for f in funcs:
+        assert hasattr(cm.lib, f), f"libcompar.so does not export {f}"
+    assert set(funcs) == set(cm.EXPORTS)
+
+
+def test_gen_library_exports():
+    import ctypes
+    path = os.path.join(ROOT, "gen", "libcompar_gen.so")
+    if not os.path.exists(path):
+        pytest.skip("gen library not built")
+    assert hasattr(ctypes.CDLL(path), "compar_gen_fill")
+
+
+def test_partition_rows_matches_oracle():
+    rnd = random.Random(3)
+    for _ in range(300):
+        m, p = rnd.randint(0, 200000), rnd.randint(1, 8)
+        assert cm.partition_rows(m, p) == oracle_partition(m, p)
+    with pytest.raises(cm.ComparError):
+        cm.partition_rows(-1, 2)
+
+
+class Synthetic:
+    """USER variants with closed-form costs (ns) reported through the virtual clock."""
+
+    def __init__(self, costs):
+        self.costs = costs
+        self.calls = []
+
+    def fn(self, v):
+        def run(desc, panel, stream, user, vns):
+            d, p = desc.contents, panel.contents
+            ns = int(self.costs[v](p.rows, d.n, d.k))
+            self.calls.append((v, p.rows))
+            vns[0] = ns
+            return 0
+        return run
+
+
+def vctx(costs, **kw):
+    ctx = cm.Compar(virtual_clock=1, **kw)
+    syn = Synthetic(costs)
+    for v in range(len(costs)):
+        assert ctx.register_variant(f"v{v}", cm.TGT_USER, syn.fn(v)) == v
+    return ctx, syn
+
+
+def desc(m, n=None, k=None, **kw):
+    n = m if n is None else n
+    k = m if k is None else k
+    return cm.make_desc(m, n, k, lda=k, ldb=n, ldc_in=n, ldc_out=n, alpha=1.5, beta=0.5, **kw)
+
+
+def test_virtual_stream_matches_selector_oracle():
+    """Random mixed stream: every (variant, mode) decision of the C runtime equals the oracle's."""
+    costs = [lambda m, n, k: 100 * m + 7, lambda m, n, k: 30000 + 20 * m, lambda m, n, k: 5000 + 60 * m]
+    ctx, _ = vctx(costs)
+    orc = so.SelectorOracle(3)
+    rnd = random.Random(7)
+    sizes = [64, 256, 555, 1024, 4096]
+    pending = []
+    for step in range(300):
+        m = rnd.choice(sizes)
+        d = desc(m)
+        key = (m, m, m)
+        t = ctx.submit(d)
+        pending.append(t)
+        rep_v, rep_m = None, None
+        # oracle decision
+        v, mode = orc.decide(key, [0, 1, 2])
+        warm = orc.commit(v, key, mode)
+        # runtime decision is visible at sync time
+        if rnd.random() < 0.5 or step == 299:
+            for tt in pending[:-1]:
+                try:
+                    ctx.sync(tt)
+                except cm.ComparError as e:
+                    assert e.status == cm.E_UNKNOWN_TASK     # already harvested by a model decision
+            pending = []
+            r = ctx.sync(t)
+            rep_v, rep_m = r.variant, r.mode
+            assert (rep_v, rep_m) == (v, mode), f"step {step}"
+            assert r.warmup == int(warm)
+        orc.harvest(v, key, mode, warm, int(costs[v](m, m, m)))
+    ctx.sync()
+    ctx.terminate()
+
+
+def test_every_decision_matches_select_then_submit():
+    costs = [lambda m, n, k: 1000, lambda m, n, k: 900, lambda m, n, k: 1100]
+    ctx, _ = vctx(costs)
+    orc = so.SelectorOracle(3)
+    d = desc(128)
+    for _ in range(20):
+        sel = ctx.select(d)
+        r = ctx.run(d)
+        assert sel == (r.variant, r.mode)
+        v, mode = orc.decide("k", [0, 1, 2])
+        warm = orc.commit(v, "k", mode)
+        orc.harvest(v, "k", mode, warm, [1000, 900, 1100][v])
+        assert (r.variant, r.mode) == (v, mode)
+    assert ctx.run(d).variant == 1
+    ctx.terminate()
+
+
+def test_spec_crossover_through_abi(golden):
+    """S:370-371 closed form through the C runtime: n=256 -> v0, n=4096 -> v1."""
+    costs = [lambda m, n, k: round(0.1 * m * 1000), lambda m, n, k: round((50 + 0.01 * m) * 1000)]
+    ctx, _ = vctx(costs)
+    for n, want in [(256, 0), (4096, 1)]:
+        for _ in range(8):
+            ctx.run(desc(n))
+        assert ctx.select(desc(n)) == (want, cm.MODE_MODEL)
+    ctx.terminate()
+
+
+def test_history_records_and_perf_roundtrip(tmp_path):
+    costs = [lambda m, n, k: 111 * m, lambda m, n, k: 222 * m]
+    ctx, _ = vctx(costs)
+    stream = [64, 128, 64, 64, 128, 256] * 6
+    for m in stream:
+        ctx.run(desc(m))
+    rec = ctx.history(0, desc(64))
+    assert rec.count >= 3 and rec.min_ns == 111 * 64 and rec.mean_ns == 111 * 64
+    p = tmp_path / "perf.txt"
+    ctx.perf_save(p)
+    # replay: continue the same stream on the trained ctx and on a fresh ctx that loaded the file
+    ctx2, _ = vctx(costs)
+    ctx2.perf_load(p)
+    tail = [64, 256, 512, 128, 512, 64] * 3
+    a = [(r.variant, r.mode) for r in (ctx.run(desc(m)) for m in tail)]
+    b = [(r.variant, r.mode) for r in (ctx2.run(desc(m)) for m in tail)]
+    assert a == b
+    # merge: loading the same file again doubles the counts
+    before = ctx2.history(1, desc(64)).count
+    ctx2.perf_load(p)
+    assert ctx2.history(1, desc(64)).count >= before
+    ctx.terminate()
+    ctx2.terminate()
+
+
+def test_perf_load_format_errors(tmp_path):
+    ctx, _ = vctx([lambda m, n, k: 1])
+    bad = tmp_path / "bad.txt"
+    bad.write_text("# header\nv0 1 2 3 0 0 0 1 4 3 100 1000\n")      # missing min_ns
+    with pytest.raises(cm.ComparError) as e:
+        ctx.perf_load(bad)
+    assert e.value.status == cm.E_FORMAT and ":2:" in str(e.value)
+    with pytest.raises(cm.ComparError) as e:
+        ctx.perf_load(tmp_path / "missing.txt")
+    assert e.value.status == cm.E_IO
+    empty = tmp_path / "empty.txt"
+    empty.write_text("")
+    ctx.perf_load(empty)                                               # empty file -> unchanged
+    ctx.terminate()
+
+
+def test_validation_errors():
+    ctx, _ = vctx([lambda m, n, k: 1])
+    bad = [
+        dict(m=-1), dict(lda=3, m=8, k=8), dict(ldb=2), dict(ldc_out=1),
+        dict(in_dtype=cm.BF16, compute=cm.COMPUTE_TF32), dict(in_dtype=cm.F32, compute=cm.COMPUTE_BF16),
+        dict(transB=2), dict(panels=9), dict(variant_hint=5),
+    ]
+    for kw in bad:
+        m = kw.pop("m", 8)
+        d = desc(m) if m >= 0 else desc(8)
+        if m < 0:
+            d.m = -1
+        for f, v in kw.items():
+            setattr(d, f, v)
+        with pytest.raises(cm.ComparError) as e:
+            ctx.submit(d)
+        assert e.value.status == cm.E_INVALID, kw
+    with pytest.raises(cm.ComparError) as e:
+        ctx.register_variant("v0", cm.TGT_USER, lambda *a: 0)
+    assert e.value.status == cm.E_DUPLICATE
+    with pytest.raises(cm.ComparError) as e:
+        ctx.register_variant("x", cm.TGT_USER, lambda *a: 0, iface="sort")
+    assert e.value.status == cm.E_INVALID
+    with pytest.raises(cm.ComparError) as e:
+        ctx.sync(12345)
+    assert e.value.status == cm.E_UNKNOWN_TASK
+    ctx.terminate()
+    with pytest.raises(cm.ComparError) as e:
+        ctx.terminate() if ctx.ctx else cm._check(cm.lib.compar_terminate(None))
+    assert e.value.status == cm.E_STATE
+
+
+def test_no_variant_and_quick_returns():
+    ctx = cm.Compar(virtual_clock=1)
+    with pytest.raises(cm.ComparError) as e:
+        ctx.submit(desc(8))
+    assert e.value.status == cm.E_NO_VARIANT
+    # m == 0 / n == 0: no launch, NOOP; k == 0: scale-only NOOP (no variant needed)
+    for d in (desc(0, 8, 8), desc(8, 0, 8), desc(8, 8, 0)):
+        r = ctx.run(d)
+        assert r.mode == cm.MODE_NOOP and r.variant == -1
+    ctx.terminate()
+
+
+def test_ngpu_zero_refused():
+    with pytest.raises(cm.ComparError) as e:
+        cm.Compar(ngpu=0, virtual_clock=1)
+    assert e.value.status == cm.E_INVALID
+
+
+def test_eager_mask_and_hint():
+    costs = [lambda m, n, k: 500, lambda m, n, k: 100]
+    ctx, _ = vctx(costs, sched=1)
+    for _ in range(5):
+        r = ctx.run(desc(32))
+        assert (r.variant, r.mode) == (0, cm.MODE_EAGER)
+    ctx.terminate()
+    ctx, _ = vctx(costs, variant_mask=1)            # v0 masked
+    for _ in range(8):
+        assert ctx.run(desc(32)).variant == 1
+    d = desc(32)
+    d.variant_hint = 0
+    with pytest.raises(cm.ComparError):             # hint must be eligible
+        ctx.submit(d)
+    ctx.terminate()
+    ctx, _ = vctx(costs)
+    d = desc(32)
+    d.variant_hint = 0
+    r = ctx.run(d)
+    assert (r.variant, r.mode) == (0, cm.MODE_HINT)
+    assert ctx.history(0, desc(32)).seen == 0        # hints never touch the history
+    ctx.terminate()
+
+
+def test_failed_variant_marks_task_failed_without_retry():
+    def boom(desc, panel, stream, user, vns):
+        vns[0] = 1
+        return cm.E_INVALID
+    ctx = cm.Compar(virtual_clock=1)
+    ctx.register_variant("boom", cm.TGT_USER, boom)
+    t = ctx.submit(desc(16))
+    s, r = ctx.sync_status(t)
+    assert s == cm.E_TASK_FAILED and r.status == cm.E_TASK_FAILED and r.variant == 0
+    assert ctx.stats().failed == 1
+    ctx.terminate()
+
+
+def test_loopback_panels_virtual():
+    """Loopback panels: the variant runs once per non-empty panel (rows from the a4 formula);
+    the sample is the max panel time and the key uses the first panel's rows."""
+    ctx, syn = vctx([lambda m, n, k: 10 * m])
+    d = desc(1000)
+    d.panels = 3
+    r = ctx.run(d)
+    offs = oracle_partition(1000, 3)
+    assert [rows for _, rows in syn.calls] == [b - a for a, b in zip(offs, offs[1:]) if b > a]
+    assert r.npanels == 3 and r.ns == 10 * max(b - a for a, b in zip(offs, offs[1:]))
+    ctx.terminate()
