@@ -24,8 +24,8 @@ __device__ __forceinline__ uint16_t bf16_rne(float f) {
     return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
 }
 
-__global__ void fill_kernel(void *dst, int dtype, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int tag,
-                            int dist, int transposed) {
+__global__ void fill_kernel(void *dst, int dtype, int64_t rows, int64_t cols, int64_t ld, int64_t row0, int64_t col0,
+                            uint64_t seed, int tag, int dist, int transposed) {
     // storage extents
     const int64_t srows = transposed ? cols : rows, scols = transposed ? rows : cols;
     const int64_t total = srows * scols;
@@ -33,8 +33,8 @@ __global__ void fill_kernel(void *dst, int dtype, int64_t rows, int64_t cols, in
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t sr = idx / scols, sc = idx - sr * scols;
-        const uint64_t i = static_cast<uint64_t>(transposed ? sc : sr);
-        const uint64_t j = static_cast<uint64_t>(transposed ? sr : sc);
+        const uint64_t i = static_cast<uint64_t>(row0 + (transposed ? sc : sr));
+        const uint64_t j = static_cast<uint64_t>(col0 + (transposed ? sr : sc));
         const float v = value_f32(splitmix64(base ^ (i << 28) ^ j), dist);
         if (dtype == 0)
             static_cast<float *>(dst)[sr * ld + sc] = v;
@@ -45,15 +45,15 @@ __global__ void fill_kernel(void *dst, int dtype, int64_t rows, int64_t cols, in
 
 }  // namespace
 
-extern "C" int compar_gen_fill(void *dst, int dtype, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int tag,
-                               int dist, int transposed, void *stream) {
-    if (rows < 0 || cols < 0 || (dtype != 0 && dtype != 1) || dist < 0 || dist > 2) return 1;
+extern "C" int compar_gen_fill(void *dst, int dtype, int64_t rows, int64_t cols, int64_t ld, int64_t row0, int64_t col0,
+                               uint64_t seed, int tag, int dist, int transposed, void *stream) {
+    if (rows < 0 || cols < 0 || row0 < 0 || col0 < 0 || (dtype != 0 && dtype != 1) || dist < 0 || dist > 2) return 1;
     if (rows == 0 || cols == 0) return 0;
     if (!dst || ld < (transposed ? rows : cols)) return 1;
     int64_t total = rows * cols;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     fill_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        dst, dtype, rows, cols, ld, seed, tag, dist, transposed);
+        dst, dtype, rows, cols, ld, row0, col0, seed, tag, dist, transposed);
     return static_cast<int>(cudaGetLastError());
 }

@@ -19,14 +19,15 @@
 extern "C" {
 #endif
 
-/* Fill a rows x cols LOGICAL matrix into device memory `dst` (row pitch `ld` elements).
+/* Fill a rows x cols block of a LOGICAL matrix, whose top-left element is logical (row0, col0),
+ * into device memory `dst` (row pitch `ld` elements) — e.g. one rank's row panel of A.
  *   dtype: 0 = FP32, 1 = BF16 bit patterns;  dist: 0 = U, 1 = P, 2 = I;
  *   transposed = 1 stores logical (i, j) at dst[j * ld + i] (e.g. B^T for transB; ld >= rows),
  *   else at dst[i * ld + j] (ld >= cols).
  *   stream: cudaStream_t or NULL.  Asynchronous.  Returns 0 on success, else a cudaError_t
  *   value (1 = invalid argument). */
-int compar_gen_fill(void *dst, int dtype, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int tag, int dist,
-                    int transposed, void *stream);
+int compar_gen_fill(void *dst, int dtype, int64_t rows, int64_t cols, int64_t ld, int64_t row0, int64_t col0,
+                    uint64_t seed, int tag, int dist, int transposed, void *stream);
 
 #ifdef __cplusplus
 }

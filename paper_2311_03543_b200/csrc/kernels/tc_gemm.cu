@@ -43,6 +43,12 @@ struct TcCfg {
     static constexpr int B_ATOM_N = 128 / ELEM;    // N elements per 128-byte MN atom
     static constexpr int B_BOXES = kTransB ? 1 : BN / B_ATOM_N;
     static constexpr uint32_t B_BOX_BYTES = kTransB ? B_BYTES : BK * 128;
+    // MN-major B: BF16 uses the canonical SWIZZLE_128B atom (8 K-rows x 128 B, SBO 1024);
+    // 32-bit TF32 requires the 32-byte-granule SWIZZLE_128B_BASE32B atom (4 K-rows x 128 B,
+    // descriptor layout type 1, SBO 512) loaded by TMA with SWIZZLE_128B_ATOM_32B.
+    static constexpr bool B_BASE32 = !kBF16 && !kTransB;
+    static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
+    static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
     // Instruction descriptor: D=F32 [4,6), A/B format [7,10)/[10,13) (1 BF16, 2 TF32),
     // a_major=K [15], b_major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
@@ -156,8 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
                         const uint64_t adesc = ptx::smem_desc_sw128(sa + j * 32, 16, 1024);
                         const uint64_t bdesc = kTransB ? ptx::smem_desc_sw128(sb + j * 32, 16, 1024)
-                                                       : ptx::smem_desc_sw128(sb + j * C::UMMA_K * 128,
-                                                                              C::B_BOX_BYTES, 1024);
+                                                       : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_BOX_BYTES,
+                                                                        C::B_SBO, C::B_LAYOUT);
                         if (kBF16)
                             ptx::mma_bf16(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
                         else
@@ -244,9 +250,10 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
     });
     if (attr_err != cudaSuccess) return attr_err;
     CUtensorMap ta, tb;
-    if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, true)) return cudaErrorInvalidValue;
-    bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, C::BN, C::BK, true)
-                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N, true);
+    if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, Swz::B128)) return cudaErrorInvalidValue;
+    bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, C::BN, C::BK, Swz::B128)
+                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N,
+                                    C::B_BASE32 ? Swz::B128_32B : Swz::B128);
     if (!ok) return cudaErrorInvalidValue;
     TcParams p;
     p.m = g.m, p.n = g.n, p.k = g.k;

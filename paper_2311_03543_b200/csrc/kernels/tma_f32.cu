@@ -190,9 +190,9 @@ cudaError_t launch_t(const GemmLaunch &g) {
     });
     if (attr != cudaSuccess) return attr;
     CUtensorMap ta, tb;
-    if (!get_tmap_2d(&ta, g.A, 4, g.m, g.k, g.lda, BM, BK, true)) return cudaErrorInvalidValue;
-    bool ok = kTransB ? get_tmap_2d(&tb, g.B, 4, g.n, g.k, g.ldb, BN, BK, true)
-                      : get_tmap_2d(&tb, g.B, 4, g.k, g.n, g.ldb, BK, BN, false);
+    if (!get_tmap_2d(&ta, g.A, 4, g.m, g.k, g.lda, BM, BK, Swz::B128)) return cudaErrorInvalidValue;
+    bool ok = kTransB ? get_tmap_2d(&tb, g.B, 4, g.n, g.k, g.ldb, BN, BK, Swz::B128)
+                      : get_tmap_2d(&tb, g.B, 4, g.k, g.n, g.ldb, BK, BN, Swz::None);
     if (!ok) return cudaErrorInvalidValue;
     TmaParams p;
     p.m = g.m, p.n = g.n, p.k = g.k, p.alpha = g.alpha, p.beta = g.beta;

@@ -21,7 +21,7 @@ void resolve() {
 }  // namespace
 
 bool make_tmap_2d(CUtensorMap *out, const void *base, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
-                  uint32_t box_rows, uint32_t box_cols, bool swizzle128) {
+                  uint32_t box_rows, uint32_t box_cols, Swz swizzle) {
     std::call_once(g_once, resolve);
     if (!g_encode) return false;
     // FP32 operands of the TF32 variant are moved as raw FP32 bits; the tensor core reads
@@ -32,7 +32,7 @@ bool make_tmap_2d(CUtensorMap *out, const void *base, int elem_bytes, int64_t ro
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(out, dt, 2, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          static_cast<CUtensorMapSwizzle>(static_cast<int>(swizzle)),
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -61,8 +61,8 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 }  // namespace
 
 bool get_tmap_2d(CUtensorMap *out, const void *ptr, int elem, int64_t rows, int64_t cols, int64_t ld, uint32_t br,
-                 uint32_t bc, bool sw) {
-    MapKey key{ptr, rows, cols, ld, br, bc, elem, sw ? 1 : 0};
+                 uint32_t bc, Swz sw) {
+    MapKey key{ptr, rows, cols, ld, br, bc, elem, static_cast<int>(sw)};
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_maps.find(key);
     if (it != g_maps.end()) {

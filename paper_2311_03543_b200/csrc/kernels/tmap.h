@@ -7,15 +7,23 @@
 
 namespace compar {
 
+// Shared-memory swizzle of a TMA box (must match the UMMA descriptor layout type / the
+// consumer's address arithmetic).
+enum class Swz : int {
+    None = CU_TENSOR_MAP_SWIZZLE_NONE,
+    B128 = CU_TENSOR_MAP_SWIZZLE_128B,              // 16-byte chunks XOR (row & 7), 1024-byte atom
+    B128_32B = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B  // 32-byte chunks within a 128-byte span
+};
+
 // 2-D row-major tensor: `rows` x `cols` elements, row pitch `ld` elements of `elem_bytes`.
-// Box = box_rows x box_cols elements; `swizzle128` selects CU_TENSOR_MAP_SWIZZLE_128B.
-// Out-of-bounds box elements are zero-filled by the hardware.  Returns false on failure.
+// Box = box_rows x box_cols elements.  Out-of-bounds box elements are zero-filled by the
+// hardware.  Returns false on failure.
 bool make_tmap_2d(CUtensorMap *out, const void *base, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
-                  uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+                  uint32_t box_rows, uint32_t box_cols, Swz swizzle);
 
 // Cached wrapper: tensor maps are keyed by (ptr, shape, ld, box, swizzle) so repeated
 // submissions on the same buffers skip the host-side encode (SURVEY §7 hard part 4).
 bool get_tmap_2d(CUtensorMap *out, const void *ptr, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
-                 uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+                 uint32_t box_rows, uint32_t box_cols, Swz swizzle);
 
 }  // namespace compar

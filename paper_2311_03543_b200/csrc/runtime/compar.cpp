@@ -188,7 +188,6 @@ compar_status validate(Ctx *c, const compar_gemm_desc *d) {
     if (d->panels < 0 || d->panels > COMPAR_MAX_PANELS) return fail(COMPAR_E_INVALID, "panels out of range");
     if (d->world && d->panels > 1) return fail(COMPAR_E_INVALID, "world and loopback panels are exclusive");
     if (d->world && !c->virt && !c->comm) return fail(COMPAR_E_STATE, "world=1 needs compar_comm_init");
-    if (d->world && d->mem == COMPAR_MEM_HOST) return fail(COMPAR_E_INVALID, "world mode takes device buffers");
     if (d->variant_hint < -1 || d->variant_hint >= static_cast<int>(c->variants.size()))
         return fail(COMPAR_E_INVALID, "variant_hint out of range");
     if (d->m == 0 || d->n == 0) return COMPAR_OK;
@@ -660,27 +659,38 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
     const float *Cin = d->C_in;
     float *Cout = d->C_out;
     const bool host = d->mem == COMPAR_MEM_HOST && !c->virt;
-    const size_t a_bytes = gemm ? static_cast<size_t>(d->m - 1) * d->lda * eb + static_cast<size_t>(d->k) * eb : 0;
+    // Rows this process owns: the whole m, or this rank's panel in world mode.
+    int64_t mloc = d->m;
+    if (t.world) {
+        std::vector<int64_t> offs;
+        partition(d->m, c->nranks, offs);
+        mloc = offs[c->rank + 1] - offs[c->rank];
+    }
+    const bool root_b = !t.world || c->rank == 0;  // this process holds B
+    const size_t a_bytes =
+        (gemm && mloc > 0) ? static_cast<size_t>(mloc - 1) * d->lda * eb + static_cast<size_t>(d->k) * eb : 0;
     const size_t b_rows = d->transB ? d->n : d->k;
     const size_t b_width = d->transB ? d->k : d->n;
     const size_t b_bytes = gemm ? (b_rows - 1) * d->ldb * eb + b_width * eb : 0;
-    const size_t cin_bytes =
-        (work && d->beta != 0.f) ? static_cast<size_t>(d->m - 1) * d->ldc_in * 4 + static_cast<size_t>(d->n) * 4 : 0;
-    const size_t cout_bytes = work ? static_cast<size_t>(d->m - 1) * d->ldc_out * 4 + static_cast<size_t>(d->n) * 4 : 0;
+    const size_t cin_bytes = (work && mloc > 0 && d->beta != 0.f)
+                                 ? static_cast<size_t>(mloc - 1) * d->ldc_in * 4 + static_cast<size_t>(d->n) * 4
+                                 : 0;
+    const size_t cout_bytes =
+        (work && mloc > 0) ? static_cast<size_t>(mloc - 1) * d->ldc_out * 4 + static_cast<size_t>(d->n) * 4 : 0;
     if (host && work) {
         if ((s = ensure_buffer(&c->staging[0], &c->staging_bytes[0], a_bytes)) != COMPAR_OK) return s;
-        if ((s = ensure_buffer(&c->staging[1], &c->staging_bytes[1], b_bytes)) != COMPAR_OK) return s;
+        if (root_b && (s = ensure_buffer(&c->staging[1], &c->staging_bytes[1], b_bytes)) != COMPAR_OK) return s;
         if ((s = ensure_buffer(&c->staging[3], &c->staging_bytes[3], cout_bytes)) != COMPAR_OK) return s;
         const bool inplace = d->C_in == d->C_out && d->ldc_in == d->ldc_out;
         if (cin_bytes && !inplace && (s = ensure_buffer(&c->staging[2], &c->staging_bytes[2], cin_bytes)) != COMPAR_OK)
             return s;
         A = c->staging[0];
-        B = c->staging[1];
+        if (root_b) B = c->staging[1];
         Cout = static_cast<float *>(c->staging[3]);
         Cin = cin_bytes ? (inplace ? Cout : static_cast<float *>(c->staging[2])) : nullptr;
     }
     // World mode, non-root ranks: B arrives in a replica.
-    if (t.world && c->rank != 0 && gemm && !c->virt) {
+    if (!root_b && gemm && !c->virt) {
         if (d->B_replica) {
             B = d->B_replica;
         } else {
@@ -725,15 +735,15 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
         cudaEventRecord(t.begin, st);
         if (host) {
             if (a_bytes) cudaMemcpyAsync(const_cast<void *>(A), d->A, a_bytes, cudaMemcpyHostToDevice, st);
-            if (b_bytes) cudaMemcpyAsync(const_cast<void *>(B), d->B, b_bytes, cudaMemcpyHostToDevice, st);
+            if (b_bytes && root_b) cudaMemcpyAsync(const_cast<void *>(B), d->B, b_bytes, cudaMemcpyHostToDevice, st);
             if (cin_bytes) cudaMemcpyAsync(const_cast<float *>(Cin), d->C_in, cin_bytes, cudaMemcpyHostToDevice, st);
-            c->stats.bytes_h2d += static_cast<int64_t>(a_bytes + b_bytes + cin_bytes);
+            c->stats.bytes_h2d += static_cast<int64_t>(a_bytes + (root_b ? b_bytes : 0) + cin_bytes);
         }
         if (t.world && c->nranks > 1 && gemm) {
             t.bc0 = get_event(c);
             t.bc1 = get_event(c);
             cudaEventRecord(t.bc0, st);
-            void *buf = const_cast<void *>(c->rank == 0 ? d->B : B);
+            void *buf = const_cast<void *>(B);
             ncclResult_t r = ncclBroadcast(buf, buf, b_bytes, ncclChar, 0, c->comm, st);
             if (r != ncclSuccess) t.status = COMPAR_E_NCCL;
             cudaEventRecord(t.bc1, st);

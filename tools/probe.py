@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 import gen  # noqa: E402
 from paper_2311_03543_b200 import compar as cm  # noqa: E402
-from tests._gpu_util import device_matrix  # noqa: E402
+from gen.device import device_matrix  # noqa: E402
 
 
 def time_variant(ctx, name, m, n, k, reps=10, transB=0):
