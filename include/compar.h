@@ -122,7 +122,8 @@ typedef struct {
     compar_mem mem;             /* HOST: A, B, C_in, C_out are host pointers (pinned for speed);
                                    the library stages them through its own device buffers and
                                    copies C_out back before the task's stop event.               */
-    void *stream;               /* cudaStream_t to order the task on; NULL: the library stream    */
+    void *stream;               /* cudaStream_t to order the task on; NULL: the CUDA legacy default
+                                   stream (ordered after the caller's default-stream work)        */
     int panels;                 /* loopback row panels on this device (1..COMPAR_MAX_PANELS);
                                    0 or 1: a single launch over all m rows                       */
     int world;                  /* 1: SPMD row-panel split across the ranks of compar_comm_init.

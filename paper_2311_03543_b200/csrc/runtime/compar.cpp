@@ -649,7 +649,9 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
     Task t;
     t.id = c->next_task++;
     t.world = d->world != 0;
-    cudaStream_t st = d->stream ? static_cast<cudaStream_t>(d->stream) : c->stream;
+    // NULL is the CUDA legacy default stream (the CUDA convention, and torch's default stream),
+    // so a task is ordered after work the caller queued there.
+    cudaStream_t st = static_cast<cudaStream_t>(d->stream);
     const int eb = elem_bytes(d->in_dtype);
     const bool work = d->m > 0 && d->n > 0;
     const bool gemm = work && d->k > 0 && d->alpha != 0.f;
