@@ -70,7 +70,9 @@ typedef enum {
     COMPAR_TGT_TMA_F32 = 1,     /* built-in (b): TMA + mbarrier pipeline, FP32 FFMA             */
     COMPAR_TGT_TC_TF32 = 2,     /* built-in (c): tcgen05/TMEM tensor cores, TF32 in, FP32 acc    */
     COMPAR_TGT_TC_BF16 = 3,     /* built-in (c): tcgen05/TMEM tensor cores, BF16 in, FP32 acc    */
-    COMPAR_TGT_USER = 4
+    COMPAR_TGT_USER = 4,
+    COMPAR_TGT_TC2_TF32 = 5,    /* built-in (c), CTA-pair form: tcgen05.mma.cta_group::2, 256x256 tiles */
+    COMPAR_TGT_TC2_BF16 = 6     /* built-in (c), CTA-pair form, BF16                                    */
 } compar_target;
 
 /* Why a task ran the variant it ran. */

@@ -10,6 +10,7 @@ namespace compar {
 cudaError_t preload_tc_kernels();
 cudaError_t preload_tma_kernels();
 cudaError_t preload_simt_kernels();
+cudaError_t preload_tc2_kernels();
 
 namespace {
 
@@ -54,6 +55,7 @@ cudaError_t preload_kernels() {
     if (e == cudaSuccess) e = preload_tc_kernels();
     if (e == cudaSuccess) e = preload_tma_kernels();
     if (e == cudaSuccess) e = preload_simt_kernels();
+    if (e == cudaSuccess) e = preload_tc2_kernels();
     return e;
 }
 

@@ -23,7 +23,9 @@ cm = pytest.importorskip("paper_2311_03543_b200.compar")
 VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tma_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tc_tf32": (cm.F32, cm.COMPUTE_TF32, 5e-3),
-            "tc_bf16": (cm.BF16, cm.COMPUTE_BF16, 5e-3)}
+            "tc_bf16": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
+            "tc_tf32_2sm": (cm.F32, cm.COMPUTE_TF32, 5e-3),
+            "tc_bf16_2sm": (cm.BF16, cm.COMPUTE_BF16, 5e-3)}
 
 SHAPES = [(1, 1, 1), (7, 13, 5), (64, 64, 64), (65, 127, 129), (129, 257, 70), (128, 256, 64),
           (300, 520, 1000), (1000, 777, 333), (257, 1, 100), (1, 300, 4097)]
@@ -165,12 +167,12 @@ def test_host_memory_mode_matches_device(ctx):
     Bh = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).pin_memory()
     Ch = torch.from_numpy(C0.copy()).pin_memory()
     d = cm.make_desc(m, n, k, A=Ah, B=Bh, C_in=Ch, C_out=Ch, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
-                     compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST)
+                     compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST, variant_hint=vid(ctx, "tc_bf16"))
     r = ctx.run(d)
     assert r.status == 0 and r.total_ns >= r.ns > 0
     Cd = to_device(C0)
     d2 = cm.make_desc(m, n, k, A=to_device(A, "bf16"), B=to_device(B, "bf16"), C_in=Cd, C_out=Cd, alpha=1.5,
-                      beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16)
+                      beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, variant_hint=vid(ctx, "tc_bf16"))
     ctx.run(d2)
     assert torch.equal(Ch, Cd.cpu())
     ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5, dtype="bf16")
@@ -187,7 +189,7 @@ def test_world_size_one_nccl(ctx):
         B = device_matrix(gen.TAG_B, k, n, dtype="bf16")
         C0 = device_matrix(gen.TAG_C, m, n)
         C1, C2 = C0.clone(), C0.clone()
-        kw = dict(alpha=1.5, beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16)
+        kw = dict(alpha=1.5, beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, variant_hint=vid(c, "tc_bf16"))
         c.run(cm.make_desc(m, n, k, A=A, B=B, C_in=C1, C_out=C1, world=1, **kw))
         c.run(cm.make_desc(m, n, k, A=A, B=B, C_in=C2, C_out=C2, **kw))
         assert torch.equal(C1, C2)
@@ -196,6 +198,8 @@ def test_world_size_one_nccl(ctx):
 
 
 @pytest.mark.parametrize("name,shape", [("tc_bf16", (8192, 8192, 8192)), ("tc_tf32", (8192, 8192, 8192)),
+                                        ("tc_bf16_2sm", (8192, 8192, 8192)), ("tc_tf32_2sm", (8192, 8192, 8192)),
+                                        ("tc_bf16_2sm", (32768, 32768, 32768)), ("tc_bf16_2sm", (65536, 256, 4096)),
                                         ("tc_bf16", (65536, 256, 4096)), ("tc_tf32", (65536, 256, 4096)),
                                         ("tc_bf16", (32768, 32768, 32768))])
 def test_full_size_sampled(ctx, name, shape):

@@ -74,12 +74,15 @@ def test_config1_calibration_trace():
     B = device_matrix(gen.TAG_B, m, m)
     Cd = device_matrix(gen.TAG_C, m, m)
     d = cm.make_desc(m, m, m, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, compute=cm.COMPUTE_TF32)
-    trace = [ctx.run(d) for _ in range(13)]
-    assert [r.variant for r in trace[:12]] == [0, 1, 2] * 4
-    assert [r.mode for r in trace[:3]] == [cm.MODE_WARMUP] * 3
-    assert trace[12].mode == cm.MODE_MODEL
-    means = [ctx.history(v, d).mean_ns for v in range(3)]
-    assert trace[12].variant == int(np.argmin(means))
+    tf32_ok = {cm.TGT_SIMT_F32, cm.TGT_TMA_F32, cm.TGT_TC_TF32, cm.TGT_TC2_TF32}
+    E = [v for v, (_, tgt) in enumerate(ctx.variants()) if tgt in tf32_ok]
+    n_cal = 4 * len(E)
+    trace = [ctx.run(d) for _ in range(n_cal + 1)]
+    assert [r.variant for r in trace[:n_cal]] == E * 4
+    assert [r.mode for r in trace[:len(E)]] == [cm.MODE_WARMUP] * len(E)
+    assert trace[n_cal].mode == cm.MODE_MODEL
+    means = [ctx.history(v, d).mean_ns for v in E]
+    assert trace[n_cal].variant == E[int(np.argmin(means))]
     st = ctx.stats()
-    assert st.launches == 13 and st.harvested == 10
+    assert st.launches == n_cal + 1 and st.harvested == 3 * len(E) + 1
     ctx.terminate()

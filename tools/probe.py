@@ -15,14 +15,14 @@ from gen.device import device_matrix  # noqa: E402
 def time_variant(ctx, name, m, n, k, reps=10, transB=0):
     names = [v for v, _ in ctx.variants()]
     vid = names.index(name)
-    bf = name == "tc_bf16"
+    bf = "bf16" in name
     dt = "bf16" if bf else "f32"
     A = device_matrix(gen.TAG_A, m, k, dtype=dt)
     B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(transB))
     Cd = device_matrix(gen.TAG_C, m, n)
     d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5,
                      in_dtype=cm.BF16 if bf else cm.F32,
-                     compute=cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if name == "tc_tf32" else cm.COMPUTE_F32_STRICT),
+                     compute=cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else cm.COMPUTE_F32_STRICT),
                      transB=transB, variant_hint=vid, ldb=(k if transB else n))
     for _ in range(3):
         ctx.run(d)
@@ -33,7 +33,9 @@ def time_variant(ctx, name, m, n, k, reps=10, transB=0):
 
 if __name__ == "__main__":
     ctx = cm.Compar()
-    cases = [("tc_bf16", 8192, 8192, 8192), ("tc_bf16", 8192, 8192, 8192, 1), ("tc_tf32", 8192, 8192, 8192),
+    cases = [("tc_bf16_2sm", 8192, 8192, 8192), ("tc_bf16_2sm", 32768, 32768, 32768), ("tc_tf32_2sm", 8192, 8192, 8192),
+             ("tc_bf16_2sm", 65536, 256, 4096), ("tc_bf16_2sm", 4096, 4096, 4096), ("tc_bf16_2sm", 1024, 1024, 1024),
+             ("tc_bf16", 8192, 8192, 8192), ("tc_bf16", 8192, 8192, 8192, 1), ("tc_tf32", 8192, 8192, 8192),
              ("tc_bf16", 65536, 256, 4096), ("tc_bf16", 4096, 4096, 4096), ("tma_f32", 4096, 4096, 4096),
              ("simt_f32", 4096, 4096, 4096), ("tma_f32", 1024, 1024, 1024), ("simt_f32", 1024, 1024, 1024),
              ("tc_tf32", 1024, 1024, 1024), ("simt_f32", 64, 64, 64), ("tma_f32", 64, 64, 64),
