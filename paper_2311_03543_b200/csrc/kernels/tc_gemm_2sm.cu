@@ -9,13 +9,14 @@
 // the B traffic (L2 -> SMEM and SMEM -> tensor core) relative to the 1-SM 128 x 256 tile.
 //
 // Synchronisation (all mbarriers at identical smem offsets in both CTAs):
-//   full[s]   leader only; count 2 (leader arrive.expect_tx(both CTAs' bytes) + peer remote
-//             arrive); both CTAs' TMA loads (cta_group::2) complete_tx on it;
+//   full[s]   leader only; count 1 (leader arrive.expect_tx(both CTAs' bytes)); both CTAs'
+//             TMA loads (cta_group::2) complete_tx on it;
 //   empty[s]  each CTA; the leader's tcgen05.commit multicasts an arrival to both;
 //   tfull[a]  each CTA; leader commit multicast when accumulator a is final;
 //   tempty[a] leader only; count 8 = 4 epilogue warps x 2 CTAs (remote arrivals).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -26,7 +27,7 @@ namespace compar {
 namespace {
 
 constexpr int kThreads2 = 192;
-constexpr int kGroupM2 = 8;  // 256-row cluster tiles per raster band
+constexpr int kGroupM2 = 8;  // default 256-row cluster tiles per raster band (COMPAR_TC_GROUP overrides)
 
 template <bool kBF16, bool kTransB>
 struct Tc2Cfg {
@@ -60,14 +61,15 @@ struct Tc2Params {
     float *C_out;
     int64_t ldc_out;
     int m_blocks, n_blocks, num_kb;  // m_blocks in 256-row pair tiles
+    int group_m;
     int cvec;
 };
 
-__device__ __forceinline__ void tile_coords2(int t, int m_blocks, int n_blocks, int &mb, int &nb) {
-    const int per_group = kGroupM2 * n_blocks;
+__device__ __forceinline__ void tile_coords2(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
+    const int per_group = group * n_blocks;
     const int g = t / per_group;
-    const int first_m = g * kGroupM2;
-    const int gm = min(m_blocks - first_m, kGroupM2);
+    const int first_m = g * group;
+    const int gm = min(m_blocks - first_m, group);
     const int r = t - g * per_group;
     mb = first_m + r % gm;
     nb = r / gm;
@@ -95,7 +97,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
         for (int s = 0; s < C::STAGES; ++s) {
-            ptx::mbar_init(full0 + 8 * s, 2);
+            ptx::mbar_init(full0 + 8 * s, 1);
             ptx::mbar_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -118,7 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             uint32_t phase = 0;
             for (int t = cluster; t < num_tiles; t += nclusters) {
                 int mb, nb;
-                tile_coords2(t, p.m_blocks, p.n_blocks, mb, nb);
+                tile_coords2(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM;
                 const int32_t bcol = nb * C::BN + static_cast<int32_t>(rank) * C::BN_CTA;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -127,10 +129,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const uint32_t sb = sa + C::A_BYTES;
                     const uint32_t fb_local = full0 + 8 * stage;
                     const uint32_t fb = ptx::leader_addr(fb_local);
-                    if (leader)
-                        ptx::mbar_arrive_expect_tx(fb_local, 2 * C::STAGE_BYTES);
-                    else
-                        ptx::mbar_arrive_cluster(fb);
+                    // Only the leader arrives (count 1) and expects both CTAs' bytes; the peer's TMA
+                    // bytes can land before that arrive (tx-count transiently negative) but the phase
+                    // cannot complete without it, and the peer cannot run a phase ahead because it
+                    // waits on its own empty[s], released only after the leader consumed stage s.
+                    // (A remote arrive here would need a release.cluster fence = MEMBAR.GPU per k-step.)
+                    if (leader) ptx::mbar_arrive_expect_tx(fb_local, 2 * C::STAGE_BYTES);
                     ptx::tma_load_2d_2sm(sa, &tmA, fb, kb * C::BK, arow);
                     if (kTransB) {
                         ptx::tma_load_2d_2sm(sb, &tmB, fb, kb * C::BK, bcol);
@@ -193,7 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const uint32_t tempty_leader = ptx::leader_addr(tempty0);
         for (int t = cluster; t < num_tiles; t += nclusters, ++local) {
             int mb, nb;
-            tile_coords2(t, p.m_blocks, p.n_blocks, mb, nb);
+            tile_coords2(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
@@ -273,6 +277,11 @@ cudaError_t launch_tc2_t(const GemmLaunch &g) {
     p.m_blocks = static_cast<int>((g.m + 2 * C::BM - 1) / (2 * C::BM));
     p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
+    static const int group_env = [] {
+        const char *s = std::getenv("COMPAR_TC_GROUP");
+        return s ? std::atoi(s) : 0;
+    }();
+    p.group_m = group_env > 0 ? group_env : kGroupM2;
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     const int tiles = p.m_blocks * p.n_blocks;

@@ -1,0 +1,199 @@
+"""Selector evaluation on real cudaEvent timings (BASELINE configs 1, 2, 5).
+
+* config 1: 64^3 FP32 — calibration trace, chosen variant, host submit overhead;
+* config 2: square sweep 256..4096 FP32 (F32_STRICT and TF32) — regret at every size and the
+  variant crossover points;
+* config 5a: tall-skinny 65536x256x4096 (BF16, TF32) — regret;
+* config 5b: mixed stream of 200 tasks (shapes drawn with numpy PCG64 seed 7), FP32 under TF32,
+  beta = 0 — steady-state per-shape regret, stream time vs sum of per-shape best, selection
+  accuracy of the history selector vs the eager scheduler.
+
+Regret(size) = T(selected)/min_v T(v) - 1, T = median of R timed executions of each eligible
+variant measured exhaustively in the same run (variant_hint, history untouched).
+usage: python tools/selector_sweep.py [out.json]
+"""
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+from gen.device import device_matrix  # noqa: E402
+from paper_2311_03543_b200 import compar as cm  # noqa: E402
+
+R = 10
+TF32_T = {cm.TGT_SIMT_F32, cm.TGT_TMA_F32, cm.TGT_TC_TF32, cm.TGT_TC2_TF32}
+STRICT_T = {cm.TGT_SIMT_F32, cm.TGT_TMA_F32}
+BF16_T = {cm.TGT_TC_BF16, cm.TGT_TC2_BF16}
+
+
+class Problem:
+    def __init__(self, m, n, k, dtype="f32", beta=0.5):
+        self.m, self.n, self.k, self.dt, self.beta = m, n, k, dtype, beta
+        self.A = device_matrix(gen.TAG_A, m, k, dtype=dtype)
+        self.B = device_matrix(gen.TAG_B, k, n, dtype=dtype)
+        self.C = device_matrix(gen.TAG_C, m, n)
+
+    def desc(self, compute, hint=-1):
+        bf = self.dt == "bf16"
+        return cm.make_desc(self.m, self.n, self.k, A=self.A, B=self.B, C_in=self.C, C_out=self.C, alpha=1.5,
+                            beta=self.beta, in_dtype=cm.BF16 if bf else cm.F32, compute=compute, variant_hint=hint)
+
+
+def eligible(ctx, targets):
+    return [v for v, (_, t) in enumerate(ctx.variants()) if t in targets]
+
+
+def exhaustive(ctx, prob, compute, E):
+    med = {}
+    for v in E:
+        d = prob.desc(compute, v)
+        ctx.run(d)
+        med[v] = statistics.median(ctx.run(d).ns for _ in range(R))
+    return med
+
+
+def selected_runs(ctx, prob, compute):
+    """Train the selector for this key (calibration), then R model-mode executions."""
+    d = prob.desc(compute)
+    trace = []
+    while True:
+        r = ctx.run(d)
+        trace.append((r.variant, r.mode))
+        if r.mode == cm.MODE_MODEL or len(trace) > 64:
+            break
+    model = [ctx.run(d) for _ in range(R)]
+    return trace, model
+
+
+def regret_case(ctx, names, prob, compute, targets):
+    E = eligible(ctx, targets)
+    trace, model = selected_runs(ctx, prob, compute)
+    med = exhaustive(ctx, prob, compute, E)
+    chosen = model[-1].variant
+    best = min(med, key=med.get)
+    reg = med[chosen] / med[best] - 1.0
+    return {"shape": [prob.m, prob.n, prob.k], "dtype": prob.dt, "compute": compute,
+            "eligible": [names[v] for v in E], "chosen": names[chosen], "best": names[best],
+            "regret": reg, "median_ns": {names[v]: med[v] for v in E},
+            "calibration_runs": len(trace) - 1, "chosen_stable": len({r.variant for r in model}) == 1}
+
+
+def main(out_path):
+    torch.cuda.set_device(0)
+    res = {"R": R}
+    ctx = cm.Compar()
+    names = [n for n, _ in ctx.variants()]
+
+    # ---- config 1: 64^3, calibration trace + host overhead
+    c1 = []
+    for compute, T in ((cm.COMPUTE_F32_STRICT, STRICT_T), (cm.COMPUTE_TF32, TF32_T)):
+        prob = Problem(64, 64, 64)
+        d = prob.desc(compute)
+        trace = []
+        t_host = []
+        for _ in range(4 * len(eligible(ctx, T)) + R):
+            t0 = time.perf_counter()
+            t = ctx.submit(d)
+            t_host.append(time.perf_counter() - t0)
+            r = ctx.sync(t)
+            trace.append([names[r.variant], r.mode, r.ns])
+        med = exhaustive(ctx, prob, compute, eligible(ctx, T))
+        chosen = [v for v in range(len(names)) if names[v] == trace[-1][0]][0]
+        c1.append({"compute": compute, "trace": trace, "chosen": trace[-1][0],
+                   "regret": med[chosen] / min(med.values()) - 1.0,
+                   "median_ns": {names[v]: x for v, x in med.items()},
+                   "host_submit_us_median": statistics.median(t_host) * 1e6})
+    res["config1"] = c1
+
+    # ---- config 2: square sweep
+    sizes = [256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096]
+    c2 = {"F32_STRICT": [], "TF32": []}
+    for s in sizes:
+        prob = Problem(s, s, s)
+        c2["F32_STRICT"].append(regret_case(ctx, names, prob, cm.COMPUTE_F32_STRICT, STRICT_T))
+        c2["TF32"].append(regret_case(ctx, names, prob, cm.COMPUTE_TF32, TF32_T))
+        del prob
+        torch.cuda.empty_cache()
+    # crossovers: smallest size from which variant X's median beats Y's (within the 1.5x grid)
+    cross = {}
+    for mode, rows in c2.items():
+        vs = rows[0]["eligible"]
+        for x in vs:
+            for y in vs:
+                if x == y:
+                    continue
+                wins = [r["shape"][0] for r in rows if r["median_ns"][x] < r["median_ns"][y]]
+                loses = [r["shape"][0] for r in rows if r["median_ns"][x] >= r["median_ns"][y]]
+                if wins and loses and min(wins) > min(loses):
+                    cross[f"{mode}: {x} beats {y} from"] = min(wins)
+    c2["crossovers"] = cross
+    c2["max_regret"] = max(r["regret"] for rows in (c2["F32_STRICT"], c2["TF32"]) for r in rows)
+    res["config2"] = c2
+
+    # ---- config 5a: tall-skinny
+    c5a = []
+    prob = Problem(65536, 256, 4096, "bf16")
+    c5a.append(regret_case(ctx, names, prob, cm.COMPUTE_BF16, BF16_T))
+    del prob
+    prob = Problem(65536, 256, 4096, "f32")
+    c5a.append(regret_case(ctx, names, prob, cm.COMPUTE_TF32, TF32_T))
+    del prob
+    torch.cuda.empty_cache()
+    res["config5a"] = c5a
+    ctx.terminate()
+
+    # ---- config 5b: mixed stream, history vs eager
+    shapes = [(64, 64, 64), (256, 256, 256), (1024, 1024, 1024), (4096, 4096, 4096), (8192, 8192, 8192),
+              (65536, 256, 4096), (4096, 4096, 256)]
+    rng = np.random.Generator(np.random.PCG64(7))
+    stream = [shapes[i] for i in rng.integers(0, len(shapes), 200)]
+    probs = {s: Problem(*s, beta=0.0) for s in shapes}
+    best = {}
+    ctxb = cm.Compar()
+    E = eligible(ctxb, TF32_T)
+    for s, p in probs.items():
+        med = exhaustive(ctxb, p, cm.COMPUTE_TF32, E)
+        best[s] = (min(med, key=med.get), min(med.values()), {names[v]: x for v, x in med.items()})
+    ctxb.terminate()
+    c5b = {"tasks": len(stream), "shapes": [list(s) for s in shapes],
+           "best": {str(list(s)): names[b[0]] for s, b in best.items()}}
+    for sched, label in ((0, "history"), (1, "eager")):
+        c = cm.Compar(sched=sched)
+        chosen, total_ns = [], 0
+        t0 = time.perf_counter()
+        for s in stream:
+            r = c.run(probs[s].desc(cm.COMPUTE_TF32))
+            chosen.append((s, r.variant, r.mode))
+            total_ns += r.ns
+        wall = time.perf_counter() - t0
+        steady = [(s, v) for (s, v, mode) in chosen if mode in (cm.MODE_MODEL, cm.MODE_EAGER)]
+        acc = sum(1 for s, v in steady if v == best[s][0]) / max(1, len(steady))
+        per_shape = {}
+        for s in shapes:
+            vs = [v for (ss, v) in steady if ss == s]
+            if vs:
+                v = max(set(vs), key=vs.count)
+                per_shape[str(list(s))] = {"chosen": names[v],
+                                           "regret": best[s][2][names[v]] / best[s][1] - 1.0}
+        c5b[label] = {"kernel_ms_total": total_ns / 1e6, "wall_s": wall, "selection_accuracy_steady": acc,
+                      "per_shape": per_shape}
+        c.terminate()
+    c5b["sum_of_best_ms"] = sum(best[s][1] for s in stream) / 1e6
+    res["config5b"] = c5b
+    out = json.dumps(res, indent=1)
+    if out_path:
+        with open(out_path, "w") as f:
+            f.write(out)
+    print(out)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else None)
