@@ -27,6 +27,7 @@ cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16);  // variant (c),
 cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha == 0: C_out = beta*C_in
 cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
 cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)
+int *sched_workspace(cudaStream_t s);                        // {next, done} tile counters for persistent kernels
 
 // TMA eligibility (the selector's constraint filter).
 inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {

@@ -1,0 +1,31 @@
+// Per-stream tile-scheduler workspace for the persistent tcgen05 kernels.
+//
+// Each persistent launch draws output tiles from a global atomic counter, so the set of tiles
+// in flight is always a contiguous range in raster order however the CTAs drift relative to
+// each other (a static round-robin schedule lets CTAs drift apart by whole tiles over a long
+// K, which destroys L2 reuse between CTAs that share A rows / B columns — DESIGN.md §5).
+// The counter pair {next, done} is zeroed once and re-zeroed by the last CTA of every launch;
+// launches on one stream are ordered, so one pair per stream is enough.
+#include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+
+#include "kernels.h"
+
+namespace compar {
+
+int *sched_workspace(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, int *> slots;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = slots.find(s);
+    if (it != slots.end()) return it->second;
+    int *p = nullptr;
+    if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    slots.emplace(s, p);
+    return p;
+}
+
+}  // namespace compar

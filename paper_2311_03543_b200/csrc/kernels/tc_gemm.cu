@@ -6,15 +6,18 @@
 // (kind::tf32), FP32 accumulation in TMEM, FP32 C (R1-R6).
 //
 // Structure (DESIGN.md §5 "tc_gemm"), persistent, warp-specialised, one CTA per SM:
-//   warp 0      TMA producer: A tile 128 x BK (K-major, SWIZZLE_128B) and B tile BK x 256
-//               (row-major B = MN-major: 128-byte N atoms; transB = K-major) into a
-//               4-stage shared-memory ring guarded by full/empty mbarriers;
+//   warp 0      tile scheduler + TMA producer: draws the next output tile from a global atomic
+//               counter (tiles leave in raster order, so the tiles in flight stay a contiguous
+//               band however CTAs drift — L2 reuse survives long K), publishes it in a 4-deep
+//               smem tile ring, then streams the A tile 128 x BK (K-major, SWIZZLE_128B) and
+//               B tile BK x 256 (row-major B = MN-major 128-byte N atoms; transB = K-major) into
+//               a 4-stage shared-memory ring guarded by full/empty mbarriers;
 //   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.mma M=128 N=256 per
 //               UMMA_K slice into one of two TMEM accumulators (2 x 256 columns), then
 //               tcgen05.commit -> empty[stage] / tmem_full[acc];
 //   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> alpha*acc + beta*C_in -> st.global, then
 //               tmem_empty[acc] — so tile i's epilogue overlaps tile i+1's mainloop.
-// Tiles are visited in GROUP_M-row bands so concurrently-resident CTAs share A/B in L2.
+// Raster: GROUP_M-row bands so concurrently-resident CTAs share A/B panels in L2.
 // Edges: TMA zero-fills out-of-bounds boxes; the epilogue predicates rows/cols.
 #include <cuda.h>
 
@@ -29,6 +32,7 @@ namespace {
 
 constexpr int kThreads = 192;
 constexpr int kGroupM = 16;
+constexpr int kTileRing = 4;
 
 template <bool kBF16, bool kTransB>
 struct TcCfg {
@@ -49,7 +53,7 @@ struct TcCfg {
     static constexpr bool B_BASE32 = !kBF16 && !kTransB;
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 512;
     // Instruction descriptor: D=F32 [4,6), A/B format [7,10)/[10,13) (1 BF16, 2 TF32),
     // a_major=K [15], b_major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
@@ -66,6 +70,7 @@ struct TcParams {
     int64_t ldc_out;
     int m_blocks, n_blocks, num_kb;
     int cvec;
+    int *sched;  // {next, done}: zero on entry, re-zeroed by the last CTA
 };
 
 __device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int &mb, int &nb) {
@@ -89,7 +94,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t empty0 = full0 + 8 * C::STAGES;
     const uint32_t tfull0 = empty0 + 8 * C::STAGES;
     const uint32_t tempty0 = tfull0 + 16;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
+    const uint32_t rfull0 = tempty0 + 16;                 // tile ring: published
+    const uint32_t rempty0 = rfull0 + 8 * kTileRing;      // tile ring: consumed by MMA + 4 epilogue warps
+    const uint32_t ring0 = rempty0 + 8 * kTileRing;       // int tile ids
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + 480);
     const uint32_t smem0 = ptx::smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,6 +112,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(tfull0 + 8 * a, 1);
             ptx::mbar_init(tempty0 + 8 * a, 4);
         }
+        for (int r = 0; r < kTileRing; ++r) {
+            ptx::mbar_init(rfull0 + 8 * r, 1);
+            ptx::mbar_init(rempty0 + 8 * r, 5);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_slot));
@@ -113,11 +125,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     const int num_tiles = p.m_blocks * p.n_blocks;
+    // Consumer side of the tile ring: returns the i-th tile of this CTA (>= num_tiles: done).
+    auto next_tile = [&](int i) -> int {
+        const int slot = i % kTileRing;
+        ptx::mbar_wait(rfull0 + 8 * slot, (i / kTileRing) & 1);
+        const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(rempty0 + 8 * slot);
+        return t;
+    };
+
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
+        if (lane == 0) {  // ---------------- scheduler + TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int i = 0;; ++i) {
+                const int slot = i % kTileRing;
+                ptx::mbar_wait(rempty0 + 8 * slot, ((i / kTileRing) & 1) ^ 1);
+                const int t = atomicAdd(&p.sched[0], 1);
+                ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
+                ptx::mbar_arrive(rfull0 + 8 * slot);
+                if (t >= num_tiles) break;
                 int mb, nb;
                 tile_coords(t, p.m_blocks, p.n_blocks, mb, nb);
                 for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -141,12 +169,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            // last CTA out re-arms the counters for the next launch on this stream
+            __threadfence();
+            if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+                p.sched[0] = 0;
+                p.sched[1] = 0;
+            }
         }
     } else if (warp == 1) {  // ---------------- MMA issuer
         int stage = 0;
         uint32_t phase = 0;
-        int local = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        for (int local = 0;; ++local) {
+            const int t = next_tile(local);
+            if (t >= num_tiles) break;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
@@ -182,8 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {  // ---------------- epilogue warps 2..5
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        int local = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        for (int local = 0;; ++local) {
+            const int t = next_tile(local);
+            if (t >= num_tiles) break;
             int mb, nb;
             tile_coords(t, p.m_blocks, p.n_blocks, mb, nb);
             const int acc = local & 1;
@@ -264,6 +300,8 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
+    p.sched = sched_workspace(g.stream);
+    if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
     const int grid = tiles < g.num_sms ? tiles : g.num_sms;
     tc_gemm_kernel<kBF16, kTransB><<<grid, kThreads, C::SMEM, g.stream>>>(ta, tb, p);

@@ -13,7 +13,12 @@
 //             TMA loads (cta_group::2) complete_tx on it;
 //   empty[s]  each CTA; the leader's tcgen05.commit multicasts an arrival to both;
 //   tfull[a]  each CTA; leader commit multicast when accumulator a is final;
-//   tempty[a] leader only; count 8 = 4 epilogue warps x 2 CTAs (remote arrivals).
+//   tempty[a] leader only; count 8 = 4 epilogue warps x 2 CTAs (remote arrivals);
+//   rfull[r]  each CTA: tile id r of the dynamic schedule published (leader producer writes
+//             both CTAs' ring slots through DSMEM and arrives on both);
+//   rempty[r] leader only; count 10 = leader MMA + 4 leader epilogue + peer producer + 4 peer
+//             epilogue warps.
+// Tiles come from a global atomic counter drawn by the leader's producer (see sched.cpp).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -28,6 +33,7 @@ namespace {
 
 constexpr int kThreads2 = 192;
 constexpr int kGroupM2 = 8;  // default 256-row cluster tiles per raster band (COMPAR_TC_GROUP overrides)
+constexpr int kRing2 = 4;
 
 template <bool kBF16, bool kTransB>
 struct Tc2Cfg {
@@ -47,7 +53,7 @@ struct Tc2Cfg {
     static constexpr bool B_BASE32 = !kBF16 && !kTransB;
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 512;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
                                       ((kTransB ? 0u : 1u) << 16) | ((uint32_t(BN) >> 3) << 17) |
                                       ((uint32_t(2 * BM) >> 4) << 24);
@@ -63,6 +69,7 @@ struct Tc2Params {
     int m_blocks, n_blocks, num_kb;  // m_blocks in 256-row pair tiles
     int group_m;
     int cvec;
+    int *sched;  // {next, done}
 };
 
 __device__ __forceinline__ void tile_coords2(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
@@ -73,6 +80,12 @@ __device__ __forceinline__ void tile_coords2(int t, int m_blocks, int n_blocks, 
     const int r = t - g * per_group;
     mb = first_m + r % gm;
     nb = r / gm;
+}
+
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t peer_rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(peer_rank));
+    return r;
 }
 
 template <bool kBF16, bool kTransB>
@@ -87,7 +100,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const uint32_t empty0 = full0 + 8 * C::STAGES;
     const uint32_t tfull0 = empty0 + 8 * C::STAGES;
     const uint32_t tempty0 = tfull0 + 16;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
+    const uint32_t rfull0 = tempty0 + 16;
+    const uint32_t rempty0 = rfull0 + 8 * kRing2;
+    const uint32_t ring0 = rempty0 + 8 * kRing2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + 480);
     const uint32_t smem0 = ptx::smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,6 +120,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             ptx::mbar_init(tfull0 + 8 * a, 1);
             ptx::mbar_init(tempty0 + 8 * a, 8);
         }
+        for (int r = 0; r < kRing2; ++r) {
+            ptx::mbar_init(rfull0 + 8 * r, 1);
+            ptx::mbar_init(rempty0 + 8 * r, 10);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm<512>(ptx::smem_u32(tmem_slot));
@@ -113,12 +133,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     const int num_tiles = p.m_blocks * p.n_blocks;
-    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const uint32_t rempty_leader = ptx::leader_addr(rempty0);
+    // Consumer side of the tile ring (both CTAs): the i-th tile of this pair.
+    auto next_tile = [&](int i) -> int {
+        const int slot = i % kRing2;
+        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRing2) & 1);
+        const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(rempty_leader + 8 * slot);
+        return t;
+    };
+
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+        if (lane == 0) {  // ---------------- scheduler (leader) + TMA producer (both CTAs)
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster; t < num_tiles; t += nclusters) {
+            for (int i = 0;; ++i) {
+                int t;
+                if (leader) {
+                    const int slot = i % kRing2;
+                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, ((i / kRing2) & 1) ^ 1);
+                    t = atomicAdd(&p.sched[0], 1);
+                    ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
+                    ptx::st_shared_cluster_u32(peer_addr(ring0 + 4 * slot, 1), static_cast<uint32_t>(t));
+                    ptx::mbar_arrive(rfull0 + 8 * slot);
+                    ptx::mbar_arrive_cluster(peer_addr(rfull0 + 8 * slot, 1));
+                } else {  // single-lane consumer (no __syncwarp: the other lanes are parked)
+                    const int slot = i % kRing2;
+                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRing2) & 1);
+                    t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
+                    ptx::mbar_arrive_cluster(rempty_leader + 8 * slot);
+                }
+                if (t >= num_tiles) break;
                 int mb, nb;
                 tile_coords2(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM;
@@ -150,16 +196,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     }
                 }
             }
+            if (leader) {  // last pair out re-arms the counters for the next launch on this stream
+                __threadfence();
+                if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x >> 1) - 1) {
+                    p.sched[0] = 0;
+                    p.sched[1] = 0;
+                }
+            }
         }
     } else if (warp == 1) {
         if (leader) {  // ---------------- MMA issuer (leader CTA only)
             int stage = 0;
             uint32_t phase = 0;
-            int local = 0;
-            for (int t = cluster; t < num_tiles; t += nclusters, ++local) {
+            for (int local = 0;; ++local) {
+                const int t = next_tile(local);
+                if (t >= num_tiles) break;
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
-                ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+                ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C::BN;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -193,9 +247,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
     } else {  // ---------------- epilogue warps 2..5 (both CTAs, own TMEM rows)
         const int q = warp & 3;
-        int local = 0;
         const uint32_t tempty_leader = ptx::leader_addr(tempty0);
-        for (int t = cluster; t < num_tiles; t += nclusters, ++local) {
+        for (int local = 0;; ++local) {
+            const int t = next_tile(local);
+            if (t >= num_tiles) break;
             int mb, nb;
             tile_coords2(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
@@ -284,6 +339,8 @@ cudaError_t launch_tc2_t(const GemmLaunch &g) {
     p.group_m = group_env > 0 ? group_env : kGroupM2;
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
+    p.sched = sched_workspace(g.stream);
+    if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
     const int max_clusters = g.num_sms / 2;
     const int clusters = tiles < max_clusters ? tiles : max_clusters;
