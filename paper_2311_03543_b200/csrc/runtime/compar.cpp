@@ -66,6 +66,7 @@ struct Task {
     compar_status status = COMPAR_OK;
     std::vector<PanelRun> panels;
     cudaEvent_t begin = nullptr, end = nullptr, bc0 = nullptr, bc1 = nullptr;
+    std::vector<cudaEvent_t> extra;  // per-slab broadcast events (world mode)
     bool world = false;
 };
 
@@ -91,6 +92,12 @@ struct Ctx {
     int64_t *red_buf = nullptr;  // device scalar for the rank-consistent sample all-reduce
     compar_reduce_fn reduce_hook = nullptr;
     void *reduce_user = nullptr;
+    // world-mode broadcast pipeline
+    cudaStream_t comm_stream = nullptr;
+    void *bpacked = nullptr;  // root: B packed into contiguous N-slabs
+    size_t bpacked_bytes = 0;
+    bool bcast_loopback = false;  // 1 rank: emulate the broadcast with D2D copies (tests the slab path)
+    int bcast_reserve_sms = 16;   // SMs left free for NCCL while a slab GEMM overlaps a broadcast
 };
 
 std::mutex g_live_mu;
@@ -158,6 +165,8 @@ void release_task_events(Ctx *c, Task &t) {
     put_event(c, t.end);
     put_event(c, t.bc0);
     put_event(c, t.bc1);
+    for (auto &e : t.extra) put_event(c, e);
+    t.extra.clear();
 }
 int64_t elapsed_ns(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
@@ -187,7 +196,7 @@ compar_status validate(Ctx *c, const compar_gemm_desc *d) {
     if (d->mem != COMPAR_MEM_DEVICE && d->mem != COMPAR_MEM_HOST) return fail(COMPAR_E_INVALID, "bad mem");
     if (d->panels < 0 || d->panels > COMPAR_MAX_PANELS) return fail(COMPAR_E_INVALID, "panels out of range");
     if (d->world && d->panels > 1) return fail(COMPAR_E_INVALID, "world and loopback panels are exclusive");
-    if (d->world && !c->virt && !c->comm) return fail(COMPAR_E_STATE, "world=1 needs compar_comm_init");
+    // world = 1 without compar_comm_init is a 1-rank world (plain launch, or the loopback pipeline)
     if (d->variant_hint < -1 || d->variant_hint >= static_cast<int>(c->variants.size()))
         return fail(COMPAR_E_INVALID, "variant_hint out of range");
     if (d->m == 0 || d->n == 0) return COMPAR_OK;
@@ -381,14 +390,14 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
 
 // ---------------------------------------------------------------- running a variant on a panel
 compar_status run_builtin(Ctx *c, compar_target t, const compar_gemm_desc *d, const compar_panel &p,
-                          cudaStream_t s) {
+                          cudaStream_t s, int sms = 0) {
     GemmLaunch g;
     g.m = p.rows, g.n = d->n, g.k = d->k;
     g.alpha = d->alpha, g.beta = d->beta;
     g.A = p.A, g.lda = d->lda, g.B = p.B, g.ldb = d->ldb, g.transB = d->transB;
     g.C_in = p.C_in, g.ldc_in = d->ldc_in, g.C_out = p.C_out, g.ldc_out = d->ldc_out;
     g.stream = s;
-    g.num_sms = c->num_sms;
+    g.num_sms = sms > 0 ? sms : c->num_sms;
     cudaError_t e;
     switch (t) {
         case COMPAR_TGT_SIMT_F32: e = launch_simt_f32(g); break;
@@ -413,6 +422,118 @@ compar_status run_scale(Ctx *c, const compar_gemm_desc *d, const compar_panel &p
     cudaError_t e = launch_scale(g);
     c->stats.launches++;
     if (e != cudaSuccess) return fail(COMPAR_E_TASK_FAILED, std::string("scale: ") + cudaGetErrorString(e));
+    return COMPAR_OK;
+}
+
+// ---------------------------------------------------------------- world mode: B broadcast + panel GEMM
+// SURVEY §8(a) a5 / §8(e).  B is cut into `bcast_chunks` contiguous N-slabs (row-major B: packed
+// on the root by the copy engine with cudaMemcpy2DAsync; transB: slabs are already contiguous
+// row ranges of B^T), each slab is broadcast with ncclBroadcast on the library's comm stream,
+// and a non-root rank multiplies its A panel by slab j as soon as slab j has landed (event
+// hand-off), so slab j+1 travels while slab j is multiplied.  Every C element still sums its
+// full K in order, so C is bitwise identical to the single-GPU result.  The root multiplies
+// with its own B (one launch).  Slab GEMMs that overlap a pending broadcast leave
+// bcast_reserve_sms SMs free so NCCL's kernels are never starved by the persistent GEMM.
+template <class F>
+compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *Bloc,
+                             size_t b_bytes, F &&launch_on) {
+    const int eb = elem_bytes(d->in_dtype);
+    const bool loop = c->nranks == 1;              // loopback emulation on one GPU
+    const bool root = !loop && c->rank == 0;
+    const int64_t K = d->k, N = d->n;
+    int chunks = c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1;
+    int64_t w = ((N + chunks - 1) / chunks + 255) / 256 * 256;
+    if (w >= N) w = N;
+    int nslab = static_cast<int>((N + w - 1) / w);
+    const bool packable = d->transB ? ((K * eb) % 16 == 0) : ((w * eb) % 16 == 0 && ((N - (nslab - 1) * w) * eb) % 16 == 0);
+    if (!packable) nslab = 1;
+    const bool slabbed = nslab > 1;
+    compar_status s;
+    // buffers: the root (or loopback) packs into bpacked; receivers (or loopback) use the replica
+    void *packed = nullptr, *replica = const_cast<void *>(Bloc);
+    const size_t slab_total = static_cast<size_t>(K) * N * eb;
+    if (slabbed && (root || loop)) {
+        if ((s = ensure_buffer(&c->bpacked, &c->bpacked_bytes, slab_total)) != COMPAR_OK) return s;
+        packed = c->bpacked;
+    }
+    if (loop) {
+        if ((s = ensure_buffer(&c->breplica, &c->breplica_bytes, std::max(slab_total, b_bytes))) != COMPAR_OK) return s;
+        replica = c->breplica;
+    }
+    t.bc0 = get_event(c);
+    t.bc1 = get_event(c);
+    cudaEvent_t ready = get_event(c);
+    t.extra.push_back(ready);
+    cudaEventRecord(ready, st);                     // inputs / previous users of the buffers are done
+    cudaStreamWaitEvent(c->comm_stream, ready, 0);
+    cudaEventRecord(t.bc0, c->comm_stream);
+    std::vector<cudaEvent_t> landed;
+    ncclResult_t nr = ncclSuccess;
+    if (!slabbed) {
+        // one raw broadcast of the B region (any ld), then the plain panel GEMM
+        if (loop)
+            cudaMemcpyAsync(replica, Bloc, b_bytes, cudaMemcpyDeviceToDevice, c->comm_stream);
+        else
+            nr = ncclBroadcast(root ? Bloc : replica, root ? const_cast<void *>(Bloc) : replica, b_bytes, ncclChar, 0,
+                               c->comm, c->comm_stream);
+    } else {
+        for (int j = 0; j < nslab; ++j) {
+            const int64_t col0 = j * w, wj = std::min(w, N - col0);
+            const size_t off = static_cast<size_t>(K) * col0 * eb, bytes = static_cast<size_t>(K) * wj * eb;
+            char *pk = static_cast<char *>(packed) + off;
+            char *rp = static_cast<char *>(replica) + off;
+            const char *src = static_cast<const char *>(root || loop ? Bloc : nullptr);
+            if (root || loop) {
+                if (d->transB)
+                    cudaMemcpy2DAsync(pk, K * eb, src + col0 * d->ldb * eb, d->ldb * eb, K * eb, wj,
+                                      cudaMemcpyDeviceToDevice, c->comm_stream);
+                else
+                    cudaMemcpy2DAsync(pk, wj * eb, src + col0 * eb, d->ldb * eb, wj * eb, K, cudaMemcpyDeviceToDevice,
+                                      c->comm_stream);
+            }
+            if (loop)
+                cudaMemcpyAsync(rp, pk, bytes, cudaMemcpyDeviceToDevice, c->comm_stream);
+            else if (nr == ncclSuccess)
+                nr = ncclBroadcast(pk, root ? pk : rp, bytes, ncclChar, 0, c->comm, c->comm_stream);
+            cudaEvent_t ev = get_event(c);
+            t.extra.push_back(ev);
+            landed.push_back(ev);
+            cudaEventRecord(ev, c->comm_stream);
+        }
+    }
+    cudaEventRecord(t.bc1, c->comm_stream);
+    if (nr != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclBroadcast: ") + ncclGetErrorString(nr));
+    const int reserve_sms = std::max(2, c->num_sms - c->bcast_reserve_sms);
+    for (auto &pr : t.panels) {
+        pr.start = get_event(c);
+        pr.stop = get_event(c);
+        cudaEventRecord(pr.start, st);
+        compar_status r = COMPAR_OK;
+        if (root) {
+            r = launch_on(d, pr.p, reserve_sms);     // the root already holds B
+        } else if (!slabbed) {
+            cudaStreamWaitEvent(st, t.bc1, 0);
+            compar_panel pp = pr.p;
+            pp.B = replica;
+            r = launch_on(d, pp, 0);
+        } else {
+            for (int j = 0; j < nslab && r == COMPAR_OK; ++j) {
+                const int64_t col0 = j * w, wj = std::min(w, N - col0);
+                cudaStreamWaitEvent(st, landed[j], 0);
+                compar_gemm_desc dj = *d;
+                dj.n = wj;
+                dj.ldb = d->transB ? K : wj;
+                compar_panel pj = pr.p;
+                pj.B = static_cast<const char *>(replica) + static_cast<size_t>(K) * col0 * eb;
+                pj.C_in = pr.p.C_in ? pr.p.C_in + col0 : nullptr;
+                pj.C_out = pr.p.C_out + col0;
+                r = launch_on(&dj, pj, j + 1 < nslab ? reserve_sms : 0);
+            }
+        }
+        if (r != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+        cudaEventRecord(pr.stop, st);
+    }
+    cudaStreamWaitEvent(st, t.bc1, 0);              // the task ends after its broadcast (B reusable)
     return COMPAR_OK;
 }
 
@@ -496,6 +617,9 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
             return cuda_fail(e, "kernel preload (is this an sm_100 device?)");
         }
         cudaMalloc(reinterpret_cast<void **>(&c->red_buf), sizeof(int64_t));
+        cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+        c->bcast_loopback = env_int("COMPAR_BCAST_LOOPBACK", 0) != 0;
+        c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", 16);
     }
     {
         std::lock_guard<std::mutex> lk(g_live_mu);
@@ -543,6 +667,11 @@ compar_status compar_terminate(void *ctx) {
         for (auto &b : c->staging)
             if (b) cudaFree(b);
         if (c->breplica) cudaFree(c->breplica);
+        if (c->bpacked) cudaFree(c->bpacked);
+        if (c->comm_stream) {
+            cudaStreamSynchronize(c->comm_stream);
+            cudaStreamDestroy(c->comm_stream);
+        }
         if (c->red_buf) cudaFree(c->red_buf);
         for (auto e : c->pool) cudaEventDestroy(e);
         if (c->comm) ncclCommDestroy(c->comm);
@@ -747,33 +876,27 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             if (cin_bytes) cudaMemcpyAsync(const_cast<float *>(Cin), d->C_in, cin_bytes, cudaMemcpyHostToDevice, st);
             c->stats.bytes_h2d += static_cast<int64_t>(a_bytes + (root_b ? b_bytes : 0) + cin_bytes);
         }
-        if (t.world && c->nranks > 1 && gemm) {
-            t.bc0 = get_event(c);
-            t.bc1 = get_event(c);
-            cudaEventRecord(t.bc0, st);
-            void *buf = const_cast<void *>(B);
-            ncclResult_t r = ncclBroadcast(buf, buf, b_bytes, ncclChar, 0, c->comm, st);
-            if (r != ncclSuccess) t.status = COMPAR_E_NCCL;
-            cudaEventRecord(t.bc1, st);
-        }
-        for (auto &pr : t.panels) {
-            pr.start = get_event(c);
-            pr.stop = get_event(c);
-            cudaEventRecord(pr.start, st);
-            compar_status r;
-            if (!gemm) {
-                r = run_scale(c, d, pr.p, st);
-            } else {
-                const Variant &var = c->variants[t.variant];
-                if (var.target == COMPAR_TGT_USER) {
-                    r = var.fn(d, &pr.p, st, var.user, nullptr);
-                    c->stats.launches++;
-                } else {
-                    r = run_builtin(c, var.target, d, pr.p, st);
-                }
+        const Variant *var = gemm ? &c->variants[t.variant] : nullptr;
+        auto launch_on = [&](const compar_gemm_desc *dd, const compar_panel &pp, int sms) -> compar_status {
+            if (!gemm) return run_scale(c, dd, pp, st);
+            if (var->target == COMPAR_TGT_USER) {
+                c->stats.launches++;
+                return var->fn(dd, &pp, st, var->user, nullptr);
             }
-            if (r != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
-            cudaEventRecord(pr.stop, st);
+            return run_builtin(c, var->target, dd, pp, st, sms);
+        };
+        const bool bcast = t.world && gemm && (c->nranks > 1 || c->bcast_loopback);
+        if (!bcast) {
+            for (auto &pr : t.panels) {
+                pr.start = get_event(c);
+                pr.stop = get_event(c);
+                cudaEventRecord(pr.start, st);
+                if (launch_on(d, pr.p, 0) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+                cudaEventRecord(pr.stop, st);
+            }
+        } else {
+            compar_status r = world_pipeline(c, d, t, st, B, b_bytes, launch_on);
+            if (r != COMPAR_OK && t.status == COMPAR_OK) t.status = r;
         }
         if (host) {
             cudaMemcpyAsync(d->C_out, Cout, cout_bytes, cudaMemcpyDeviceToHost, st);

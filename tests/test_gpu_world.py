@@ -1,0 +1,89 @@
+"""World-mode (multi-GPU) path on one GPU (-m gpu): the N-slab broadcast pipeline is exercised in
+loopback (COMPAR_BCAST_LOOPBACK=1: the NCCL broadcast of each slab is emulated by a D2D copy on
+the comm stream, the GEMM consumes the received slabs exactly as a non-root rank does).  The
+result must be BITWISE equal to the plain single-launch call (every C element still sums its
+full K in order — DESIGN.md §6), for row-major and transposed B and ragged slab widths."""
+import os
+
+import numpy as np
+import pytest
+
+import gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from gen.device import device_matrix  # noqa: E402
+from oracle import gemm as og  # noqa: E402
+
+cm = pytest.importorskip("paper_2311_03543_b200.compar")
+
+
+@pytest.fixture(scope="module")
+def loop_ctx():
+    old = os.environ.get("COMPAR_BCAST_LOOPBACK")
+    os.environ["COMPAR_BCAST_LOOPBACK"] = "1"
+    ctxs = {}
+
+    def get(chunks):
+        if chunks not in ctxs:
+            ctxs[chunks] = cm.Compar(bcast_chunks=chunks)
+        return ctxs[chunks]
+    yield get
+    for c in ctxs.values():
+        c.terminate()
+    if old is None:
+        os.environ.pop("COMPAR_BCAST_LOOPBACK", None)
+    else:
+        os.environ["COMPAR_BCAST_LOOPBACK"] = old
+
+
+CASES = [("tc_bf16", 1000, 1000, 700, 0), ("tc_bf16", 1000, 1000, 700, 1), ("tc_bf16_2sm", 777, 2048, 512, 0),
+         ("tc_tf32", 300, 1280, 256, 0), ("tc_tf32_2sm", 512, 1030, 300, 1), ("simt_f32", 200, 600, 100, 0)]
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 4])
+@pytest.mark.parametrize("name,m,n,k,tb", CASES)
+def test_loopback_slab_pipeline_bitwise(loop_ctx, chunks, name, m, n, k, tb):
+    ctx = loop_ctx(chunks)
+    names = [v for v, _ in ctx.variants()]
+    bf = "bf16" in name
+    dt = "bf16" if bf else "f32"
+    compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else cm.COMPUTE_F32_STRICT)
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))
+    C0 = device_matrix(gen.TAG_C, m, n)
+    outs = []
+    for world in (0, 1):
+        Cd = C0.clone()
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, ldb=(k if tb else n), alpha=1.5, beta=0.5,
+                         in_dtype=cm.BF16 if bf else cm.F32, compute=compute, transB=tb, world=world,
+                         variant_hint=names.index(name))
+        r = ctx.run(d)
+        assert r.status == 0
+        if world:
+            assert r.total_ns >= r.ns
+        outs.append(Cd.cpu())
+    assert torch.equal(outs[0], outs[1])
+    if chunks == 4:   # and the pipeline result matches the oracle
+        got = outs[1].double().numpy()
+        ref = og.gemm(gen.matrix(gen.TAG_A, m, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt),
+                      gen.matrix(gen.TAG_C, m, n), alpha=1.5, beta=0.5, dtype=dt)
+        assert og.rel_fro(got, ref) <= (1e-5 if name == "simt_f32" else 5e-3)
+
+
+def test_loopback_world_host_memory(loop_ctx):
+    """World mode + HOST buffers (the e2e path of bench.py at N > 1) through the slab pipeline."""
+    ctx = loop_ctx(4)
+    m, n, k = 640, 1536, 512
+    A = gen.matrix(gen.TAG_A, m, k, dtype="bf16")
+    B = gen.matrix(gen.TAG_B, k, n, dtype="bf16")
+    C0 = gen.matrix(gen.TAG_C, m, n)
+    Ah = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Bh = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Ch = torch.from_numpy(C0.copy()).pin_memory()
+    d = cm.make_desc(m, n, k, A=Ah, B=Bh, C_in=Ch, C_out=Ch, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
+                     compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST, world=1)
+    ctx.run(d)
+    ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5, dtype="bf16")
+    assert og.rel_fro(Ch.double().numpy(), ref) <= 5e-3
