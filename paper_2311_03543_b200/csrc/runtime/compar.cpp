@@ -53,6 +53,7 @@ struct Variant {
 struct PanelRun {
     compar_panel p{};
     cudaEvent_t start = nullptr, stop = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sub;  // per-chunk kernel spans (host pipeline)
     int64_t virtual_ns = 0;
 };
 
@@ -98,6 +99,9 @@ struct Ctx {
     size_t bpacked_bytes = 0;
     bool bcast_loopback = false;  // 1 rank: emulate the broadcast with D2D copies (tests the slab path)
     int bcast_reserve_sms = 16;   // SMs left free for NCCL while a slab GEMM overlaps a broadcast
+    // host-memory pipeline
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    int host_chunks = 8;
 };
 
 std::mutex g_live_mu;
@@ -160,6 +164,11 @@ void release_task_events(Ctx *c, Task &t) {
     for (auto &p : t.panels) {
         put_event(c, p.start);
         put_event(c, p.stop);
+        for (auto &s : p.sub) {
+            put_event(c, s.first);
+            put_event(c, s.second);
+        }
+        p.sub.clear();
     }
     put_event(c, t.begin);
     put_event(c, t.end);
@@ -356,7 +365,14 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
         }
     }
     for (size_t i = 0; i < t.panels.size(); ++i) {
-        const int64_t ns = c->virt ? t.panels[i].virtual_ns : elapsed_ns(t.panels[i].start, t.panels[i].stop);
+        int64_t ns = 0;
+        if (c->virt) {
+            ns = t.panels[i].virtual_ns;
+        } else if (!t.panels[i].sub.empty()) {  // host pipeline: sum of the chunk kernels
+            for (auto &s : t.panels[i].sub) ns += elapsed_ns(s.first, s.second);
+        } else {
+            ns = elapsed_ns(t.panels[i].start, t.panels[i].stop);
+        }
         if (i < COMPAR_MAX_PANELS) rep->panel_ns[i] = ns;
         sample = std::max(sample, ns);
     }
@@ -537,6 +553,75 @@ compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStr
     return COMPAR_OK;
 }
 
+// ---------------------------------------------------------------- host-memory tasks: copy/compute overlap
+// mem = HOST (the end-to-end path): B goes up first, then A and C_in row chunks stream host->device
+// on one copy engine while the GEMM runs on the previous chunk and finished C chunks stream back on
+// the other copy engine.  Every C element is computed by exactly one chunk launch over its full K,
+// so the result equals the unchunked call bitwise.  The history sample is the sum of the chunk
+// kernel times.
+template <class F>
+compar_status host_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *A,
+                            const void *B, const float *Cin, float *Cout, size_t b_bytes, F &&launch_on) {
+    const int eb = elem_bytes(d->in_dtype);
+    const int64_t M = d->m, K = d->k, N = d->n;
+    const int64_t per = (M + c->host_chunks - 1) / c->host_chunks;
+    const int64_t rows = std::max<int64_t>(256, (per + 255) / 256 * 256);
+    const int nchunk = static_cast<int>((M + rows - 1) / rows);
+    cudaEvent_t ready = get_event(c);
+    t.extra.push_back(ready);
+    cudaEventRecord(ready, st);
+    cudaStreamWaitEvent(c->h2d_stream, ready, 0);
+    cudaStreamWaitEvent(c->d2h_stream, ready, 0);
+    cudaMemcpyAsync(const_cast<void *>(B), d->B, b_bytes, cudaMemcpyHostToDevice, c->h2d_stream);
+    c->stats.bytes_h2d += static_cast<int64_t>(b_bytes);
+    PanelRun &pr = t.panels[0];
+    pr.start = get_event(c);
+    pr.stop = get_event(c);
+    cudaEventRecord(pr.start, st);
+    compar_status r = COMPAR_OK;
+    for (int i = 0; i < nchunk && r == COMPAR_OK; ++i) {
+        const int64_t r0 = i * rows, ri = std::min(rows, M - r0);
+        const size_t a_off = static_cast<size_t>(r0) * d->lda * eb;
+        const size_t a_len = static_cast<size_t>(ri - 1) * d->lda * eb + static_cast<size_t>(K) * eb;
+        cudaMemcpyAsync(static_cast<char *>(const_cast<void *>(A)) + a_off, static_cast<const char *>(d->A) + a_off,
+                        a_len, cudaMemcpyHostToDevice, c->h2d_stream);
+        c->stats.bytes_h2d += static_cast<int64_t>(a_len);
+        if (d->beta != 0.f) {
+            const size_t c_len = static_cast<size_t>(ri - 1) * d->ldc_in * 4 + static_cast<size_t>(N) * 4;
+            cudaMemcpyAsync(const_cast<float *>(Cin) + r0 * d->ldc_in, d->C_in + r0 * d->ldc_in, c_len,
+                            cudaMemcpyHostToDevice, c->h2d_stream);
+            c->stats.bytes_h2d += static_cast<int64_t>(c_len);
+        }
+        cudaEvent_t in = get_event(c);
+        t.extra.push_back(in);
+        cudaEventRecord(in, c->h2d_stream);
+        cudaStreamWaitEvent(st, in, 0);
+        compar_panel pc = pr.p;
+        pc.row0 = r0;
+        pc.rows = ri;
+        pc.A = static_cast<const char *>(A) + a_off;
+        pc.C_in = Cin ? Cin + r0 * d->ldc_in : nullptr;
+        pc.C_out = Cout + r0 * d->ldc_out;
+        std::pair<cudaEvent_t, cudaEvent_t> span{get_event(c), get_event(c)};
+        cudaEventRecord(span.first, st);
+        r = launch_on(d, pc, 0);
+        cudaEventRecord(span.second, st);
+        pr.sub.push_back(span);
+        cudaStreamWaitEvent(c->d2h_stream, span.second, 0);
+        const size_t o_len = static_cast<size_t>(ri - 1) * d->ldc_out * 4 + static_cast<size_t>(N) * 4;
+        cudaMemcpyAsync(d->C_out + r0 * d->ldc_out, Cout + r0 * d->ldc_out, o_len, cudaMemcpyDeviceToHost,
+                        c->d2h_stream);
+        c->stats.bytes_d2h += static_cast<int64_t>(o_len);
+    }
+    cudaEventRecord(pr.stop, st);
+    cudaEvent_t out = get_event(c);
+    t.extra.push_back(out);
+    cudaEventRecord(out, c->d2h_stream);
+    cudaStreamWaitEvent(st, out, 0);                // the task ends when C is back on the host
+    if (r != COMPAR_OK) return COMPAR_E_TASK_FAILED;
+    return COMPAR_OK;
+}
+
 }  // namespace
 }  // namespace compar
 
@@ -620,6 +705,9 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
         c->bcast_loopback = env_int("COMPAR_BCAST_LOOPBACK", 0) != 0;
         c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", 16);
+        cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking);
+        c->host_chunks = env_int("COMPAR_HOST_CHUNKS", 8);
     }
     {
         std::lock_guard<std::mutex> lk(g_live_mu);
@@ -668,9 +756,11 @@ compar_status compar_terminate(void *ctx) {
             if (b) cudaFree(b);
         if (c->breplica) cudaFree(c->breplica);
         if (c->bpacked) cudaFree(c->bpacked);
-        if (c->comm_stream) {
-            cudaStreamSynchronize(c->comm_stream);
-            cudaStreamDestroy(c->comm_stream);
+        for (cudaStream_t s : {c->comm_stream, c->h2d_stream, c->d2h_stream}) {
+            if (s) {
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+            }
         }
         if (c->red_buf) cudaFree(c->red_buf);
         for (auto e : c->pool) cudaEventDestroy(e);
@@ -870,7 +960,8 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
         t.begin = get_event(c);
         t.end = get_event(c);
         cudaEventRecord(t.begin, st);
-        if (host) {
+        const bool pipelined = host && gemm && !t.world && t.panels.size() == 1 && c->host_chunks > 1 && d->m >= 512;
+        if (host && !pipelined) {
             if (a_bytes) cudaMemcpyAsync(const_cast<void *>(A), d->A, a_bytes, cudaMemcpyHostToDevice, st);
             if (b_bytes && root_b) cudaMemcpyAsync(const_cast<void *>(B), d->B, b_bytes, cudaMemcpyHostToDevice, st);
             if (cin_bytes) cudaMemcpyAsync(const_cast<float *>(Cin), d->C_in, cin_bytes, cudaMemcpyHostToDevice, st);
@@ -886,7 +977,10 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             return run_builtin(c, var->target, dd, pp, st, sms);
         };
         const bool bcast = t.world && gemm && (c->nranks > 1 || c->bcast_loopback);
-        if (!bcast) {
+        if (pipelined) {
+            compar_status r = host_pipeline(c, d, t, st, A, B, Cin, Cout, b_bytes, launch_on);
+            if (r != COMPAR_OK && t.status == COMPAR_OK) t.status = r;
+        } else if (!bcast) {
             for (auto &pr : t.panels) {
                 pr.start = get_event(c);
                 pr.stop = get_event(c);
@@ -898,7 +992,7 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             compar_status r = world_pipeline(c, d, t, st, B, b_bytes, launch_on);
             if (r != COMPAR_OK && t.status == COMPAR_OK) t.status = r;
         }
-        if (host) {
+        if (host && !pipelined) {
             cudaMemcpyAsync(d->C_out, Cout, cout_bytes, cudaMemcpyDeviceToHost, st);
             c->stats.bytes_d2h += static_cast<int64_t>(cout_bytes);
         }

@@ -179,6 +179,33 @@ def test_host_memory_mode_matches_device(ctx):
     assert og.rel_fro(Ch.numpy(), ref) <= 5e-3
 
 
+@pytest.mark.parametrize("name", ["tc_bf16", "tc_tf32_2sm", "simt_f32"])
+def test_host_pipeline_ragged_separate_cin(ctx, name):
+    """mem = HOST with row chunks (copy/compute overlap), ragged m, C_in != C_out, padded ld."""
+    dtype_id, compute, tol = VARIANTS[name]
+    dt = "bf16" if dtype_id == cm.BF16 else "f32"
+    m, n, k = 1000, 264, 136
+    A = gen.matrix(gen.TAG_A, m, k, dtype=dt)
+    B = gen.matrix(gen.TAG_B, k, n, dtype=dt)
+    C0 = gen.matrix(gen.TAG_C, m, n)
+
+    def host(x, ld):
+        buf = np.zeros((x.shape[0], ld), dtype=x.dtype)
+        buf[:, :x.shape[1]] = x
+        t = torch.from_numpy(buf.view(np.int16)).view(torch.bfloat16) if x.dtype == np.uint16 else torch.from_numpy(buf)
+        return t.pin_memory()
+    Ah, Bh, Cih = host(A, k + 8), host(B, n + 8), host(C0, n + 4)
+    Coh = torch.zeros((m, n + 12), dtype=torch.float32).pin_memory()
+    d = cm.make_desc(m, n, k, A=Ah, B=Bh, C_in=Cih, C_out=Coh, lda=k + 8, ldb=n + 8, ldc_in=n + 4, ldc_out=n + 12,
+                     alpha=1.5, beta=0.5, in_dtype=dtype_id, compute=compute, mem=cm.MEM_HOST,
+                     variant_hint=vid(ctx, name))
+    r = ctx.run(d)
+    assert r.status == 0
+    ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5, dtype=dt)
+    assert og.rel_fro(Coh[:, :n].double().numpy(), ref) <= tol
+    assert torch.all(Coh[:, n:] == 0)
+
+
 def test_world_size_one_nccl(ctx):
     """SPMD path with a 1-rank NCCL communicator: world = 1 equals the plain call."""
     c = cm.Compar()

@@ -38,7 +38,7 @@ def loop_ctx():
         os.environ["COMPAR_BCAST_LOOPBACK"] = old
 
 
-CASES = [("tc_bf16", 1000, 1000, 700, 0), ("tc_bf16", 1000, 1000, 704, 1), ("tc_bf16_2sm", 777, 2048, 512, 0),
+CASES = [("tc_bf16", 1000, 1000, 704, 0), ("tc_bf16", 1000, 1000, 704, 1), ("tc_bf16_2sm", 777, 2048, 512, 0),
          ("tc_tf32", 300, 1280, 256, 0), ("tc_tf32_2sm", 512, 1030, 300, 1), ("simt_f32", 200, 600, 100, 0)]
 
 
