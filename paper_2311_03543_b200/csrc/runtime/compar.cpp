@@ -608,10 +608,10 @@ compar_status host_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStre
         cudaEventRecord(span.second, st);
         pr.sub.push_back(span);
         cudaStreamWaitEvent(c->d2h_stream, span.second, 0);
-        const size_t o_len = static_cast<size_t>(ri - 1) * d->ldc_out * 4 + static_cast<size_t>(N) * 4;
-        cudaMemcpyAsync(d->C_out + r0 * d->ldc_out, Cout + r0 * d->ldc_out, o_len, cudaMemcpyDeviceToHost,
-                        c->d2h_stream);
-        c->stats.bytes_d2h += static_cast<int64_t>(o_len);
+        // 2-D copy: only the n valid columns of each row go back (the ld gap on the host is untouched)
+        cudaMemcpy2DAsync(d->C_out + r0 * d->ldc_out, d->ldc_out * 4, Cout + r0 * d->ldc_out, d->ldc_out * 4, N * 4, ri,
+                          cudaMemcpyDeviceToHost, c->d2h_stream);
+        c->stats.bytes_d2h += static_cast<int64_t>(ri * N * 4);
     }
     cudaEventRecord(pr.stop, st);
     cudaEvent_t out = get_event(c);
@@ -992,9 +992,10 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             compar_status r = world_pipeline(c, d, t, st, B, b_bytes, launch_on);
             if (r != COMPAR_OK && t.status == COMPAR_OK) t.status = r;
         }
-        if (host && !pipelined) {
-            cudaMemcpyAsync(d->C_out, Cout, cout_bytes, cudaMemcpyDeviceToHost, st);
-            c->stats.bytes_d2h += static_cast<int64_t>(cout_bytes);
+        if (host && !pipelined && mloc > 0) {
+            cudaMemcpy2DAsync(d->C_out, d->ldc_out * 4, Cout, d->ldc_out * 4, d->n * 4, mloc, cudaMemcpyDeviceToHost, st);
+            c->stats.bytes_d2h += static_cast<int64_t>(mloc * d->n * 4);
+            (void)cout_bytes;
         }
         cudaEventRecord(t.end, st);
     }
