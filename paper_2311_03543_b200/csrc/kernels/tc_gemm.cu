@@ -21,6 +21,7 @@
 // Edges: TMA zero-fills out-of-bounds boxes; the epilogue predicates rows/cols.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -71,13 +72,15 @@ struct TcParams {
     int m_blocks, n_blocks, num_kb;
     int cvec;
     int *sched;  // {next, done}: zero on entry, re-zeroed by the last CTA
+    int group_m;
+    int serp;    // 1: alternate the K direction between consecutive waves (L2 reuse at wave seams)
 };
 
-__device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int &mb, int &nb) {
-    const int per_group = kGroupM * n_blocks;
+__device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
+    const int per_group = group * n_blocks;
     const int g = t / per_group;
-    const int first_m = g * kGroupM;
-    const int gm = min(m_blocks - first_m, kGroupM);
+    const int first_m = g * group;
+    const int gm = min(m_blocks - first_m, group);
     const int r = t - g * per_group;
     mb = first_m + r % gm;
     nb = r / gm;
@@ -147,8 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_arrive(rfull0 + 8 * slot);
                 if (t >= num_tiles) break;
                 int mb, nb;
-                tile_coords(t, p.m_blocks, p.n_blocks, mb, nb);
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+                const bool rev = p.serp && ((t / static_cast<int>(gridDim.x)) & 1);
+                for (int it = 0; it < p.num_kb; ++it) {
+                    const int kb = rev ? p.num_kb - 1 - it : it;
                     ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int t = next_tile(local);
             if (t >= num_tiles) break;
             int mb, nb;
-            tile_coords(t, p.m_blocks, p.n_blocks, mb, nb);
+            tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
@@ -302,6 +307,16 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
+    static const int group_env = [] {
+        const char *s = std::getenv("COMPAR_TC1_GROUP");
+        return s ? std::atoi(s) : 0;
+    }();
+    static const int serp_env = [] {
+        const char *s = std::getenv("COMPAR_TC_SERP");
+        return s ? std::atoi(s) : 0;
+    }();
+    p.group_m = group_env > 0 ? group_env : kGroupM;
+    p.serp = serp_env;
     const int tiles = p.m_blocks * p.n_blocks;
     const int grid = tiles < g.num_sms ? tiles : g.num_sms;
     tc_gemm_kernel<kBF16, kTransB><<<grid, kThreads, C::SMEM, g.stream>>>(ta, tb, p);
