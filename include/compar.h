@@ -72,7 +72,9 @@ typedef enum {
     COMPAR_TGT_TC_BF16 = 3,     /* built-in (c): tcgen05/TMEM tensor cores, BF16 in, FP32 acc    */
     COMPAR_TGT_USER = 4,
     COMPAR_TGT_TC2_TF32 = 5,    /* built-in (c), CTA-pair form: tcgen05.mma.cta_group::2, 256x256 tiles */
-    COMPAR_TGT_TC2_BF16 = 6     /* built-in (c), CTA-pair form, BF16                                    */
+    COMPAR_TGT_TC2_BF16 = 6,    /* built-in (c), CTA-pair form, BF16                                    */
+    COMPAR_TGT_TCW_TF32 = 7,    /* built-in (c), wide CTA-pair form: 256x512 pair tile, 2 accumulators  */
+    COMPAR_TGT_TCW_BF16 = 8     /* built-in (c), wide CTA-pair form, BF16                               */
 } compar_target;
 
 /* Why a task ran the variant it ran. */

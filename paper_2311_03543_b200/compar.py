@@ -20,7 +20,8 @@ STATUS_NAMES = ["OK", "E_INVALID", "E_STATE", "E_DUPLICATE", "E_NO_VARIANT", "E_
                 "E_UNKNOWN_TASK", "E_IO", "E_FORMAT", "E_OOM"]
 F32, BF16 = 0, 1
 COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
-TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER, TGT_TC2_TF32, TGT_TC2_BF16 = 0, 1, 2, 3, 4, 5, 6
+TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER, TGT_TC2_TF32, TGT_TC2_BF16, TGT_TCW_TF32, TGT_TCW_BF16 = \
+    0, 1, 2, 3, 4, 5, 6, 7, 8
 MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP = 0, 1, 2, 3, 4, 5
 MEM_DEVICE, MEM_HOST = 0, 1
 TASK_ALL = (1 << 64) - 1

@@ -24,6 +24,7 @@ cudaError_t launch_simt_f32(const GemmLaunch &g);            // variant (a)
 cudaError_t launch_tma_f32(const GemmLaunch &g);             // variant (b)
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16);  // variant (c): tcgen05 TF32 / BF16
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16);  // variant (c), CTA-pair (cta_group::2)
+cudaError_t launch_tc_gemm_2sm_wide(const GemmLaunch &g, bool bf16);  // variant (c), wide CTA-pair 256x512
 cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha == 0: C_out = beta*C_in
 cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
 cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)

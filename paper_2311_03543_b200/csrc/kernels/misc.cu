@@ -11,6 +11,7 @@ cudaError_t preload_tc_kernels();
 cudaError_t preload_tma_kernels();
 cudaError_t preload_simt_kernels();
 cudaError_t preload_tc2_kernels();
+cudaError_t preload_tcw_kernels();
 
 namespace {
 
@@ -56,6 +57,7 @@ cudaError_t preload_kernels() {
     if (e == cudaSuccess) e = preload_tma_kernels();
     if (e == cudaSuccess) e = preload_simt_kernels();
     if (e == cudaSuccess) e = preload_tc2_kernels();
+    if (e == cudaSuccess) e = preload_tcw_kernels();
     return e;
 }
 

@@ -25,7 +25,9 @@ VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tc_tf32": (cm.F32, cm.COMPUTE_TF32, 5e-3),
             "tc_bf16": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
             "tc_tf32_2sm": (cm.F32, cm.COMPUTE_TF32, 5e-3),
-            "tc_bf16_2sm": (cm.BF16, cm.COMPUTE_BF16, 5e-3)}
+            "tc_bf16_2sm": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
+            "tc_tf32_2sm_w": (cm.F32, cm.COMPUTE_TF32, 5e-3),
+            "tc_bf16_2sm_w": (cm.BF16, cm.COMPUTE_BF16, 5e-3)}
 
 SHAPES = [(1, 1, 1), (7, 13, 5), (64, 64, 64), (65, 127, 129), (129, 257, 70), (128, 256, 64),
           (300, 520, 1000), (1000, 777, 333), (257, 1, 100), (1, 300, 4097)]
@@ -227,6 +229,8 @@ def test_world_size_one_nccl(ctx):
 @pytest.mark.parametrize("name,shape", [("tc_bf16", (8192, 8192, 8192)), ("tc_tf32", (8192, 8192, 8192)),
                                         ("tc_bf16_2sm", (8192, 8192, 8192)), ("tc_tf32_2sm", (8192, 8192, 8192)),
                                         ("tc_bf16_2sm", (32768, 32768, 32768)), ("tc_bf16_2sm", (65536, 256, 4096)),
+                                        ("tc_bf16_2sm_w", (32768, 32768, 32768)), ("tc_tf32_2sm_w", (8192, 8192, 8192)),
+                                        ("tc_bf16_2sm_w", (65536, 256, 4096)),
                                         ("tc_bf16", (65536, 256, 4096)), ("tc_tf32", (65536, 256, 4096)),
                                         ("tc_bf16", (32768, 32768, 32768))])
 def test_full_size_sampled(ctx, name, shape):

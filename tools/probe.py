@@ -33,7 +33,8 @@ def time_variant(ctx, name, m, n, k, reps=10, transB=0):
 
 if __name__ == "__main__":
     ctx = cm.Compar()
-    cases = [("tc_bf16_2sm", 8192, 8192, 8192), ("tc_bf16_2sm", 32768, 32768, 32768), ("tc_tf32_2sm", 8192, 8192, 8192),
+    cases = [("tc_bf16_2sm_w", 8192, 8192, 8192), ("tc_bf16_2sm_w", 32768, 32768, 32768), ("tc_bf16_2sm_w", 65536, 256, 4096),
+             ("tc_tf32_2sm_w", 8192, 8192, 8192), ("tc_bf16_2sm", 8192, 8192, 8192), ("tc_bf16_2sm", 32768, 32768, 32768), ("tc_tf32_2sm", 8192, 8192, 8192),
              ("tc_bf16_2sm", 65536, 256, 4096), ("tc_bf16_2sm", 4096, 4096, 4096), ("tc_bf16_2sm", 1024, 1024, 1024),
              ("tc_bf16", 8192, 8192, 8192), ("tc_bf16", 8192, 8192, 8192, 1), ("tc_tf32", 8192, 8192, 8192),
              ("tc_bf16", 65536, 256, 4096), ("tc_bf16", 4096, 4096, 4096), ("tma_f32", 4096, 4096, 4096),

@@ -50,7 +50,7 @@ if __name__ == "__main__":
         Cd = device_matrix(gen.TAG_C, s, s)
         flops = 2.0 * s ** 3
         res = {}
-        for v in ("tc_bf16", "tc_bf16_2sm"):
+        for v in ("tc_bf16", "tc_bf16_2sm", "tc_bf16_2sm_w"):
             d = cm.make_desc(s, s, s, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
                              compute=cm.COMPUTE_BF16, variant_hint=names.index(v))
             res[v] = sustained(lambda: ctx.submit(d), flops, secs)
