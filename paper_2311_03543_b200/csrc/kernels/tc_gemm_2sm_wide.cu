@@ -48,7 +48,7 @@ struct TcWCfg {
     static constexpr bool B_BASE32 = !kBF16 && !kTransB;
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 512;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 512 + kEpiWarpsW * 4096;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
                                       ((kTransB ? 0u : 1u) << 16) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
 };
@@ -98,6 +98,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     const uint32_t rempty0 = rfull0 + 8 * kRingW;
     const uint32_t ring0 = rempty0 + 8 * kRingW;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + 480);
+    float *epi_buf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + 512);  // 8 x 4 KB
     const uint32_t smem0 = ptx::smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -244,61 +245,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             if (t >= num_tiles) break;
             int mb, nb;
             tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
-            const int64_t row = static_cast<int64_t>(mb) * 2 * C::BM + rank * C::BM + q * 32 + lane;
-            const bool row_ok = row < p.m;
-            float *crow = p.C_out + row * p.ldc_out;
-            const float *cin = p.C_in + row * p.ldc_in;
+            // The warp owns rows [row_base, row_base + 32) x accumulator h (256 columns).  Each 32x32
+            // chunk goes TMEM -> registers (thread = row) -> swizzled smem -> registers (thread =
+            // column), so C_in loads and C_out stores are whole 128-byte rows per warp instruction.
+            const int64_t row_base = static_cast<int64_t>(mb) * 2 * C::BM + rank * C::BM + q * 32;
             const int64_t colh = static_cast<int64_t>(nb) * C::BN + 256 * h;
-            const bool fast = p.cvec && row_ok && colh + 256 <= p.n;
             const bool ldc = p.beta != 0.f;
-            float4 ci[8];
-            if (fast && ldc) {
-#pragma unroll
-                for (int v = 0; v < 8; ++v) ci[v] = *reinterpret_cast<const float4 *>(cin + colh + 4 * v);
-            }
+            float *buf = epi_buf + (warp - 2) * 1024;
             ptx::mbar_wait(tfull, local & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < 8; ++c) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 256 * h + c * 32, r);
-                ptx::tmem_ld_wait();
-                const int64_t col0 = colh + c * 32;
-                if (fast) {
-                    float4 nx[8];
-                    if (ldc && c + 1 < 8) {
+                const int64_t col = colh + c * 32 + lane;
+                const bool col_ok = col < p.n;
+                float cv[32];
+                if (ldc) {  // 32 coalesced row loads in flight while the TMEM load completes
 #pragma unroll
-                        for (int v = 0; v < 8; ++v) nx[v] = *reinterpret_cast<const float4 *>(cin + col0 + 32 + 4 * v);
-                    }
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        float4 o;
-                        o.x = p.alpha * __uint_as_float(r[4 * v + 0]);
-                        o.y = p.alpha * __uint_as_float(r[4 * v + 1]);
-                        o.z = p.alpha * __uint_as_float(r[4 * v + 2]);
-                        o.w = p.alpha * __uint_as_float(r[4 * v + 3]);
-                        if (ldc) {
-                            o.x = fmaf(p.beta, ci[v].x, o.x);
-                            o.y = fmaf(p.beta, ci[v].y, o.y);
-                            o.z = fmaf(p.beta, ci[v].z, o.z);
-                            o.w = fmaf(p.beta, ci[v].w, o.w);
-                        }
-                        *reinterpret_cast<float4 *>(crow + col0 + 4 * v) = o;
-                    }
-                    if (ldc && c + 1 < 8) {
-#pragma unroll
-                        for (int v = 0; v < 8; ++v) ci[v] = nx[v];
-                    }
-                } else if (row_ok) {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        if (col0 + e < p.n) {
-                            float o = p.alpha * __uint_as_float(r[e]);
-                            if (ldc) o = fmaf(p.beta, cin[col0 + e], o);
-                            crow[col0 + e] = o;
-                        }
+                    for (int rr = 0; rr < 32; ++rr) {
+                        const int64_t row = row_base + rr;
+                        cv[rr] = (row < p.m && col_ok) ? p.C_in[row * p.ldc_in + col] : 0.f;
                     }
                 }
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                    *reinterpret_cast<float4 *>(buf + lane * 32 + ((g ^ (lane & 7)) << 2)) =
+                        make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                    __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
+                __syncwarp();
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int64_t row = row_base + rr;
+                    const float v = buf[rr * 32 + ((((lane >> 2) ^ (rr & 7)) << 2) | (lane & 3))];
+                    float o = p.alpha * v;
+                    if (ldc) o = fmaf(p.beta, cv[rr], o);
+                    if (row < p.m && col_ok) p.C_out[row * p.ldc_out + col] = o;
+                }
+                __syncwarp();
             }
             ptx::tc_fence_before();
             __syncwarp();
