@@ -6,14 +6,18 @@
 // [256,512)) that share the A tile, so per SM the L2 -> SMEM traffic per FLOP is 3/4 of the
 // 256 x 256 pair tile and 1/2 of the 1-SM 128 x 256 tile (on a power-capped B200 the
 // bytes moved per FLOP set the clock).  The two accumulators fill all 512 TMEM columns, so a
-// tile's epilogue is not overlapped with the next tile's MMAs; instead the producer keeps
-// prefetching the next tile's K-blocks during the epilogue and 8 epilogue warps (two per TMEM lane
-// quarter, one per accumulator) drain TMEM with the C_in loads software-pipelined one chunk ahead.
+// tile's epilogue is not overlapped with the next tile's MMAs; the producer keeps prefetching the
+// next tile's K-blocks meanwhile, and the epilogue itself is asynchronous bulk traffic:
+//   per 32 x 32 chunk: TMA load of C_in (issued two chunks ahead) -> tcgen05.ld -> alpha*acc +
+//   beta*C_in in registers -> st.shared (SWIZZLE_128B layout) -> TMA store of C_out,
+// double-buffered per epilogue warp, so C moves as full 128-byte lines and out-of-range rows /
+// columns are clipped by the TMA unit (no predication).
 //
 // B column split (cta_group::2 takes N/2 columns of B from each CTA, at the same smem offset):
 // CTA r holds, per accumulator h, pair columns [256 h + 128 r, +128) as 128/ATOM MN-atoms.
 // Synchronisation as in tc_gemm_2sm.cu, with one accumulator set: tfull (leader commit multicast),
-// tempty (leader only, count 16 = 8 epilogue warps x 2 CTAs).
+// tempty (leader only, count 8 = 4 epilogue warps x 2 CTAs); cbar[w][b]: C_in chunk landed.
+// Eligibility adds the TMA rule for C: 16-byte aligned C_in/C_out, ldc * 4 % 16 == 0.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -26,7 +30,7 @@
 namespace compar {
 namespace {
 
-constexpr int kEpiWarpsW = 8;
+constexpr int kEpiWarpsW = 4;
 constexpr int kThreadsW = 64 + 32 * kEpiWarpsW;
 constexpr int kGroupW = 4;
 constexpr int kRingW = 4;
@@ -48,7 +52,8 @@ struct TcWCfg {
     static constexpr bool B_BASE32 = !kBF16 && !kTransB;
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 512 + kEpiWarpsW * 4096;
+    static constexpr uint32_t EPI_BYTES = kEpiWarpsW * 2 * 4096;   // 2 x (32 x 32 fp32) per epilogue warp
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
                                       ((kTransB ? 0u : 1u) << 16) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
 };
@@ -56,13 +61,8 @@ struct TcWCfg {
 struct TcWParams {
     int64_t m, n, k;
     float alpha, beta;
-    const float *C_in;
-    int64_t ldc_in;
-    float *C_out;
-    int64_t ldc_out;
     int m_blocks, n_blocks, num_kb;  // 256-row x 512-column pair tiles
     int group_m;
-    int cvec;
     int *sched;
 };
 
@@ -85,21 +85,23 @@ __device__ __forceinline__ uint32_t peer_addr_w(uint32_t local, uint32_t peer_ra
 template <bool kBF16, bool kTransB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     tc_gemm_2sm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                            const __grid_constant__ CUtensorMap tmCo, const __grid_constant__ CUtensorMap tmCi,
                             TcWParams p) {
     using C = TcWCfg<kBF16, kTransB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+    const uint32_t smem0 = ptx::smem_u32(smem);
+    const uint32_t epi0 = smem0 + C::STAGES * C::STAGE_BYTES;          // 1024-aligned chunk buffers
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
     const uint32_t full0 = ptx::smem_u32(bars);
     const uint32_t empty0 = full0 + 8 * C::STAGES;
     const uint32_t tfull = empty0 + 8 * C::STAGES;
     const uint32_t tempty = tfull + 8;
     const uint32_t rfull0 = tempty + 8;
     const uint32_t rempty0 = rfull0 + 8 * kRingW;
-    const uint32_t ring0 = rempty0 + 8 * kRingW;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + 480);
-    float *epi_buf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + 512);  // 8 x 4 KB
-    const uint32_t smem0 = ptx::smem_u32(smem);
+    const uint32_t cbar0 = rempty0 + 8 * kRingW;                        // 2 per epilogue warp
+    const uint32_t ring0 = cbar0 + 16 * kEpiWarpsW;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -108,6 +110,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmCo);
+        ptx::prefetch_tmap(&tmCi);
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(full0 + 8 * s, 1);
             ptx::mbar_init(empty0 + 8 * s, 1);
@@ -118,6 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             ptx::mbar_init(rfull0 + 8 * r, 1);
             ptx::mbar_init(rempty0 + 8 * r, kConsumers);
         }
+        for (int b = 0; b < 2 * kEpiWarpsW; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm<512>(ptx::smem_u32(tmem_slot));
@@ -236,59 +241,86 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 __syncwarp();
             }
         }
-    } else {  // ---------------- epilogue warps 2..9: (lane quarter q, accumulator h)
+    } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, 16 chunks of 32 x 32
         const int q = warp & 3;
-        const int h = (warp - 2) >> 2;
+        const int ew = warp - 2;
+        const uint32_t buf[2] = {epi0 + (2 * ew) * 4096, epi0 + (2 * ew + 1) * 4096};
+        const uint32_t cbar[2] = {cbar0 + 16 * ew, cbar0 + 16 * ew + 8};
+        uint32_t loads[2] = {0, 0};                       // C_in loads issued per buffer (parity)
         const uint32_t tempty_leader = ptx::leader_addr(tempty);
+        const bool ldc = p.beta != 0.f;
+        const uint32_t swz = lane * 128;                  // this thread's row in a chunk buffer
         for (int local = 0;; ++local) {
             const int t = next_tile(local);
             if (t >= num_tiles) break;
             int mb, nb;
             tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
-            // The warp owns rows [row_base, row_base + 32) x accumulator h (256 columns).  Each 32x32
-            // chunk goes TMEM -> registers (thread = row) -> swizzled smem -> registers (thread =
-            // column), so C_in loads and C_out stores are whole 128-byte rows per warp instruction.
-            const int64_t row_base = static_cast<int64_t>(mb) * 2 * C::BM + rank * C::BM + q * 32;
-            const int64_t colh = static_cast<int64_t>(nb) * C::BN + 256 * h;
-            const bool ldc = p.beta != 0.f;
-            float *buf = epi_buf + (warp - 2) * 1024;
+            const int32_t row_base = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM + q * 32;
+            const int32_t col_base = nb * C::BN;
+            auto chunk_col = [&](int idx) { return col_base + 256 * (idx >> 3) + 32 * (idx & 7); };
+            if (lane == 0) {
+                ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
+                if (ldc) {
+                    for (int b = 0; b < 2; ++b) {
+                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
+                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], chunk_col(b), row_base);
+                    }
+                }
+            }
+            if (ldc) ++loads[0], ++loads[1];              // warp-uniform phase bookkeeping
+            __syncwarp();
             ptx::mbar_wait(tfull, local & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < 8; ++c) {
+            for (int idx = 0; idx < 16; ++idx) {
+                const int b = idx & 1;
                 uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 256 * h + c * 32, r);
-                const int64_t col = colh + c * 32 + lane;
-                const bool col_ok = col < p.n;
-                float cv[32];
-                if (ldc) {  // 32 coalesced row loads in flight while the TMEM load completes
+                ptx::tmem_ld_32x32b_x32(
+                    tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 256 * (idx >> 3) + 32 * (idx & 7), r);
+                ptx::tmem_ld_wait();
+                if (ldc) {
+                    ptx::mbar_wait(cbar[b], (loads[b] - 1) & 1);
+                } else if (idx >= 2) {
+                    if (lane == 0) ptx::bulk_wait_read<1>();   // store idx-2 has left buf[b]
+                    __syncwarp();
+                }
 #pragma unroll
-                    for (int rr = 0; rr < 32; ++rr) {
-                        const int64_t row = row_base + rr;
-                        cv[rr] = (row < p.m && col_ok) ? p.C_in[row * p.ldc_in + col] : 0.f;
+                for (int g = 0; g < 8; ++g) {
+                    const uint32_t a = buf[b] + swz + ((g ^ (lane & 7)) << 4);
+                    float4 o;
+                    o.x = p.alpha * __uint_as_float(r[4 * g + 0]);
+                    o.y = p.alpha * __uint_as_float(r[4 * g + 1]);
+                    o.z = p.alpha * __uint_as_float(r[4 * g + 2]);
+                    o.w = p.alpha * __uint_as_float(r[4 * g + 3]);
+                    if (ldc) {
+                        const float4 ci = ptx::lds128(a);
+                        o.x = fmaf(p.beta, ci.x, o.x);
+                        o.y = fmaf(p.beta, ci.y, o.y);
+                        o.z = fmaf(p.beta, ci.z, o.z);
+                        o.w = fmaf(p.beta, ci.w, o.w);
+                    }
+                    ptx::sts128(a, o);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tmCo, buf[b], chunk_col(idx), row_base);
+                    ptx::bulk_commit();
+                    if (ldc && idx + 2 < 16) {            // refill buf[b] with chunk idx+2 once it is read
+                        ptx::bulk_wait_read<0>();
+                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
+                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], chunk_col(idx + 2), row_base);
                     }
                 }
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int g = 0; g < 8; ++g)
-                    *reinterpret_cast<float4 *>(buf + lane * 32 + ((g ^ (lane & 7)) << 2)) =
-                        make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
-                                    __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
-                __syncwarp();
-#pragma unroll
-                for (int rr = 0; rr < 32; ++rr) {
-                    const int64_t row = row_base + rr;
-                    const float v = buf[rr * 32 + ((((lane >> 2) ^ (rr & 7)) << 2) | (lane & 3))];
-                    float o = p.alpha * v;
-                    if (ldc) o = fmaf(p.beta, cv[rr], o);
-                    if (row < p.m && col_ok) p.C_out[row * p.ldc_out + col] = o;
-                }
+                if (ldc && idx + 2 < 16) ++loads[b];
                 __syncwarp();
             }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
         }
+        if (lane == 0) ptx::bulk_wait<0>();               // all C stores complete before exit
+        __syncwarp();
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -308,16 +340,21 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, tco, tci;
     if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, Swz::B128)) return cudaErrorInvalidValue;
     bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, 128, C::BK, Swz::B128)
                       : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N,
                                     C::B_BASE32 ? Swz::B128_32B : Swz::B128);
     if (!ok) return cudaErrorInvalidValue;
+    if (!get_tmap_2d(&tco, g.C_out, 4, g.m, g.n, g.ldc_out, 32, 32, Swz::B128)) return cudaErrorInvalidValue;
+    if (g.beta != 0.f) {
+        if (!get_tmap_2d(&tci, g.C_in, 4, g.m, g.n, g.ldc_in, 32, 32, Swz::B128)) return cudaErrorInvalidValue;
+    } else {
+        tci = tco;  // unused
+    }
     TcWParams p;
     p.m = g.m, p.n = g.n, p.k = g.k;
     p.alpha = g.alpha, p.beta = g.beta;
-    p.C_in = g.C_in, p.ldc_in = g.ldc_in, p.C_out = g.C_out, p.ldc_out = g.ldc_out;
     p.m_blocks = static_cast<int>((g.m + 2 * C::BM - 1) / (2 * C::BM));
     p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
@@ -326,14 +363,12 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
         return s ? std::atoi(s) : 0;
     }();
     p.group_m = group_env > 0 ? group_env : kGroupW;
-    p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
-             (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
     const int max_clusters = g.num_sms / 2;
     const int clusters = tiles < max_clusters ? tiles : max_clusters;
-    tc_gemm_2sm_wide_kernel<kBF16, kTransB><<<2 * clusters, kThreadsW, C::SMEM, g.stream>>>(ta, tb, p);
+    tc_gemm_2sm_wide_kernel<kBF16, kTransB><<<2 * clusters, kThreadsW, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     return cudaGetLastError();
 }
 

@@ -255,10 +255,15 @@ bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, co
     const int eb = (t == COMPAR_TGT_TC_BF16 || t == COMPAR_TGT_TC2_BF16 || t == COMPAR_TGT_TCW_BF16) ? 2 : 4;
     if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;
     if ((d->lda * eb) % 16 != 0 || (d->ldb * eb) % 16 != 0) return false;
+    // the wide variant also moves C with TMA (loads of C_in, stores of C_out)
+    const bool tma_c = t == COMPAR_TGT_TCW_TF32 || t == COMPAR_TGT_TCW_BF16;
+    if (tma_c && ((d->ldc_out * 4) % 16 != 0 || (d->beta != 0.f && (d->ldc_in * 4) % 16 != 0))) return false;
     if (c->virt) return true;
     for (const auto &p : plan.panels) {
         if (reinterpret_cast<uintptr_t>(p.A) % 16 != 0) return false;
         if (p.B && reinterpret_cast<uintptr_t>(p.B) % 16 != 0) return false;
+        if (tma_c && reinterpret_cast<uintptr_t>(p.C_out) % 16 != 0) return false;
+        if (tma_c && d->beta != 0.f && reinterpret_cast<uintptr_t>(p.C_in) % 16 != 0) return false;
     }
     return true;
 }
