@@ -123,9 +123,12 @@ typedef struct {
     const void *B;  int64_t ldb;
     const float *C_in;  int64_t ldc_in;   /* may alias C_out exactly (in place)                 */
     float *C_out;       int64_t ldc_out;
-    compar_mem mem;             /* HOST: A, B, C_in, C_out are host pointers (pinned for speed);
-                                   the library stages them through its own device buffers and
-                                   copies C_out back before the task's stop event.               */
+    compar_mem mem;             /* HOST: A, B, C_in, C_out are host pointers (pinned for overlap);
+                                   the library stages them through its own device buffers: B
+                                   first, then A / C_in row chunks up and C_out chunks down on two
+                                   copy streams while the GEMM runs on the previous chunk; only the
+                                   n valid columns of each C_out row are written on the host.  The
+                                   task's end event follows the last D2H copy.                   */
     void *stream;               /* cudaStream_t to order the task on; NULL: the CUDA legacy default
                                    stream (ordered after the caller's default-stream work)        */
     int panels;                 /* loopback row panels on this device (1..COMPAR_MAX_PANELS);
@@ -133,9 +136,12 @@ typedef struct {
     int world;                  /* 1: SPMD row-panel split across the ranks of compar_comm_init.
                                    A and C_* then point at THIS rank's panel (rows
                                    [o_r, o_{r+1}) of compar_partition_rows(m, nranks)), B is read
-                                   on rank 0 and broadcast with NCCL to the other ranks.         */
-    void *B_replica;            /* world mode, rank != 0: device buffer (k*n elements, same layout
-                                   as B) to receive B; NULL: a library-owned buffer is used       */
+                                   on rank 0 and broadcast with NCCL (in bcast_chunks N-slabs,
+                                   overlapped with the slab GEMMs) to the other ranks.  Without a
+                                   communicator world = 1 is a 1-rank world.  Combines with HOST. */
+    void *B_replica;            /* world mode, rank != 0: device workspace of >= k*n elements that
+                                   receives B (its layout afterwards is the library's slab layout,
+                                   unspecified to the caller); NULL: a library-owned buffer       */
     int variant_hint;           /* -1: run the selector; >= 0: force that registry index          */
 } compar_gemm_desc;
 
