@@ -1,0 +1,35 @@
+"""Small-shape run of every built-in variant (target for compute-sanitizer memcheck / racecheck /
+synccheck): ragged shapes, transB, beta 0 / non-zero, host mode, loopback panels."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+from gen.device import device_matrix  # noqa: E402
+from paper_2311_03543_b200 import compar as cm  # noqa: E402
+
+only = sys.argv[1:]  # optional variant names
+ctx = cm.Compar()
+names = [v for v, _ in ctx.variants()]
+for name in names:
+    if only and name not in only:
+        continue
+    bf = "bf16" in name
+    dt = "bf16" if bf else "f32"
+    compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else cm.COMPUTE_F32_STRICT)
+    for (m, n, k, tb, beta, panels) in [(77, 136, 72, 0, 0.5, 1), (300, 264, 136, 1, 0.0, 3), (129, 520, 264, 0, -1.0, 2)]:
+        A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+        B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))
+        Cd = device_matrix(gen.TAG_C, m, n)
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, ldb=(k if tb else n), alpha=1.5, beta=beta,
+                         in_dtype=cm.BF16 if bf else cm.F32, compute=compute, transB=tb, panels=panels,
+                         variant_hint=names.index(name))
+        r = ctx.run(d)
+        assert r.status == 0, (name, m, n, k)
+    print(f"{name}: ok", flush=True)
+torch.cuda.synchronize()
+ctx.terminate()
