@@ -105,7 +105,7 @@ typedef struct {
     int calib_k;                /* timed calibration samples per (variant,key); <0: COMPAR_CALIB_K or 3 */
     int calib_warmup;           /* discarded first executions per (variant,key); <0: COMPAR_CALIB_WARMUP or 1 */
     const char *perf_model_path;/* NULL: COMPAR_PERF_MODEL; if the file exists it is merged at init */
-    int bcast_chunks;           /* SPMD broadcast of B in this many N-slabs; <0: COMPAR_BCAST_CHUNKS or 4 */
+    int bcast_chunks;           /* SPMD broadcast of B in this many N-slabs; <0: COMPAR_BCAST_CHUNKS or 8 */
     int builtins;               /* <0 or 1: register simt_f32, tma_f32, tc_tf32, tc_bf16 at init */
     int virtual_clock;          /* 1: host-only mode, no CUDA call at all: USER variants report
                                    synthetic ns through their virtual_ns argument (tests) */

@@ -393,7 +393,7 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
     // all ranks keep an identical history (rank-consistent decisions).
     if (t.world && c->nranks > 1 && t.history && c->reduce_hook) {
         c->reduce_hook(&sample, c->reduce_user);
-    } else if (t.world && c->comm && c->nranks > 1 && t.history) {
+    } else if (t.world && c->comm && (c->nranks > 1 || c->bcast_loopback) && t.history) {
         cudaMemcpyAsync(c->red_buf, &sample, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
         ncclResult_t r = ncclAllReduce(c->red_buf, c->red_buf, 1, ncclInt64, ncclMax, c->comm, c->stream);
         cudaMemcpyAsync(&sample, c->red_buf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
@@ -465,6 +465,7 @@ compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStr
     const int eb = elem_bytes(d->in_dtype);
     const bool loop = c->nranks == 1;              // loopback emulation on one GPU
     const bool root = !loop && c->rank == 0;
+    const bool use_nccl = c->comm != nullptr;      // loopback with a 1-rank communicator still calls NCCL
     const int64_t K = d->k, N = d->n;
     int chunks = c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1;
     int64_t w = ((N + chunks - 1) / chunks + 255) / 256 * 256;
@@ -496,11 +497,11 @@ compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStr
     ncclResult_t nr = ncclSuccess;
     if (!slabbed) {
         // one raw broadcast of the B region (any ld), then the plain panel GEMM
-        if (loop)
+        if (loop && !use_nccl)
             cudaMemcpyAsync(replica, Bloc, b_bytes, cudaMemcpyDeviceToDevice, c->comm_stream);
         else
-            nr = ncclBroadcast(root ? Bloc : replica, root ? const_cast<void *>(Bloc) : replica, b_bytes, ncclChar, 0,
-                               c->comm, c->comm_stream);
+            nr = ncclBroadcast(root || loop ? Bloc : replica, root ? const_cast<void *>(Bloc) : replica, b_bytes,
+                               ncclChar, 0, c->comm, c->comm_stream);
     } else {
         for (int j = 0; j < nslab; ++j) {
             const int64_t col0 = j * w, wj = std::min(w, N - col0);
@@ -516,7 +517,7 @@ compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStr
                     cudaMemcpy2DAsync(pk, wj * eb, src + col0 * eb, d->ldb * eb, wj * eb, K, cudaMemcpyDeviceToDevice,
                                       c->comm_stream);
             }
-            if (loop)
+            if (loop && !use_nccl)
                 cudaMemcpyAsync(rp, pk, bytes, cudaMemcpyDeviceToDevice, c->comm_stream);
             else if (nr == ncclSuccess)
                 nr = ncclBroadcast(pk, root ? pk : rp, bytes, ncclChar, 0, c->comm, c->comm_stream);
@@ -672,7 +673,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     }
     if (cfg.calib_k < 0) cfg.calib_k = env_int("COMPAR_CALIB_K", 3);
     if (cfg.calib_warmup < 0) cfg.calib_warmup = env_int("COMPAR_CALIB_WARMUP", 1);
-    if (cfg.bcast_chunks < 0) cfg.bcast_chunks = env_int("COMPAR_BCAST_CHUNKS", 4);
+    if (cfg.bcast_chunks < 0) cfg.bcast_chunks = env_int("COMPAR_BCAST_CHUNKS", 8);
     if (cfg.builtins < 0) cfg.builtins = 1;
     if (cfg.variant_mask < 0) {
         const char *s = std::getenv("COMPAR_VARIANT_MASK");

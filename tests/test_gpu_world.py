@@ -72,6 +72,39 @@ def test_loopback_slab_pipeline_bitwise(loop_ctx, chunks, name, m, n, k, tb):
         assert og.rel_fro(got, ref) <= (1e-5 if name == "simt_f32" else 5e-3)
 
 
+@pytest.mark.parametrize("tb", [0, 1])
+def test_loopback_through_nccl_one_rank(tb):
+    """Same pipeline, but every slab goes through ncclBroadcast on a real 1-rank communicator
+    (send = packed slab, recv = replica slab) and every harvested sample through ncclAllReduce —
+    the NCCL call sites of the N-GPU path, exercised on one GPU, with the selector calibrating."""
+    old = os.environ.get("COMPAR_BCAST_LOOPBACK")
+    os.environ["COMPAR_BCAST_LOOPBACK"] = "1"
+    try:
+        ctx = cm.Compar(bcast_chunks=4)
+        ctx.comm_init(1, 0, cm.comm_unique_id())
+    finally:
+        if old is None:
+            os.environ.pop("COMPAR_BCAST_LOOPBACK", None)
+        else:
+            os.environ["COMPAR_BCAST_LOOPBACK"] = old
+    try:
+        m, n, k = 1024, 2048, 512
+        A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
+        B = device_matrix(gen.TAG_B, k, n, dtype="bf16", transposed=bool(tb))
+        C0 = device_matrix(gen.TAG_C, m, n)
+        kw = dict(ldb=(k if tb else n), alpha=1.5, beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, transB=tb)
+        for _ in range(14):           # calibration (3 variants x 4) then model mode, all through world=1
+            Cw = C0.clone()
+            r = ctx.run(cm.make_desc(m, n, k, A=A, B=B, C_in=Cw, C_out=Cw, world=1, **kw))
+            assert r.status == 0 and r.bcast_ns >= 0
+        assert r.mode == cm.MODE_MODEL
+        Cp = C0.clone()
+        ctx.run(cm.make_desc(m, n, k, A=A, B=B, C_in=Cp, C_out=Cp, variant_hint=r.variant, **kw))
+        assert torch.equal(Cw, Cp)
+    finally:
+        ctx.terminate()
+
+
 def test_loopback_world_host_memory(loop_ctx):
     """World mode + HOST buffers (the e2e path of bench.py at N > 1) through the slab pipeline."""
     ctx = loop_ctx(4)
