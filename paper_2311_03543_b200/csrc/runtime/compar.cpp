@@ -48,6 +48,7 @@ struct Variant {
     compar_target target;
     compar_gemm_fn fn;
     void *user;
+    int hid;  // interned history id of `name`
 };
 
 struct PanelRun {
@@ -269,16 +270,16 @@ bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, co
 }
 
 void eligible_set(Ctx *c, const compar_gemm_desc *d, const Plan &plan, std::vector<int> &idx,
-                  std::vector<std::string> &names) {
+                  std::vector<int> &hids) {
     idx.clear();
-    names.clear();
+    hids.clear();
     for (size_t v = 0; v < c->variants.size(); ++v) {
         if (v < 63 && (c->cfg.variant_mask >> v) & 1) continue;
         const Variant &var = c->variants[v];
         if (!admits(var.target, d->in_dtype, d->compute)) continue;
         if (!constraints_ok(c, var.target, d, plan)) continue;
         idx.push_back(static_cast<int>(v));
-        names.push_back(var.name);
+        hids.push_back(var.hid);
     }
 }
 
@@ -364,8 +365,9 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
     rep->warmup = t.warm ? 1 : 0;
     rep->npanels = static_cast<int>(t.panels.size());
     int64_t sample = 0;
-    if (!c->virt && t.end) {
-        cudaError_t e = cudaEventSynchronize(t.end);
+    cudaEvent_t last = t.end ? t.end : (t.panels.empty() ? nullptr : t.panels.back().stop);
+    if (!c->virt && last) {
+        cudaError_t e = cudaEventSynchronize(last);
         if (e != cudaSuccess && t.status == COMPAR_OK) {
             t.status = COMPAR_E_TASK_FAILED;
             t_err = std::string("task execution failed: ") + cudaGetErrorString(e);
@@ -384,7 +386,8 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
         sample = std::max(sample, ns);
     }
     if (!c->virt) {
-        rep->total_ns = elapsed_ns(t.begin, t.end);
+        rep->total_ns = t.begin ? elapsed_ns(t.begin, t.end)
+                                : (t.panels.empty() ? 0 : elapsed_ns(t.panels.front().start, t.panels.back().stop));
         rep->bcast_ns = elapsed_ns(t.bc0, t.bc1);
     } else {
         for (auto &p : t.panels) rep->total_ns += p.virtual_ns;
@@ -403,7 +406,7 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
     rep->ns = sample;
     rep->status = t.status;
     if (t.history && t.status == COMPAR_OK && !t.warm && t.variant >= 0) {
-        c->hist.harvest(c->variants[t.variant].name, t.key, sample);
+        c->hist.harvest(c->variants[t.variant].hid, t.key, sample);
         c->stats.harvested++;
     }
     if (t.status != COMPAR_OK) c->stats.failed++;
@@ -798,7 +801,7 @@ compar_status compar_register_variant(void *ctx, const char *iface, const char *
     for (const auto &v : c->variants)
         if (v.name == name) return fail(COMPAR_E_DUPLICATE, std::string("duplicate variant ") + name);
     if (c->variants.size() >= 64) return fail(COMPAR_E_INVALID, "too many variants");
-    c->variants.push_back(Variant{name, target, fn, user});
+    c->variants.push_back(Variant{name, target, fn, user, c->hist.intern(name)});
     if (out_id) *out_id = static_cast<int>(c->variants.size()) - 1;
     return COMPAR_OK;
 }
@@ -830,7 +833,7 @@ namespace {
 compar_status choose(Ctx *c, const compar_gemm_desc *d, const Plan &plan, bool commit, int *variant, int *mode,
                      bool *warm) {
     std::vector<int> idx;
-    std::vector<std::string> names;
+    std::vector<int> names;  // interned history ids, in registry order
     eligible_set(c, d, plan, idx, names);
     *warm = false;
     if (d->variant_hint >= 0) {
@@ -969,9 +972,14 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             }
         }
     } else if (work) {
-        t.begin = get_event(c);
-        t.end = get_event(c);
-        cudaEventRecord(t.begin, st);
+        // The plain single-launch task (device memory, one panel, no broadcast) uses the panel's
+        // start/stop events as the task span: two event records per task instead of four.
+        const bool simple = !host && t.panels.size() == 1 && !(t.world && gemm && (c->nranks > 1 || c->bcast_loopback));
+        if (!simple) {
+            t.begin = get_event(c);
+            t.end = get_event(c);
+            cudaEventRecord(t.begin, st);
+        }
         const bool pipelined = host && gemm && !t.world && t.panels.size() == 1 && c->host_chunks > 1 && d->m >= 512;
         if (host && !pipelined) {
             if (a_bytes) cudaMemcpyAsync(const_cast<void *>(A), d->A, a_bytes, cudaMemcpyHostToDevice, st);
@@ -1009,7 +1017,7 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             c->stats.bytes_d2h += static_cast<int64_t>(mloc * d->n * 4);
             (void)cout_bytes;
         }
-        cudaEventRecord(t.end, st);
+        if (t.end) cudaEventRecord(t.end, st);
     }
     if (task_out) *task_out = t.id;
     c->tasks.emplace(t.id, std::move(t));
@@ -1050,7 +1058,7 @@ compar_status compar_perf_save(void *ctx, const char *path) {
     for (const auto &kv : c->hist.table()) {
         const Key &k = kv.first.second;
         const Record &r = kv.second;
-        f << kv.first.first << ' ' << k.m << ' ' << k.n << ' ' << k.k << ' ' << k.dtype << ' ' << k.compute << ' '
+        f << c->hist.name(kv.first.first) << ' ' << k.m << ' ' << k.n << ' ' << k.k << ' ' << k.dtype << ' ' << k.compute << ' '
           << k.transB << ' ' << k.beta0 << ' ' << r.seen << ' ' << r.count << ' ' << u128_str(r.sum_ns) << ' '
           << u128_str(r.sumsq_ns) << ' ' << r.min_ns << '\n';
     }
@@ -1097,7 +1105,7 @@ compar_status compar_history_get(void *ctx, int variant, const compar_gemm_desc 
     Plan plan;
     build_plan(c, d, plan, d->A, d->B, d->C_in, d->C_out);
     std::memset(out, 0, sizeof(*out));
-    const Record *r = c->hist.find(c->variants[variant].name, plan.key);
+    const Record *r = c->hist.find(c->variants[variant].hid, plan.key);
     if (r) {
         out->seen = r->seen;
         out->count = r->count;

@@ -46,26 +46,31 @@ public:
     int calib_warmup = 1;
     int calib_k = 3;
 
-    // Records are keyed by variant NAME so a loaded perf model applies to whichever registry
-    // index that name gets (SPEC S:393-401 persistence).
-    Record &rec(const std::string &variant, const Key &k) { return table_[{variant, k}]; }
-    const Record *find(const std::string &variant, const Key &k) const {
-        auto it = table_.find({variant, k});
+    // Records belong to variant NAMES (so a loaded perf model applies to whichever registry index
+    // that name gets); names are interned to small ids for the hot path.
+    int intern(const std::string &name);
+    const std::string &name(int id) const { return names_[id]; }
+
+    Record &rec(int id, const Key &k) { return table_[{id, k}]; }
+    const Record *find(int id, const Key &k) const {
+        auto it = table_.find({id, k});
         return it == table_.end() ? nullptr : &it->second;
     }
     // True if any eligible variant is still calibrating for this key.
-    bool calibrating(const std::vector<std::string> &names, const Key &k);
-    // Decision over the ordered eligible list (indices into `names`): returns position in list.
-    int decide(const std::vector<std::string> &names, const Key &k, Mode *mode);
+    bool calibrating(const std::vector<int> &ids, const Key &k);
+    // Decision over the ordered eligible list: returns the position in `ids`.
+    int decide(const std::vector<int> &ids, const Key &k, Mode *mode);
     // Account an assigned execution; returns true if it is a warm-up.
-    bool commit(const std::string &variant, const Key &k);
-    void harvest(const std::string &variant, const Key &k, int64_t ns);
+    bool commit(int id, const Key &k);
+    void harvest(int id, const Key &k, int64_t ns);
 
-    const std::map<std::pair<std::string, Key>, Record> &table() const { return table_; }
+    const std::map<std::pair<int, Key>, Record> &table() const { return table_; }
     void merge(const std::string &variant, const Key &k, const Record &r);
 
 private:
-    std::map<std::pair<std::string, Key>, Record> table_;
+    std::map<std::string, int> ids_;
+    std::vector<std::string> names_;
+    std::map<std::pair<int, Key>, Record> table_;
 };
 
 }  // namespace compar
