@@ -84,7 +84,9 @@ typedef enum {
     COMPAR_MODE_MODEL = 2,      /* model: argmin of the mean measured ns                            */
     COMPAR_MODE_EAGER = 3,      /* eager scheduler: first eligible variant, no history              */
     COMPAR_MODE_HINT = 4,       /* caller forced variant_hint; history untouched                    */
-    COMPAR_MODE_NOOP = 5        /* quick return (m==0 or n==0) or scale-only (k==0 or alpha==0)     */
+    COMPAR_MODE_NOOP = 5,       /* quick return (m==0 or n==0) or scale-only (k==0 or alpha==0)     */
+    COMPAR_MODE_PREDICT = 6     /* predict scheduler: argmin of fitted-model predictions for a key
+                                   this variant has no samples of yet                              */
 } compar_mode;
 
 typedef enum { COMPAR_MEM_DEVICE = 0, COMPAR_MEM_HOST = 1 } compar_mem;
@@ -101,7 +103,8 @@ typedef struct {
                                    GPU, see compar_comm_init).  <0: COMPAR_NGPU or 1.  0: E_INVALID
                                    — there is no CPU class to fall back to (R15).      */
     int device;                 /* CUDA ordinal; <0: the caller's current device                */
-    int sched;                  /* 0 history, 1 eager; <0: COMPAR_SCHED=history|eager           */
+    int sched;                  /* 0 history, 1 eager, 2 predict (history + per-variant cost model for
+                                   unseen shapes); <0: COMPAR_SCHED=history|eager|predict */
     int calib_k;                /* timed calibration samples per (variant,key); <0: COMPAR_CALIB_K or 3 */
     int calib_warmup;           /* discarded first executions per (variant,key); <0: COMPAR_CALIB_WARMUP or 1 */
     const char *perf_model_path;/* NULL: COMPAR_PERF_MODEL; if the file exists it is merged at init */

@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1
 COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
-MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP = 0, 1, 2, 3, 4, 5
+MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
 
 
 def admits(target: int, in_dtype: int, compute: int) -> bool:
@@ -106,7 +106,7 @@ class SelectorOracle:
 
     def commit(self, v: int, key, mode: int) -> bool:
         """Account a submitted execution; returns True if it is a warm-up."""
-        if mode in (MODE_EAGER, MODE_HINT, MODE_NOOP):
+        if mode in (MODE_EAGER, MODE_HINT, MODE_NOOP):  # MODE_PREDICT executions are accounted
             return False
         r = self.rec(v, key)
         warm = r.seen < self.calib_warmup
@@ -126,3 +126,62 @@ class SelectorOracle:
     def mean_ns(self, v: int, key) -> float:
         r = self.rec(v, key)
         return r.sum_ns / r.count if r.count else float("inf")
+
+    # ---- NEXT-2 "predict" scheduler (PAPER.md P:224 / P:308 "additional training").
+    # key = (m, n, k, dtype, compute, transB, beta0).  Written from the definition: weighted least
+    # squares with weights 1/t^2 over every non-empty subset of the features {1, GFLOP, MB},
+    # keep the non-negative solution of least relative residual.
+    MIN_FIT_KEYS = 3
+
+    @staticmethod
+    def features(key):
+        m, n, k, dtype, _compute, _tb, beta0 = key
+        eb = 2.0 if dtype == BF16 else 4.0
+        return [1.0, 2.0 * m * n * k * 1e-9, (eb * (m * k + k * n) + 4.0 * m * n * (1.0 if beta0 else 2.0)) * 1e-6]
+
+    def predict(self, v: int, key):
+        import numpy as np
+        pts = [(self.features(kk), r.sum_ns / r.count) for (vv, kk), r in self.hist.items()
+               if vv == v and r.count > 0 and kk[3:6] == key[3:6]]
+        if len(pts) < self.MIN_FIT_KEYS:
+            return None
+        X = np.array([p[0] for p in pts])
+        t = np.array([p[1] for p in pts])
+        wt = 1.0 / (t * t + 1.0)
+        best = None
+        for mask in range(1, 8):
+            cols = [j for j in range(3) if mask >> j & 1]
+            Xs = X[:, cols]
+            a = (Xs * wt[:, None]).T @ Xs
+            b = (Xs * wt[:, None]).T @ t
+            try:
+                w = np.linalg.solve(a, b)
+            except np.linalg.LinAlgError:
+                continue
+            if (w < 0).any():
+                continue
+            full = np.zeros(3)
+            full[cols] = w
+            res = float((((X @ full) - t) / t) ** 2 @ np.ones(len(t)))
+            if best is None or res < best[0]:
+                best = (res, full)
+        if best is None:
+            return None
+        return float(np.array(self.features(key)) @ best[1])
+
+    def decide_predict(self, key, eligible):
+        """Measured mean where (v, key) has samples, else the fitted prediction; None if some
+        eligible variant has neither (the caller then calibrates)."""
+        best = None
+        for v in eligible:
+            r = self.rec(v, key)
+            if r.count > 0:
+                est, pred = r.sum_ns / r.count, False
+            else:
+                est = self.predict(v, key)
+                pred = True
+                if est is None:
+                    return None
+            if best is None or est < best[1]:
+                best = (v, est, pred)
+        return best[0], (MODE_PREDICT if best[2] else MODE_MODEL)

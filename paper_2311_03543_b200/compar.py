@@ -22,7 +22,8 @@ F32, BF16 = 0, 1
 COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER, TGT_TC2_TF32, TGT_TC2_BF16, TGT_TCW_TF32, TGT_TCW_BF16 = \
     0, 1, 2, 3, 4, 5, 6, 7, 8
-MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP = 0, 1, 2, 3, 4, 5
+MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
+SCHED_HISTORY, SCHED_EAGER, SCHED_PREDICT = 0, 1, 2
 MEM_DEVICE, MEM_HOST = 0, 1
 TASK_ALL = (1 << 64) - 1
 MAX_PANELS = 8

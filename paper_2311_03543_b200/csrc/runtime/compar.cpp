@@ -357,6 +357,19 @@ compar_status harvest_key(Ctx *c, const Key &k) {
     return COMPAR_OK;
 }
 
+compar_status harvest_all(Ctx *c) {
+    std::vector<uint64_t> ids;
+    for (auto &kv : c->tasks)
+        if (kv.second.history) ids.push_back(kv.first);
+    for (uint64_t id : ids) {
+        auto it = c->tasks.find(id);
+        compar_report rep;
+        finish_task(c, it->second, &rep);
+        c->tasks.erase(it);
+    }
+    return COMPAR_OK;
+}
+
 compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
     std::memset(rep, 0, sizeof(*rep));
     rep->task = t.id;
@@ -672,7 +685,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     if (cfg.ngpu != 1) return fail(COMPAR_E_INVALID, "one GPU per process (use compar_comm_init for SPMD)");
     if (cfg.sched < 0) {
         const char *s = std::getenv("COMPAR_SCHED");
-        cfg.sched = (s && std::strcmp(s, "eager") == 0) ? 1 : 0;
+        cfg.sched = (s && std::strcmp(s, "eager") == 0) ? 1 : (s && std::strcmp(s, "predict") == 0) ? 2 : 0;
     }
     if (cfg.calib_k < 0) cfg.calib_k = env_int("COMPAR_CALIB_K", 3);
     if (cfg.calib_warmup < 0) cfg.calib_warmup = env_int("COMPAR_CALIB_WARMUP", 1);
@@ -849,6 +862,20 @@ compar_status choose(Ctx *c, const compar_gemm_desc *d, const Plan &plan, bool c
         *mode = kEager;
         return COMPAR_OK;
     }
+    if (c->cfg.sched == 2) {
+        // "predict" scheduler (NEXT-2): every pending sample is harvested first (the fit reads all
+        // keys), then measured means / model predictions decide; unknown variants fall back to
+        // calibration below.
+        harvest_all(c);
+        Mode pm;
+        const int ppos = c->hist.decide_predict(names, plan.key, &pm);
+        if (ppos >= 0) {
+            *variant = idx[ppos];
+            *mode = pm;
+            if (commit) *warm = c->hist.commit(names[ppos], plan.key);
+            return COMPAR_OK;
+        }
+    }
     if (!c->hist.calibrating(names, plan.key)) harvest_key(c, plan.key);
     Mode m;
     const int pos = c->hist.decide(names, plan.key, &m);
@@ -952,7 +979,7 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             return s;
         }
         t.warm = warm;
-        t.history = (t.mode == kWarmup || t.mode == kCalib || t.mode == kModel);
+        t.history = (t.mode == kWarmup || t.mode == kCalib || t.mode == kModel || t.mode == kPredict);
     } else {
         t.mode = kNoop;
     }

@@ -1,5 +1,9 @@
 #include "history.h"
 
+#include <array>
+#include <cmath>
+#include <utility>
+
 namespace compar {
 
 int History::intern(const std::string &name) {
@@ -66,6 +70,117 @@ void History::harvest(int id, const Key &k, int64_t ns) {
     ++r.count;
     r.sum_ns += static_cast<unsigned __int128>(ns);
     r.sumsq_ns += static_cast<unsigned __int128>(ns) * static_cast<unsigned __int128>(ns);
+}
+
+void History::features(const Key &k, double *x) {
+    const double m = static_cast<double>(k.m), n = static_cast<double>(k.n), kk = static_cast<double>(k.k);
+    const double eb = k.dtype == 1 ? 2.0 : 4.0;
+    x[0] = 1.0;
+    x[1] = 2.0 * m * n * kk * 1e-9;
+    x[2] = (eb * (m * kk + kk * n) + 4.0 * m * n * (k.beta0 ? 1.0 : 2.0)) * 1e-6;
+}
+
+namespace {
+// Solve the s x s system a * w = b (Gaussian elimination, partial pivoting); false if singular.
+bool solve(int s, double a[3][3], double b[3], double w[3]) {
+    for (int c = 0; c < s; ++c) {
+        int p = c;
+        for (int r = c + 1; r < s; ++r)
+            if (std::fabs(a[r][c]) > std::fabs(a[p][c])) p = r;
+        if (std::fabs(a[p][c]) < 1e-300) return false;
+        if (p != c) {
+            for (int j = 0; j < s; ++j) std::swap(a[p][j], a[c][j]);
+            std::swap(b[p], b[c]);
+        }
+        for (int r = c + 1; r < s; ++r) {
+            const double f = a[r][c] / a[c][c];
+            for (int j = c; j < s; ++j) a[r][j] -= f * a[c][j];
+            b[r] -= f * b[c];
+        }
+    }
+    for (int c = s - 1; c >= 0; --c) {
+        double v = b[c];
+        for (int j = c + 1; j < s; ++j) v -= a[c][j] * w[j];
+        w[c] = v / a[c][c];
+    }
+    return true;
+}
+}  // namespace
+
+bool History::predict(int id, const Key &q, double *ns) const {
+    // samples of the same family: (x, t) with t = mean ns
+    std::vector<std::pair<std::array<double, 3>, double>> pts;
+    for (const auto &kv : table_) {
+        if (kv.first.first != id || kv.second.count == 0) continue;
+        const Key &k = kv.first.second;
+        if (k.dtype != q.dtype || k.compute != q.compute || k.transB != q.transB) continue;
+        std::array<double, 3> x;
+        features(k, x.data());
+        pts.push_back({x, static_cast<double>(kv.second.sum_ns) / static_cast<double>(kv.second.count)});
+    }
+    if (static_cast<int>(pts.size()) < kMinFitKeys) return false;
+    double best_res = 0, best_w[3] = {0, 0, 0};
+    bool found = false;
+    for (int mask = 1; mask < 8; ++mask) {
+        int cols[3], s = 0;
+        for (int j = 0; j < 3; ++j)
+            if (mask >> j & 1) cols[s++] = j;
+        double a[3][3] = {}, b[3] = {}, w[3] = {};
+        for (const auto &p : pts) {
+            const double wt = 1.0 / (p.second * p.second + 1.0);
+            for (int r = 0; r < s; ++r) {
+                b[r] += wt * p.first[cols[r]] * p.second;
+                for (int c2 = 0; c2 < s; ++c2) a[r][c2] += wt * p.first[cols[r]] * p.first[cols[c2]];
+            }
+        }
+        if (!solve(s, a, b, w)) continue;
+        bool nonneg = true;
+        for (int r = 0; r < s; ++r) nonneg = nonneg && w[r] >= 0.0;
+        if (!nonneg) continue;
+        double full[3] = {0, 0, 0};
+        for (int r = 0; r < s; ++r) full[cols[r]] = w[r];
+        double res = 0;
+        for (const auto &p : pts) {
+            const double pr = full[0] * p.first[0] + full[1] * p.first[1] + full[2] * p.first[2];
+            const double e = (pr - p.second) / p.second;
+            res += e * e;
+        }
+        if (!found || res < best_res) {
+            found = true;
+            best_res = res;
+            for (int j = 0; j < 3; ++j) best_w[j] = full[j];
+        }
+    }
+    if (!found) return false;
+    double x[3];
+    features(q, x);
+    *ns = best_w[0] * x[0] + best_w[1] * x[1] + best_w[2] * x[2];
+    return true;
+}
+
+int History::decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode) const {
+    int best = -1;
+    double best_est = 0;
+    bool best_pred = false;
+    for (size_t i = 0; i < ids.size(); ++i) {
+        const Record *r = find(ids[i], k);
+        double est;
+        bool pred = false;
+        if (r && r->count > 0) {
+            est = static_cast<double>(r->sum_ns) / static_cast<double>(r->count);
+        } else if (predict(ids[i], k, &est)) {
+            pred = true;
+        } else {
+            return -1;
+        }
+        if (best < 0 || est < best_est) {
+            best = static_cast<int>(i);
+            best_est = est;
+            best_pred = pred;
+        }
+    }
+    *mode = best_pred ? kPredict : kModel;
+    return best;
 }
 
 void History::merge(const std::string &variant, const Key &k, const Record &in) {

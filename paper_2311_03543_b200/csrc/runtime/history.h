@@ -39,7 +39,7 @@ struct Record {
     int64_t min_ns = 0;
 };
 
-enum Mode { kWarmup = 0, kCalib = 1, kModel = 2, kEager = 3, kHint = 4, kNoop = 5 };
+enum Mode { kWarmup = 0, kCalib = 1, kModel = 2, kEager = 3, kHint = 4, kNoop = 5, kPredict = 6 };
 
 class History {
 public:
@@ -66,6 +66,19 @@ public:
 
     const std::map<std::pair<int, Key>, Record> &table() const { return table_; }
     void merge(const std::string &variant, const Key &k, const Record &r);
+
+    // ---- performance-model generalisation ("additional
+    // training of these models").  For an unseen key, variant v's time is predicted from its own
+    // measured keys of the same (dtype, compute, transB) family with
+    //     t ~ w0 + w1 * flops + w2 * bytes,     w >= 0,
+    // fitted by relative-error least squares (weights 1/t^2) over every non-empty feature subset,
+    // keeping the non-negative solution of least weighted residual.  Needs >= kMinFitKeys keys.
+    static constexpr int kMinFitKeys = 3;
+    static void features(const Key &k, double *x);   // x[0..2] = 1, GFLOP, MB
+    bool predict(int id, const Key &k, double *ns) const;
+    // Decision of the "predict" scheduler: measured mean where (v, key) has samples, prediction
+    // otherwise; returns -1 (caller falls back to calibration) if some variant has neither.
+    int decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode) const;
 
 private:
     std::map<std::string, int> ids_;

@@ -269,6 +269,36 @@ def test_failed_variant_marks_task_failed_without_retry():
     ctx.terminate()
 
 
+def test_predict_scheduler_matches_oracle():
+    """NEXT-2 through the C ABI (sched = predict): after training on four sizes, unseen sizes are
+    decided from the fitted models without calibration; every decision equals the oracle's."""
+    cost = [lambda m, n, k: 40_000 + 800.0 * 2 * m * n * k * 1e-9,
+            lambda m, n, k: 4_000 + 2_500.0 * 2 * m * n * k * 1e-9,
+            lambda m, n, k: 20_000 + 1_200.0 * 2 * m * n * k * 1e-9]
+    ctx, _ = vctx(cost, sched=cm.SCHED_PREDICT)
+    orc = so.SelectorOracle(3)
+
+    def key(s):
+        return (s, s, s, so.F32, so.COMPUTE_F32_STRICT, 0, 0)
+
+    def step(s):
+        d = desc(s)
+        r = ctx.run(d)
+        got = (r.variant, r.mode)
+        dp = orc.decide_predict(key(s), [0, 1, 2])
+        exp = dp if dp is not None else orc.decide(key(s), [0, 1, 2])
+        warm = orc.commit(exp[0], key(s), exp[1])
+        orc.harvest(exp[0], key(s), exp[1], warm, int(cost[exp[0]](s, s, s)))
+        assert got == exp, (s, got, exp)
+        return got
+    for s in (200, 400, 800, 1600):
+        for _ in range(12):
+            step(s)
+    modes = [step(s)[1] for s in (300, 3000, 1000, 7000, 300)]
+    assert modes[:4] == [cm.MODE_PREDICT] * 4
+    ctx.terminate()
+
+
 def test_loopback_panels_virtual():
     """Loopback panels: the variant runs once per non-empty panel (rows from the a4 formula);
     the sample is the max panel time and the key uses the first panel's rows."""

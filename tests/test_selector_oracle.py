@@ -100,6 +100,29 @@ def test_admits_table():
     assert so.tma_ok(4, [0, 256], [64, 8]) and not so.tma_ok(4, [4], [64]) and not so.tma_ok(2, [0], [9])
 
 
+def _key(s, beta0=0):
+    return (s, s, s, so.F32, so.COMPUTE_TF32, 0, beta0)
+
+
+def test_predict_recovers_closed_form():
+    """NEXT-2 pin: with exact affine costs t = a + b * GFLOP the weighted fit recovers them, so the
+    prediction at an unseen size equals the closed form and the decision is its argmin."""
+    sel = so.SelectorOracle(2)
+    cost = [lambda s: 50_000 + 900.0 * 2 * s ** 3 * 1e-9, lambda s: 5_000 + 2_000.0 * 2 * s ** 3 * 1e-9]
+    for s in (256, 512, 1024, 2048):
+        for _ in range(8):
+            v, mode = sel.decide(_key(s), [0, 1])
+            warm = sel.commit(v, _key(s), mode)
+            sel.harvest(v, _key(s), mode, warm, round(cost[v](s)))
+    for s in (3000, 600, 8192):
+        for v in (0, 1):
+            assert sel.predict(v, _key(s)) == pytest.approx(cost[v](s), rel=1e-3)   # samples are integer ns
+        v, mode = sel.decide_predict(_key(s), [0, 1])
+        assert mode == so.MODE_PREDICT and v == min((0, 1), key=lambda t: cost[t](s))
+    # not enough keys for a variant -> no prediction
+    assert so.SelectorOracle(2).decide_predict(_key(64), [0, 1]) is None
+
+
 @pytest.mark.parametrize("m,p,expect", [
     (32768, 8, [0, 4096, 8192, 12288, 16384, 20480, 24576, 28672, 32768]),
     (32768, 2, [0, 16384, 32768]),

@@ -165,7 +165,7 @@ def main(out_path):
     ctxb.terminate()
     c5b = {"tasks": len(stream), "shapes": [list(s) for s in shapes],
            "best": {str(list(s)): names[b[0]] for s, b in best.items()}}
-    for sched, label in ((0, "history"), (1, "eager")):
+    for sched, label in ((0, "history"), (1, "eager"), (2, "predict")):
         c = cm.Compar(sched=sched)
         chosen, total_ns = [], 0
         t0 = time.perf_counter()
@@ -174,7 +174,10 @@ def main(out_path):
             chosen.append((s, r.variant, r.mode))
             total_ns += r.ns
         wall = time.perf_counter() - t0
-        steady = [(s, v) for (s, v, mode) in chosen if mode in (cm.MODE_MODEL, cm.MODE_EAGER)]
+        c5b.setdefault("calibration_runs", {})[label] = sum(
+            1 for (_, _, mode) in chosen if mode in (cm.MODE_WARMUP, cm.MODE_CALIB))
+        c5b.setdefault("predicted_runs", {})[label] = sum(1 for (_, _, mode) in chosen if mode == cm.MODE_PREDICT)
+        steady = [(s, v) for (s, v, mode) in chosen if mode in (cm.MODE_MODEL, cm.MODE_EAGER, cm.MODE_PREDICT)]
         acc = sum(1 for s, v in steady if v == best[s][0]) / max(1, len(steady))
         per_shape = {}
         for s in shapes:
