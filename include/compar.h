@@ -60,7 +60,10 @@ typedef enum { COMPAR_F32 = 0, COMPAR_BF16 = 1 } compar_dtype;             /* st
 /* Arithmetic the caller accepts (precision class, R4):
  *   F32_STRICT: FP32 FFMA only  -> eligible targets SIMT_F32, TMA_F32
  *   TF32:       FP32 storage, TF32 tensor cores allowed -> SIMT_F32, TMA_F32, TC_TF32
- *   BF16:       BF16 storage (in_dtype must be BF16)    -> TC_BF16                    */
+ *   BF16:       BF16 storage (in_dtype must be BF16)    -> TC_BF16 (+ pair forms), SIMT_BF16
+ * The tcgen05 and TMA targets further require the TMA alignment rule (16-byte aligned bases and
+ * row pitches); SIMT_F32 / SIMT_BF16 accept any shape and alignment, so every valid descriptor
+ * has at least one eligible built-in.                                                        */
 typedef enum { COMPAR_COMPUTE_F32_STRICT = 0, COMPAR_COMPUTE_TF32 = 1, COMPAR_COMPUTE_BF16 = 2 } compar_compute;
 
 /* Target of a variant (the paper's `target` clause).  USER variants are
@@ -74,7 +77,8 @@ typedef enum {
     COMPAR_TGT_TC2_TF32 = 5,    /* built-in (c), CTA-pair form: tcgen05.mma.cta_group::2, 256x256 tiles */
     COMPAR_TGT_TC2_BF16 = 6,    /* built-in (c), CTA-pair form, BF16                                    */
     COMPAR_TGT_TCW_TF32 = 7,    /* built-in (c), wide CTA-pair form: 256x512 pair tile, 2 accumulators  */
-    COMPAR_TGT_TCW_BF16 = 8     /* built-in (c), wide CTA-pair form, BF16                               */
+    COMPAR_TGT_TCW_BF16 = 8,    /* built-in (c), wide CTA-pair form, BF16                               */
+    COMPAR_TGT_SIMT_BF16 = 9    /* built-in (a), BF16 operands widened to FP32, FFMA; any shape/alignment */
 } compar_target;
 
 /* Why a task ran the variant it ran. */
@@ -113,7 +117,16 @@ typedef struct {
     int virtual_clock;          /* 1: host-only mode, no CUDA call at all: USER variants report
                                    synthetic ns through their virtual_ns argument (tests) */
     int64_t variant_mask;       /* bit v set: variant v is masked (never eligible); <0: COMPAR_VARIANT_MASK or 0 */
+    int calib_order;            /* calibration order over the eligible variants of an unseen key:
+                                   COMPAR_CALIB_INTERLEAVED: least-seen first (v0 v1 v2 v0 v1 v2 ...,
+                                   SPEC S:369); COMPAR_CALIB_BLOCKED: W + K executions of v0, then
+                                   of v1, ... so every timed sample follows a run of the same
+                                   variant (R19: on the power-capped B200 a sample taken
+                                   right after a low-power kernel runs at boost clocks).
+                                   <0: COMPAR_CALIB_ORDER=interleaved|blocked, else BLOCKED        */
 } compar_config;
+
+enum { COMPAR_CALIB_INTERLEAVED = 0, COMPAR_CALIB_BLOCKED = 1 };
 
 /* One GEMM task.  Sizes are the FULL problem; see `world` for SPMD panels. */
 typedef struct {

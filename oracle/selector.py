@@ -27,6 +27,7 @@ from dataclasses import dataclass, field
 
 # precision classes / targets (mirror include/compar.h values; restated, not imported)
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER = 0, 1, 2, 3, 4
+TGT_SIMT_BF16 = 9
 F32, BF16 = 0, 1
 COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
 MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
@@ -37,7 +38,7 @@ def admits(target: int, in_dtype: int, compute: int) -> bool:
     if target == TGT_USER:
         return True
     if compute == COMPUTE_BF16:
-        return in_dtype == BF16 and target == TGT_TC_BF16
+        return in_dtype == BF16 and target in (TGT_TC_BF16, TGT_SIMT_BF16)
     if in_dtype != F32:
         return False
     if compute == COMPUTE_F32_STRICT:
@@ -67,6 +68,7 @@ class SelectorOracle:
     calib_warmup: int = 1      # W
     calib_k: int = 3           # K_cal
     eager: bool = False
+    blocked: bool = False      # calibration order (R19); False = SPEC S:369 interleaving
     hist: dict = field(default_factory=dict)   # (v, key) -> Record
 
     def rec(self, v: int, key) -> Record:
@@ -85,7 +87,10 @@ class SelectorOracle:
         need = self.calib_warmup + self.calib_k
         seen = [self.rec(v, key).seen for v in eligible]
         if min(seen) < need:                                   # step 4: calibration
-            best = min(range(len(eligible)), key=lambda t: (seen[t], eligible[t]))
+            if self.blocked:   # R19: finish one variant's W + K executions before the next
+                best = next(t for t in range(len(eligible)) if seen[t] < need)
+            else:
+                best = min(range(len(eligible)), key=lambda t: (seen[t], eligible[t]))
             v = eligible[best]
             return v, (MODE_WARMUP if seen[best] < self.calib_warmup else MODE_CALIB)
         best_v = None                                           # step 5: model

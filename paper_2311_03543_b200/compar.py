@@ -22,8 +22,10 @@ F32, BF16 = 0, 1
 COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER, TGT_TC2_TF32, TGT_TC2_BF16, TGT_TCW_TF32, TGT_TCW_BF16 = \
     0, 1, 2, 3, 4, 5, 6, 7, 8
+TGT_SIMT_BF16 = 9
 MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
 SCHED_HISTORY, SCHED_EAGER, SCHED_PREDICT = 0, 1, 2
+CALIB_INTERLEAVED, CALIB_BLOCKED = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 TASK_ALL = (1 << 64) - 1
 MAX_PANELS = 8
@@ -33,7 +35,8 @@ UNIQUE_ID_BYTES = 128
 class Config(C.Structure):
     _fields_ = [("ngpu", C.c_int), ("device", C.c_int), ("sched", C.c_int), ("calib_k", C.c_int),
                 ("calib_warmup", C.c_int), ("perf_model_path", C.c_char_p), ("bcast_chunks", C.c_int),
-                ("builtins", C.c_int), ("virtual_clock", C.c_int), ("variant_mask", C.c_int64)]
+                ("builtins", C.c_int), ("virtual_clock", C.c_int), ("variant_mask", C.c_int64),
+                ("calib_order", C.c_int)]
 
 
 class GemmDesc(C.Structure):
@@ -174,7 +177,7 @@ class Compar:
     """One runtime context (compar_init ... compar_terminate)."""
 
     def __init__(self, ngpu=-1, device=-1, sched=-1, calib_k=-1, calib_warmup=-1, perf_model_path=None,
-                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1):
+                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1, calib_order=-1):
         cfg = Config()
         lib.compar_config_default(C.byref(cfg))
         cfg.ngpu, cfg.device, cfg.sched = ngpu, device, sched
@@ -183,6 +186,7 @@ class Compar:
         cfg.perf_model_path = self._path
         cfg.bcast_chunks, cfg.builtins, cfg.virtual_clock = bcast_chunks, builtins, virtual_clock
         cfg.variant_mask = variant_mask
+        cfg.calib_order = calib_order
         self.ctx = C.c_void_p()
         self._callbacks = []     # keep ctypes thunks alive
         _check(lib.compar_init(C.byref(cfg), C.byref(self.ctx)))

@@ -21,6 +21,7 @@ struct GemmLaunch {
 };
 
 cudaError_t launch_simt_f32(const GemmLaunch &g);            // variant (a)
+cudaError_t launch_simt_bf16(const GemmLaunch &g);           // variant (a), BF16 operands
 cudaError_t launch_tma_f32(const GemmLaunch &g);             // variant (b)
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16);  // variant (c): tcgen05 TF32 / BF16
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16);  // variant (c), CTA-pair (cta_group::2)

@@ -11,6 +11,8 @@
 //     transposed (As[k][m]) so both operands are read as float4 along M / N;
 //   * register-prefetch double buffering: tile k+1 is loaded while tile k is multiplied;
 //   * any shape: edges are predicated (no padding required), transB supported.
+#include <cuda_bf16.h>
+
 #include "kernels.h"
 
 namespace compar {
@@ -18,6 +20,10 @@ namespace {
 
 constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
 
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// Four consecutive elements of row r starting at column c, widened to FP32 (exact for BF16).
 template <bool kVec>
 __device__ __forceinline__ float4 load_row4(const float *__restrict__ base, int64_t ld, int64_t r, int64_t c,
                                             int64_t R, int64_t C) {
@@ -35,7 +41,29 @@ __device__ __forceinline__ float4 load_row4(const float *__restrict__ base, int6
     return v;
 }
 
-template <bool kVecA, bool kVecB, bool kTransB>
+template <bool kVec>
+__device__ __forceinline__ float4 load_row4(const __nv_bfloat16 *__restrict__ base, int64_t ld, int64_t r, int64_t c,
+                                            int64_t R, int64_t C) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r >= R) return v;
+    const __nv_bfloat16 *p = base + r * ld + c;
+    if (kVec && c + 3 < C) {
+        const uint2 u = *reinterpret_cast<const uint2 *>(p);   // 4 x BF16 in one 8-byte load
+        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+        v = make_float4(lo.x, lo.y, hi.x, hi.y);
+    } else {
+        if (c + 0 < C) v.x = to_f32(p[0]);
+        if (c + 1 < C) v.y = to_f32(p[1]);
+        if (c + 2 < C) v.z = to_f32(p[2]);
+        if (c + 3 < C) v.w = to_f32(p[3]);
+    }
+    return v;
+}
+
+// T = float (variant a) or __nv_bfloat16 (simt_bf16: BF16 operands widened exactly to FP32 on load,
+// FP32 FFMA accumulation — the any-shape fallback of the BF16 precision class).
+template <typename T, bool kVecA, bool kVecB, bool kTransB>
 __global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
     __shared__ __align__(16) float As[2][BK][BM];
     __shared__ __align__(16) float Bs[2][BK][BN];
@@ -44,8 +72,8 @@ __global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
     const int tx = tid & 15, ty = tid >> 4;
     const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
-    const float *__restrict__ A = static_cast<const float *>(g.A);
-    const float *__restrict__ B = static_cast<const float *>(g.B);
+    const T *__restrict__ A = static_cast<const T *>(g.A);
+    const T *__restrict__ B = static_cast<const T *>(g.B);
 
     // Load mapping. A (m x k): thread -> row tid/2, k quad (tid&1)*4.
     const int a_r = tid >> 1, a_k = (tid & 1) * 4;
@@ -145,40 +173,47 @@ __global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
     }
 }
 
-template <bool VA, bool VB, bool TB>
+template <typename T, bool VA, bool VB, bool TB>
 cudaError_t launch_t(const GemmLaunch &g) {
     dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM));
-    simt_f32_kernel<VA, VB, TB><<<grid, THREADS, 0, g.stream>>>(g);
+    simt_f32_kernel<T, VA, VB, TB><<<grid, THREADS, 0, g.stream>>>(g);
     return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_simt(const GemmLaunch &g) {
+    if ((g.m + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
+    // 4-element vector loads need ld % 4 == 0 and a 4-element-aligned base (16 B FP32, 8 B BF16)
+    const uintptr_t va_mask = 4 * sizeof(T) - 1;
+    const bool va = ((g.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.A) & va_mask) == 0);
+    const bool vb = ((g.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.B) & va_mask) == 0);
+    if (g.transB) {
+        if (va && vb) return launch_t<T, true, true, true>(g);
+        if (va) return launch_t<T, true, false, true>(g);
+        if (vb) return launch_t<T, false, true, true>(g);
+        return launch_t<T, false, false, true>(g);
+    }
+    if (va && vb) return launch_t<T, true, true, false>(g);
+    if (va) return launch_t<T, true, false, false>(g);
+    if (vb) return launch_t<T, false, true, false>(g);
+    return launch_t<T, false, false, false>(g);
 }
 
 }  // namespace
 
-cudaError_t launch_simt_f32(const GemmLaunch &g) {
-    if ((g.m + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
-    const bool va = ((g.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
-    const bool vb = ((g.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
-    if (g.transB) {
-        if (va && vb) return launch_t<true, true, true>(g);
-        if (va) return launch_t<true, false, true>(g);
-        if (vb) return launch_t<false, true, true>(g);
-        return launch_t<false, false, true>(g);
-    }
-    if (va && vb) return launch_t<true, true, false>(g);
-    if (va) return launch_t<true, false, false>(g);
-    if (vb) return launch_t<false, true, false>(g);
-    return launch_t<false, false, false>(g);
-}
+cudaError_t launch_simt_f32(const GemmLaunch &g) { return launch_simt<float>(g); }
+cudaError_t launch_simt_bf16(const GemmLaunch &g) { return launch_simt<__nv_bfloat16>(g); }
 
 }  // namespace compar
 
 namespace compar {
 cudaError_t preload_simt_kernels() {
     cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, simt_f32_kernel<true, true, false>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<true, true, true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<false, false, false>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<false, false, true>);
+    cudaError_t e = cudaFuncGetAttributes(&a, simt_f32_kernel<float, true, true, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<float, true, true, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<float, false, false, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<float, false, false, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, simt_f32_kernel<__nv_bfloat16, true, true, false>);
     return e;
 }
 }  // namespace compar

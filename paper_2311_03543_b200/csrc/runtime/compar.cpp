@@ -236,7 +236,8 @@ bool admits(compar_target t, compar_dtype dt, compar_compute cp) {
         case COMPAR_TGT_TCW_TF32: return dt == COMPAR_F32 && cp == COMPAR_COMPUTE_TF32;
         case COMPAR_TGT_TC_BF16:
         case COMPAR_TGT_TC2_BF16:
-        case COMPAR_TGT_TCW_BF16: return dt == COMPAR_BF16 && cp == COMPAR_COMPUTE_BF16;
+        case COMPAR_TGT_TCW_BF16:
+        case COMPAR_TGT_SIMT_BF16: return dt == COMPAR_BF16 && cp == COMPAR_COMPUTE_BF16;
     }
     return false;
 }
@@ -251,8 +252,9 @@ struct Plan {
 bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, const Plan &plan) {
     if (t == COMPAR_TGT_USER) return true;
     const int64_t mrows = plan.key.m;
-    if ((t == COMPAR_TGT_SIMT_F32 || t == COMPAR_TGT_TMA_F32) && (mrows + 127) / 128 > 65535) return false;
-    if (t == COMPAR_TGT_SIMT_F32) return true;
+    const bool simt = t == COMPAR_TGT_SIMT_F32 || t == COMPAR_TGT_SIMT_BF16;
+    if ((simt || t == COMPAR_TGT_TMA_F32) && (mrows + 127) / 128 > 65535) return false;
+    if (simt) return true;
     const int eb = (t == COMPAR_TGT_TC_BF16 || t == COMPAR_TGT_TC2_BF16 || t == COMPAR_TGT_TCW_BF16) ? 2 : 4;
     if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;
     if ((d->lda * eb) % 16 != 0 || (d->ldb * eb) % 16 != 0) return false;
@@ -447,6 +449,7 @@ compar_status run_builtin(Ctx *c, compar_target t, const compar_gemm_desc *d, co
         case COMPAR_TGT_TC2_BF16: e = launch_tc_gemm_2sm(g, true); break;
         case COMPAR_TGT_TCW_TF32: e = launch_tc_gemm_2sm_wide(g, false); break;
         case COMPAR_TGT_TCW_BF16: e = launch_tc_gemm_2sm_wide(g, true); break;
+        case COMPAR_TGT_SIMT_BF16: e = launch_simt_bf16(g); break;
         default: return fail(COMPAR_E_INVALID, "not a built-in target");
     }
     c->stats.launches++;
@@ -667,6 +670,7 @@ void compar_config_default(compar_config *cfg) {
     cfg->builtins = -1;
     cfg->virtual_clock = 0;
     cfg->variant_mask = -1;
+    cfg->calib_order = -1;
 }
 
 const char *compar_last_error(void *) { return t_err.c_str(); }
@@ -690,6 +694,12 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     if (cfg.calib_k < 0) cfg.calib_k = env_int("COMPAR_CALIB_K", 3);
     if (cfg.calib_warmup < 0) cfg.calib_warmup = env_int("COMPAR_CALIB_WARMUP", 1);
     if (cfg.bcast_chunks < 0) cfg.bcast_chunks = env_int("COMPAR_BCAST_CHUNKS", 8);
+    if (cfg.calib_order < 0) {
+        const char *s = std::getenv("COMPAR_CALIB_ORDER");
+        cfg.calib_order = (s && std::strcmp(s, "interleaved") == 0) ? COMPAR_CALIB_INTERLEAVED : COMPAR_CALIB_BLOCKED;
+    }
+    if (cfg.calib_order != COMPAR_CALIB_INTERLEAVED && cfg.calib_order != COMPAR_CALIB_BLOCKED)
+        return fail(COMPAR_E_INVALID, "calib_order must be INTERLEAVED (0) or BLOCKED (1)");
     if (cfg.builtins < 0) cfg.builtins = 1;
     if (cfg.variant_mask < 0) {
         const char *s = std::getenv("COMPAR_VARIANT_MASK");
@@ -700,6 +710,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     c->virt = cfg.virtual_clock != 0;
     c->hist.calib_k = cfg.calib_k;
     c->hist.calib_warmup = cfg.calib_warmup;
+    c->hist.calib_blocked = cfg.calib_order == COMPAR_CALIB_BLOCKED;
     const char *pp = cfg.perf_model_path ? cfg.perf_model_path : std::getenv("COMPAR_PERF_MODEL");
     if (pp) c->perf_path = pp;
     c->cfg.perf_model_path = nullptr;
@@ -749,6 +760,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         compar_register_variant(c, "gemm", "tc_bf16_2sm", COMPAR_TGT_TC2_BF16, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_tf32_2sm_w", COMPAR_TGT_TCW_TF32, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_bf16_2sm_w", COMPAR_TGT_TCW_BF16, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "simt_bf16", COMPAR_TGT_SIMT_BF16, nullptr, nullptr, &id);
     }
     *ctx = c;
     if (!c->perf_path.empty()) {
@@ -807,7 +819,7 @@ compar_status compar_register_variant(void *ctx, const char *iface, const char *
     if (!name || !*name || std::strlen(name) > 63) return fail(COMPAR_E_INVALID, "bad variant name");
     for (const char *p = name; *p; ++p)
         if (*p == ' ' || *p == '\t' || *p == '\n') return fail(COMPAR_E_INVALID, "variant name has whitespace");
-    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_TCW_BF16) return fail(COMPAR_E_INVALID, "unknown target");
+    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_SIMT_BF16) return fail(COMPAR_E_INVALID, "unknown target");
     if (target == COMPAR_TGT_USER && !fn) return fail(COMPAR_E_INVALID, "USER variant needs a launch function");
     if (target != COMPAR_TGT_USER && c->virt) return fail(COMPAR_E_INVALID, "built-in targets need CUDA");
     std::lock_guard<std::mutex> lk(c->mu);

@@ -24,12 +24,19 @@ bool History::calibrating(const std::vector<int> &ids, const Key &k) {
 
 int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode) {
     const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
-    // Calibration: least-seen eligible variant, first in registry order on ties.
+    // Calibration.  Interleaved: least-seen eligible variant, first in registry order on ties.
+    // Blocked: first variant (in eligibility order) that has not completed its W + K executions.
     int best = -1;
     int64_t best_seen = 0;
     for (size_t i = 0; i < ids.size(); ++i) {
         const int64_t s = rec(ids[i], k).seen;
-        if (best < 0 || s < best_seen) {
+        if (calib_blocked) {
+            if (s < need) {
+                best = static_cast<int>(i);
+                best_seen = s;
+                break;
+            }
+        } else if (best < 0 || s < best_seen) {
             best = static_cast<int>(i);
             best_seen = s;
         }

@@ -7,7 +7,8 @@
 //     128-bit integer sums of ns and ns^2, min — the mean is order-independent and the
 //     argmin comparison exact (cross-multiplication), so decisions are deterministic;
 //   * calibration: while some eligible variant has seen < W + K, pick argmin seen
-//     (ties -> lowest registry index); the first W executions are warm-ups (dropped);
+//     (ties -> lowest registry index; "interleaved") or the first variant in eligibility order with
+//     seen < W + K ("blocked", R19); the first W executions of a variant are warm-ups (dropped);
 //   * model: argmin mean ns over eligible variants with count > 0 (ties -> lowest index).
 #pragma once
 #include <cstdint>
@@ -45,6 +46,7 @@ class History {
 public:
     int calib_warmup = 1;
     int calib_k = 3;
+    bool calib_blocked = true;
 
     // Records belong to variant NAMES (so a loaded perf model applies to whichever registry index
     // that name gets); names are interned to small ids for the hot path.

@@ -27,7 +27,9 @@ VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tc_tf32_2sm": (cm.F32, cm.COMPUTE_TF32, 5e-3),
             "tc_bf16_2sm": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
             "tc_tf32_2sm_w": (cm.F32, cm.COMPUTE_TF32, 5e-3),
-            "tc_bf16_2sm_w": (cm.BF16, cm.COMPUTE_BF16, 5e-3)}
+            "tc_bf16_2sm_w": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
+            # FP32 accumulation of exactly-widened BF16 operands: held to the strict-FP32 bound
+            "simt_bf16": (cm.BF16, cm.COMPUTE_BF16, 1e-5)}
 
 SHAPES = [(1, 1, 1), (7, 13, 5), (64, 64, 64), (65, 127, 129), (129, 257, 70), (128, 256, 64),
           (300, 520, 1000), (1000, 777, 333), (257, 1, 100), (1, 300, 4097)]

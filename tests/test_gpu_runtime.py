@@ -65,10 +65,11 @@ def test_real_event_selector_crossover(golden):
     ctx.terminate()
 
 
-def test_config1_calibration_trace():
-    """Config 1 (64^3 FP32, COMPUTE_TF32): 3 eligible variants x (1 warm-up + 3 timed) = 12
-    calibration runs in registry order, then model mode picks the measured argmin."""
-    ctx = cm.Compar()
+@pytest.mark.parametrize("order", [cm.CALIB_INTERLEAVED, cm.CALIB_BLOCKED])
+def test_config1_calibration_trace(order):
+    """Config 1 (64^3 FP32, COMPUTE_TF32): each eligible variant x (1 warm-up + 3 timed)
+    calibration runs in registry order (interleaved or blocked), then model mode picks the argmin."""
+    ctx = cm.Compar(calib_order=order)
     m = 64
     A = device_matrix(gen.TAG_A, m, m)
     B = device_matrix(gen.TAG_B, m, m)
@@ -78,8 +79,12 @@ def test_config1_calibration_trace():
     E = [v for v, (_, tgt) in enumerate(ctx.variants()) if tgt in tf32_ok]
     n_cal = 4 * len(E)
     trace = [ctx.run(d) for _ in range(n_cal + 1)]
-    assert [r.variant for r in trace[:n_cal]] == E * 4
-    assert [r.mode for r in trace[:len(E)]] == [cm.MODE_WARMUP] * len(E)
+    if order == cm.CALIB_INTERLEAVED:
+        assert [r.variant for r in trace[:n_cal]] == E * 4
+        assert [r.mode for r in trace[:len(E)]] == [cm.MODE_WARMUP] * len(E)
+    else:
+        assert [r.variant for r in trace[:n_cal]] == [v for v in E for _ in range(4)]
+        assert [r.mode for r in trace[:n_cal]] == ([cm.MODE_WARMUP] + [cm.MODE_CALIB] * 3) * len(E)
     assert trace[n_cal].mode == cm.MODE_MODEL
     means = [ctx.history(v, d).mean_ns for v in E]
     assert trace[n_cal].variant == E[int(np.argmin(means))]

@@ -78,11 +78,12 @@ def desc(m, n=None, k=None, **kw):
     return cm.make_desc(m, n, k, lda=k, ldb=n, ldc_in=n, ldc_out=n, alpha=1.5, beta=0.5, **kw)
 
 
-def test_virtual_stream_matches_selector_oracle():
+@pytest.mark.parametrize("order", [cm.CALIB_INTERLEAVED, cm.CALIB_BLOCKED])
+def test_virtual_stream_matches_selector_oracle(order):
     """Random mixed stream: every (variant, mode) decision of the C runtime equals the oracle's."""
     costs = [lambda m, n, k: 100 * m + 7, lambda m, n, k: 30000 + 20 * m, lambda m, n, k: 5000 + 60 * m]
-    ctx, _ = vctx(costs)
-    orc = so.SelectorOracle(3)
+    ctx, _ = vctx(costs, calib_order=order)
+    orc = so.SelectorOracle(3, blocked=order == cm.CALIB_BLOCKED)
     rnd = random.Random(7)
     sizes = [64, 256, 555, 1024, 4096]
     pending = []
@@ -113,10 +114,11 @@ def test_virtual_stream_matches_selector_oracle():
     ctx.terminate()
 
 
-def test_every_decision_matches_select_then_submit():
+@pytest.mark.parametrize("order", [cm.CALIB_INTERLEAVED, cm.CALIB_BLOCKED])
+def test_every_decision_matches_select_then_submit(order):
     costs = [lambda m, n, k: 1000, lambda m, n, k: 900, lambda m, n, k: 1100]
-    ctx, _ = vctx(costs)
-    orc = so.SelectorOracle(3)
+    ctx, _ = vctx(costs, calib_order=order)
+    orc = so.SelectorOracle(3, blocked=order == cm.CALIB_BLOCKED)
     d = desc(128)
     for _ in range(20):
         sel = ctx.select(d)
@@ -276,7 +278,7 @@ def test_predict_scheduler_matches_oracle():
             lambda m, n, k: 4_000 + 2_500.0 * 2 * m * n * k * 1e-9,
             lambda m, n, k: 20_000 + 1_200.0 * 2 * m * n * k * 1e-9]
     ctx, _ = vctx(cost, sched=cm.SCHED_PREDICT)
-    orc = so.SelectorOracle(3)
+    orc = so.SelectorOracle(3, blocked=True)      # runtime default calibration order (R19)
 
     def key(s):
         return (s, s, s, so.F32, so.COMPUTE_F32_STRICT, 0, 0)

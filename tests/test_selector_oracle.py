@@ -39,6 +39,18 @@ def test_config1_calibration_plan():
     assert trace[12] == (1, so.MODE_MODEL)
 
 
+def test_blocked_calibration_plan():
+    """R19 blocked order: W + K executions of each variant back to back, in eligibility order."""
+    sel = so.SelectorOracle(3, blocked=True)
+    trace = run_stream(sel, "k", [2, 0, 1], lambda v: [30, 10, 20][v], 13)
+    assert [v for v, _ in trace[:12]] == [2] * 4 + [0] * 4 + [1] * 4
+    assert [m for _, m in trace[:12]] == ([so.MODE_WARMUP] + [so.MODE_CALIB] * 3) * 3
+    assert trace[12] == (1, so.MODE_MODEL)
+    # a variant that becomes eligible later is calibrated next, as a block
+    trace = run_stream(sel, "k", [2, 0, 1, 3], lambda v: [30, 10, 20, 5][v], 5)
+    assert [v for v, _ in trace] == [3, 3, 3, 3, 3] and trace[-1][1] == so.MODE_MODEL
+
+
 def test_spec_s370_closed_form_crossover(golden):
     """cost0 = 0.1n, cost1 = 50 + 0.01n -> n=256 -> 0, n=4096 -> 1."""
     g = golden("selector_crossover.txt")
@@ -96,6 +108,7 @@ def test_admits_table():
     assert el(f32, so.COMPUTE_F32_STRICT) == [0, 1]
     assert el(f32, so.COMPUTE_TF32) == [0, 1, 2]
     assert el(bf16, so.COMPUTE_BF16) == [3]
+    assert so.admits(so.TGT_SIMT_BF16, bf16, so.COMPUTE_BF16) and not so.admits(so.TGT_SIMT_BF16, f32, so.COMPUTE_TF32)
     assert el(bf16, so.COMPUTE_TF32) == []
     assert so.tma_ok(4, [0, 256], [64, 8]) and not so.tma_ok(4, [4], [64]) and not so.tma_ok(2, [0], [9])
 

@@ -92,7 +92,7 @@ def test_spmd_world2_rank_consistent_decisions():
             offs = partition_rows(m, world)
             assert (row0, nrows) == (offs[rank], offs[rank + 1] - offs[rank])
     # and equal the selector oracle fed with max-over-ranks costs
-    orc = so.SelectorOracle(2)
+    orc = so.SelectorOracle(2, blocked=True)      # the runtime's default calibration order (R19)
     for m, (v, mode, ns) in zip(SIZES, out[0][0]):
         offs = partition_rows(m, world)
         key = offs[1] - offs[0]
