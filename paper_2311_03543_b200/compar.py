@@ -56,7 +56,8 @@ class Panel(C.Structure):
 class Report(C.Structure):
     _fields_ = [("task", C.c_uint64), ("variant", C.c_int), ("mode", C.c_int), ("warmup", C.c_int),
                 ("status", C.c_int), ("npanels", C.c_int), ("ns", C.c_int64),
-                ("panel_ns", C.c_int64 * MAX_PANELS), ("bcast_ns", C.c_int64), ("total_ns", C.c_int64)]
+                ("panel_ns", C.c_int64 * MAX_PANELS), ("bcast_ns", C.c_int64), ("total_ns", C.c_int64),
+                ("batch", C.c_int)]
 
 
 class Record(C.Structure):

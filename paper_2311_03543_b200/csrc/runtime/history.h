@@ -38,6 +38,7 @@ struct Record {
     unsigned __int128 sum_ns = 0;
     unsigned __int128 sumsq_ns = 0;
     int64_t min_ns = 0;
+    int64_t warm_ns = 0;  // last discarded warm-up time (sizes the calibration batch, a8 / c13)
 };
 
 enum Mode { kWarmup = 0, kCalib = 1, kModel = 2, kEager = 3, kHint = 4, kNoop = 5, kPredict = 6 };

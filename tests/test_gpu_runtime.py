@@ -89,5 +89,40 @@ def test_config1_calibration_trace(order):
     means = [ctx.history(v, d).mean_ns for v in E]
     assert trace[n_cal].variant == E[int(np.argmin(means))]
     st = ctx.stats()
-    assert st.launches == n_cal + 1 and st.harvested == 3 * len(E) + 1
+    assert st.launches == sum(r.batch for r in trace) and st.harvested == 3 * len(E) + 1
+    ctx.terminate()
+
+
+@pytest.mark.parametrize("compute,dt", [(cm.COMPUTE_TF32, "f32"), (cm.COMPUTE_BF16, "bf16")])
+def test_batched_calibration_timing(compute, dt):
+    """a8 / c13: timed calibration runs of microsecond kernels repeat the launch r > 1 times per
+    event pair (warm-ups and model runs do not), and C_out is still written exactly once per task:
+    in place, C_{t+1} = 2AB - C_t on integer inputs is checked bitwise after every execution."""
+    from oracle import gemm as og
+    from tests._gpu_util import to_device, to_host_f64
+    m = n = k = 64
+    A = gen.matrix(gen.TAG_A, m, k, gen.DIST_I, dt)
+    B = gen.matrix(gen.TAG_B, k, n, gen.DIST_I, dt)
+    C = gen.matrix(gen.TAG_C, m, n, gen.DIST_I, "f32").astype(np.float64)
+    Ad, Bd, Cd = to_device(A, dt), to_device(B, dt), to_device(C.astype(np.float32))
+    ctx = cm.Compar()
+    d = cm.make_desc(m, n, k, A=Ad, B=Bd, C_in=Cd, C_out=Cd, alpha=2.0, beta=-1.0,
+                     in_dtype=cm.BF16 if dt == "bf16" else cm.F32, compute=compute)
+    reps = []
+    for _ in range(40):
+        r = ctx.run(d)
+        reps.append(r)
+        C = og.gemm(A, B, C, alpha=2.0, beta=-1.0, dtype=dt)
+        np.testing.assert_array_equal(to_host_f64(Cd), C)
+        if r.mode == cm.MODE_MODEL:
+            break
+    assert reps[-1].mode == cm.MODE_MODEL and reps[-1].batch == 1
+    assert all(r.batch == 1 for r in reps if r.mode == cm.MODE_WARMUP)
+    # the c13 rule: r = ceil(50 us / warm-up ns) (<= 64) when the variant's warm-up ran < 20 us
+    warm = {r.variant: r.ns for r in reps if r.mode == cm.MODE_WARMUP}
+    cal = [r for r in reps if r.mode == cm.MODE_CALIB]
+    expect = {v: (min(64, -(-50000 // ns)) if ns < 20000 else 1) for v, ns in warm.items()}
+    assert [r.batch for r in cal] == [expect[r.variant] for r in cal]
+    assert any(r.batch > 1 for r in cal)
+    assert ctx.stats().launches == sum(r.batch for r in reps)
     ctx.terminate()
