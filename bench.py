@@ -339,7 +339,7 @@ def main():
                "gpu_launches": int(launches),
                "selector": {"calibration_runs_before_timing": calib_runs, "chosen": chosen,
                             "variants_in_timed_region": used,
-                            "eligible": [n for n, t in ctx.variants() if t in (cm.TGT_TC_BF16, cm.TGT_TC2_BF16, cm.TGT_TCW_BF16, cm.TGT_SIMT_BF16)]},
+                            "eligible": [n for n, t in ctx.variants() if t in cm.TARGETS_BF16]},
                "clocks": clocks, "e2e": e2e}
     if world > 1:
         dist.barrier()

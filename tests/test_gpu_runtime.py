@@ -75,7 +75,7 @@ def test_config1_calibration_trace(order):
     B = device_matrix(gen.TAG_B, m, m)
     Cd = device_matrix(gen.TAG_C, m, m)
     d = cm.make_desc(m, m, m, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, compute=cm.COMPUTE_TF32)
-    tf32_ok = {cm.TGT_SIMT_F32, cm.TGT_TMA_F32, cm.TGT_TC_TF32, cm.TGT_TC2_TF32, cm.TGT_TCW_TF32}
+    tf32_ok = set(cm.TARGETS_TF32)
     E = [v for v, (_, tgt) in enumerate(ctx.variants()) if tgt in tf32_ok]
     n_cal = 4 * len(E)
     trace = [ctx.run(d) for _ in range(n_cal + 1)]

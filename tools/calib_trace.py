@@ -43,7 +43,7 @@ def main():
     ctx = cm.Compar()
     names = [n for n, _ in ctx.variants()]
     E = [i for i, (_, t) in enumerate(ctx.variants())
-         if t in (cm.TGT_TC_BF16, cm.TGT_TC2_BF16, cm.TGT_TCW_BF16, cm.TGT_SIMT_BF16)]
+         if t in cm.TARGETS_BF16]
 
     def hinted(seq):
         tr = []

@@ -29,9 +29,9 @@ from gen.device import device_matrix  # noqa: E402
 from paper_2311_03543_b200 import compar as cm  # noqa: E402
 
 R = 10
-TF32_T = {cm.TGT_SIMT_F32, cm.TGT_TMA_F32, cm.TGT_TC_TF32, cm.TGT_TC2_TF32, cm.TGT_TCW_TF32}
-STRICT_T = {cm.TGT_SIMT_F32, cm.TGT_TMA_F32}
-BF16_T = {cm.TGT_TC_BF16, cm.TGT_TC2_BF16, cm.TGT_TCW_BF16, cm.TGT_SIMT_BF16}
+TF32_T = set(cm.TARGETS_TF32)
+STRICT_T = set(cm.TARGETS_STRICT)
+BF16_T = set(cm.TARGETS_BF16)
 
 
 class Problem:
