@@ -124,7 +124,13 @@ typedef struct {
                                    variant (R19: on the power-capped B200 a sample taken
                                    right after a low-power kernel runs at boost clocks).
                                    <0: COMPAR_CALIB_ORDER=interleaved|blocked, else BLOCKED        */
+    int lanes;                  /* task-parallel world: library streams (workers) per GPU; model-
+                                   mode samples of lanes > 1 are not added to the history (they
+                                   overlap other lanes) and calibration executions run alone.
+                                   <1: COMPAR_LANES or 1                                           */
 } compar_config;
+
+enum { COMPAR_WORLD_LOCAL = 0, COMPAR_WORLD_PANELS = 1, COMPAR_WORLD_TASKS = 2 };
 
 enum { COMPAR_CALIB_INTERLEAVED = 0, COMPAR_CALIB_BLOCKED = 1 };
 
@@ -154,7 +160,17 @@ typedef struct {
                                    [o_r, o_{r+1}) of compar_partition_rows(m, nranks)), B is read
                                    on rank 0 and broadcast with NCCL (in bcast_chunks N-slabs,
                                    overlapped with the slab GEMMs) to the other ranks.  Without a
-                                   communicator world = 1 is a 1-rank world.  Combines with HOST. */
+                                   communicator world = 1 is a 1-rank world.  Combines with HOST.
+                                   2 (COMPAR_WORLD_TASKS): task-parallel world:
+                                   the WHOLE task runs on one worker = (rank, lane) chosen by the
+                                   dmda placer (expected completion = worker ready time +
+                                   predicted ns, dependencies tracked on the byte ranges of A, B,
+                                   C_in (read) and C_out (written)).  Every rank submits the same
+                                   task sequence with pointers to its own copies; only the owner
+                                   launches, on a library lane stream that first waits for
+                                   `stream`.  C_out is then valid on the owner rank only
+                                   (report.rank).  compar_sync is collective in this mode (all
+                                   ranks, same order).  Device memory only.                     */
     void *B_replica;            /* world mode, rank != 0: device workspace of >= k*n elements that
                                    receives B (its layout afterwards is the library's slab layout,
                                    unspecified to the caller); NULL: a library-owned buffer       */
@@ -193,6 +209,7 @@ typedef struct {
                                    repeats the kernel r = ceil(50 us / warm-up) times (<= 64) and
                                    records span / r; the r - 1 extra
                                    launches write a library scratch C, so C_out is written once */
+    int rank, lane;             /* worker that ran the task (task-parallel world); else rank, 0    */
 } compar_report;
 
 typedef struct {
@@ -263,6 +280,10 @@ compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, 
  * virtual-clock mode; fn = NULL restores the default. */
 typedef void (*compar_reduce_fn)(int64_t *value, void *user);
 compar_status compar_set_reduce_hook(void *ctx, compar_reduce_fn fn, void *user);
+/* Same for the task-parallel world's sample exchange: in-place element-wise max of buf[0..n)
+ * over all ranks (the owner of each task contributes its ns, the others -1). */
+typedef void (*compar_reduce_n_fn)(int64_t *buf, int n, void *user);
+compar_status compar_set_reduce_n_hook(void *ctx, compar_reduce_n_fn fn, void *user);
 
 /* ---- introspection / fixtures ---- */
 compar_status compar_stats_get(void *ctx, compar_stats *out);

@@ -30,6 +30,7 @@ TARGETS_BF16 = (TGT_TC_BF16, TGT_TC2_BF16, TGT_TCW_BF16, TGT_SIMT_BF16)
 MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
 SCHED_HISTORY, SCHED_EAGER, SCHED_PREDICT = 0, 1, 2
 CALIB_INTERLEAVED, CALIB_BLOCKED = 0, 1
+WORLD_LOCAL, WORLD_PANELS, WORLD_TASKS = 0, 1, 2
 MEM_DEVICE, MEM_HOST = 0, 1
 TASK_ALL = (1 << 64) - 1
 MAX_PANELS = 8
@@ -40,7 +41,7 @@ class Config(C.Structure):
     _fields_ = [("ngpu", C.c_int), ("device", C.c_int), ("sched", C.c_int), ("calib_k", C.c_int),
                 ("calib_warmup", C.c_int), ("perf_model_path", C.c_char_p), ("bcast_chunks", C.c_int),
                 ("builtins", C.c_int), ("virtual_clock", C.c_int), ("variant_mask", C.c_int64),
-                ("calib_order", C.c_int)]
+                ("calib_order", C.c_int), ("lanes", C.c_int)]
 
 
 class GemmDesc(C.Structure):
@@ -61,7 +62,7 @@ class Report(C.Structure):
     _fields_ = [("task", C.c_uint64), ("variant", C.c_int), ("mode", C.c_int), ("warmup", C.c_int),
                 ("status", C.c_int), ("npanels", C.c_int), ("ns", C.c_int64),
                 ("panel_ns", C.c_int64 * MAX_PANELS), ("bcast_ns", C.c_int64), ("total_ns", C.c_int64),
-                ("batch", C.c_int)]
+                ("batch", C.c_int), ("rank", C.c_int), ("lane", C.c_int)]
 
 
 class Record(C.Structure):
@@ -77,11 +78,13 @@ class Stats(C.Structure):
 GEMM_FN = C.CFUNCTYPE(C.c_int, C.POINTER(GemmDesc), C.POINTER(Panel), C.c_void_p, C.c_void_p,
                       C.POINTER(C.c_int64))
 REDUCE_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_void_p)
+REDUCE_N_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_int, C.c_void_p)
 
 EXPORTS = ["compar_config_default", "compar_init", "compar_terminate", "compar_register_variant",
            "compar_variant_count", "compar_variant_info", "compar_gemm_submit", "compar_sync", "compar_select",
            "compar_perf_save", "compar_perf_load", "compar_history_get", "compar_partition_rows",
-           "compar_comm_unique_id", "compar_comm_init", "compar_set_reduce_hook", "compar_stats_get",
+           "compar_comm_unique_id", "compar_comm_init", "compar_set_reduce_hook", "compar_set_reduce_n_hook",
+           "compar_stats_get",
            "compar_last_error", "compar_debug_spin"]
 
 
@@ -107,6 +110,7 @@ def _load():
         "compar_comm_unique_id": (st, [vp, i]),
         "compar_comm_init": (st, [vp, i, i, vp, i]),
         "compar_set_reduce_hook": (st, [vp, REDUCE_FN, vp]),
+        "compar_set_reduce_n_hook": (st, [vp, REDUCE_N_FN, vp]),
         "compar_stats_get": (st, [vp, C.POINTER(Stats)]),
         "compar_last_error": (C.c_char_p, [vp]),
         "compar_debug_spin": (st, [vp, i64]),
@@ -182,7 +186,7 @@ class Compar:
     """One runtime context (compar_init ... compar_terminate)."""
 
     def __init__(self, ngpu=-1, device=-1, sched=-1, calib_k=-1, calib_warmup=-1, perf_model_path=None,
-                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1, calib_order=-1):
+                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1, calib_order=-1, lanes=-1):
         cfg = Config()
         lib.compar_config_default(C.byref(cfg))
         cfg.ngpu, cfg.device, cfg.sched = ngpu, device, sched
@@ -192,6 +196,7 @@ class Compar:
         cfg.bcast_chunks, cfg.builtins, cfg.virtual_clock = bcast_chunks, builtins, virtual_clock
         cfg.variant_mask = variant_mask
         cfg.calib_order = calib_order
+        cfg.lanes = lanes
         self.ctx = C.c_void_p()
         self._callbacks = []     # keep ctypes thunks alive
         _check(lib.compar_init(C.byref(cfg), C.byref(self.ctx)))
@@ -273,6 +278,12 @@ class Compar:
         cfn = REDUCE_FN(fn) if fn is not None else REDUCE_FN()
         self._callbacks.append(cfn)
         _check(lib.compar_set_reduce_hook(self.ctx, cfn, None), self.ctx)
+
+    def set_reduce_n_hook(self, fn):
+        """fn(buf: POINTER(c_int64), n: int, user) -> None: in-place element-wise max over ranks."""
+        cfn = REDUCE_N_FN(fn) if fn is not None else REDUCE_N_FN()
+        self._callbacks.append(cfn)
+        _check(lib.compar_set_reduce_n_hook(self.ctx, cfn, None), self.ctx)
 
     def stats(self) -> Stats:
         s = Stats()

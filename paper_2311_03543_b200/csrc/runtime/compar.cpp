@@ -7,7 +7,9 @@
 //                                unregister-after-wait rule;
 //   * history selector        <- "the STARPU decision-making process relies on ... models"
 //                                (P:224), algorithm in history.{h,cpp};
-//   * row panels + NCCL bcast <- BASELINE.json north star (multi-GPU, one process per GPU).
+//   * row panels + NCCL bcast <- BASELINE.json north star (multi-GPU, one process per GPU);
+//   * task-parallel world     <- StarPU "mapping, scheduling" across workers, dmda
+//                                placement in dmda.{h,cpp}.
 #include "compar.h"
 
 #include <cuda_runtime.h>
@@ -28,6 +30,7 @@
 #include <vector>
 
 #include "../kernels/kernels.h"
+#include "dmda.h"
 #include "history.h"
 
 namespace compar {
@@ -71,6 +74,12 @@ struct Task {
     cudaEvent_t begin = nullptr, end = nullptr, bc0 = nullptr, bc1 = nullptr;
     std::vector<cudaEvent_t> extra;  // per-slab broadcast events (world mode)
     bool world = false;
+    // task-parallel world (world = COMPAR_WORLD_TASKS)
+    bool tasks = false;
+    bool remote = false;   // placed on another rank: no launch here, sample arrives by exchange
+    int owner = 0, lane = 0;
+    bool have_xns = false;
+    int64_t xns = 0;       // exchanged sample (-2: the owner's execution failed)
 };
 
 struct Ctx {
@@ -104,6 +113,17 @@ struct Ctx {
     // host-memory pipeline
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     int host_chunks = 8;
+    // task-parallel world
+    Placer placer;
+    bool placer_ready = false;
+    std::vector<cudaStream_t> lane_streams;
+    std::vector<cudaEvent_t> lane_done;
+    cudaEvent_t sub_event = nullptr, cal_fence = nullptr;
+    bool cal_fence_set = false;
+    compar_reduce_n_fn reduce_n_hook = nullptr;
+    void *reduce_n_user = nullptr;
+    int64_t *xbuf = nullptr;  // device buffer of the NCCL sample exchange
+    size_t xbuf_n = 0;
     // batched calibration timing (a8 / c13)
     int64_t batch_below_ns = 20000;
     void *scratch = nullptr;  // C_out of the r - 1 extra launches
@@ -210,13 +230,16 @@ compar_status validate(Ctx *c, const compar_gemm_desc *d) {
     if (d->transB != 0 && d->transB != 1) return fail(COMPAR_E_INVALID, "transB must be 0 or 1");
     if (d->mem != COMPAR_MEM_DEVICE && d->mem != COMPAR_MEM_HOST) return fail(COMPAR_E_INVALID, "bad mem");
     if (d->panels < 0 || d->panels > COMPAR_MAX_PANELS) return fail(COMPAR_E_INVALID, "panels out of range");
+    if (d->world < COMPAR_WORLD_LOCAL || d->world > COMPAR_WORLD_TASKS) return fail(COMPAR_E_INVALID, "bad world");
     if (d->world && d->panels > 1) return fail(COMPAR_E_INVALID, "world and loopback panels are exclusive");
+    if (d->world == COMPAR_WORLD_TASKS && d->mem != COMPAR_MEM_DEVICE)
+        return fail(COMPAR_E_INVALID, "the task-parallel world takes device buffers");
     // world = 1 without compar_comm_init is a 1-rank world (plain launch, or the loopback pipeline)
     if (d->variant_hint < -1 || d->variant_hint >= static_cast<int>(c->variants.size()))
         return fail(COMPAR_E_INVALID, "variant_hint out of range");
     if (d->m == 0 || d->n == 0) return COMPAR_OK;
     if (d->k > 0 && d->alpha != 0.f) {
-        if (!c->virt && (!d->A || (!d->B && !(d->world && c->rank != 0))))
+        if (!c->virt && (!d->A || (!d->B && !(d->world == COMPAR_WORLD_PANELS && c->rank != 0))))
             return fail(COMPAR_E_INVALID, "A/B NULL");
         if (d->lda < d->k) return fail(COMPAR_E_INVALID, "lda < k");
         if (d->ldb < (d->transB ? d->k : d->n)) return fail(COMPAR_E_INVALID, "ldb too small");
@@ -308,7 +331,7 @@ compar_status build_plan(Ctx *c, const compar_gemm_desc *d, Plan &plan, const vo
     const int eb = elem_bytes(d->in_dtype);
     plan.panels.clear();
     std::vector<int64_t> offs;
-    if (d->world) {
+    if (d->world == COMPAR_WORLD_PANELS) {
         partition(d->m, c->nranks, offs);
         compar_panel p{};
         p.index = c->rank;
@@ -349,12 +372,95 @@ compar_status build_plan(Ctx *c, const compar_gemm_desc *d, Plan &plan, const vo
 // ---------------------------------------------------------------- harvest
 compar_status finish_task(Ctx *c, Task &t, compar_report *rep);
 
+// Waits for a local task and returns its history sample: max over panels of the kernel span
+// (batched calibration: span / r; host pipeline: sum of the chunk kernels).
+int64_t measure(Ctx *c, Task &t, compar_report *rep) {
+    int64_t sample = 0;
+    cudaEvent_t last = t.end ? t.end : (t.panels.empty() ? nullptr : t.panels.back().stop);
+    if (!c->virt && last) {
+        cudaError_t e = cudaEventSynchronize(last);
+        if (e != cudaSuccess && t.status == COMPAR_OK) {
+            t.status = COMPAR_E_TASK_FAILED;
+            t_err = std::string("task execution failed: ") + cudaGetErrorString(e);
+        }
+    }
+    for (size_t i = 0; i < t.panels.size(); ++i) {
+        int64_t ns = 0;
+        if (c->virt) {
+            ns = t.panels[i].virtual_ns;
+        } else if (!t.panels[i].sub.empty()) {  // host pipeline: sum of the chunk kernels
+            for (auto &s : t.panels[i].sub) ns += elapsed_ns(s.first, s.second);
+        } else if (t.panels[i].start) {
+            const int64_t r = t.panels[i].batch;
+            ns = (elapsed_ns(t.panels[i].start, t.panels[i].stop) + r / 2) / r;
+            if (rep) rep->batch = std::max(rep->batch, t.panels[i].batch);
+        }
+        if (rep && i < COMPAR_MAX_PANELS) rep->panel_ns[i] = ns;
+        sample = std::max(sample, ns);
+    }
+    return sample;
+}
+
+// Task-parallel world, several ranks: the owner of each task contributes its sample, the others
+// -1, and an element-wise max over the ranks gives every rank the same samples (so the replicated
+// history and placer stay identical).  Collective: every rank calls it with the same task list.
+compar_status exchange_samples(Ctx *c, const std::vector<Task *> &ts) {
+    if (ts.empty()) return COMPAR_OK;
+    std::vector<int64_t> buf(ts.size(), -1);
+    for (size_t i = 0; i < ts.size(); ++i) {
+        Task &t = *ts[i];
+        if (t.remote) continue;
+        const int64_t ns = measure(c, t, nullptr);
+        buf[i] = t.status == COMPAR_OK ? ns : -2;
+    }
+    if (c->nranks > 1) {
+        const int n = static_cast<int>(buf.size());
+        if (c->reduce_n_hook) {
+            c->reduce_n_hook(buf.data(), n, c->reduce_n_user);
+        } else if (c->comm) {
+            if (c->xbuf_n < buf.size()) {
+                if (c->xbuf) cudaFree(c->xbuf);
+                c->xbuf = nullptr;
+                c->xbuf_n = 0;
+                if (cudaMalloc(&c->xbuf, buf.size() * sizeof(int64_t)) != cudaSuccess)
+                    return fail(COMPAR_E_OOM, "sample exchange buffer");
+                c->xbuf_n = buf.size();
+            }
+            cudaMemcpyAsync(c->xbuf, buf.data(), buf.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
+            const ncclResult_t r = ncclAllReduce(c->xbuf, c->xbuf, buf.size(), ncclInt64, ncclMax, c->comm, c->stream);
+            cudaMemcpyAsync(buf.data(), c->xbuf, buf.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
+            if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("sample exchange: ") + ncclGetErrorString(r));
+        } else {
+            return fail(COMPAR_E_STATE, "task-parallel world over several ranks needs a communicator or a reduce hook");
+        }
+    }
+    for (size_t i = 0; i < ts.size(); ++i) {
+        ts[i]->xns = buf[i];
+        ts[i]->have_xns = true;
+    }
+    return COMPAR_OK;
+}
+
+// The task-parallel tasks among `ids` whose samples have not been exchanged yet (id order).
+compar_status exchange_ids(Ctx *c, const std::vector<uint64_t> &ids) {
+    if (c->nranks <= 1) return COMPAR_OK;
+    std::vector<Task *> xs;
+    for (uint64_t id : ids) {
+        auto it = c->tasks.find(id);
+        if (it != c->tasks.end() && it->second.tasks && !it->second.have_xns) xs.push_back(&it->second);
+    }
+    return exchange_samples(c, xs);
+}
+
 // Step 6: before a model decision, every pending execution of this key is harvested in
 // task-id order (std::map iterates in id order).
 compar_status harvest_key(Ctx *c, const Key &k) {
     std::vector<uint64_t> ids;
     for (auto &kv : c->tasks)
         if (kv.second.history && kv.second.key == k) ids.push_back(kv.first);
+    compar_status s = exchange_ids(c, ids);
+    if (s != COMPAR_OK) return s;
     for (uint64_t id : ids) {
         auto it = c->tasks.find(id);
         compar_report rep;
@@ -368,6 +474,8 @@ compar_status harvest_all(Ctx *c) {
     std::vector<uint64_t> ids;
     for (auto &kv : c->tasks)
         if (kv.second.history) ids.push_back(kv.first);
+    compar_status s = exchange_ids(c, ids);
+    if (s != COMPAR_OK) return s;
     for (uint64_t id : ids) {
         auto it = c->tasks.find(id);
         compar_report rep;
@@ -384,35 +492,27 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
     rep->mode = t.mode;
     rep->warmup = t.warm ? 1 : 0;
     rep->npanels = static_cast<int>(t.panels.size());
-    int64_t sample = 0;
-    cudaEvent_t last = t.end ? t.end : (t.panels.empty() ? nullptr : t.panels.back().stop);
-    if (!c->virt && last) {
-        cudaError_t e = cudaEventSynchronize(last);
-        if (e != cudaSuccess && t.status == COMPAR_OK) {
+    rep->rank = t.tasks ? t.owner : c->rank;
+    rep->lane = t.lane;
+    int64_t sample = measure(c, t, rep);
+    if (t.tasks && t.have_xns) {  // task-parallel world: the owner's sample, identical on all ranks
+        if (t.xns == -2 && t.status == COMPAR_OK) {
             t.status = COMPAR_E_TASK_FAILED;
-            t_err = std::string("task execution failed: ") + cudaGetErrorString(e);
+            t_err = "task failed on its owner rank";
         }
+        sample = t.xns > 0 ? t.xns : 0;
+        rep->panel_ns[0] = sample;
+    } else if (t.tasks && t.remote) {
+        t.status = COMPAR_E_STATE;
+        t_err = "remote task synced without the collective sample exchange";
     }
-    for (size_t i = 0; i < t.panels.size(); ++i) {
-        int64_t ns = 0;
-        if (c->virt) {
-            ns = t.panels[i].virtual_ns;
-        } else if (!t.panels[i].sub.empty()) {  // host pipeline: sum of the chunk kernels
-            for (auto &s : t.panels[i].sub) ns += elapsed_ns(s.first, s.second);
-        } else {
-            const int64_t r = t.panels[i].batch;
-            ns = (elapsed_ns(t.panels[i].start, t.panels[i].stop) + r / 2) / r;
-            rep->batch = std::max(rep->batch, t.panels[i].batch);
-        }
-        if (i < COMPAR_MAX_PANELS) rep->panel_ns[i] = ns;
-        sample = std::max(sample, ns);
-    }
-    if (!c->virt) {
+    if (!c->virt && !t.remote) {
         rep->total_ns = t.begin ? elapsed_ns(t.begin, t.end)
                                 : (t.panels.empty() ? 0 : elapsed_ns(t.panels.front().start, t.panels.back().stop));
         rep->bcast_ns = elapsed_ns(t.bc0, t.bc1);
     } else {
         for (auto &p : t.panels) rep->total_ns += p.virtual_ns;
+        if (t.remote) rep->total_ns = sample;
     }
     // SPMD: every rank harvests the same task sequence; the sample is the max over ranks so
     // all ranks keep an identical history (rank-consistent decisions).
@@ -681,6 +781,7 @@ void compar_config_default(compar_config *cfg) {
     cfg->virtual_clock = 0;
     cfg->variant_mask = -1;
     cfg->calib_order = -1;
+    cfg->lanes = -1;
 }
 
 const char *compar_last_error(void *) { return t_err.c_str(); }
@@ -708,6 +809,8 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         const char *s = std::getenv("COMPAR_CALIB_ORDER");
         cfg.calib_order = (s && std::strcmp(s, "interleaved") == 0) ? COMPAR_CALIB_INTERLEAVED : COMPAR_CALIB_BLOCKED;
     }
+    if (cfg.lanes < 1) cfg.lanes = env_int("COMPAR_LANES", 1);
+    if (cfg.lanes < 1 || cfg.lanes > 16) return fail(COMPAR_E_INVALID, "lanes must be in 1..16");
     if (cfg.calib_order != COMPAR_CALIB_INTERLEAVED && cfg.calib_order != COMPAR_CALIB_BLOCKED)
         return fail(COMPAR_E_INVALID, "calib_order must be INTERLEAVED (0) or BLOCKED (1)");
     if (cfg.builtins < 0) cfg.builtins = 1;
@@ -815,6 +918,14 @@ compar_status compar_terminate(void *ctx) {
             }
         }
         if (c->red_buf) cudaFree(c->red_buf);
+        if (c->xbuf) cudaFree(c->xbuf);
+        for (size_t l = 0; l < c->lane_streams.size(); ++l) {
+            cudaStreamSynchronize(c->lane_streams[l]);
+            cudaStreamDestroy(c->lane_streams[l]);
+            cudaEventDestroy(c->lane_done[l]);
+        }
+        if (c->sub_event) cudaEventDestroy(c->sub_event);
+        if (c->cal_fence) cudaEventDestroy(c->cal_fence);
         for (auto e : c->pool) cudaEventDestroy(e);
         if (c->comm) ncclCommDestroy(c->comm);
         cudaStreamDestroy(c->stream);
@@ -867,6 +978,25 @@ compar_status compar_variant_info(void *ctx, int id, char *name, int name_len, i
 namespace {
 
 // Decide (variant, mode) for a plan; `commit` accounts the execution in the history.
+// Task-parallel world: the lane streams, their "last work" events, the submission event and the
+// calibration fence, created on first use.
+compar_status ensure_lanes(Ctx *c) {
+    if (!c->lane_streams.empty()) return COMPAR_OK;
+    const int L = c->placer.lanes();
+    for (int l = 0; l < L; ++l) {
+        cudaStream_t s = nullptr;
+        cudaEvent_t e = nullptr;
+        cudaError_t err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (err != cudaSuccess) return cuda_fail(err, "lane stream");
+        c->lane_streams.push_back(s);
+        c->lane_done.push_back(e);
+    }
+    cudaError_t err = cudaEventCreateWithFlags(&c->sub_event, cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&c->cal_fence, cudaEventDisableTiming);
+    return err == cudaSuccess ? COMPAR_OK : cuda_fail(err, "lane events");
+}
+
 // Batched calibration timing (reading c13): a timed calibration execution of a
 // built-in whose reference time t (the variant's warm-up on this key, else its fastest sample)
 // is below batch_below_ns repeats the launch r = ceil(50 us / t) times (<= 64) between one event
@@ -879,6 +1009,7 @@ int calib_batch(Ctx *c, const Task &t) {
     const int hid = c->variants[t.variant].hid;
     const Record *r = c->hist.find(hid, t.key);
     if (r && r->warm_ns == 0 && r->count == 0) {
+        if (t.tasks && c->nranks > 1) return 1;  // harvesting would be a collective here
         harvest_key(c, t.key);
         r = c->hist.find(hid, t.key);
     }
@@ -961,7 +1092,8 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
     c->stats.submits++;
     Task t;
     t.id = c->next_task++;
-    t.world = d->world != 0;
+    t.world = d->world == COMPAR_WORLD_PANELS;
+    t.tasks = d->world == COMPAR_WORLD_TASKS;
     // NULL is the CUDA legacy default stream (the CUDA convention, and torch's default stream),
     // so a task is ordered after work the caller queued there.
     cudaStream_t st = static_cast<cudaStream_t>(d->stream);
@@ -1019,7 +1151,8 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
     t.key = plan.key;
     if (gemm) {
         bool warm = false;
-        s = choose(c, d, plan, true, &t.variant, &t.mode, &warm);
+        // task-parallel world: the history is charged only once the placement succeeded
+        s = choose(c, d, plan, !t.tasks, &t.variant, &t.mode, &warm);
         if (s != COMPAR_OK) {
             c->stats.failed++;
             return s;
@@ -1029,6 +1162,41 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
     } else {
         t.mode = kNoop;
     }
+    std::vector<uint64_t> deps;  // task-parallel world: earlier tasks on other lanes to wait for
+    if (t.tasks) {
+        // dmda placement (dmda.h): worker = argmin predicted end over the allowed workers
+        if (!c->placer_ready) {
+            c->placer.configure(c->nranks, c->cfg.lanes);
+            c->placer_ready = true;
+        }
+        Access acc;
+        auto span = [](const void *p, size_t bytes) {
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(p);
+            return Span{lo, lo + bytes};
+        };
+        if (gemm && d->A && a_bytes) acc.reads.push_back(span(d->A, a_bytes));
+        if (gemm && d->B && b_bytes) acc.reads.push_back(span(d->B, b_bytes));
+        if (d->C_in && cin_bytes) acc.reads.push_back(span(d->C_in, cin_bytes));
+        if (d->C_out && cout_bytes) acc.writes.push_back(span(d->C_out, cout_bytes));
+        int64_t exec = 0;  // predicted ns: the variant's measured mean for the key, else unknown (0)
+        if (gemm) {
+            const Record *r = c->hist.find(c->variants[t.variant].hid, plan.key);
+            if (r && r->count > 0) exec = static_cast<int64_t>(r->sum_ns / static_cast<unsigned __int128>(r->count));
+        }
+        int64_t end = 0;
+        const int w = c->placer.place(acc, exec, &end, &deps);
+        if (w < 0) {
+            c->stats.failed++;
+            return fail(COMPAR_E_INVALID, "task reads data last written by pending tasks on different ranks");
+        }
+        t.owner = c->placer.rank_of(w);
+        t.lane = w % c->placer.lanes();
+        t.remote = t.owner != c->rank;
+        c->placer.commit(t.id, w, end, acc);
+        if (t.history) t.warm = c->hist.commit(c->variants[t.variant].hid, plan.key);
+        // lanes > 1: model-mode executions overlap other lanes, so their times are not samples
+        if (c->placer.lanes() > 1 && (t.mode == kModel || t.mode == kPredict)) t.history = false;
+    }
     for (const auto &p : plan.panels) {
         PanelRun pr;
         pr.p = p;
@@ -1037,14 +1205,37 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
 
     if (c->virt) {
         // Virtual clock: USER variants report synthetic ns; nothing touches CUDA.
-        if (gemm) {
+        if (gemm && !t.remote) {
             const Variant &var = c->variants[t.variant];
             for (auto &pr : t.panels) {
                 compar_status r = var.fn(d, &pr.p, nullptr, var.user, &pr.virtual_ns);
                 if (r != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
             }
         }
-    } else if (work) {
+    } else if (work && !t.remote) {
+        const bool calib_task = t.mode == kWarmup || t.mode == kCalib;
+        if (t.tasks) {  // run on this worker's lane stream, after `stream` and the dependencies
+            if ((s = ensure_lanes(c)) != COMPAR_OK) return s;
+            cudaStream_t ls = c->lane_streams[t.lane];
+            cudaEventRecord(c->sub_event, st);
+            cudaStreamWaitEvent(ls, c->sub_event, 0);
+            for (uint64_t dep : deps) {
+                auto it = c->tasks.find(dep);
+                if (it == c->tasks.end() || it->second.remote) continue;
+                const Task &dt = it->second;
+                cudaEvent_t ev = dt.end ? dt.end : (dt.panels.empty() ? nullptr : dt.panels.back().stop);
+                if (ev) cudaStreamWaitEvent(ls, ev, 0);
+            }
+            if (c->placer.lanes() > 1) {  // calibration runs alone on the GPU
+                if (calib_task) {
+                    for (int l = 0; l < c->placer.lanes(); ++l)
+                        if (l != t.lane) cudaStreamWaitEvent(ls, c->lane_done[l], 0);
+                } else if (c->cal_fence_set) {
+                    cudaStreamWaitEvent(ls, c->cal_fence, 0);
+                }
+            }
+            st = ls;
+        }
         // The plain single-launch task (device memory, one panel, no broadcast) uses the panel's
         // start/stop events as the task span: two event records per task instead of four.
         const bool simple = !host && t.panels.size() == 1 && !(t.world && gemm && (c->nranks > 1 || c->bcast_loopback));
@@ -1098,6 +1289,13 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             (void)cout_bytes;
         }
         if (t.end) cudaEventRecord(t.end, st);
+        if (t.tasks) {
+            cudaEventRecord(c->lane_done[t.lane], st);
+            if (calib_task && c->placer.lanes() > 1) {
+                cudaEventRecord(c->cal_fence, st);
+                c->cal_fence_set = true;
+            }
+        }
     }
     if (task_out) *task_out = t.id;
     c->tasks.emplace(t.id, std::move(t));
@@ -1112,14 +1310,23 @@ compar_status compar_sync(void *ctx, uint64_t task, compar_report *out) {
     std::memset(&rep, 0, sizeof(rep));
     compar_status st = COMPAR_OK;
     if (task == COMPAR_TASK_ALL) {
+        std::vector<uint64_t> ids;
+        for (auto &kv : c->tasks) ids.push_back(kv.first);
+        compar_status xs = exchange_ids(c, ids);  // collective in the task-parallel world
+        if (xs != COMPAR_OK) return xs;
         for (auto &kv : c->tasks) {
             compar_status s = finish_task(c, kv.second, &rep);
             if (s != COMPAR_OK) st = s;
         }
         c->tasks.clear();
+        // a full sync drains every worker: ready times and tracked accesses restart from zero
+        c->placer.reset();
+        c->cal_fence_set = false;
     } else {
         auto it = c->tasks.find(task);
         if (it == c->tasks.end()) return fail(COMPAR_E_UNKNOWN_TASK, "unknown or already-synced task");
+        compar_status xs = exchange_ids(c, {task});
+        if (xs != COMPAR_OK) return xs;
         st = finish_task(c, it->second, &rep);
         c->tasks.erase(it);
     }
@@ -1220,6 +1427,7 @@ compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, 
         return fail(COMPAR_E_INVALID, "bad communicator arguments");
     std::lock_guard<std::mutex> lk(c->mu);
     if (c->comm) return fail(COMPAR_E_STATE, "communicator already initialised");
+    c->placer_ready = false;  // workers = nranks x lanes from the next task-parallel submit
     if (c->virt) {
         c->nranks = nranks;
         c->rank = rank;
@@ -1250,6 +1458,15 @@ compar_status compar_set_reduce_hook(void *ctx, compar_reduce_fn fn, void *user)
     std::lock_guard<std::mutex> lk(c->mu);
     c->reduce_hook = fn;
     c->reduce_user = user;
+    return COMPAR_OK;
+}
+
+compar_status compar_set_reduce_n_hook(void *ctx, compar_reduce_n_fn fn, void *user) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->reduce_n_hook = fn;
+    c->reduce_n_user = user;
     return COMPAR_OK;
 }
 
