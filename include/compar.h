@@ -78,7 +78,10 @@ typedef enum {
     COMPAR_TGT_TC2_BF16 = 6,    /* built-in (c), CTA-pair form, BF16                                    */
     COMPAR_TGT_TCW_TF32 = 7,    /* built-in (c), wide CTA-pair form: 256x512 pair tile, 2 accumulators  */
     COMPAR_TGT_TCW_BF16 = 8,    /* built-in (c), wide CTA-pair form, BF16                               */
-    COMPAR_TGT_SIMT_BF16 = 9    /* built-in (a), BF16 operands widened to FP32, FFMA; any shape/alignment */
+    COMPAR_TGT_SIMT_BF16 = 9,   /* built-in (a), BF16 operands widened to FP32, FFMA; any shape/alignment */
+    /* the "sort" interface */
+    COMPAR_TGT_SORT_RADIX = 20,   /* built-in: onesweep LSD radix sort, 4 x 8-bit passes, any n      */
+    COMPAR_TGT_SORT_BITONIC = 21  /* built-in: single-CTA shared-memory bitonic network, n <= 16384  */
 } compar_target;
 
 /* Why a task ran the variant it ran. */
@@ -177,6 +180,27 @@ typedef struct {
     int variant_hint;           /* -1: run the selector; >= 0: force that registry index          */
 } compar_gemm_desc;
 
+/* ---- the "sort" interface ----
+ * "the sort function, two parameters are utilized: an array of floats and a
+ * scalar integer".  sort(keys, n) rearranges keys[0..n) IN PLACE into ascending order (DESIGN.md
+ * R24): FP32 in IEEE 754 totalOrder (-NaN < -Inf < ... < -0 < +0 < ... < +Inf < +NaN, so the
+ * result is unique as bit patterns), or uint32 / int32.  Same registry, selector, history
+ * (key = (n, key type)), tasks and reports as the GEMM interface. */
+typedef enum { COMPAR_KEY_U32 = 0, COMPAR_KEY_I32 = 1, COMPAR_KEY_F32 = 2 } compar_key_type;
+
+typedef struct {
+    int64_t n;                  /* number of keys, 0 <= n < 2^30                                    */
+    compar_key_type key_type;
+    void *keys;                 /* device array of n 4-byte keys, sorted in place; the caller
+                                   keeps it alive and unmodified until compar_sync              */
+    void *stream;               /* cudaStream_t; NULL: the legacy default stream                 */
+    int variant_hint;           /* -1: run the selector; >= 0: force that registry index          */
+} compar_sort_desc;
+
+/* User sort variant: sort d->keys on `stream` (virtual-clock mode: store a synthetic cost in
+ * *virtual_ns and touch no CUDA). */
+typedef compar_status (*compar_sort_fn)(const compar_sort_desc *d, void *stream, void *user, int64_t *virtual_ns);
+
 /* The rows one variant launch covers (a loopback panel, or this rank's panel). */
 typedef struct {
     int index;                  /* panel number r                                                  */
@@ -237,6 +261,10 @@ compar_status compar_terminate(void *ctx);
 compar_status compar_register_variant(void *ctx, const char *iface, const char *name,
                                       compar_target target, compar_gemm_fn fn, void *user,
                                       int *out_id);
+/* A variant of the "sort" interface: target SORT_RADIX / SORT_BITONIC (built-ins, fn ignored) or
+ * USER with fn.  Same registry (indices, names, mask) as the GEMM variants. */
+compar_status compar_register_sort_variant(void *ctx, const char *name, compar_target target,
+                                           compar_sort_fn fn, void *user, int *out_id);
 compar_status compar_variant_count(void *ctx, int *n);
 compar_status compar_variant_info(void *ctx, int id, char *name, int name_len, int *target);
 
@@ -247,6 +275,11 @@ compar_status compar_variant_info(void *ctx, int id, char *name, int name_len, i
  * pending samples of the same key (blocking on them) so decisions are a pure function of the
  * submission sequence. */
 compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t *task);
+/* The sort interface: validates (E_INVALID: n out of range, bad key type, NULL keys), selects
+ * among the eligible sort variants (history key = (n, key type); sort_bitonic needs n <= 16384),
+ * launches asynchronously.  n <= 1: no launch, mode NOOP.  Sort tasks of one context are
+ * serialised with each other (they share the library's radix scratch). */
+compar_status compar_sort_submit(void *ctx, const compar_sort_desc *d, uint64_t *task);
 /* Blocks until the task's stop event(s); harvests its sample into the history; fills *out
  * (may be NULL).  task == COMPAR_TASK_ALL syncs every outstanding task (out gets the last).
  * A failed variant -> E_TASK_FAILED (status also in out).  After return the library holds no

@@ -23,6 +23,8 @@ COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER, TGT_TC2_TF32, TGT_TC2_BF16, TGT_TCW_TF32, TGT_TCW_BF16 = \
     0, 1, 2, 3, 4, 5, 6, 7, 8
 TGT_SIMT_BF16 = 9
+TGT_SORT_RADIX, TGT_SORT_BITONIC = 20, 21
+KEY_U32, KEY_I32, KEY_F32 = 0, 1, 2
 # built-in targets by precision class (the §8(b) eligibility table; include/compar.h)
 TARGETS_STRICT = (TGT_SIMT_F32, TGT_TMA_F32)
 TARGETS_TF32 = TARGETS_STRICT + (TGT_TC_TF32, TGT_TC2_TF32, TGT_TCW_TF32)
@@ -53,6 +55,11 @@ class GemmDesc(C.Structure):
                 ("B_replica", C.c_void_p), ("variant_hint", C.c_int)]
 
 
+class SortDesc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("key_type", C.c_int), ("keys", C.c_void_p), ("stream", C.c_void_p),
+                ("variant_hint", C.c_int)]
+
+
 class Panel(C.Structure):
     _fields_ = [("index", C.c_int), ("row0", C.c_int64), ("rows", C.c_int64), ("A", C.c_void_p),
                 ("B", C.c_void_p), ("C_in", C.c_void_p), ("C_out", C.c_void_p)]
@@ -77,11 +84,13 @@ class Stats(C.Structure):
 
 GEMM_FN = C.CFUNCTYPE(C.c_int, C.POINTER(GemmDesc), C.POINTER(Panel), C.c_void_p, C.c_void_p,
                       C.POINTER(C.c_int64))
+SORT_FN = C.CFUNCTYPE(C.c_int, C.POINTER(SortDesc), C.c_void_p, C.c_void_p, C.POINTER(C.c_int64))
 REDUCE_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_void_p)
 REDUCE_N_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_int, C.c_void_p)
 
 EXPORTS = ["compar_config_default", "compar_init", "compar_terminate", "compar_register_variant",
            "compar_variant_count", "compar_variant_info", "compar_gemm_submit", "compar_sync", "compar_select",
+           "compar_register_sort_variant", "compar_sort_submit",
            "compar_perf_save", "compar_perf_load", "compar_history_get", "compar_partition_rows",
            "compar_comm_unique_id", "compar_comm_init", "compar_set_reduce_hook", "compar_set_reduce_n_hook",
            "compar_stats_get",
@@ -101,6 +110,8 @@ def _load():
         "compar_variant_count": (st, [vp, C.POINTER(i)]),
         "compar_variant_info": (st, [vp, i, C.c_char_p, i, C.POINTER(i)]),
         "compar_gemm_submit": (st, [vp, C.POINTER(GemmDesc), C.POINTER(C.c_uint64)]),
+        "compar_register_sort_variant": (st, [vp, C.c_char_p, i, SORT_FN, vp, C.POINTER(i)]),
+        "compar_sort_submit": (st, [vp, C.POINTER(SortDesc), C.POINTER(C.c_uint64)]),
         "compar_sync": (st, [vp, C.c_uint64, C.POINTER(Report)]),
         "compar_select": (st, [vp, C.POINTER(GemmDesc), C.POINTER(i), C.POINTER(i)]),
         "compar_perf_save": (st, [vp, C.c_char_p]),
@@ -160,6 +171,17 @@ def _ptr(x):
     if isinstance(x, int):
         return x
     return x.data_ptr()
+
+
+def make_sort_desc(keys, n=None, key_type=None, stream=None, variant_hint=-1) -> SortDesc:
+    d = SortDesc()
+    if n is None:
+        n = keys.numel()
+    if key_type is None:
+        import torch
+        key_type = {torch.float32: KEY_F32, torch.int32: KEY_I32}.get(keys.dtype, KEY_U32)
+    d.n, d.key_type, d.keys, d.stream, d.variant_hint = int(n), int(key_type), _ptr(keys), stream, int(variant_hint)
+    return d
 
 
 def make_desc(m, n, k, *, A=None, B=None, C_in=None, C_out=None, lda=None, ldb=None, ldc_in=None, ldc_out=None,
@@ -223,6 +245,14 @@ class Compar:
                                            C.byref(out)), self.ctx)
         return out.value
 
+    def register_sort_variant(self, name, target=TGT_USER, fn=None) -> int:
+        out = C.c_int()
+        cfn = SORT_FN(fn) if fn is not None else SORT_FN()
+        self._callbacks.append(cfn)
+        _check(lib.compar_register_sort_variant(self.ctx, name.encode() if name is not None else None, target, cfn,
+                                                None, C.byref(out)), self.ctx)
+        return out.value
+
     def variants(self) -> list[tuple[str, int]]:
         n = C.c_int()
         _check(lib.compar_variant_count(self.ctx, C.byref(n)), self.ctx)
@@ -251,6 +281,16 @@ class Compar:
 
     def run(self, desc: GemmDesc) -> Report:
         return self.sync(self.submit(desc))
+
+    def sort_submit(self, desc: "SortDesc") -> int:
+        t = C.c_uint64()
+        _check(lib.compar_sort_submit(self.ctx, C.byref(desc), C.byref(t)), self.ctx)
+        return t.value
+
+    def sort(self, keys, n=None, key_type=None, stream=None, variant_hint=-1) -> Report:
+        """The sort interface: sort `keys` (a CUDA tensor / device address) in place."""
+        return self.sync(self.sort_submit(make_sort_desc(keys, n=n, key_type=key_type, stream=stream,
+                                                         variant_hint=variant_hint)))
 
     def select(self, desc: GemmDesc) -> tuple[int, int]:
         v, m = C.c_int(), C.c_int()

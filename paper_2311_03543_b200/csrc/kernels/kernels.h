@@ -22,6 +22,13 @@ struct GemmLaunch {
 
 cudaError_t launch_simt_f32(const GemmLaunch &g);            // variant (a)
 cudaError_t launch_simt_bf16(const GemmLaunch &g);           // variant (a), BF16 operands
+
+// The sort interface (sort.cu): in-place ascending sort of n 4-byte keys (key_type 0 u32, 1 i32,
+// 2 f32 totalOrder).  The radix sort needs sort_radix_scratch_bytes(n) of device scratch.
+size_t sort_radix_scratch_bytes(int64_t n);
+int64_t sort_bitonic_max();
+cudaError_t launch_sort_radix(void *keys, int64_t n, int key_type, void *scratch, cudaStream_t s, int num_sms);
+cudaError_t launch_sort_bitonic(void *keys, int64_t n, int key_type, cudaStream_t s);
 cudaError_t launch_tma_f32(const GemmLaunch &g);             // variant (b)
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16);  // variant (c): tcgen05 TF32 / BF16
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16);  // variant (c), CTA-pair (cta_group::2)

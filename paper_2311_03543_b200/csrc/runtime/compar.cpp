@@ -46,12 +46,16 @@ compar_status cuda_fail(cudaError_t e, const char *what) {
     return fail(COMPAR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+enum Iface { kGemm = 0, kSort = 1 };
+
 struct Variant {
     std::string name;
     compar_target target;
     compar_gemm_fn fn;
     void *user;
     int hid;  // interned history id of `name`
+    int iface = kGemm;
+    compar_sort_fn sfn = nullptr;
 };
 
 struct PanelRun {
@@ -124,6 +128,11 @@ struct Ctx {
     void *reduce_n_user = nullptr;
     int64_t *xbuf = nullptr;  // device buffer of the NCCL sample exchange
     size_t xbuf_n = 0;
+    // sort interface
+    void *sort_scratch = nullptr;
+    size_t sort_scratch_bytes = 0;
+    cudaEvent_t sort_done = nullptr;  // end of the last sort task (sort tasks share the scratch)
+    bool sort_done_set = false;
     // batched calibration timing (a8 / c13)
     int64_t batch_below_ns = 20000;
     void *scratch = nullptr;  // C_out of the r - 1 extra launches
@@ -306,6 +315,7 @@ void eligible_set(Ctx *c, const compar_gemm_desc *d, const Plan &plan, std::vect
     for (size_t v = 0; v < c->variants.size(); ++v) {
         if (v < 63 && (c->cfg.variant_mask >> v) & 1) continue;
         const Variant &var = c->variants[v];
+        if (var.iface != kGemm) continue;
         if (!admits(var.target, d->in_dtype, d->compute)) continue;
         if (!constraints_ok(c, var.target, d, plan)) continue;
         idx.push_back(static_cast<int>(v));
@@ -875,6 +885,8 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         compar_register_variant(c, "gemm", "tc_tf32_2sm_w", COMPAR_TGT_TCW_TF32, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_bf16_2sm_w", COMPAR_TGT_TCW_BF16, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "simt_bf16", COMPAR_TGT_SIMT_BF16, nullptr, nullptr, &id);
+        compar_register_sort_variant(c, "sort_radix", COMPAR_TGT_SORT_RADIX, nullptr, nullptr, &id);
+        compar_register_sort_variant(c, "sort_bitonic", COMPAR_TGT_SORT_BITONIC, nullptr, nullptr, &id);
     }
     *ctx = c;
     if (!c->perf_path.empty()) {
@@ -911,6 +923,8 @@ compar_status compar_terminate(void *ctx) {
         if (c->breplica) cudaFree(c->breplica);
         if (c->bpacked) cudaFree(c->bpacked);
         if (c->scratch) cudaFree(c->scratch);
+        if (c->sort_scratch) cudaFree(c->sort_scratch);
+        if (c->sort_done) cudaEventDestroy(c->sort_done);
         for (cudaStream_t s : {c->comm_stream, c->h2d_stream, c->d2h_stream}) {
             if (s) {
                 cudaStreamSynchronize(s);
@@ -950,6 +964,29 @@ compar_status compar_register_variant(void *ctx, const char *iface, const char *
         if (v.name == name) return fail(COMPAR_E_DUPLICATE, std::string("duplicate variant ") + name);
     if (c->variants.size() >= 64) return fail(COMPAR_E_INVALID, "too many variants");
     c->variants.push_back(Variant{name, target, fn, user, c->hist.intern(name)});
+    if (out_id) *out_id = static_cast<int>(c->variants.size()) - 1;
+    return COMPAR_OK;
+}
+
+compar_status compar_register_sort_variant(void *ctx, const char *name, compar_target target, compar_sort_fn fn,
+                                           void *user, int *out_id) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!name || !*name || std::strlen(name) > 63) return fail(COMPAR_E_INVALID, "bad variant name");
+    for (const char *p = name; *p; ++p)
+        if (*p == ' ' || *p == '\t' || *p == '\n') return fail(COMPAR_E_INVALID, "variant name has whitespace");
+    if (target != COMPAR_TGT_SORT_RADIX && target != COMPAR_TGT_SORT_BITONIC && target != COMPAR_TGT_USER)
+        return fail(COMPAR_E_INVALID, "not a sort target");
+    if (target == COMPAR_TGT_USER && !fn) return fail(COMPAR_E_INVALID, "USER variant needs a sort function");
+    if (target != COMPAR_TGT_USER && c->virt) return fail(COMPAR_E_INVALID, "built-in targets need CUDA");
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (const auto &v : c->variants)
+        if (v.name == name) return fail(COMPAR_E_DUPLICATE, std::string("duplicate variant ") + name);
+    if (c->variants.size() >= 64) return fail(COMPAR_E_INVALID, "too many variants");
+    Variant v{name, target, nullptr, user, c->hist.intern(name)};
+    v.iface = kSort;
+    v.sfn = fn;
+    c->variants.push_back(v);
     if (out_id) *out_id = static_cast<int>(c->variants.size()) - 1;
     return COMPAR_OK;
 }
@@ -1020,16 +1057,27 @@ int calib_batch(Ctx *c, const Task &t) {
     return static_cast<int>(std::min<int64_t>(64, (target + ref - 1) / ref));
 }
 
+// Steps 3-7 over an eligible set (registry indices idx, history ids names), any interface.
+compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector<int> &names, const Key &key,
+                          int hint, bool commit, int *variant, int *mode, bool *warm);
+
 compar_status choose(Ctx *c, const compar_gemm_desc *d, const Plan &plan, bool commit, int *variant, int *mode,
                      bool *warm) {
     std::vector<int> idx;
     std::vector<int> names;  // interned history ids, in registry order
     eligible_set(c, d, plan, idx, names);
+    return choose_core(c, idx, names, plan.key, d->variant_hint, commit, variant, mode, warm);
+}
+
+compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector<int> &names, const Key &key,
+                          int hint, bool commit, int *variant, int *mode, bool *warm) {
+    Plan plan;  // (only .key is used below)
+    plan.key = key;
     *warm = false;
-    if (d->variant_hint >= 0) {
-        if (std::find(idx.begin(), idx.end(), d->variant_hint) == idx.end())
+    if (hint >= 0) {
+        if (std::find(idx.begin(), idx.end(), hint) == idx.end())
             return fail(COMPAR_E_INVALID, "variant_hint is not eligible for this task");
-        *variant = d->variant_hint;
+        *variant = hint;
         *mode = kHint;
         return COMPAR_OK;
     }
@@ -1039,8 +1087,8 @@ compar_status choose(Ctx *c, const compar_gemm_desc *d, const Plan &plan, bool c
         *mode = kEager;
         return COMPAR_OK;
     }
-    if (c->cfg.sched == 2) {
-        // "predict" scheduler (NEXT-2): every pending sample is harvested first (the fit reads all
+    if (c->cfg.sched == 2 && key.compute >= 0) {
+        // "predict" scheduler (NEXT-2; GEMM keys — its features are FLOPs and bytes): every pending sample is harvested first (the fit reads all
         // keys), then measured means / model predictions decide; unknown variants fall back to
         // calibration below.
         harvest_all(c);
@@ -1296,6 +1344,84 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
                 c->cal_fence_set = true;
             }
         }
+    }
+    if (task_out) *task_out = t.id;
+    c->tasks.emplace(t.id, std::move(t));
+    return COMPAR_OK;
+}
+
+compar_status compar_sort_submit(void *ctx, const compar_sort_desc *d, uint64_t *task_out) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!d) return fail(COMPAR_E_INVALID, "desc is NULL");
+    if (d->n < 0 || d->n >= (int64_t(1) << 30)) return fail(COMPAR_E_INVALID, "n out of range [0, 2^30)");
+    if (d->key_type < COMPAR_KEY_U32 || d->key_type > COMPAR_KEY_F32) return fail(COMPAR_E_INVALID, "bad key_type");
+    if (d->n > 0 && !d->keys && !c->virt) return fail(COMPAR_E_INVALID, "keys NULL");
+    if (d->variant_hint < -1 || d->variant_hint >= static_cast<int>(c->variants.size()))
+        return fail(COMPAR_E_INVALID, "variant_hint out of range");
+    c->stats.submits++;
+    Task t;
+    t.id = c->next_task++;
+    t.key = Key{d->n, 0, 0, 100 + static_cast<int>(d->key_type), -1, 0, 0};
+    cudaStream_t st = static_cast<cudaStream_t>(d->stream);
+    const bool work = d->n > 1;  // 0 or 1 keys are sorted already
+    if (work) {
+        std::vector<int> idx, names;
+        for (size_t v = 0; v < c->variants.size(); ++v) {
+            if (v < 63 && (c->cfg.variant_mask >> v) & 1) continue;
+            const Variant &var = c->variants[v];
+            if (var.iface != kSort) continue;
+            if (var.target == COMPAR_TGT_SORT_BITONIC && d->n > sort_bitonic_max()) continue;
+            idx.push_back(static_cast<int>(v));
+            names.push_back(var.hid);
+        }
+        if (idx.empty() && d->variant_hint < 0) return fail(COMPAR_E_NO_VARIANT, "no eligible sort variant");
+        bool warm = false;
+        compar_status s = choose_core(c, idx, names, t.key, d->variant_hint, true, &t.variant, &t.mode, &warm);
+        if (s != COMPAR_OK) {
+            c->stats.failed++;
+            return s;
+        }
+        t.warm = warm;
+        t.history = (t.mode == kWarmup || t.mode == kCalib || t.mode == kModel || t.mode == kPredict);
+        PanelRun pr;
+        pr.p.rows = d->n;
+        const Variant &var = c->variants[t.variant];
+        if (c->virt) {
+            if (var.sfn(d, nullptr, var.user, &pr.virtual_ns) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+        } else {
+            if (var.target == COMPAR_TGT_SORT_RADIX) {
+                s = ensure_buffer(&c->sort_scratch, &c->sort_scratch_bytes, sort_radix_scratch_bytes(d->n));
+                if (s != COMPAR_OK) return s;
+            }
+            if (!c->sort_done) cudaEventCreateWithFlags(&c->sort_done, cudaEventDisableTiming);
+            if (c->sort_done_set) cudaStreamWaitEvent(st, c->sort_done, 0);
+            pr.start = get_event(c);
+            pr.stop = get_event(c);
+            cudaEventRecord(pr.start, st);
+            cudaError_t e = cudaSuccess;
+            if (var.target == COMPAR_TGT_SORT_RADIX) {
+                e = launch_sort_radix(d->keys, d->n, d->key_type, c->sort_scratch, st, c->num_sms);
+                c->stats.launches += 5;
+            } else if (var.target == COMPAR_TGT_SORT_BITONIC) {
+                e = launch_sort_bitonic(d->keys, d->n, d->key_type, st);
+                c->stats.launches += 1;
+            } else {
+                c->stats.launches++;
+                if (var.sfn(d, st, var.user, nullptr) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+            }
+            if (e != cudaSuccess) {
+                t.status = COMPAR_E_TASK_FAILED;
+                t_err = std::string("sort launch: ") + cudaGetErrorString(e);
+            }
+            cudaEventRecord(pr.stop, st);
+            cudaEventRecord(c->sort_done, st);
+            c->sort_done_set = true;
+        }
+        t.panels.push_back(pr);
+    } else {
+        t.mode = kNoop;
     }
     if (task_out) *task_out = t.id;
     c->tasks.emplace(t.id, std::move(t));

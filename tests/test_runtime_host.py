@@ -312,3 +312,27 @@ def test_loopback_panels_virtual():
     assert [rows for _, rows in syn.calls] == [b - a for a, b in zip(offs, offs[1:]) if b > a]
     assert r.npanels == 3 and r.ns == 10 * max(b - a for a, b in zip(offs, offs[1:]))
     ctx.terminate()
+
+
+def test_sort_interface_selector_virtual(golden):
+    """NEXT-3: the sort interface shares the registry and the selector — the S:370-371 closed-form
+    crossover through compar_sort_submit with USER sort variants on the virtual clock."""
+    ctx = cm.Compar(virtual_clock=1)
+    costs = [lambda n: round(0.1 * n * 1000), lambda n: round((50 + 0.01 * n) * 1000)]
+    for v in range(2):
+        def fn(desc, stream, user, vns, v=v):
+            vns[0] = costs[v](desc.contents.n)
+            return 0
+        assert ctx.register_sort_variant(f"s{v}", cm.TGT_USER, fn) == v
+    for n, want in ((256, 0), (4096, 1)):
+        d = cm.make_sort_desc(0x1000, n=n, key_type=cm.KEY_F32)
+        for _ in range(9):                 # 2 variants x (1 warm-up + 3 timed), then model
+            r = ctx.sync(ctx.sort_submit(d))
+        assert r.mode == cm.MODE_MODEL and r.variant == want
+    # n <= 1 is a no-op; a GEMM-interface USER variant is never eligible for sort and vice versa
+    assert ctx.sync(ctx.sort_submit(cm.make_sort_desc(0x1000, n=1, key_type=cm.KEY_F32))).mode == cm.MODE_NOOP
+    with pytest.raises(cm.ComparError):
+        ctx.sort_submit(cm.make_sort_desc(0x1000, n=1 << 30, key_type=cm.KEY_F32))
+    with pytest.raises(cm.ComparError):
+        ctx.register_sort_variant("bad", cm.TGT_TC_BF16, None)
+    ctx.terminate()
