@@ -1,5 +1,6 @@
 """Small-shape run of every built-in variant (target for compute-sanitizer memcheck / racecheck /
-synccheck): ragged shapes, transB, beta 0 / non-zero, host mode, loopback panels."""
+synccheck): ragged shapes, transB, beta 0 / non-zero, host mode, loopback panels; the sort variants
+on ragged n with FP32 keys (incl. multi-tile radix sorts)."""
 import os
 import sys
 
@@ -17,6 +18,13 @@ ctx = cm.Compar()
 names = [v for v, _ in ctx.variants()]
 for name in names:
     if only and name not in only:
+        continue
+    if name.startswith("sort_"):
+        for n in ([2, 1000, 16384] if name == "sort_bitonic" else [2, 1000, 16384, 70001]):
+            x = torch.randn(n, device="cuda")
+            r = ctx.sort(x, variant_hint=names.index(name))
+            assert r.status == 0 and bool((x[1:] >= x[:-1]).all()), (name, n)
+        print(f"{name}: ok", flush=True)
         continue
     bf = "bf16" in name
     dt = "bf16" if bf else "f32"
