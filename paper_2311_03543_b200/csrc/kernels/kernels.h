@@ -33,6 +33,9 @@ cudaError_t launch_tma_f32(const GemmLaunch &g);             // variant (b)
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16);  // variant (c): tcgen05 TF32 / BF16
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16);  // variant (c), CTA-pair (cta_group::2)
 cudaError_t launch_tc_gemm_2sm_wide(const GemmLaunch &g, bool bf16);  // variant (c), wide CTA-pair 256x512
+// variant (c), CTA-pair kernel with TMA C epilogue (tc_gemm_2sm_mc.cu): `pairs` = 1 (cluster of 2) or
+// 2 (cluster of 4, B shared by TMA multicast); needs TMA-compatible C.  Reached through launch_tc_gemm_2sm.
+cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16, int pairs);
 cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha == 0: C_out = beta*C_in
 cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
 cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)

@@ -12,6 +12,7 @@ cudaError_t preload_tma_kernels();
 cudaError_t preload_simt_kernels();
 cudaError_t preload_tc2_kernels();
 cudaError_t preload_tcw_kernels();
+cudaError_t preload_tcm_kernels();
 
 namespace {
 
@@ -58,6 +59,7 @@ cudaError_t preload_kernels() {
     if (e == cudaSuccess) e = preload_simt_kernels();
     if (e == cudaSuccess) e = preload_tc2_kernels();
     if (e == cudaSuccess) e = preload_tcw_kernels();
+    if (e == cudaSuccess) e = preload_tcm_kernels();
     return e;
 }
 

@@ -357,6 +357,16 @@ cudaError_t launch_tc2_t(const GemmLaunch &g) {
 }  // namespace
 
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16) {
+    // C movable by TMA (16-byte aligned, ldc * 4 % 16 == 0): the TMA-epilogue form of the same
+    // pair tile (tc_gemm_2sm_mc.cu; 134 vs 164 us on config 5a).  COMPAR_TC2_PAIRS=2 selects its
+    // cluster-of-4 B-multicast form (measured, not faster: DESIGN.md §5).  Otherwise: row stores.
+    static const int pairs = [] {
+        const char *s = std::getenv("COMPAR_TC2_PAIRS");
+        return s ? std::atoi(s) : 1;
+    }();
+    if (pairs > 0 && tma_compatible(g.C_out, g.ldc_out, 4) &&
+        (g.beta == 0.f || tma_compatible(g.C_in, g.ldc_in, 4)))
+        return launch_tc_gemm_pairs(g, bf16, pairs);
     if (bf16) return g.transB ? launch_tc2_t<true, true>(g) : launch_tc2_t<true, false>(g);
     return g.transB ? launch_tc2_t<false, true>(g) : launch_tc2_t<false, false>(g);
 }

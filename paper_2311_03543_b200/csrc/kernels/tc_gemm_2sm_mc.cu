@@ -1,0 +1,432 @@
+// Variant (c), multicast CTA-pair form "tc_*_2sm_mc": two tcgen05 CTA pairs share B through
+// TMA multicast (cluster of 4 CTAs) for sm_100a.
+//
+// Same math as tc_gemm.cu / tc_gemm_2sm.cu (C_out = alpha*A*B + beta*C_in, BF16 / TF32 in, FP32
+// TMEM accumulation; R1-R6).  A cluster of four CTAs = two CTA pairs stacked along M
+// owns a 512 x 256 output tile; pair p (CTAs 2p, 2p+1) computes rows [256 p, 256 p + 256) with
+// one tcgen05.mma.cta_group::2 M=256 N=256 per UMMA_K slice, exactly as tc_gemm_2sm.cu.  The two
+// pairs need the same B tile, so CTA r of pair p loads only half of its 128-column B slice and
+// multicasts it to CTA r of both pairs: per SM the L2 -> SMEM traffic per FLOP is that of the
+// wide 256 x 512 pair tile (tc_gemm_2sm_wide.cu), while each CTA's accumulator stays 128 x 256
+// (256 TMEM columns), so two accumulators alternate and tile i's epilogue overlaps tile i+1's
+// MMAs (the wide kernel's 512-column accumulator cannot).  Epilogue as in the wide
+// kernel: TMA load of C_in two chunks ahead, alpha*acc + beta*C_in in registers, swizzled smem
+// staging, TMA store of C_out.
+//
+// Synchronisation (all mbarriers at identical smem offsets in every CTA):
+//   full[s]   pair leaders; count 1 (leader arrive.expect_tx of both pair CTAs' bytes); the pair's
+//             A loads and the B multicasts of both pairs complete_tx on the destination's pair
+//             leader barrier;
+//   empty[s]  every CTA; count 2: both pair leaders' tcgen05.commit multicast to all four CTAs
+//             (a B slot is rewritten by the other pair's multicast, so it must be free in both);
+//   tfull[a]  every CTA; the pair leader's commit multicast to its pair;
+//   tempty[a] pair leaders; count 8 = 4 epilogue warps x 2 CTAs of the pair;
+//   rfull/rempty  the tile ring: CTA 0's producer draws tile ids from the global counter
+//             (sched.cpp) and publishes them to all four CTAs over DSMEM;
+//   cbar[w][b] C_in chunk landed (epilogue warp w, buffer b).
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "tmap.h"
+
+namespace compar {
+namespace {
+
+constexpr int kEpiWarpsM = 4;
+constexpr int kThreadsM = 64 + 32 * kEpiWarpsM;
+constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
+constexpr int kRingM = 4;
+
+template <bool kBF16, bool kTransB, int kPairs>
+struct TcMCfg {
+    static constexpr int BM = 128;              // A rows per CTA (UMMA_M = 256 per pair)
+    static constexpr int BN = 256;              // UMMA_N; each CTA holds BN/2 columns of B
+    static constexpr int BN_CTA = BN / 2;
+    static constexpr int ELEM = kBF16 ? 2 : 4;
+    static constexpr int BK = 128 / ELEM;
+    static constexpr int UMMA_K = 32 / ELEM;
+    static constexpr int STAGES = 6;
+    static constexpr uint32_t A_BYTES = BM * 128;
+    static constexpr uint32_t B_BYTES = BN_CTA * 128;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int B_ATOM_N = 128 / ELEM;
+    // B boxes of one CTA's 128-column slice; each of the kPairs pairs loads 1/kPairs of them
+    static constexpr int B_BOXES = kTransB ? 2 : BN_CTA / B_ATOM_N;
+    static constexpr uint32_t B_BOX_BYTES = B_BYTES / B_BOXES;
+    static constexpr bool B_BASE32 = !kBF16 && !kTransB;
+    static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
+    static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
+    static constexpr uint32_t B_LBO = kTransB ? 16 : BK * 128;   // MN-major: stride between N atoms
+    static constexpr uint32_t EPI_BYTES = kEpiWarpsM * 2 * 4096;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
+    static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
+                                      ((kTransB ? 0u : 1u) << 16) | ((uint32_t(BN) >> 3) << 17) |
+                                      ((uint32_t(2 * BM) >> 4) << 24);
+};
+
+struct TcMParams {
+    int64_t m, n, k;
+    float alpha, beta;
+    int m_blocks, n_blocks, num_kb;  // 512-row x 256-column cluster tiles
+    int group_m;
+    int *sched;
+};
+
+__device__ __forceinline__ void tile_coords_m(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
+    const int per_group = group * n_blocks;
+    const int g = t / per_group;
+    const int first_m = g * group;
+    const int gm = min(m_blocks - first_m, group);
+    const int r = t - g * per_group;
+    mb = first_m + r % gm;
+    nb = r / gm;
+}
+
+template <bool kBF16, bool kTransB, int kPairs>
+__global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 1)
+    tc_gemm_2sm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmCo, const __grid_constant__ CUtensorMap tmCi,
+                          TcMParams p) {
+    using C = TcMCfg<kBF16, kTransB, kPairs>;
+    constexpr int kCluster = 2 * kPairs;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t smem0 = ptx::smem_u32(smem);
+    const uint32_t epi0 = smem0 + C::STAGES * C::STAGE_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
+    const uint32_t full0 = ptx::smem_u32(bars);
+    const uint32_t empty0 = full0 + 8 * C::STAGES;
+    const uint32_t tfull0 = empty0 + 8 * C::STAGES;
+    const uint32_t tempty0 = tfull0 + 16;
+    const uint32_t rfull0 = tempty0 + 16;
+    const uint32_t rempty0 = rfull0 + 8 * kRingM;
+    const uint32_t cbar0 = rempty0 + 8 * kRingM;
+    const uint32_t ring0 = cbar0 + 16 * kEpiWarpsM;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();   // 0..3
+    const uint32_t pr = rank & 1;                    // rank inside the pair
+    const uint32_t pair = rank >> 1;                 // 0: rows [0,256) of the tile, 1: [256,512)
+    const uint32_t pleader = rank & 2;               // cluster rank of this pair's MMA leader
+    const bool leader = pr == 0;
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << pleader);
+    const uint16_t b_mask = static_cast<uint16_t>(kPairs == 2 ? (1u << pr) | (1u << (pr + 2)) : 0u);
+    // consumers of a tile-ring slot: 4 epilogue warps per CTA, producers of CTAs 1..3, 2 MMA warps
+    constexpr int kConsumers = kCluster * kEpiWarpsM + (kCluster - 1) + kPairs;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmCo);
+        ptx::prefetch_tmap(&tmCi);
+        for (int s = 0; s < C::STAGES; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, kPairs);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull0 + 8 * a, 1);
+            ptx::mbar_init(tempty0 + 8 * a, 2 * kEpiWarpsM);
+        }
+        for (int r = 0; r < kRingM; ++r) {
+            ptx::mbar_init(rfull0 + 8 * r, 1);
+            ptx::mbar_init(rempty0 + 8 * r, kConsumers);
+        }
+        for (int b = 0; b < 2 * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm<512>(ptx::smem_u32(tmem_slot));
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_tiles = p.m_blocks * p.n_blocks;
+    const uint32_t rempty_root = ptx::mapa_rank(rempty0, 0);
+    auto next_tile = [&](int i) -> int {  // whole-warp consumer of the tile ring
+        const int slot = i % kRingM;
+        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingM) & 1);
+        const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
+        return t;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- scheduler (CTA 0) + TMA producer (every CTA)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0;; ++i) {
+                int t;
+                const int slot = i % kRingM;
+                if (rank == 0) {
+                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, ((i / kRingM) & 1) ^ 1);
+                    t = atomicAdd(&p.sched[0], 1);
+                    ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
+                    for (uint32_t q = 1; q < kCluster; ++q)
+                        ptx::st_shared_cluster_u32(ptx::mapa_rank(ring0 + 4 * slot, q), static_cast<uint32_t>(t));
+                    ptx::mbar_arrive(rfull0 + 8 * slot);
+                    for (uint32_t q = 1; q < kCluster; ++q)
+                        ptx::mbar_arrive_cluster(ptx::mapa_rank(rfull0 + 8 * slot, q));
+                } else {
+                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingM) & 1);
+                    t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
+                    ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
+                }
+                if (t >= num_tiles) break;
+                int mb, nb;
+                tile_coords_m(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+                const int32_t arow = mb * (kCluster * C::BM) + static_cast<int32_t>(rank) * C::BM;
+                const int32_t bcol = nb * C::BN + static_cast<int32_t>(pr) * C::BN_CTA;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    ptx::mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
+                    const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
+                    const uint32_t sb = sa + C::A_BYTES;
+                    const uint32_t fb_local = full0 + 8 * stage;
+                    const uint32_t fb = ptx::mapa_rank(fb_local, pleader);
+                    // The pair leader arms its barrier with both pair CTAs' bytes (A from each, B
+                    // halves arriving from both pairs' multicasts).  Bytes may land before the arm
+                    // (transiently negative tx); no CTA runs a phase ahead, because every producer
+                    // first waits for empty[s], i.e. for both pairs to have consumed the slot.
+                    if (leader) ptx::mbar_arrive_expect_tx(fb_local, 2 * C::STAGE_BYTES);
+                    ptx::tma_load_2d_2sm(sa, &tmA, fb, kb * C::BK, arow);
+#pragma unroll
+                    for (int b = pair * (C::B_BOXES / kPairs); b < (pair + 1) * (C::B_BOXES / kPairs); ++b) {
+                        const int32_t c0 = kTransB ? kb * C::BK : bcol + b * C::B_ATOM_N;
+                        const int32_t c1 = kTransB ? bcol + b * (C::BN_CTA / 2) : kb * C::BK;
+                        if (kPairs == 2)
+                            ptx::tma_load_2d_2sm_mc(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1, b_mask);
+                        else
+                            ptx::tma_load_2d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1);
+                    }
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            if (rank == 0) {  // last cluster out re-arms the counters for the next launch on this stream
+                __threadfence();
+                if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x / kCluster) - 1) {
+                    p.sched[0] = 0;
+                    p.sched[1] = 0;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {  // ---------------- MMA issuer (pair leaders)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int local = 0;; ++local) {
+                const int t = next_tile(local);
+                if (t >= num_tiles) break;
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * C::BN;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    ptx::mbar_wait(full0 + 8 * stage, phase);
+                    ptx::tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
+                        const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                        for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
+                            const uint64_t adesc = ptx::smem_desc(sa + j * 32, 16, 1024, 2);
+                            const uint64_t bdesc = kTransB ? ptx::smem_desc(sb + j * 32, 16, 1024, 2)
+                                                           : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_LBO,
+                                                                            C::B_SBO, C::B_LAYOUT);
+                            if (kBF16)
+                                ptx::mma_bf16_2sm(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+                            else
+                                ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+                        }
+                        ptx::tc_commit_2sm_mc(empty0 + 8 * stage, kPairs == 2 ? 0xF : 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (lane == 0) ptx::tc_commit_2sm_mc(tfull0 + 8 * acc, pair_mask);
+                __syncwarp();
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, 8 chunks of 32 x 32
+        const int q = warp & 3;
+        const int ew = warp - 2;
+        const uint32_t buf[2] = {epi0 + (2 * ew) * 4096, epi0 + (2 * ew + 1) * 4096};
+        const uint32_t cbar[2] = {cbar0 + 16 * ew, cbar0 + 16 * ew + 8};
+        uint32_t loads[2] = {0, 0};
+        const uint32_t tempty_leader = ptx::mapa_rank(tempty0, pleader);
+        const bool ldc = p.beta != 0.f;
+        const uint32_t swz = lane * 128;
+        constexpr int kChunks = C::BN / 32;
+        for (int local = 0;; ++local) {
+            const int t = next_tile(local);
+            if (t >= num_tiles) break;
+            int mb, nb;
+            tile_coords_m(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            const int32_t row_base = mb * (kCluster * C::BM) + static_cast<int32_t>(rank) * C::BM + q * 32;
+            const int32_t col_base = nb * C::BN;
+            if (lane == 0) {
+                ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
+                if (ldc) {
+                    for (int b = 0; b < 2; ++b) {
+                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
+                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], col_base + 32 * b, row_base);
+                    }
+                }
+            }
+            if (ldc) ++loads[0], ++loads[1];
+            __syncwarp();
+            ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int idx = 0; idx < kChunks; ++idx) {
+                const int b = idx & 1;
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx, r);
+                ptx::tmem_ld_wait();
+                if (idx == kChunks - 1) {                 // accumulator drained: free it for tile + 2
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+                }
+                if (ldc) {
+                    ptx::mbar_wait(cbar[b], (loads[b] - 1) & 1);
+                } else if (idx >= 2) {
+                    if (lane == 0) ptx::bulk_wait_read<1>();
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const uint32_t a = buf[b] + swz + ((g ^ (lane & 7)) << 4);
+                    float4 o;
+                    o.x = p.alpha * __uint_as_float(r[4 * g + 0]);
+                    o.y = p.alpha * __uint_as_float(r[4 * g + 1]);
+                    o.z = p.alpha * __uint_as_float(r[4 * g + 2]);
+                    o.w = p.alpha * __uint_as_float(r[4 * g + 3]);
+                    if (ldc) {
+                        const float4 ci = ptx::lds128(a);
+                        o.x = fmaf(p.beta, ci.x, o.x);
+                        o.y = fmaf(p.beta, ci.y, o.y);
+                        o.z = fmaf(p.beta, ci.z, o.z);
+                        o.w = fmaf(p.beta, ci.w, o.w);
+                    }
+                    ptx::sts128(a, o);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tmCo, buf[b], col_base + 32 * idx, row_base);
+                    ptx::bulk_commit();
+                    if (ldc && idx + 2 < kChunks) {
+                        ptx::bulk_wait_read<0>();
+                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
+                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], col_base + 32 * (idx + 2), row_base);
+                    }
+                }
+                if (ldc && idx + 2 < kChunks) ++loads[b];
+                __syncwarp();
+            }
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
+        __syncwarp();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
+template <bool kBF16, bool kTransB, int kPairs>
+cudaError_t launch_tcm_t(const GemmLaunch &g) {
+    using C = TcMCfg<kBF16, kTransB, kPairs>;
+    constexpr int kCluster = 2 * kPairs;
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    static int max_clusters = 0;
+    std::call_once(attr_once, [] {
+        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (attr_err != cudaSuccess) return;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = kCluster, at.val.clusterDim.y = 1, at.val.clusterDim.z = 1;
+        cfg.gridDim = dim3(kCluster * 64), cfg.blockDim = dim3(kThreadsM), cfg.dynamicSmemBytes = C::SMEM;
+        cfg.attrs = &at, cfg.numAttrs = 1;
+        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs>, &cfg);
+        if (std::getenv("COMPAR_VERBOSE")) std::fprintf(stderr, "tc_gemm_2sm_mc: max active %d-CTA clusters = %d\n", kCluster, max_clusters);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    if (max_clusters <= 0) return cudaErrorInvalidConfiguration;
+    CUtensorMap ta, tb, tco, tci;
+    if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, Swz::B128)) return cudaErrorInvalidValue;
+    bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, C::BN_CTA / 2, C::BK, Swz::B128)
+                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N,
+                                    C::B_BASE32 ? Swz::B128_32B : Swz::B128);
+    if (!ok) return cudaErrorInvalidValue;
+    if (!get_tmap_2d(&tco, g.C_out, 4, g.m, g.n, g.ldc_out, 32, 32, Swz::B128)) return cudaErrorInvalidValue;
+    if (g.beta != 0.f) {
+        if (!get_tmap_2d(&tci, g.C_in, 4, g.m, g.n, g.ldc_in, 32, 32, Swz::B128)) return cudaErrorInvalidValue;
+    } else {
+        tci = tco;  // unused
+    }
+    TcMParams p;
+    p.m = g.m, p.n = g.n, p.k = g.k;
+    p.alpha = g.alpha, p.beta = g.beta;
+    p.m_blocks = static_cast<int>((g.m + kCluster * C::BM - 1) / (kCluster * C::BM));
+    p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
+    p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
+    static const int group_env = [] {
+        const char *s = std::getenv("COMPAR_TCM_GROUP");
+        return s ? std::atoi(s) : 0;
+    }();
+    p.group_m = group_env > 0 ? group_env : kGroupM4;
+    p.sched = sched_workspace(g.stream);
+    if (!p.sched) return cudaErrorMemoryAllocation;
+    const int tiles = p.m_blocks * p.n_blocks;
+    int clusters = g.num_sms / kCluster < max_clusters ? g.num_sms / kCluster : max_clusters;
+    if (clusters < 1) clusters = 1;
+    if (tiles < clusters) clusters = tiles;
+    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16, int pairs) {
+    if (pairs == 2) {
+        if (bf16) return g.transB ? launch_tcm_t<true, true, 2>(g) : launch_tcm_t<true, false, 2>(g);
+        return g.transB ? launch_tcm_t<false, true, 2>(g) : launch_tcm_t<false, false, 2>(g);
+    }
+    if (bf16) return g.transB ? launch_tcm_t<true, true, 1>(g) : launch_tcm_t<true, false, 1>(g);
+    return g.transB ? launch_tcm_t<false, true, 1>(g) : launch_tcm_t<false, false, 1>(g);
+}
+
+cudaError_t preload_tcm_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, false, 2>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, true, 2>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, false, 2>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, true, 2>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, false, 1>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, true, 1>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, false, 1>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, true, 1>);
+    return e;
+}
+
+}  // namespace compar

@@ -46,7 +46,7 @@ def vid(ctx, name):
     return [n for n, _ in ctx.variants()].index(name)
 
 
-def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, seed=11):
+def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, seed=11, ldc_pad=4):
     dtype_id, compute, tol = VARIANTS[name]
     dt = "bf16" if dtype_id == cm.BF16 else "f32"
     A = gen.matrix(gen.TAG_A, m, k, dist, dt, seed=seed)
@@ -55,7 +55,7 @@ def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, see
     lda = k + (-k) % pad
     ldb_cols = k if transB else n
     ldb = ldb_cols + (-ldb_cols) % pad
-    ldc = n + (-n) % 4
+    ldc = n + (-n) % 4 if ldc_pad == 4 else n + ldc_pad
     Ad = to_device(A, dt, lda)
     Bd = to_device(np.ascontiguousarray(B.T) if transB else B, dt, ldb)
     Cd = to_device(C0, "f32", ldc)
@@ -87,6 +87,26 @@ def test_parity_exact_integers(ctx, name, transB, shape):
     m, n, k = shape
     got, ref, _ = run_case(ctx, name, m, n, k, dist=gen.DIST_I, beta=-1.0, transB=transB)
     np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["tc_tf32_2sm", "tc_bf16_2sm"])
+@pytest.mark.parametrize("shape", [(300, 519, 1000), (777, 255, 129)], ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("beta", [0.5, 0.0])
+def test_2sm_row_store_epilogue(ctx, name, shape, beta):
+    """tc_*_2sm with a C that TMA cannot move (ldc * 4 % 16 != 0): the launcher falls back to
+    the per-thread row-store epilogue kernel (tc_gemm_2sm.cu); same tolerance."""
+    m, n, k = shape
+    got, ref, tol = run_case(ctx, name, m, n, k, beta=beta, ldc_pad=1)
+    assert og.rel_fro(got, ref) <= tol
+
+
+@pytest.mark.parametrize("name", ["tc_tf32_2sm", "tc_bf16_2sm", "tc_tf32_2sm_w", "tc_bf16_2sm_w"])
+@pytest.mark.parametrize("transB", [0, 1])
+@pytest.mark.parametrize("beta", [0.5, 0.0])
+def test_pair_kernels_ragged_tiles(ctx, name, transB, beta):
+    """Several pair tiles plus ragged M/N/K tails through the TMA-epilogue pair kernels."""
+    got, ref, tol = run_case(ctx, name, 777, 600, 333, beta=beta, transB=transB)
+    assert og.rel_fro(got, ref) <= tol
 
 
 @pytest.mark.parametrize("name", list(VARIANTS))

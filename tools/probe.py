@@ -41,6 +41,8 @@ if __name__ == "__main__":
              ("simt_f32", 4096, 4096, 4096), ("tma_f32", 1024, 1024, 1024), ("simt_f32", 1024, 1024, 1024),
              ("tc_tf32", 1024, 1024, 1024), ("simt_f32", 64, 64, 64), ("tma_f32", 64, 64, 64),
              ("tc_tf32", 64, 64, 64), ("tc_bf16", 32768, 32768, 32768)]
+    if len(sys.argv) > 1:   # name:m:n:k[:transB],...
+        cases = [tuple(x.split(":")[:1] + [int(v) for v in x.split(":")[1:]]) for x in sys.argv[1].split(",")]
     for c in cases:
         name, m, n, k = c[:4]
         tb = c[4] if len(c) > 4 else 0
