@@ -40,6 +40,13 @@ cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha 
 cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
 cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)
 int *sched_workspace(cudaStream_t s);                        // {next, done} tile counters for persistent kernels
+struct SkWorkspace {                                         // stream-K partials (tc_gemm_2sm_mc.cu)
+    unsigned *flags = nullptr;
+    float *partial = nullptr;
+    int cap = 0;
+    uint32_t epoch = 0;
+};
+SkWorkspace *sk_workspace(cudaStream_t s, int clusters);
 
 // TMA eligibility (the selector's constraint filter).
 inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {

@@ -28,4 +28,25 @@ int *sched_workspace(cudaStream_t s) {
     return p;
 }
 
+// Stream-K workspace (tc_gemm_2sm_mc.cu): per cluster one flag word and one 256 x 256 FP32
+// partial accumulator; `epoch` counts the stream-K launches on this stream, so flags never need
+// resetting (a flag reaches 8 * epoch when that launch's partial is published).
+SkWorkspace *sk_workspace(cudaStream_t s, int clusters) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, SkWorkspace> slots;
+    std::lock_guard<std::mutex> lk(mu);
+    SkWorkspace &w = slots[s];
+    if (w.cap < clusters) {
+        if (w.flags) cudaFree(w.flags);
+        if (w.partial) cudaFree(w.partial);
+        w = SkWorkspace{};
+        const int cap = clusters < 128 ? 128 : clusters;
+        if (cudaMalloc(&w.flags, cap * sizeof(unsigned)) != cudaSuccess) return nullptr;
+        if (cudaMemset(w.flags, 0, cap * sizeof(unsigned)) != cudaSuccess) return nullptr;
+        if (cudaMalloc(&w.partial, static_cast<size_t>(cap) * 256 * 256 * sizeof(float)) != cudaSuccess) return nullptr;
+        w.cap = cap;
+    }
+    return &w;
+}
+
 }  // namespace compar

@@ -21,6 +21,18 @@ namespace {
 constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
 
 __device__ __forceinline__ float to_f32(float x) { return x; }
+
+// Two independent FP32 FMAs in one sm_100 FFMA2 (fma.rn.f32x2): {c0, c1} = a * {b0, b1} + {c0, c1},
+// each with one RN rounding exactly as fmaf, so results are bitwise those of scalar FFMA.  The
+// broadcast of `a` folds into FFMA2's scalar-operand form (no extra MOV).
+__device__ __forceinline__ void ffma2(float &c0, float &c1, float a, float b0, float b1) {
+    unsigned long long c, b, aa;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(c0), "f"(c1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(aa), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
+}
 __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
 
 // Four consecutive elements of row r starting at column c, widened to FP32 (exact for BF16).
@@ -131,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 8; j += 2) ffma2(acc[i][j], acc[i][j + 1], a[i], b[j], b[j + 1]);
         }
         if (kt + 1 < nk) sstore(buf ^ 1);
         __syncthreads();

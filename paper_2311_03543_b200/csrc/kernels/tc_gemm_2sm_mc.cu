@@ -38,7 +38,7 @@ namespace compar {
 namespace {
 
 constexpr int kEpiWarpsM = 4;
-constexpr int kThreadsM = 64 + 32 * kEpiWarpsM;
+constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;   // producer, MMA, 4 epilogue, 2nd producer
 constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
 constexpr int kRingM = 4;
 
@@ -75,6 +75,17 @@ struct TcMParams {
     int m_blocks, n_blocks, num_kb;  // 512-row x 256-column cluster tiles
     int group_m;
     int *sched;
+    // stream-K (kPairs == 1 only): static (tile, k-block) ranges per cluster
+    int sk, sk_clusters;
+    int nprod;             // TMA producer warps per CTA (1 or 2)
+    unsigned *flags;       // per cluster: published HEAD partials, 8 per launch (epoch)
+    float *partial;        // per cluster: 256 x 256 FP32 raw accumulator
+    unsigned epoch;
+};
+
+enum { kFull = 0, kHead = 1, kTail = 2 };
+struct Item {
+    int tile, kb0, kb1, kind;
 };
 
 __device__ __forceinline__ void tile_coords_m(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
@@ -107,6 +118,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     const uint32_t rempty0 = rfull0 + 8 * kRingM;
     const uint32_t cbar0 = rempty0 + 8 * kRingM;
     const uint32_t ring0 = cbar0 + 16 * kEpiWarpsM;
+    const uint32_t tload = ring0 + 4 * kRingM;                    // stream-K partial loaded (pair leader)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,7 +130,8 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     const uint16_t pair_mask = static_cast<uint16_t>(0x3u << pleader);
     const uint16_t b_mask = static_cast<uint16_t>(kPairs == 2 ? (1u << pr) | (1u << (pr + 2)) : 0u);
     // consumers of a tile-ring slot: 4 epilogue warps per CTA, producers of CTAs 1..3, 2 MMA warps
-    constexpr int kConsumers = kCluster * kEpiWarpsM + (kCluster - 1) + kPairs;
+    // (+ every CTA's second producer warp when p.nprod == 2)
+    const int kConsumers = kCluster * kEpiWarpsM + (kCluster - 1) + kPairs + (p.nprod == 2 ? kCluster : 0);
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -137,6 +150,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             ptx::mbar_init(rempty0 + 8 * r, kConsumers);
         }
         for (int b = 0; b < 2 * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
+        ptx::mbar_init(tload, 2 * kEpiWarpsM);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm<512>(ptx::smem_u32(tmem_slot));
@@ -147,42 +161,80 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
 
     const int num_tiles = p.m_blocks * p.n_blocks;
     const uint32_t rempty_root = ptx::mapa_rank(rempty0, 0);
-    auto next_tile = [&](int i) -> int {  // whole-warp consumer of the tile ring
-        const int slot = i % kRingM;
-        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingM) & 1);
+    const int cl = static_cast<int>(blockIdx.x) / kCluster;   // this cluster's index in the grid
+    // Work item j of this cluster.  Dynamic mode: whole tiles from the tile ring (the call is the
+    // ring consumer: the whole warp arrives once).  Stream-K mode (p.sk): the static range of
+    // (tile, k-block) units [cl*U/C, (cl+1)*U/C) in the order HEAD (first k-blocks of the range's
+    // last tile; raw accumulator published to the workspace), FULL tiles, TAIL (last k-blocks of
+    // the range's first tile; continues the accumulator chain from the previous cluster's HEAD).
+    auto sk_item = [&](int j, Item &it) -> bool {
+        const int64_t U = static_cast<int64_t>(num_tiles) * p.num_kb;
+        const int64_t s0 = U * cl / p.sk_clusters, e0 = U * (cl + 1) / p.sk_clusters;
+        const int t0 = static_cast<int>(s0 / p.num_kb), a = static_cast<int>(s0 % p.num_kb);
+        const int t1 = static_cast<int>(e0 / p.num_kb), b = static_cast<int>(e0 % p.num_kb);
+        const int has_head = b != 0, has_tail = a != 0;
+        const int first_full = has_tail ? t0 + 1 : t0;
+        const int n_full = t1 - first_full;
+        if (j < has_head) {
+            it = Item{t1, 0, b, kHead};
+        } else if (j < has_head + n_full) {
+            it = Item{first_full + j - has_head, 0, p.num_kb, kFull};
+        } else if (j == has_head + n_full && has_tail) {
+            it = Item{t0, a, p.num_kb, kTail};
+        } else {
+            return false;
+        }
+        return true;
+    };
+    auto next_item = [&](int j, Item &it) -> bool {  // whole-warp consumer (MMA and epilogue warps)
+        if (p.sk) return sk_item(j, it);
+        const int slot = j % kRingM;
+        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (j / kRingM) & 1);
         const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
-        return t;
+        it = Item{t, 0, p.num_kb, kFull};
+        return t < num_tiles;
     };
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- scheduler (CTA 0) + TMA producer (every CTA)
-            int stage = 0;
-            uint32_t phase = 0;
+    if (warp == 0 || warp == 6) {
+        // ---------------- scheduler (CTA 0 warp 0) + TMA producers: with p.nprod == 2, warp 0
+        // issues the even and warp 6 the odd k-steps (two independent issue streams per SM).
+        const int me = warp == 0 ? 0 : 1;
+        if (lane == 0 && me < p.nprod) {
+            uint32_t kstep = 0;
             for (int i = 0;; ++i) {
-                int t;
-                const int slot = i % kRingM;
-                if (rank == 0) {
-                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, ((i / kRingM) & 1) ^ 1);
-                    t = atomicAdd(&p.sched[0], 1);
-                    ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
-                    for (uint32_t q = 1; q < kCluster; ++q)
-                        ptx::st_shared_cluster_u32(ptx::mapa_rank(ring0 + 4 * slot, q), static_cast<uint32_t>(t));
-                    ptx::mbar_arrive(rfull0 + 8 * slot);
-                    for (uint32_t q = 1; q < kCluster; ++q)
-                        ptx::mbar_arrive_cluster(ptx::mapa_rank(rfull0 + 8 * slot, q));
+                Item it;
+                if (p.sk) {
+                    if (!sk_item(i, it)) break;
                 } else {
-                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingM) & 1);
-                    t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
-                    ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
+                    int t;
+                    const int slot = i % kRingM;
+                    if (rank == 0 && me == 0) {
+                        ptx::mbar_wait_cluster(rempty0 + 8 * slot, ((i / kRingM) & 1) ^ 1);
+                        t = atomicAdd(&p.sched[0], 1);
+                        ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
+                        for (uint32_t q = 1; q < kCluster; ++q)
+                            ptx::st_shared_cluster_u32(ptx::mapa_rank(ring0 + 4 * slot, q), static_cast<uint32_t>(t));
+                        ptx::mbar_arrive(rfull0 + 8 * slot);
+                        for (uint32_t q = 1; q < kCluster; ++q)
+                            ptx::mbar_arrive_cluster(ptx::mapa_rank(rfull0 + 8 * slot, q));
+                    } else {
+                        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingM) & 1);
+                        t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
+                        ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
+                    }
+                    if (t >= num_tiles) break;
+                    it = Item{t, 0, p.num_kb, kFull};
                 }
-                if (t >= num_tiles) break;
                 int mb, nb;
-                tile_coords_m(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+                tile_coords_m(it.tile, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * (kCluster * C::BM) + static_cast<int32_t>(rank) * C::BM;
                 const int32_t bcol = nb * C::BN + static_cast<int32_t>(pr) * C::BN_CTA;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = it.kb0; kb < it.kb1; ++kb, ++kstep) {
+                    if (p.nprod == 2 && (kstep & 1) != static_cast<uint32_t>(me)) continue;
+                    const int stage = static_cast<int>(kstep % C::STAGES);
+                    const uint32_t phase = (kstep / C::STAGES) & 1;
                     ptx::mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
@@ -203,13 +255,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                         else
                             ptx::tma_load_2d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1);
                     }
-                    if (++stage == C::STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
             }
-            if (rank == 0) {  // last cluster out re-arms the counters for the next launch on this stream
+            if (rank == 0 && me == 0) {  // last cluster out re-arms the counters for the next launch on this stream
                 __threadfence();
                 if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x / kCluster) - 1) {
                     p.sched[0] = 0;
@@ -222,14 +270,16 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             int stage = 0;
             uint32_t phase = 0;
             for (int local = 0;; ++local) {
-                const int t = next_tile(local);
-                if (t >= num_tiles) break;
+                Item it;
+                if (!next_item(local, it)) break;
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
+                if (it.kind == kTail) ptx::mbar_wait_cluster(tload, 0);   // partial accumulator in TMEM
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C::BN;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                const bool carry = it.kind == kTail;
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     ptx::mbar_wait(full0 + 8 * stage, phase);
                     ptx::tc_fence_after();
                     if (lane == 0) {
@@ -241,10 +291,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                             const uint64_t bdesc = kTransB ? ptx::smem_desc(sb + j * 32, 16, 1024, 2)
                                                            : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_LBO,
                                                                             C::B_SBO, C::B_LAYOUT);
+                            const uint32_t accum = carry || ((kb | j) != 0);
                             if (kBF16)
-                                ptx::mma_bf16_2sm(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+                                ptx::mma_bf16_2sm(d_tmem, adesc, bdesc, C::IDESC, accum);
                             else
-                                ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+                                ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, C::IDESC, accum);
                         }
                         ptx::tc_commit_2sm_mc(empty0 + 8 * stage, kPairs == 2 ? 0xF : 0x3);
                     }
@@ -268,13 +319,70 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         const bool ldc = p.beta != 0.f;
         const uint32_t swz = lane * 128;
         constexpr int kChunks = C::BN / 32;
+        // this thread's row of the cluster's 256 x 256 stream-K partial (rows = pair tile rows)
+        const int prow = static_cast<int>(rank) * C::BM + q * 32 + lane;
         for (int local = 0;; ++local) {
-            const int t = next_tile(local);
-            if (t >= num_tiles) break;
+            Item it;
+            if (!next_item(local, it)) break;
+            if (p.sk) {
+                Item nx;
+                if (sk_item(local + 1, nx) && nx.kind == kTail) {
+                    // Load the previous cluster's HEAD partial into the accumulator item local+1
+                    // will use (drained in iteration local-1), then release the MMA warp.
+                    const int src = cl - 1;
+                    if (lane == 0) ptx::spin_until_geq(p.flags + src, 2u * kEpiWarpsM * p.epoch);
+                    __syncwarp();
+                    const float *part = p.partial + (static_cast<size_t>(src) * 256 + prow) * 256;
+                    const int nacc = (local + 1) & 1;
+#pragma unroll 1
+                    for (int idx = 0; idx < kChunks; ++idx) {
+                        uint32_t r[32];
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) {
+                            const float4 x = __ldcg(reinterpret_cast<const float4 *>(part + 32 * idx) + v);
+                            r[4 * v + 0] = __float_as_uint(x.x);
+                            r[4 * v + 1] = __float_as_uint(x.y);
+                            r[4 * v + 2] = __float_as_uint(x.z);
+                            r[4 * v + 3] = __float_as_uint(x.w);
+                        }
+                        ptx::tmem_st_32x32b_x32(
+                            tmem_base + (static_cast<uint32_t>(q * 32) << 16) + nacc * C::BN + 32 * idx, r);
+                    }
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_rank(tload, pleader));
+                }
+            }
             int mb, nb;
-            tile_coords_m(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+            tile_coords_m(it.tile, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
+            if (it.kind == kHead) {  // publish the raw accumulator (no alpha / beta) for the next cluster
+                ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+                ptx::tc_fence_after();
+                float *part = p.partial + (static_cast<size_t>(cl) * 256 + prow) * 256;
+#pragma unroll 1
+                for (int idx = 0; idx < kChunks; ++idx) {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx,
+                                            r);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int v = 0; v < 8; ++v)
+                        __stcg(reinterpret_cast<float4 *>(part + 32 * idx) + v,
+                               make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                           __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
+                }
+                ptx::tc_fence_before();
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+                    atomicAdd(p.flags + cl, 1u);
+                }
+                continue;
+            }
             const int32_t row_base = mb * (kCluster * C::BM) + static_cast<int32_t>(rank) * C::BM + q * 32;
             const int32_t col_base = nb * C::BN;
             if (lane == 0) {
@@ -339,6 +447,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 __syncwarp();
             }
         }
+        if (p.sk) {  // a cluster without a HEAD item still advances its flag by one launch
+            Item h;
+            if (!(sk_item(0, h) && h.kind == kHead) && lane == 0) atomicAdd(p.flags + cl, 1u);
+        }
         if (lane == 0) ptx::bulk_wait<0>();
         __syncwarp();
     }
@@ -401,6 +513,25 @@ cudaError_t launch_tcm_t(const GemmLaunch &g) {
     int clusters = g.num_sms / kCluster < max_clusters ? g.num_sms / kCluster : max_clusters;
     if (clusters < 1) clusters = 1;
     if (tiles < clusters) clusters = tiles;
+    // Stream-K when whole tiles would leave the last wave badly filled (> 3 % idle): every
+    // cluster gets the same number of (tile, k-block) units; a tile split between two clusters
+    // continues the same MMA chain from a published FP32 partial, so C is bitwise the
+    // data-parallel result.  COMPAR_STREAMK=0 never, =1 whenever the grid allows it.
+    const char *sk_s = std::getenv("COMPAR_STREAMK");   // read per launch (tests flip it)
+    const int sk_env = sk_s ? std::atoi(sk_s) : -1;
+    const int waves = (tiles + clusters - 1) / clusters;
+    const bool sk_ok = kPairs == 1 && tiles >= clusters && (tiles % clusters != 0 || sk_env == 2);
+    (void)waves;  // auto mode measured slower: stream-K only on request
+    p.sk = sk_ok && sk_env >= 1;
+    p.sk_clusters = clusters;
+    p.flags = nullptr, p.partial = nullptr, p.epoch = 0;
+    const char *np_s = std::getenv("COMPAR_TC2_PRODUCERS");
+    p.nprod = np_s && std::atoi(np_s) == 1 ? 1 : 2;
+    if (p.sk) {
+        SkWorkspace *w = sk_workspace(g.stream, clusters);
+        if (!w) return cudaErrorMemoryAllocation;
+        p.flags = w->flags, p.partial = w->partial, p.epoch = ++w->epoch;
+    }
     tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     return cudaGetLastError();
 }

@@ -25,6 +25,17 @@
 namespace compar {
 namespace {
 
+// {c0, c1} = a * {b0, b1} + {c0, c1} as one sm_100 FFMA2 (fma.rn.f32x2): two RN FMAs, bitwise
+// equal to two fmaf calls (see simt_f32.cu).
+__device__ __forceinline__ void ffma2(float &c0, float &c1, float a, float b0, float b1) {
+    unsigned long long c, b, aa;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(c0), "f"(c1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(aa), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
+}
+
 constexpr int BM = 128, BN = 128, BK = 32, STAGES = 4;
 constexpr int kConsumers = 256, kThreads = kConsumers + 32;
 constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BK * BN * 4, STAGE_BYTES = A_BYTES + B_BYTES;
@@ -125,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int i = 0; i < 8; ++i) {
                         const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, b[j], acc[i][j]);
+                        for (int j = 0; j < 8; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
                     }
                 }
             }

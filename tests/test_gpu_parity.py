@@ -109,6 +109,37 @@ def test_pair_kernels_ragged_tiles(ctx, name, transB, beta):
     assert og.rel_fro(got, ref) <= tol
 
 
+@pytest.mark.parametrize("name", ["tc_tf32_2sm", "tc_bf16_2sm"])
+@pytest.mark.parametrize("shape,transB,beta", [((65536, 256, 4096), 0, 0.5), ((4864, 1280, 1000), 1, 0.0),
+                                               ((4800, 1200, 776), 0, 0.5), ((19000, 304, 200), 0, 0.5)],
+                         ids=["5a", "ragged-t", "ragged", "short-k"])
+def test_stream_k_bitwise(ctx, monkeypatch, name, shape, transB, beta):
+    """Stream-K (a tile's k-blocks split between two clusters, the second continuing the MMA
+    chain from the first's published FP32 partial) gives C BITWISE equal to the data-parallel
+    schedule, and within tolerance of the oracle on sampled rows."""
+    dtype_id, compute, tol = VARIANTS[name]
+    dt = "bf16" if dtype_id == cm.BF16 else "f32"
+    m, n, k = shape
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(transB))
+    C0 = device_matrix(gen.TAG_C, m, n)
+    outs = []
+    for sk in ("0", "1", "1"):
+        monkeypatch.setenv("COMPAR_STREAMK", sk)
+        Cd = C0.clone()
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=beta, in_dtype=dtype_id,
+                         compute=compute, transB=transB, ldb=k if transB else n, variant_hint=vid(ctx, name),
+                         stream=torch.cuda.current_stream().cuda_stream)
+        assert ctx.run(d).status == 0
+        outs.append(Cd)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    rows = np.unique(np.linspace(0, m - 1, 40).astype(np.int64))
+    got = outs[1][torch.as_tensor(rows, device="cuda")].double().cpu().numpy()
+    ref = og.gemm(gen.matrix_rows(gen.TAG_A, rows, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt),
+                  gen.matrix_rows(gen.TAG_C, rows, n), alpha=1.5, beta=beta, dtype=dt)
+    assert og.rel_fro(got, ref) <= tol
+
+
 @pytest.mark.parametrize("name", list(VARIANTS))
 def test_transB_and_beta0_nan(ctx, name):
     got, ref, tol = run_case(ctx, name, 190, 300, 260, transB=1, beta=0.0)
