@@ -40,6 +40,7 @@ def parse():
     p.add_argument("--size", type=int, default=32768)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-targets", action="store_true", help="skip the config-3 / 5a north-star block")
     return p.parse_args()
 
 
@@ -180,6 +181,65 @@ def cpu_baseline(size):
 
 
 # ---------------------------------------------------------------------------------------------
+def north_star_targets(ctx, cm, peaks, R=10):
+    """BASELINE.json north_star targets on this GPU, through the same C ABI (untimed w.r.t. the
+    headline): config 3 (8192^3 BF16, target >= 70 % of the measured burst BF16 peak) and config 5a
+    (65536x256x4096 BF16, HBM-bound: % of the measured copy bandwidth).  Each shape: selector trained
+    on the key (calibration), R model-mode runs; then regret = chosen / best - 1 over an exhaustive,
+    interleaved timing of every eligible tensor-core variant (FFMA variants: history mean)."""
+    import statistics
+
+    import torch
+
+    import gen
+    from gen.device import device_matrix
+    names = [n for n, _ in ctx.variants()]
+    out = {}
+    for key, (m, n, k) in (("config3_8192cube_bf16", (8192, 8192, 8192)),
+                           ("config5a_65536x256x4096_bf16", (65536, 256, 4096))):
+        A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
+        B = device_matrix(gen.TAG_B, k, n, dtype="bf16")
+        C = device_matrix(gen.TAG_C, m, n)
+
+        def mk(hint=-1):
+            return cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=ALPHA, beta=BETA, in_dtype=cm.BF16,
+                                compute=cm.COMPUTE_BF16, variant_hint=hint)
+        d = mk()
+        calib = 0
+        while ctx.select(d)[1] != cm.MODE_MODEL and calib < 64:
+            ctx.run(d)
+            calib += 1
+        sel = [ctx.run(d) for _ in range(R)]
+        chosen = sel[-1].variant
+        E = [v for v, (_, t) in enumerate(ctx.variants()) if t in cm.TARGETS_BF16]
+        tc = [v for v in E if names[v].startswith("tc_")]
+        descs = {v: mk(v) for v in tc}
+        for v in tc:
+            ctx.run(descs[v])
+        samples = {v: [] for v in tc}
+        for _ in range(R):
+            for v in tc:
+                samples[v].append(ctx.run(descs[v]).ns)
+        med = {names[v]: statistics.median(samples[v]) for v in tc}
+        for v in E:
+            if v not in tc:
+                med[names[v]] = ctx.history(v, d).mean_ns
+        best = min(med, key=med.get)
+        t_sel = statistics.median(r.ns for r in sel)
+        flops = 2.0 * m * n * k
+        nbytes = 2 * (m * k + k * n) + 4 * m * n * 2
+        out[key] = {"variant": names[chosen], "ms": t_sel / 1e6, "tflops": flops / t_sel / 1e3,
+                    "frac_of_bf16_burst_peak": flops / t_sel / 1e3 / peaks["bf16_tflops"],
+                    "hbm_gbs": nbytes / t_sel, "frac_of_hbm_peak": nbytes / t_sel / peaks["hbm_gbs"],
+                    "best_variant": best, "regret": med[names[chosen]] / med[best] - 1.0,
+                    "median_ns_per_variant": med, "calibration_runs": calib}
+        del A, B, C
+        torch.cuda.empty_cache()
+    out["selector_regret_max"] = max(v["regret"] for v in out.values())
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -293,6 +353,29 @@ def main():
             traffic = None
     bcast_ms = sum(r.bcast_ns for r in reps) / len(reps) / 1e6
 
+    # selector regret at the headline key (after the timed region): every eligible tensor-core
+    # variant timed 3x, interleaved, through the same call with a variant hint; FFMA variants use
+    # their calibration mean (they are ~30x slower here)
+    regret = None
+    if world == 1:
+        vn = [v for v, _ in ctx.variants()]
+        elig = [v for v, (_, t) in enumerate(ctx.variants()) if t in cm.TARGETS_BF16]
+        tcv = [v for v in elig if vn[v].startswith("tc_")]
+        hinted = {v: cm.make_desc(M, N, K, A=A, B=B, C_in=Cm, C_out=Cm, lda=K, ldb=N, ldc_in=N, ldc_out=N,
+                                  alpha=ALPHA, beta=BETA, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, stream=sp,
+                                  variant_hint=v) for v in tcv}
+        smp = {v: [] for v in tcv}
+        for _ in range(3):
+            for v in tcv:
+                smp[v].append(ctx.run(hinted[v]).ns)
+        med = {vn[v]: statistics.median(smp[v]) for v in tcv}
+        for v in elig:
+            if v not in tcv:
+                med[vn[v]] = ctx.history(v, desc).mean_ns
+        best = min(med, key=med.get)
+        regret = {"chosen": vn[reps[-1].variant], "best": best,
+                  "regret": med[vn[reps[-1].variant]] / med[best] - 1.0, "median_ns_per_variant": med}
+
     # end to end through the same C ABI call with HOST buffers (pinned), copies in the timed region
     e2e = None
     if args.e2e_steps > 0:
@@ -318,6 +401,12 @@ def main():
             dist.all_reduce(t)
             e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"] = int(t[0].item()), int(t[1].item())
 
+    targets = None
+    if world == 1 and not args.no_targets:
+        del Cm
+        torch.cuda.empty_cache()
+        targets = north_star_targets(ctx, cm, load_peaks()[0])
+
     out = None
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -337,16 +426,16 @@ def main():
                "pct_of_peak": value / peak * 100.0,
                "bcast_ms_per_step": bcast_ms,
                "gpu_launches": int(launches),
-               "selector": {"calibration_runs_before_timing": calib_runs, "chosen": chosen,
+               "selector": {"calibration_runs_before_timing": calib_runs, "chosen": chosen, "regret": regret,
                             "variants_in_timed_region": used,
                             "eligible": [n for n, t in ctx.variants() if t in cm.TARGETS_BF16]},
-               "clocks": clocks, "e2e": e2e}
+               "clocks": clocks, "e2e": e2e, "north_star_targets": targets}
     if world > 1:
         dist.barrier()
     ctx.terminate()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            del Cm, B
+            del B
             out["cpu_baseline"] = cpu_baseline(args.size)
         else:
             out["cpu_baseline"] = None
