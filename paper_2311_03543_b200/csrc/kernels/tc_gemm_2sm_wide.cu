@@ -34,6 +34,7 @@ constexpr int kEpiWarpsW = 4;
 constexpr int kThreadsW = 64 + 32 * kEpiWarpsW;
 constexpr int kGroupW = 4;
 constexpr int kRingW = 4;
+constexpr int kDelayW = 24;  // default epilogue-overlap delay in k-steps (COMPAR_TCW_DELAY overrides)
 
 template <bool kBF16, bool kTransB>
 struct TcWCfg {
@@ -63,6 +64,7 @@ struct TcWParams {
     float alpha, beta;
     int m_blocks, n_blocks, num_kb;  // 256-row x 512-column pair tiles
     int group_m;
+    int delay;       // k-steps of accumulator half 0 issued before half 1 is needed (epilogue overlap)
     int *sched;
 };
 
@@ -96,8 +98,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     const uint32_t full0 = ptx::smem_u32(bars);
     const uint32_t empty0 = full0 + 8 * C::STAGES;
     const uint32_t tfull = empty0 + 8 * C::STAGES;
-    const uint32_t tempty = tfull + 8;
-    const uint32_t rfull0 = tempty + 8;
+    const uint32_t tempty = tfull + 8;            // [2]: accumulator half h drained (leader)
+    const uint32_t rfull0 = tempty + 16;
     const uint32_t rempty0 = rfull0 + 8 * kRingW;
     const uint32_t cbar0 = rempty0 + 8 * kRingW;                        // 2 per epilogue warp
     const uint32_t ring0 = cbar0 + 16 * kEpiWarpsW;
@@ -118,6 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
         }
         ptx::mbar_init(tfull, 1);
         ptx::mbar_init(tempty, 2 * kEpiWarpsW);
+        ptx::mbar_init(tempty + 8, 2 * kEpiWarpsW);
         for (int r = 0; r < kRingW; ++r) {
             ptx::mbar_init(rfull0 + 8 * r, 1);
             ptx::mbar_init(rempty0 + 8 * r, kConsumers);
@@ -166,15 +169,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM;
                 const int32_t bcol0 = nb * C::BN + static_cast<int32_t>(rank) * 128;   // + 256 h
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                // Step order: with delay D > 0 (every tile but the CTA's first), the
+                // first D k-steps feed accumulator half 0 only, then the same D k-steps half 1 (A
+                // re-loaded), then both halves: half 0 restarts while the epilogue still drains half
+                // 1.  Each half still sums its k-steps in increasing order (bitwise = D = 0).
+                const int D = i == 0 ? 0 : min(p.delay, p.num_kb);
+                for (int st = 0; st < p.num_kb + D; ++st) {
+                    const int kb = st < D ? st : st < 2 * D ? st - D : st - D;
+                    const int hmask = st < D ? 1 : st < 2 * D ? 2 : 3;
                     ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
                     const uint32_t fb_local = full0 + 8 * stage;
                     const uint32_t fb = ptx::leader_addr(fb_local);
-                    if (leader) ptx::mbar_arrive_expect_tx(fb_local, 2 * C::STAGE_BYTES);
+                    if (leader)
+                        ptx::mbar_arrive_expect_tx(fb_local, hmask == 3 ? 2 * C::STAGE_BYTES
+                                                                         : 2 * (C::A_BYTES + C::BH_BYTES));
                     ptx::tma_load_2d_2sm(sa, &tmA, fb, kb * C::BK, arow);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
+                        if (!((hmask >> h) & 1)) continue;
                         const uint32_t sb = sa + C::A_BYTES + h * C::BH_BYTES;
                         if (kTransB) {
                             ptx::tma_load_2d_2sm(sb, &tmB, fb, kb * C::BK, bcol0 + 256 * h);
@@ -206,9 +219,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             for (int local = 0;; ++local) {
                 const int t = next_tile(local);
                 if (t >= num_tiles) break;
-                ptx::mbar_wait_cluster(tempty, (local & 1) ^ 1);
+                const int D = local == 0 ? 0 : min(p.delay, p.num_kb);
+                ptx::mbar_wait_cluster(tempty, (local & 1) ^ 1);        // half 0 drained
+                if (D == 0) ptx::mbar_wait_cluster(tempty + 8, (local & 1) ^ 1);
                 ptx::tc_fence_after();
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int st = 0; st < p.num_kb + D; ++st) {
+                    const int kb = st < D ? st : st < 2 * D ? st - D : st - D;
+                    const int hmask = st < D ? 1 : st < 2 * D ? 2 : 3;
+                    if (D > 0 && st == D) {                                  // half 1 drained
+                        ptx::mbar_wait_cluster(tempty + 8, (local & 1) ^ 1);
+                        ptx::tc_fence_after();
+                    }
                     ptx::mbar_wait(full0 + 8 * stage, phase);
                     ptx::tc_fence_after();
                     if (lane == 0) {
@@ -218,6 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                             const uint64_t adesc = ptx::smem_desc(sa + j * 32, 16, 1024, 2);
 #pragma unroll
                             for (int h = 0; h < 2; ++h) {
+                                if (!((hmask >> h) & 1)) continue;
                                 const uint32_t sb = sa + C::A_BYTES + h * C::BH_BYTES;
                                 const uint64_t bdesc = kTransB
                                                            ? ptx::smem_desc(sb + j * 32, 16, 1024, 2)
@@ -278,6 +300,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 ptx::tmem_ld_32x32b_x32(
                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 256 * (idx >> 3) + 32 * (idx & 7), r);
                 ptx::tmem_ld_wait();
+                if ((idx & 7) == 7) {                     // half idx>>3 is in registers: release it
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * (idx >> 3));
+                }
                 if (ldc) {
                     ptx::mbar_wait(cbar[b], (loads[b] - 1) & 1);
                 } else if (idx >= 2) {
@@ -315,9 +342,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 if (ldc && idx + 2 < 16) ++loads[b];
                 __syncwarp();
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
         }
         if (lane == 0) ptx::bulk_wait<0>();               // all C stores complete before exit
         __syncwarp();
@@ -363,6 +387,9 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
         return s ? std::atoi(s) : 0;
     }();
     p.group_m = group_env > 0 ? group_env : kGroupW;
+    const char *dl = std::getenv("COMPAR_TCW_DELAY");     // read per launch (tests compare D = 0)
+    p.delay = dl ? std::atoi(dl) : kDelayW;
+    if (p.delay < 0) p.delay = 0;
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;

@@ -140,6 +140,37 @@ def test_stream_k_bitwise(ctx, monkeypatch, name, shape, transB, beta):
     assert og.rel_fro(got, ref) <= tol
 
 
+@pytest.mark.parametrize("name", ["tc_tf32_2sm_w", "tc_bf16_2sm_w"])
+@pytest.mark.parametrize("shape,transB,beta", [((4096, 5120, 1000), 0, 0.5), ((4000, 5000, 200), 1, 0.0),
+                                               ((8192, 8192, 2048), 0, 0.5)], ids=["multi-tile", "short-k-t", "8k"])
+def test_wide_epilogue_overlap_bitwise(ctx, monkeypatch, name, shape, transB, beta):
+    """The wide kernel's overlapped schedule (first D k-steps into accumulator half 0 only, then
+    half 1, then both) sums every output element over k in the same order as D = 0, so C is BITWISE
+    equal for every delay (incl. D >= the number of k-steps)."""
+    dtype_id, compute, tol = VARIANTS[name]
+    dt = "bf16" if dtype_id == cm.BF16 else "f32"
+    m, n, k = shape
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(transB))
+    C0 = device_matrix(gen.TAG_C, m, n)
+    outs = []
+    for delay in ("0", "12", "3", "1000"):
+        monkeypatch.setenv("COMPAR_TCW_DELAY", delay)
+        Cd = C0.clone()
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=beta, in_dtype=dtype_id,
+                         compute=compute, transB=transB, ldb=k if transB else n, variant_hint=vid(ctx, name),
+                         stream=torch.cuda.current_stream().cuda_stream)
+        assert ctx.run(d).status == 0
+        outs.append(Cd)
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)
+    rows = np.unique(np.linspace(0, m - 1, 24).astype(np.int64))
+    got = outs[1][torch.as_tensor(rows, device="cuda")].double().cpu().numpy()
+    ref = og.gemm(gen.matrix_rows(gen.TAG_A, rows, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt),
+                  gen.matrix_rows(gen.TAG_C, rows, n), alpha=1.5, beta=beta, dtype=dt)
+    assert og.rel_fro(got, ref) <= tol
+
+
 @pytest.mark.parametrize("name", list(VARIANTS))
 def test_transB_and_beta0_nan(ctx, name):
     got, ref, tol = run_case(ctx, name, 190, 300, 260, transB=1, beta=0.0)
