@@ -176,8 +176,29 @@ def cpu_baseline(size):
         if dt > 5.0 or r >= 2048:
             break
         r = min(2048, int(r * max(1.5, (10.0 / max(dt, 1e-3)) ** 0.5)))
-    return {"value": 2.0 * r * r * K / dt / 1e12, "unit": "TFLOP/s", "cores": og.threads(), "kind": "oracle",
-            "sample": f"{r}x{r} sub-block (rows/cols spread over the matrix) x full K={K}, FP64, {dt:.1f} s"}
+    cores = og.threads()
+    # the same oracle on ONE thread, on a proportionally smaller sample (~3 s)
+    r1 = max(16, int(r / max(cores, 1) ** 0.5))
+    rows1 = np.linspace(0, size - 1, r1).astype(np.int64)
+    A1 = gen.matrix_rows(gen.TAG_A, rows1, K, dtype="bf16")
+    B1 = gen.matrix_cols(gen.TAG_B, K, rows1, dtype="bf16")
+    C1 = gen.matrix_entries(gen.TAG_C, rows1, rows1)
+    og.set_threads(1)
+    t0 = time.perf_counter()
+    og.gemm(A1, B1, C1, alpha=ALPHA, beta=BETA, dtype="bf16")
+    dt1 = time.perf_counter() - t0
+    og.set_threads(cores)
+    cpu_model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    return {"value": 2.0 * r * r * K / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"{r}x{r} sub-block (rows/cols spread over the matrix) x full K={K}, FP64, {dt:.1f} s",
+            "value_1_thread": 2.0 * r1 * r1 * K / dt1 / 1e12,
+            "sample_1_thread": f"{r1}x{r1} sub-block x full K={K}, FP64, 1 thread, {dt1:.1f} s",
+            "cpu_model": cpu_model, "affinity_cores": len(os.sched_getaffinity(0))}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -424,6 +445,8 @@ def main():
                             "frac_of_burst": achieved / peaks.get("bf16_tflops", peak),
                             "avg_launch_ms": k_avg / 1e6},
                "pct_of_peak": value / peak * 100.0,
+               "step_kernel_ms": {"mean": k_avg / 1e6, "median": statistics.median(kern_ns) / 1e6,
+                                  "min": min(kern_ns) / 1e6, "n": len(kern_ns)},
                "bcast_ms_per_step": bcast_ms,
                "gpu_launches": int(launches),
                "selector": {"calibration_runs_before_timing": calib_runs, "chosen": chosen, "regret": regret,

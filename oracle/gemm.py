@@ -43,6 +43,8 @@ def _load():
             lib.compar_oracle_gemm.argtypes = [lg, lg, lg, d, p, lg, p, lg, d, p, lg, p, lg]
             lib.compar_oracle_gemm.restype = None
             lib.compar_oracle_threads.restype = ctypes.c_int
+            lib.compar_oracle_set_threads.argtypes = [ctypes.c_int]
+            lib.compar_oracle_set_threads.restype = None
             _lib = lib
     return _lib
 
@@ -82,6 +84,11 @@ def gemm(A, B, C_in=None, alpha: float = 1.0, beta: float = 0.0, dtype: str = "f
 
 def threads() -> int:
     return int(_load().compar_oracle_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads for later oracle calls (timing only; results do not depend on it)."""
+    _load().compar_oracle_set_threads(int(n))
 
 
 def rel_fro(c_test, c_ref) -> float:

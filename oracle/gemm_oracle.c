@@ -69,3 +69,15 @@ int compar_oracle_threads(void)
     return 1;
 #endif
 }
+
+/* Set the OpenMP thread count for later calls (the bench's 1-thread vs all-threads timing of the
+ * oracle); rows are independent, so results do not depend on it. */
+void compar_oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
