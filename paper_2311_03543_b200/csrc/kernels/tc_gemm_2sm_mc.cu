@@ -78,6 +78,7 @@ struct TcMParams {
     // stream-K (kPairs == 1 only): static (tile, k-block) ranges per cluster
     int sk, sk_clusters;
     int nprod;             // TMA producer warps per CTA (1 or 2)
+    int cin_prefetch;      // L2-prefetch the tile's C_in when the tile starts (COMPAR_CIN_PREFETCH=0 disables)
     unsigned *flags;       // per cluster: published HEAD partials, 8 per launch (epoch)
     float *partial;        // per cluster: 256 x 256 FP32 raw accumulator
     unsigned epoch;
@@ -387,6 +388,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             const int32_t col_base = nb * C::BN;
             if (lane == 0) {
                 ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
+                if (ldc && p.cin_prefetch) {              // C_in of this tile -> L2 during its mainloop
+                    for (int idx = 2; idx < kChunks; ++idx) ptx::tma_prefetch_2d(&tmCi, col_base + 32 * idx, row_base);
+                }
                 if (ldc) {
                     for (int b = 0; b < 2; ++b) {
                         ptx::mbar_arrive_expect_tx(cbar[b], 4096);
@@ -525,6 +529,8 @@ cudaError_t launch_tcm_t(const GemmLaunch &g) {
     p.sk = sk_ok && sk_env >= 1;
     p.sk_clusters = clusters;
     p.flags = nullptr, p.partial = nullptr, p.epoch = 0;
+    const char *cp_s = std::getenv("COMPAR_CIN_PREFETCH");
+    p.cin_prefetch = cp_s ? std::atoi(cp_s) : 0;   // measured slower (8192^3 763 vs 737 us): opt-in
     const char *np_s = std::getenv("COMPAR_TC2_PRODUCERS");
     p.nprod = np_s && std::atoi(np_s) == 1 ? 1 : 2;
     if (p.sk) {

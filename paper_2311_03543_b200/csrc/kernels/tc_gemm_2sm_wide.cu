@@ -64,6 +64,7 @@ struct TcWParams {
     float alpha, beta;
     int m_blocks, n_blocks, num_kb;  // 256-row x 512-column pair tiles
     int group_m;
+    int cin_prefetch;  // L2-prefetch the tile's C_in when the tile starts (COMPAR_CIN_PREFETCH=0 disables)
     int delay;       // k-steps of accumulator half 0 issued before half 1 is needed (epilogue overlap)
     int *sched;
 };
@@ -282,6 +283,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             auto chunk_col = [&](int idx) { return col_base + 256 * (idx >> 3) + 32 * (idx & 7); };
             if (lane == 0) {
                 ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
+                if (ldc && p.cin_prefetch) {              // C_in of this tile -> L2 during its mainloop
+                    for (int idx = 2; idx < 16; ++idx) ptx::tma_prefetch_2d(&tmCi, chunk_col(idx), row_base);
+                }
                 if (ldc) {
                     for (int b = 0; b < 2; ++b) {
                         ptx::mbar_arrive_expect_tx(cbar[b], 4096);
@@ -387,6 +391,8 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
         return s ? std::atoi(s) : 0;
     }();
     p.group_m = group_env > 0 ? group_env : kGroupW;
+    const char *cp_s = std::getenv("COMPAR_CIN_PREFETCH");
+    p.cin_prefetch = cp_s ? std::atoi(cp_s) : 0;   // measured slower (8192^3 763 vs 737 us): opt-in
     const char *dl = std::getenv("COMPAR_TCW_DELAY");     // read per launch (tests compare D = 0)
     p.delay = dl ? std::atoi(dl) : kDelayW;
     if (p.delay < 0) p.delay = 0;

@@ -29,7 +29,8 @@ for _ in range(2000):
     cm.lib.compar_stats_get(ctx.ctx, ctypes.byref(st))
     t.append(time.perf_counter() - t0)
 print(f"ctypes no-op ABI call: {statistics.median(t) * 1e6:.2f} us")
-for label, hint in (("hint tc_tf32", names.index("tc_tf32")), ("selector (model mode)", -1)):
+cases = [("hint " + v, names.index(v)) for v in ("simt_f32", "tma_f32", "tc_tf32", "tc_tf32_2sm", "tc_tf32_2sm_w")]
+for label, hint in cases + [("selector (model mode)", -1)]:
     d = cm.make_desc(64, 64, 64, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.0, beta=0.0, compute=cm.COMPUTE_TF32,
                      variant_hint=hint)
     for _ in range(40):
