@@ -29,6 +29,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunks = 16;                       // 16 keys per lane
 constexpr int kTile = kThreads * kChunks;         // 4096 keys per tile
+constexpr int kLookback = 4;                      // predecessors read per look-back round trip
 constexpr uint32_t kAgg = 1u << 30, kIncl = 2u << 30, kCountMask = (1u << 30) - 1;
 
 template <int KT>
@@ -126,21 +127,24 @@ __global__ void __launch_bounds__(kThreads, 3) radix_pass_kernel(const uint32_t 
     // Peers (lanes with the same digit) from 8 ballots — one per digit bit — instead of
     // match.any: the ballots run on the ALU pipes, match.any / ffs on the narrow ADU / XU pipes
     // that bounded the first version (ncu: ADU 68 %, XU saturated).
+    // Keys past n (last tile only) were loaded as code 0xffffffff: digit 255 in every pass, so they
+    // rank after every real key of the tile and occupy its last sorted slots, which the scatter
+    // below never reads (i < valid_n); only their count is taken out of the published digit-255
+    // count.  No per-key validity test is needed in the ranking.
     uint16_t rank[kChunks];
 #pragma unroll
     for (int c = 0; c < kChunks; ++c) {
-        const bool valid = base + c * 32 + lane < n;
         const uint32_t d = (code[c] >> shift) & 255u;
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+        uint32_t peers = 0xffffffffu;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const uint32_t v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
             peers &= ((d >> b) & 1u) ? v : ~v;
         }
-        const uint32_t before = valid ? warp_hist[warp][d] : 0u;
+        const uint32_t before = warp_hist[warp][d];
         __syncwarp();
         rank[c] = static_cast<uint16_t>(before + __popc(peers & lt));
-        if (valid && (peers & lt) == 0) warp_hist[warp][d] = before + __popc(peers);
+        if ((peers & lt) == 0) warp_hist[warp][d] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -151,6 +155,9 @@ __global__ void __launch_bounds__(kThreads, 3) radix_pass_kernel(const uint32_t 
         warp_hist[w][tid] = run;
         run += v;
     }
+    const int64_t tile0 = static_cast<int64_t>(tile) * kTile;
+    const int valid_n = static_cast<int>(n - tile0 < kTile ? n - tile0 : kTile);
+    if (tid == 255) run -= static_cast<uint32_t>(kTile - valid_n);   // padding keys are not published
     uint32_t *st = status + static_cast<int64_t>(tile) * 256 + tid;
     __stcg(st, (tile == 0 ? kIncl : kAgg) | run);
     const uint32_t local = block_excl_scan(run, wsum);         // tile-local start of digit `tid`
@@ -158,29 +165,39 @@ __global__ void __launch_bounds__(kThreads, 3) radix_pass_kernel(const uint32_t 
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < kChunks; ++c) {
-        if (base + c * 32 + lane >= n) continue;
         const uint32_t d = (code[c] >> shift) & 255u;
         sorted[warp_hist[warp][d] + rank[c]] = code[c];
     }
     uint32_t prefix = 0;
     if (tile > 0) {
+        // Windowed look-back: the status words of kLookback predecessors are loaded together (one
+        // round trip instead of kLookback), then consumed in order until an inclusive prefix; a
+        // predecessor that has not published yet restarts the window at it after a back-off.
         for (int j = tile - 1;;) {
-            const uint32_t v = ld_relaxed_gpu(status + static_cast<int64_t>(j) * 256 + tid);
-            const uint32_t flag = v & ~kCountMask;
-            if (flag == 0) {  // predecessor still ranking: back off instead of burning issue slots
-                __nanosleep(64);
-                continue;
+            uint32_t v[kLookback];
+#pragma unroll
+            for (int w = 0; w < kLookback; ++w)
+                v[w] = j - w >= 0 ? ld_relaxed_gpu(status + static_cast<int64_t>(j - w) * 256 + tid) : kIncl;
+            int w = 0;
+            bool done = false;
+#pragma unroll
+            for (; w < kLookback; ++w) {
+                const uint32_t flag = v[w] & ~kCountMask;
+                if (flag == 0) break;
+                prefix += v[w] & kCountMask;
+                if (flag == kIncl) {
+                    done = true;
+                    break;
+                }
             }
-            prefix += v & kCountMask;
-            if (flag == kIncl) break;
-            --j;
+            if (done) break;
+            j -= w;
+            if (w < kLookback) __nanosleep(32);   // predecessor still ranking: back off
         }
         __stcg(st, kIncl | (prefix + run));
     }
     digit_base[tid] = goff + prefix - local;
     __syncthreads();
-    const int64_t t0 = static_cast<int64_t>(tile) * kTile;
-    const int valid_n = static_cast<int>(n - t0 < kTile ? n - t0 : kTile);
 #pragma unroll 4
     for (int i = tid; i < valid_n; i += kThreads) {
         const uint32_t c = sorted[i];
