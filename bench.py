@@ -232,7 +232,7 @@ def north_star_targets(ctx, cm, peaks, R=10):
             calib += 1
         sel = [ctx.run(d) for _ in range(R)]
         chosen = sel[-1].variant
-        E = [v for v, (_, t) in enumerate(ctx.variants()) if t in cm.TARGETS_BF16]
+        E = ctx.eligible(d)
         tc = [v for v in E if names[v].startswith("tc_")]
         descs = {v: mk(v) for v in tc}
         for v in tc:
@@ -380,7 +380,7 @@ def main():
     regret = None
     if world == 1:
         vn = [v for v, _ in ctx.variants()]
-        elig = [v for v, (_, t) in enumerate(ctx.variants()) if t in cm.TARGETS_BF16]
+        elig = ctx.eligible(desc)
         tcv = [v for v in elig if vn[v].startswith("tc_")]
         hinted = {v: cm.make_desc(M, N, K, A=A, B=B, C_in=Cm, C_out=Cm, lda=K, ldb=N, ldc_in=N, ldc_out=N,
                                   alpha=ALPHA, beta=BETA, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, stream=sp,
@@ -451,7 +451,7 @@ def main():
                "gpu_launches": int(launches),
                "selector": {"calibration_runs_before_timing": calib_runs, "chosen": chosen, "regret": regret,
                             "variants_in_timed_region": used,
-                            "eligible": [n for n, t in ctx.variants() if t in cm.TARGETS_BF16]},
+                            "eligible": [variant_names[v] for v in ctx.eligible(desc)]},
                "clocks": clocks, "e2e": e2e, "north_star_targets": targets}
     if world > 1:
         dist.barrier()

@@ -79,6 +79,9 @@ typedef enum {
     COMPAR_TGT_TCW_TF32 = 7,    /* built-in (c), wide CTA-pair form: 256x512 pair tile, 2 accumulators  */
     COMPAR_TGT_TCW_BF16 = 8,    /* built-in (c), wide CTA-pair form, BF16                               */
     COMPAR_TGT_SIMT_BF16 = 9,   /* built-in (a), BF16 operands widened to FP32, FFMA; any shape/alignment */
+    COMPAR_TGT_TCS_TF32 = 10,   /* built-in (c), split-K CTA-pair form: K cut into 2..8 ranges (a function */
+                                /*   of K only), partials summed in split order; small-M*N / deep-K shapes */
+    COMPAR_TGT_TCS_BF16 = 11,   /* built-in (c), split-K CTA-pair form, BF16                              */
     /* the "sort" interface */
     COMPAR_TGT_SORT_RADIX = 20,   /* built-in: onesweep LSD radix sort, 4 x 8-bit passes, any n      */
     COMPAR_TGT_SORT_BITONIC = 21  /* built-in: single-CTA shared-memory bitonic network, n <= 16384  */

@@ -47,6 +47,29 @@ struct SkWorkspace {                                         // stream-K partial
     uint32_t epoch = 0;
 };
 SkWorkspace *sk_workspace(cudaStream_t s, int clusters);
+// Split-K partial planes of the tc_*_sk variant (grown on demand, per stream).
+struct SplitWorkspace {
+    float *part = nullptr;
+    unsigned *count = nullptr;
+    size_t part_bytes = 0, count_words = 0;
+};
+SplitWorkspace *split_workspace(cudaStream_t s, size_t part_bytes, size_t count_words);
+
+// tc_*_sk (variant c, split-K form of the TMA-epilogue pair kernel): the number of K splits is a
+// function of K alone — ceil(K / BK) k-blocks (BK = 64 BF16 / 32 TF32 elements), at least 32 per
+// split, at most 8 splits — so a panel's arithmetic never depends on M (row panels stay bitwise
+// equal).  0 = not eligible (fewer than 2 splits, or a partial workspace above 1 GiB).
+inline int tc_splitk_splits(int64_t m, int64_t n, int64_t k, bool bf16) {
+    const int64_t bk = bf16 ? 64 : 32;
+    const int64_t kb = (k + bk - 1) / bk;
+    int64_t s = kb / 32;
+    if (s > 8) s = 8;
+    if (s < 2) return 0;
+    const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
+    if (tiles * s * 256 * 256 * 4 > (int64_t(1) << 30)) return 0;   // partial planes <= 1 GiB
+    return static_cast<int>(s);
+}
+cudaError_t launch_tc_gemm_splitk(const GemmLaunch &g, bool bf16);
 
 // TMA eligibility (the selector's constraint filter).
 inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {

@@ -49,4 +49,27 @@ SkWorkspace *sk_workspace(cudaStream_t s, int clusters) {
     return &w;
 }
 
+SplitWorkspace *split_workspace(cudaStream_t s, size_t part_bytes, size_t count_words) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, SplitWorkspace> slots;
+    std::lock_guard<std::mutex> lk(mu);
+    SplitWorkspace &w = slots[s];
+    if (w.part_bytes < part_bytes) {
+        if (w.part) cudaFree(w.part);
+        w.part = nullptr;
+        w.part_bytes = 0;
+        if (cudaMalloc(&w.part, part_bytes) != cudaSuccess) return nullptr;
+        w.part_bytes = part_bytes;
+    }
+    if (w.count_words < count_words) {
+        if (w.count) cudaFree(w.count);
+        w.count = nullptr;
+        w.count_words = 0;
+        if (cudaMalloc(&w.count, count_words * sizeof(unsigned)) != cudaSuccess) return nullptr;
+        if (cudaMemset(w.count, 0, count_words * sizeof(unsigned)) != cudaSuccess) return nullptr;
+        w.count_words = count_words;
+    }
+    return &w;
+}
+
 }  // namespace compar

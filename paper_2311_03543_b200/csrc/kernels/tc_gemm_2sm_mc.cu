@@ -78,13 +78,20 @@ struct TcMParams {
     // stream-K (kPairs == 1 only): static (tile, k-block) ranges per cluster
     int sk, sk_clusters;
     int nprod;             // TMA producer warps per CTA (1 or 2)
+    // split-K variant (tc_*_sk, kPairs == 1): every tile's k-blocks are cut into `splits` ranges of
+    // ksplit k-blocks; each range is one work item whose raw FP32 partial goes to plane `split` of
+    // `spart`; splitk_reduce_kernel then sums the planes in split order (fixed, so the result
+    // depends only on (K, splits), never on the schedule) and applies alpha / beta.
+    int splits, ksplit;
+    float *spart;          // [splits][m padded to 256][n padded to 256] raw FP32 partials
+    int64_t spart_ld, spart_plane;
     int cin_prefetch;      // L2-prefetch the tile's C_in when the tile starts (COMPAR_CIN_PREFETCH=0 disables)
     unsigned *flags;       // per cluster: published HEAD partials, 8 per launch (epoch)
     float *partial;        // per cluster: 256 x 256 FP32 raw accumulator
     unsigned epoch;
 };
 
-enum { kFull = 0, kHead = 1, kTail = 2 };
+enum { kFull = 0, kHead = 1, kTail = 2, kSplit = 3 };
 struct Item {
     int tile, kb0, kb1, kind;
 };
@@ -161,6 +168,13 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     const uint32_t tmem_base = *tmem_slot;
 
     const int num_tiles = p.m_blocks * p.n_blocks;
+    const int num_items = num_tiles * p.splits;                // dynamic mode: ring values are items
+    auto dyn_item = [&](int t) -> Item {
+        if (p.splits == 1) return Item{t, 0, p.num_kb, kFull};
+        const int sidx = t % p.splits;
+        const int kb0 = sidx * p.ksplit;
+        return Item{t / p.splits, kb0, min(p.num_kb, kb0 + p.ksplit), kSplit};
+    };
     const uint32_t rempty_root = ptx::mapa_rank(rempty0, 0);
     const int cl = static_cast<int>(blockIdx.x) / kCluster;   // this cluster's index in the grid
     // Work item j of this cluster.  Dynamic mode: whole tiles from the tile ring (the call is the
@@ -194,8 +208,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
-        it = Item{t, 0, p.num_kb, kFull};
-        return t < num_tiles;
+        if (t >= num_items) return false;
+        it = dyn_item(t);
+        return true;
     };
 
     if (warp == 0 || warp == 6) {
@@ -225,8 +240,8 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                         t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
                         ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
                     }
-                    if (t >= num_tiles) break;
-                    it = Item{t, 0, p.num_kb, kFull};
+                    if (t >= num_items) break;
+                    it = dyn_item(t);
                 }
                 int mb, nb;
                 tile_coords_m(it.tile, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
@@ -292,7 +307,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                             const uint64_t bdesc = kTransB ? ptx::smem_desc(sb + j * 32, 16, 1024, 2)
                                                            : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_LBO,
                                                                             C::B_SBO, C::B_LAYOUT);
-                            const uint32_t accum = carry || ((kb | j) != 0);
+                            const uint32_t accum = carry || kb != it.kb0 || j != 0;
                             if (kBF16)
                                 ptx::mma_bf16_2sm(d_tmem, adesc, bdesc, C::IDESC, accum);
                             else
@@ -359,6 +374,32 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             tile_coords_m(it.tile, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
+            if (it.kind == kSplit) {  // raw partial of k-range `sidx` -> plane sidx of the workspace
+                const int sidx = it.kb0 / p.ksplit;
+                ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+                ptx::tc_fence_after();
+                const int64_t prow_g = static_cast<int64_t>(mb) * (kCluster * C::BM) + rank * C::BM + q * 32 + lane;
+                float *part = p.spart + static_cast<size_t>(sidx) * p.spart_plane + prow_g * p.spart_ld +
+                              static_cast<int64_t>(nb) * C::BN;
+#pragma unroll 1
+                for (int idx = 0; idx < kChunks; ++idx) {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx,
+                                            r);
+                    ptx::tmem_ld_wait();
+                    if (idx == kChunks - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+                    }
+#pragma unroll
+                    for (int v = 0; v < 8; ++v)
+                        __stcg(reinterpret_cast<float4 *>(part + 32 * idx) + v,
+                               make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                           __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
+                }
+                continue;
+            }
             if (it.kind == kHead) {  // publish the raw accumulator (no alpha / beta) for the next cluster
                 ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
                 ptx::tc_fence_after();
@@ -466,8 +507,47 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     }
 }
 
+// Split-K epilogue: C_out = alpha * (P_0 + P_1 + ... + P_{S-1}) + beta * C_in, the planes summed in
+// split order; 4 consecutive columns per thread (16-byte C accesses: the variant requires TMA-style
+// C alignment), grid-stride over rows x column quads.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ part, int splits, int64_t ld,
+                                                            int64_t plane, int64_t m, int64_t n, float alpha,
+                                                            float beta, const float *__restrict__ C_in,
+                                                            int64_t ldc_in, float *__restrict__ C_out,
+                                                            int64_t ldc_out) {
+    const int64_t nq = (n + 3) / 4;
+    const int64_t total = m * nq;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = i / nq, col = (i - row * nq) * 4;
+        const float *pp = part + row * ld + col;
+        float4 a = __ldcs(reinterpret_cast<const float4 *>(pp));
+        for (int s = 1; s < splits; ++s) {
+            const float4 x = __ldcs(reinterpret_cast<const float4 *>(pp + s * plane));
+            a.x += x.x, a.y += x.y, a.z += x.z, a.w += x.w;
+        }
+        float o[4] = {alpha * a.x, alpha * a.y, alpha * a.z, alpha * a.w};
+        if (col + 4 <= n) {
+            if (beta != 0.f) {
+                const float4 ci = *reinterpret_cast<const float4 *>(C_in + row * ldc_in + col);
+                o[0] = fmaf(beta, ci.x, o[0]);
+                o[1] = fmaf(beta, ci.y, o[1]);
+                o[2] = fmaf(beta, ci.z, o[2]);
+                o[3] = fmaf(beta, ci.w, o[3]);
+            }
+            *reinterpret_cast<float4 *>(C_out + row * ldc_out + col) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+            for (int e = 0; e < 4 && col + e < n; ++e) {
+                float v = o[e];
+                if (beta != 0.f) v = fmaf(beta, C_in[row * ldc_in + col + e], v);
+                C_out[row * ldc_out + col + e] = v;
+            }
+        }
+    }
+}
+
 template <bool kBF16, bool kTransB, int kPairs>
-cudaError_t launch_tcm_t(const GemmLaunch &g) {
+cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
     using C = TcMCfg<kBF16, kTransB, kPairs>;
     constexpr int kCluster = 2 * kPairs;
     static std::once_flag attr_once;
@@ -514,9 +594,20 @@ cudaError_t launch_tcm_t(const GemmLaunch &g) {
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
+    p.splits = 1, p.ksplit = p.num_kb, p.spart = nullptr, p.spart_ld = 0, p.spart_plane = 0;
+    if (splits > 1) {
+        p.splits = splits;
+        p.ksplit = (p.num_kb + splits - 1) / splits;
+        p.spart_ld = static_cast<int64_t>(p.n_blocks) * C::BN;
+        p.spart_plane = static_cast<int64_t>(p.m_blocks) * kCluster * C::BM * p.spart_ld;
+        SplitWorkspace *w = split_workspace(g.stream, static_cast<size_t>(splits) * p.spart_plane * 4, 0);
+        if (!w) return cudaErrorMemoryAllocation;
+        p.spart = w->part;
+    }
+    const int items = tiles * p.splits;
     int clusters = g.num_sms / kCluster < max_clusters ? g.num_sms / kCluster : max_clusters;
     if (clusters < 1) clusters = 1;
-    if (tiles < clusters) clusters = tiles;
+    if (items < clusters) clusters = items;
     // Stream-K when whole tiles would leave the last wave badly filled (> 3 % idle): every
     // cluster gets the same number of (tile, k-block) units; a tile split between two clusters
     // continues the same MMA chain from a published FP32 partial, so C is bitwise the
@@ -524,7 +615,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g) {
     const char *sk_s = std::getenv("COMPAR_STREAMK");   // read per launch (tests flip it)
     const int sk_env = sk_s ? std::atoi(sk_s) : -1;
     const int waves = (tiles + clusters - 1) / clusters;
-    const bool sk_ok = kPairs == 1 && tiles >= clusters && (tiles % clusters != 0 || sk_env == 2);
+    const bool sk_ok = kPairs == 1 && p.splits == 1 && tiles >= clusters && (tiles % clusters != 0 || sk_env == 2);
     (void)waves;  // auto mode measured slower: stream-K only on request
     p.sk = sk_ok && sk_env >= 1;
     p.sk_clusters = clusters;
@@ -539,6 +630,15 @@ cudaError_t launch_tcm_t(const GemmLaunch &g) {
         p.flags = w->flags, p.partial = w->partial, p.epoch = ++w->epoch;
     }
     tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
+    if (p.splits > 1) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const int64_t quads = g.m * ((g.n + 3) / 4);
+        const int64_t blocks = (quads + 255) / 256;
+        splitk_reduce_kernel<<<static_cast<unsigned>(blocks < (1 << 30) ? blocks : (1 << 30)), 256, 0, g.stream>>>(
+            p.spart, p.splits, p.spart_ld, p.spart_plane, g.m, g.n, g.alpha, g.beta, g.C_in, g.ldc_in, g.C_out,
+            g.ldc_out);
+    }
     return cudaGetLastError();
 }
 
@@ -551,6 +651,13 @@ cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16, int pairs) {
     }
     if (bf16) return g.transB ? launch_tcm_t<true, true, 1>(g) : launch_tcm_t<true, false, 1>(g);
     return g.transB ? launch_tcm_t<false, true, 1>(g) : launch_tcm_t<false, false, 1>(g);
+}
+
+cudaError_t launch_tc_gemm_splitk(const GemmLaunch &g, bool bf16) {
+    const int s = tc_splitk_splits(g.m, g.n, g.k, bf16);
+    if (s < 2) return cudaErrorInvalidValue;
+    if (bf16) return g.transB ? launch_tcm_t<true, true, 1>(g, s) : launch_tcm_t<true, false, 1>(g, s);
+    return g.transB ? launch_tcm_t<false, true, 1>(g, s) : launch_tcm_t<false, false, 1>(g, s);
 }
 
 cudaError_t preload_tcm_kernels() {

@@ -28,11 +28,26 @@ VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tc_bf16_2sm": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
             "tc_tf32_2sm_w": (cm.F32, cm.COMPUTE_TF32, 5e-3),
             "tc_bf16_2sm_w": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
+            "tc_tf32_sk": (cm.F32, cm.COMPUTE_TF32, 5e-3),
+            "tc_bf16_sk": (cm.BF16, cm.COMPUTE_BF16, 5e-3),
             # FP32 accumulation of exactly-widened BF16 operands: held to the strict-FP32 bound
             "simt_bf16": (cm.BF16, cm.COMPUTE_BF16, 1e-5)}
 
 SHAPES = [(1, 1, 1), (7, 13, 5), (64, 64, 64), (65, 127, 129), (129, 257, 70), (128, 256, 64),
           (300, 520, 1000), (1000, 777, 333), (257, 1, 100), (1, 300, 4097)]
+
+
+def sk_splits(m, n, k, bf16):
+    """Mirror of tc_splitk_splits (kernels.h): K splits of the tc_*_sk variant, 0 = not eligible."""
+    kb = -(-k // (64 if bf16 else 32))
+    s = min(8, kb // 32)
+    tiles = -(-m // 256) * -(-n // 256)
+    return s if s >= 2 and tiles * s * 256 * 256 * 4 <= (1 << 30) else 0
+
+
+def skip_ineligible(name, m, n, k):
+    if name.endswith("_sk") and not sk_splits(m, n, k, "bf16" in name):
+        pytest.skip(f"{name} needs >= 64 k-blocks (K = {k})")
 
 
 @pytest.fixture(scope="module")
@@ -47,6 +62,7 @@ def vid(ctx, name):
 
 
 def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, seed=11, ldc_pad=4):
+    skip_ineligible(name, m, n, k)
     dtype_id, compute, tol = VARIANTS[name]
     dt = "bf16" if dtype_id == cm.BF16 else "f32"
     A = gen.matrix(gen.TAG_A, m, k, dist, dt, seed=seed)
@@ -171,6 +187,22 @@ def test_wide_epilogue_overlap_bitwise(ctx, monkeypatch, name, shape, transB, be
     assert og.rel_fro(got, ref) <= tol
 
 
+@pytest.mark.parametrize("name", ["tc_tf32_sk", "tc_bf16_sk"])
+@pytest.mark.parametrize("shape", [(300, 520, 5000), (777, 600, 8200), (256, 256, 65536), (1000, 64, 4160)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("transB,beta,dist", [(0, 0.5, gen.DIST_U), (1, 0.0, gen.DIST_U), (0, -1.0, gen.DIST_I)],
+                         ids=["U", "U-t-b0", "I"])
+def test_splitk_parity(ctx, name, shape, transB, beta, dist):
+    """tc_*_sk: K cut into 2..8 ranges (K only), planes summed in split order by the reduce kernel;
+    within tolerance on U(-1,1) and bitwise on integer inputs (all partial sums exact)."""
+    m, n, k = shape
+    got, ref, tol = run_case(ctx, name, m, n, k, dist=dist, beta=beta, transB=transB)
+    if dist == gen.DIST_I:
+        np.testing.assert_array_equal(got, ref)
+    else:
+        assert og.rel_fro(got, ref) <= tol
+
+
 @pytest.mark.parametrize("name", list(VARIANTS))
 def test_transB_and_beta0_nan(ctx, name):
     got, ref, tol = run_case(ctx, name, 190, 300, 260, transB=1, beta=0.0)
@@ -223,10 +255,11 @@ def test_scale_paths(ctx):
 
 @pytest.mark.parametrize("name", list(VARIANTS))
 def test_loopback_partition_bitwise_invariant(ctx, name):
-    """Row panels P in {2, 3, 8} give C bitwise equal to P = 1 (no split-K; a4 formula)."""
+    """Row panels P in {2, 3, 8} give C bitwise equal to P = 1 (a4 formula; the split-K variant's
+    splits depend on K only)."""
     dtype_id, compute, _ = VARIANTS[name]
     dt = "bf16" if dtype_id == cm.BF16 else "f32"
-    m, n, k = 1000, 384, 320
+    m, n, k = 1000, 384, 320 if not name.endswith("_sk") else 4160
     A = device_matrix(gen.TAG_A, m, k, dtype=dt)
     B = device_matrix(gen.TAG_B, k, n, dtype=dt)
     C0 = device_matrix(gen.TAG_C, m, n)
@@ -316,7 +349,8 @@ def test_world_size_one_nccl(ctx):
                                         ("tc_bf16_2sm_w", (32768, 32768, 32768)), ("tc_tf32_2sm_w", (8192, 8192, 8192)),
                                         ("tc_bf16_2sm_w", (65536, 256, 4096)),
                                         ("tc_bf16", (65536, 256, 4096)), ("tc_tf32", (65536, 256, 4096)),
-                                        ("tc_bf16", (32768, 32768, 32768))])
+                                        ("tc_bf16", (32768, 32768, 32768)),
+                                        ("tc_tf32_sk", (1024, 1024, 8192)), ("tc_bf16_sk", (2048, 2048, 32768))])
 def test_full_size_sampled(ctx, name, shape):
     """BASELINE.json full sizes in the bench launch configuration; checked on sampled
     entries (every 128-row tile boundary sampled + random rows/cols) against the oracle fed

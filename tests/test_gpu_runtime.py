@@ -75,8 +75,7 @@ def test_config1_calibration_trace(order):
     B = device_matrix(gen.TAG_B, m, m)
     Cd = device_matrix(gen.TAG_C, m, m)
     d = cm.make_desc(m, m, m, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, compute=cm.COMPUTE_TF32)
-    tf32_ok = set(cm.TARGETS_TF32)
-    E = [v for v, (_, tgt) in enumerate(ctx.variants()) if tgt in tf32_ok]
+    E = ctx.eligible(d)
     n_cal = 4 * len(E)
     trace = [ctx.run(d) for _ in range(n_cal + 1)]
     if order == cm.CALIB_INTERLEAVED:

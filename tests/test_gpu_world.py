@@ -93,8 +93,7 @@ def test_loopback_through_nccl_one_rank(tb):
         B = device_matrix(gen.TAG_B, k, n, dtype="bf16", transposed=bool(tb))
         C0 = device_matrix(gen.TAG_C, m, n)
         kw = dict(ldb=(k if tb else n), alpha=1.5, beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, transB=tb)
-        n_bf16 = sum(1 for _, t in ctx.variants()
-                     if t in cm.TARGETS_BF16)
+        n_bf16 = len(ctx.eligible(cm.make_desc(m, n, k, A=A, B=B, C_in=C0, C_out=C0, world=1, **kw)))
         for _ in range(4 * n_bf16 + 2):   # calibration (1 warm-up + 3 per variant), then model mode, via world=1
             Cw = C0.clone()
             r = ctx.run(cm.make_desc(m, n, k, A=A, B=B, C_in=Cw, C_out=Cw, world=1, **kw))

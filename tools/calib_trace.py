@@ -42,8 +42,8 @@ def main():
     os.environ.pop("COMPAR_CALIB_ORDER", None)
     ctx = cm.Compar()
     names = [n for n, _ in ctx.variants()]
-    E = [i for i, (_, t) in enumerate(ctx.variants())
-         if t in cm.TARGETS_BF16]
+    E = ctx.eligible(cm.make_desc(s, s, s, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
+                                  compute=cm.COMPUTE_BF16))
 
     def hinted(seq):
         tr = []

@@ -78,7 +78,7 @@ def main(out_path, secs):
                 calib += 1
             sel = [ctx.run(d) for _ in range(R)]
             chosen = sel[-1].variant
-            E = [v for v, (_, t) in enumerate(ctx.variants()) if t in targets]
+            E = [v for v in ctx.eligible(d) if ctx.variants()[v][1] in targets]
             per = {}
             tc = [v for v in E if names[v].startswith("tc_")]
             ffma = [v for v in E if v not in tc]

@@ -47,8 +47,12 @@ class Problem:
                             beta=self.beta, in_dtype=cm.BF16 if bf else cm.F32, compute=compute, variant_hint=hint)
 
 
-def eligible(ctx, targets):
-    return [v for v, (_, t) in enumerate(ctx.variants()) if t in targets]
+def eligible(ctx, targets, prob=None, compute=None):
+    E = [v for v, (_, t) in enumerate(ctx.variants()) if t in targets]
+    if prob is None:
+        return E
+    ok = set(ctx.eligible(prob.desc(compute)))   # shape constraints (TMA alignment, split-K)
+    return [v for v in E if v in ok]
 
 
 def exhaustive(ctx, prob, compute, E):
@@ -74,7 +78,7 @@ def selected_runs(ctx, prob, compute):
 
 
 def regret_case(ctx, names, prob, compute, targets):
-    E = eligible(ctx, targets)
+    E = eligible(ctx, targets, prob, compute)
     trace, model = selected_runs(ctx, prob, compute)
     med = exhaustive(ctx, prob, compute, E)
     chosen = model[-1].variant
@@ -99,13 +103,13 @@ def main(out_path):
         d = prob.desc(compute)
         trace = []
         t_host = []
-        for _ in range(4 * len(eligible(ctx, T)) + R):
+        for _ in range(4 * len(eligible(ctx, T, prob, compute)) + R):
             t0 = time.perf_counter()
             t = ctx.submit(d)
             t_host.append(time.perf_counter() - t0)
             r = ctx.sync(t)
             trace.append([names[r.variant], r.mode, r.ns])
-        med = exhaustive(ctx, prob, compute, eligible(ctx, T))
+        med = exhaustive(ctx, prob, compute, eligible(ctx, T, prob, compute))
         chosen = [v for v in range(len(names)) if names[v] == trace[-1][0]][0]
         c1.append({"compute": compute, "trace": trace, "chosen": trace[-1][0],
                    "regret": med[chosen] / min(med.values()) - 1.0,
@@ -148,6 +152,16 @@ def main(out_path):
     del prob
     torch.cuda.empty_cache()
     res["config5a"] = c5a
+
+    # ---- deep-K, small M x N (the split-K variant's sweet spot; not a BASELINE config)
+    deepk = []
+    for (m, n, k) in ((512, 512, 16384), (1024, 1024, 8192), (256, 4096, 8192), (2048, 2048, 8192)):
+        for dt, compute, T in (("bf16", cm.COMPUTE_BF16, BF16_T), ("f32", cm.COMPUTE_TF32, TF32_T)):
+            prob = Problem(m, n, k, dt)
+            deepk.append(regret_case(ctx, names, prob, compute, T))
+            del prob
+            torch.cuda.empty_cache()
+    res["deepk"] = deepk
     ctx.terminate()
 
     # ---- config 5b: mixed stream, history vs eager
@@ -158,9 +172,8 @@ def main(out_path):
     probs = {s: Problem(*s, beta=0.0) for s in shapes}
     best = {}
     ctxb = cm.Compar()
-    E = eligible(ctxb, TF32_T)
     for s, p in probs.items():
-        med = exhaustive(ctxb, p, cm.COMPUTE_TF32, E)
+        med = exhaustive(ctxb, p, cm.COMPUTE_TF32, eligible(ctxb, TF32_T, p, cm.COMPUTE_TF32))
         best[s] = (min(med, key=med.get), min(med.values()), {names[v]: x for v, x in med.items()})
     ctxb.terminate()
     c5b = {"tasks": len(stream), "shapes": [list(s) for s in shapes],
