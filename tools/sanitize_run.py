@@ -29,7 +29,10 @@ for name in names:
     bf = "bf16" in name
     dt = "bf16" if bf else "f32"
     compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else cm.COMPUTE_F32_STRICT)
-    for (m, n, k, tb, beta, panels) in [(77, 136, 72, 0, 0.5, 1), (300, 264, 136, 1, 0.0, 3), (129, 520, 264, 0, -1.0, 2)]:
+    shapes = [(77, 136, 72, 0, 0.5, 1), (300, 264, 136, 1, 0.0, 3), (129, 520, 264, 0, -1.0, 2)]
+    if name.endswith("_sk"):   # the split-K variant needs >= 64 k-blocks
+        shapes = [(77, 136, 4160, 0, 0.5, 1), (300, 264, 8200, 1, 0.0, 3), (129, 520, 4160, 0, -1.0, 2)]
+    for (m, n, k, tb, beta, panels) in shapes:
         A = device_matrix(gen.TAG_A, m, k, dtype=dt)
         B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))
         Cd = device_matrix(gen.TAG_C, m, n)
