@@ -77,8 +77,8 @@ __device__ __forceinline__ float4 load_row4(const __nv_bfloat16 *__restrict__ ba
 // FP32 FFMA accumulation — the any-shape fallback of the BF16 precision class).
 template <typename T, bool kVecA, bool kVecB, bool kTransB>
 __global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
-    __shared__ __align__(16) float As[2][BK][BM];
-    __shared__ __align__(16) float Bs[2][BK][BN];
+    __shared__ __align__(16) float As[2][BK][BM + 4];   // +4: the transposed A stores are bank-conflict free
+    __shared__ __align__(16) float Bs[2][BK][BN + 4];
 
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
