@@ -231,11 +231,14 @@ typedef struct {
     int64_t panel_ns[COMPAR_MAX_PANELS];
     int64_t bcast_ns;           /* world mode: broadcast of B, start -> last chunk landed          */
     int64_t total_ns;           /* first start event -> last stop event of the task on its stream  */
-    int batch;                  /* launches timed by one event pair: a calibration execution whose
-                                   variant's warm-up ran < COMPAR_CALIB_BATCH_NS (default 20 us)
-                                   repeats the kernel r = ceil(50 us / warm-up) times (<= 64) and
-                                   records span / r; the r - 1 extra
-                                   launches write a library scratch C, so C_out is written once */
+    int batch;                  /* launches timed by one event pair: a calibration execution on a
+                                   key whose static cost estimate t (5 us + FLOPs at 100 TFLOP/s +
+                                   compulsory bytes at 3 TB/s) is < COMPAR_CALIB_BATCH_NS (default
+                                   100 us) repeats the kernel r = ceil(200 us / t) times (<= 64, the
+                                   same r for every variant of the key), each launch between its
+                                   own event pair, and records the median launch (SURVEY §8(a) a8 /
+                                   c13, R25); the r - 1 extra launches write a library
+                                   scratch C, so C_out is written once */
     int rank, lane;             /* worker that ran the task (task-parallel world); else rank, 0    */
 } compar_report;
 

@@ -174,6 +174,11 @@ class SelectorOracle:
             return None
         return float(np.array(self.features(key)) @ best[1])
 
+    def unknown_predict(self, key, eligible):
+        """Variants with neither samples for `key` nor a fitted prediction; in predict mode only
+        these are calibrated when decide_predict returns None (all of E when nothing is known)."""
+        return [v for v in eligible if self.rec(v, key).count == 0 and self.predict(v, key) is None]
+
     def decide_predict(self, key, eligible):
         """Measured mean where (v, key) has samples, else the fitted prediction; None if some
         eligible variant has neither (the caller then calibrates)."""

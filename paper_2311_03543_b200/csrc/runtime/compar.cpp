@@ -134,7 +134,7 @@ struct Ctx {
     cudaEvent_t sort_done = nullptr;  // end of the last sort task (sort tasks share the scratch)
     bool sort_done_set = false;
     // batched calibration timing (a8 / c13)
-    int64_t batch_below_ns = 20000;
+    int64_t batch_below_ns = 100000;
     void *scratch = nullptr;  // C_out of the r - 1 extra launches
     size_t scratch_bytes = 0;
 };
@@ -405,6 +405,12 @@ int64_t measure(Ctx *c, Task &t, compar_report *rep) {
         int64_t ns = 0;
         if (c->virt) {
             ns = t.panels[i].virtual_ns;
+        } else if (!t.panels[i].sub.empty() && t.panels[i].batch > 1) {  // batched calibration: median launch
+            std::vector<int64_t> v;
+            for (auto &s : t.panels[i].sub) v.push_back(elapsed_ns(s.first, s.second));
+            std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+            ns = v[v.size() / 2];
+            if (rep) rep->batch = std::max(rep->batch, t.panels[i].batch);
         } else if (!t.panels[i].sub.empty()) {  // host pipeline: sum of the chunk kernels
             for (auto &s : t.panels[i].sub) ns += elapsed_ns(s.first, s.second);
         } else if (t.panels[i].start) {
@@ -843,7 +849,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     c->hist.calib_k = cfg.calib_k;
     c->hist.calib_warmup = cfg.calib_warmup;
     c->hist.calib_blocked = cfg.calib_order == COMPAR_CALIB_BLOCKED;
-    c->batch_below_ns = env_int("COMPAR_CALIB_BATCH_NS", 20000);
+    c->batch_below_ns = env_int("COMPAR_CALIB_BATCH_NS", 100000);
     const char *pp = cfg.perf_model_path ? cfg.perf_model_path : std::getenv("COMPAR_PERF_MODEL");
     if (pp) c->perf_path = pp;
     c->cfg.perf_model_path = nullptr;
@@ -1045,27 +1051,29 @@ compar_status ensure_lanes(Ctx *c) {
     return err == cudaSuccess ? COMPAR_OK : cuda_fail(err, "lane events");
 }
 
-// Batched calibration timing (reading c13): a timed calibration execution of a
-// built-in whose reference time t (the variant's warm-up on this key, else its fastest sample)
-// is below batch_below_ns repeats the launch r = ceil(50 us / t) times (<= 64) between one event
-// pair and records span / r, so cudaEvent resolution (~0.5 us) and launch jitter do not decide
-// between variants of a few microseconds.  If the warm-up is still pending it is harvested first
-// (calibration only; decisions depend on counts, not on this wait).
+// Batched calibration timing (reading c13; R25): a timed calibration
+// execution of a built-in on a key whose work is below batch_below_ns (100 us) repeats the launch
+// r = ceil(200 us / t) times (<= 64), each between its own event pair, and records the median
+// single-launch time, so launch / clock jitter does not decide between variants a few percent
+// apart (with 3 single-launch samples, 1024^3 TF32 picked a 6 % slower variant) while the sample
+// stays the quantity a model-mode execution measures (a batch's span / r hides launch overhead
+// that differs between kernels: it ranked tma_f32 over tc_tf32 at 64^3).
+// t is a static estimate from the key alone (5 us floor + FLOPs at 100 TFLOP/s + compulsory bytes
+// at 3 TB/s), so every variant of a key is sampled with the same r: deriving r from each variant's
+// own warm-up made the first-ever launch of a kernel (module/workspace set-up, tens of us) switch
+// batching off for that variant only, and unbatched samples lost to batched ones by the launch
+// overhead (config 1: 18 % regret).
 int calib_batch(Ctx *c, const Task &t) {
     if (c->batch_below_ns <= 0 || t.mode != kCalib || t.variant < 0) return 1;
     if (c->variants[t.variant].target == COMPAR_TGT_USER) return 1;
-    const int hid = c->variants[t.variant].hid;
-    const Record *r = c->hist.find(hid, t.key);
-    if (r && r->warm_ns == 0 && r->count == 0) {
-        if (t.tasks && c->nranks > 1) return 1;  // harvesting would be a collective here
-        harvest_key(c, t.key);
-        r = c->hist.find(hid, t.key);
-    }
-    if (!r) return 1;
-    const int64_t ref = r->warm_ns > 0 ? r->warm_ns : (r->count > 0 ? r->min_ns : 0);
-    if (ref <= 0 || ref >= c->batch_below_ns) return 1;
-    const int64_t target = 50000;
-    return static_cast<int>(std::min<int64_t>(64, (target + ref - 1) / ref));
+    const Key &k = t.key;
+    const double flops = 2.0 * static_cast<double>(k.m) * static_cast<double>(k.n) * static_cast<double>(k.k);
+    const double sin = k.dtype == COMPAR_BF16 ? 2.0 : 4.0;
+    const double bytes = sin * (static_cast<double>(k.m) * k.k + static_cast<double>(k.k) * k.n) +
+                         4.0 * static_cast<double>(k.m) * k.n * (k.beta0 ? 1.0 : 2.0);
+    const double est = 5000.0 + flops / 100e12 * 1e9 + bytes / 3e12 * 1e9;
+    if (est >= static_cast<double>(c->batch_below_ns)) return 1;
+    return static_cast<int>(std::min(64.0, std::ceil(200000.0 / est)));
 }
 
 // Steps 3-7 over an eligible set (registry indices idx, history ids names), any interface.
@@ -1109,6 +1117,23 @@ compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector
             *variant = idx[ppos];
             *mode = pm;
             if (commit) *warm = c->hist.commit(names[ppos], plan.key);
+            return COMPAR_OK;
+        }
+        // Only the variants with neither a sample nor a model are calibrated for this key (a
+        // variant eligible on too few keys to fit, e.g. the split-K one, must not send every
+        // other variant back to calibration).
+        const std::vector<int> unk = c->hist.unknown_predict(names, plan.key);
+        std::vector<int> uidx, unames;
+        for (int u : unk) {
+            uidx.push_back(idx[u]);
+            unames.push_back(names[u]);
+        }
+        if (!unames.empty() && unames.size() < names.size()) {
+            Mode m;
+            const int pos = c->hist.decide(unames, plan.key, &m);
+            *variant = uidx[pos];
+            *mode = m;
+            if (commit) *warm = c->hist.commit(unames[pos], plan.key);
             return COMPAR_OK;
         }
     }
@@ -1333,9 +1358,24 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
                 cudaEventRecord(pr.start, st);
                 compar_panel extra = pr.p;   // the r - 1 timing repeats write the scratch C
                 extra.C_out = static_cast<float *>(c->scratch);
-                for (int i = 1; i < batch; ++i)
+                for (int i = 1; i < batch; ++i) {
+                    // one event pair per launch: the sample is the median single-launch time
+                    // (the quantity model-mode samples measure), not the batch's span / r
+                    std::pair<cudaEvent_t, cudaEvent_t> span{get_event(c), get_event(c)};
+                    cudaEventRecord(span.first, st);
                     if (launch_on(d, extra, 0) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
-                if (launch_on(d, pr.p, 0) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+                    cudaEventRecord(span.second, st);
+                    pr.sub.push_back(span);
+                }
+                if (batch > 1) {
+                    std::pair<cudaEvent_t, cudaEvent_t> span{get_event(c), get_event(c)};
+                    cudaEventRecord(span.first, st);
+                    if (launch_on(d, pr.p, 0) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+                    cudaEventRecord(span.second, st);
+                    pr.sub.push_back(span);
+                } else if (launch_on(d, pr.p, 0) != COMPAR_OK) {
+                    t.status = COMPAR_E_TASK_FAILED;
+                }
                 cudaEventRecord(pr.stop, st);
             }
         } else {

@@ -190,6 +190,17 @@ int History::decide_predict(const std::vector<int> &ids, const Key &k, Mode *mod
     return best;
 }
 
+std::vector<int> History::unknown_predict(const std::vector<int> &ids, const Key &k) const {
+    std::vector<int> out;
+    for (size_t i = 0; i < ids.size(); ++i) {
+        const Record *r = find(ids[i], k);
+        double est;
+        if ((r && r->count > 0) || predict(ids[i], k, &est)) continue;
+        out.push_back(static_cast<int>(i));
+    }
+    return out;
+}
+
 void History::merge(const std::string &variant, const Key &k, const Record &in) {
     Record &r = rec(intern(variant), k);
     if (in.count > 0) r.min_ns = r.count == 0 ? in.min_ns : (in.min_ns < r.min_ns ? in.min_ns : r.min_ns);

@@ -82,6 +82,9 @@ public:
     // Decision of the "predict" scheduler: measured mean where (v, key) has samples, prediction
     // otherwise; returns -1 (caller falls back to calibration) if some variant has neither.
     int decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode) const;
+    // Positions (into ids) of the variants with neither a sample for k nor a prediction: the only
+    // ones the predict scheduler still has to calibrate for k.
+    std::vector<int> unknown_predict(const std::vector<int> &ids, const Key &k) const;
 
 private:
     std::map<std::string, int> ids_;

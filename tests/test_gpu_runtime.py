@@ -1,5 +1,7 @@
 """GPU tests of the runtime around the kernels (-m gpu): device-twin generator pin, real-event
 selector with closed-form synthetic costs, calibration trace, stats/launch accounting."""
+import math
+
 import numpy as np
 import pytest
 
@@ -117,11 +119,13 @@ def test_batched_calibration_timing(compute, dt):
             break
     assert reps[-1].mode == cm.MODE_MODEL and reps[-1].batch == 1
     assert all(r.batch == 1 for r in reps if r.mode == cm.MODE_WARMUP)
-    # the c13 rule: r = ceil(50 us / warm-up ns) (<= 64) when the variant's warm-up ran < 20 us
-    warm = {r.variant: r.ns for r in reps if r.mode == cm.MODE_WARMUP}
+    # the c13 rule as read in DESIGN.md R25: one r for every variant of the key, r = ceil(200 us / t)
+    # (<= 64) with t = 5 us + FLOPs at 100 TFLOP/s + compulsory bytes at 3 TB/s, when t < 100 us
+    s_in = 2 if dt == "bf16" else 4
+    t = 5000.0 + 2.0 * m * n * k / 100e12 * 1e9 + (s_in * (m * k + k * n) + 4 * m * n * 2) / 3e12 * 1e9
+    expect = min(64, math.ceil(200000.0 / t)) if t < 100000 else 1
     cal = [r for r in reps if r.mode == cm.MODE_CALIB]
-    expect = {v: (min(64, -(-50000 // ns)) if ns < 20000 else 1) for v, ns in warm.items()}
-    assert [r.batch for r in cal] == [expect[r.variant] for r in cal]
+    assert [r.batch for r in cal] == [expect] * len(cal)
     assert any(r.batch > 1 for r in cal)
     assert ctx.stats().launches == sum(r.batch for r in reps)
     ctx.terminate()

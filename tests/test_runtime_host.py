@@ -288,7 +288,7 @@ def test_predict_scheduler_matches_oracle():
         r = ctx.run(d)
         got = (r.variant, r.mode)
         dp = orc.decide_predict(key(s), [0, 1, 2])
-        exp = dp if dp is not None else orc.decide(key(s), [0, 1, 2])
+        exp = dp if dp is not None else orc.decide(key(s), orc.unknown_predict(key(s), [0, 1, 2]))
         warm = orc.commit(exp[0], key(s), exp[1])
         orc.harvest(exp[0], key(s), exp[1], warm, int(cost[exp[0]](s, s, s)))
         assert got == exp, (s, got, exp)

@@ -136,6 +136,31 @@ def test_predict_recovers_closed_form():
     assert so.SelectorOracle(2).decide_predict(_key(64), [0, 1]) is None
 
 
+def test_predict_calibrates_only_unknown_variants():
+    """Predict mode with a variant eligible on too few keys to fit (like the split-K variant): at a
+    new key only that variant is calibrated — until its first timed sample, after which (as for every
+    variant in predict mode) its measured mean competes with the others' predictions."""
+    sel = so.SelectorOracle(3, blocked=True)
+    cost = [lambda s: 50_000 + 900.0 * 2 * s ** 3 * 1e-9, lambda s: 5_000 + 2_000.0 * 2 * s ** 3 * 1e-9,
+            lambda s: 1_000.0]
+    for s in (256, 512, 1024, 2048):                       # variant 2 not eligible on these keys
+        for _ in range(8):
+            v, mode = sel.decide(_key(s), [0, 1])
+            warm = sel.commit(v, _key(s), mode)
+            sel.harvest(v, _key(s), mode, warm, round(cost[v](s)))
+    key = _key(3000)
+    assert sel.decide_predict(key, [0, 1, 2]) is None
+    assert sel.unknown_predict(key, [0, 1, 2]) == [2]
+    trace = []
+    while sel.decide_predict(key, [0, 1, 2]) is None:
+        v, mode = sel.decide(key, sel.unknown_predict(key, [0, 1, 2]))
+        trace.append((v, mode))
+        warm = sel.commit(v, key, mode)
+        sel.harvest(v, key, mode, warm, round(cost[v](3000)))
+    assert trace == [(2, so.MODE_WARMUP), (2, so.MODE_CALIB)]
+    assert sel.decide_predict(key, [0, 1, 2]) == (2, so.MODE_MODEL)   # its measured 1 us beats both predictions
+
+
 @pytest.mark.parametrize("m,p,expect", [
     (32768, 8, [0, 4096, 8192, 12288, 16384, 20480, 24576, 28672, 32768]),
     (32768, 2, [0, 16384, 32768]),
