@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-targets", action="store_true", help="skip the config-3 / 5a north-star block")
+    p.add_argument("--bcast", default="nccl", choices=["nccl", "ce"],
+                   help="N > 1: broadcast of B by NCCL (default) or by the copy-engine chain (compar_ce_*)")
     return p.parse_args()
 
 
@@ -293,9 +295,16 @@ def main():
     from gen.device import fill
     from paper_2311_03543_b200 import compar as cm
 
-    torch.cuda.set_device(local)
+    # COMPAR_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 with a gloo process group, so
+    # the N > 1 path (with --bcast ce) runs end to end on a one-GPU box; never a performance number
+    shared = os.environ.get("COMPAR_BENCH_SHARED_GPU") == "1"
+    coll_dev = "cpu" if shared else "cuda"
+    torch.cuda.set_device(0 if shared else local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     M = N = K = args.size
     offs = cm.partition_rows(M, world)
     r0, r1 = offs[rank], offs[rank + 1]
@@ -305,9 +314,22 @@ def main():
 
     ctx = cm.Compar()
     if world > 1:
-        uid = [cm.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(world, rank, uid[0])
+        if args.bcast == "ce":   # copy-engine chain over CUDA IPC (no NCCL, no SMs; include/compar.h)
+            def allgather(b):
+                out = [None] * world
+                dist.all_gather_object(out, b)
+                return out
+
+            def red(p, _user):
+                t = torch.tensor([p[0]], dtype=torch.int64, device=coll_dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                p[0] = int(t.item())
+            ctx.ce_init(world, rank, K * N * 2, allgather)
+            ctx.set_reduce_hook(red)
+        else:
+            uid = [cm.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.comm_init(world, rank, uid[0])
     # inputs resident in HBM: this rank's A/C panels, B on rank 0 (replica buffer elsewhere)
     A = torch.empty((max(mloc, 1), K), dtype=torch.bfloat16, device="cuda")
     Cm = torch.empty((max(mloc, 1), N), dtype=torch.float32, device="cuda")
@@ -341,7 +363,7 @@ def main():
         st1 = ctx.stats()
         ms = ev0.elapsed_time(ev1)
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, reports, st1.launches - st0.launches
@@ -355,12 +377,12 @@ def main():
         calib_runs += 1
     for _ in range(args.warmup):
         ctx.run(desc)
-    clk = ClockSampler(local)
+    clk = ClockSampler(0 if shared else local)
     clk.start()
     ms, reps, launches = timed(args.steps, desc)
     clocks = clk.stop()
     if any(r in clocks.get("reasons", []) for r in BAD_REASONS):   # rejected: re-measure once
-        clk = ClockSampler(local)
+        clk = ClockSampler(0 if shared else local)
         clk.start()
         ms, reps, launches = timed(args.steps, desc)
         clocks = clk.stop()
@@ -373,7 +395,7 @@ def main():
     kern_ns = [r.ns for r in reps]
     k_avg = sum(kern_ns) / len(kern_ns)
     if world > 1:
-        t = torch.tensor([k_avg], device="cuda", dtype=torch.float64)
+        t = torch.tensor([k_avg], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         k_avg = float(t.item())
     panel_flops = 2.0 * (offs[1] - offs[0]) * N * K
@@ -434,7 +456,7 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                "ms_per_step": ems / args.e2e_steps}
         if world > 1:
-            t = torch.tensor([h2d, d2h], device="cuda", dtype=torch.float64)
+            t = torch.tensor([h2d, d2h], device=coll_dev, dtype=torch.float64)
             dist.all_reduce(t)
             e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"] = int(t[0].item()), int(t[1].item())
 
@@ -450,9 +472,11 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                "config": {"workload": f"BASELINE config 4: gemm {M}x{N}x{K}, A/B bf16, C fp32, C=1.5AB+0.5C, "
-                                      f"row panels over {world} GPU(s) + NCCL broadcast of B",
+                                      f"row panels over {world} GPU(s) + "
+                                      f"{'copy-engine chain' if args.bcast == 'ce' else 'NCCL'} broadcast of B",
                           "m": M, "n": N, "k": K, "global_batch": None, "seq_len": None,
                           "parallelism": f"rowpanel{world}", "variant": chosen,
+                          "bcast": (args.bcast if world > 1 else None),
                           "l2": "inputs larger than L2 (A,B 2 GiB bf16; C 4 GiB fp32): no flush needed"},
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": achieved / peak, "traffic": traffic,

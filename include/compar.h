@@ -314,6 +314,20 @@ compar_status compar_comm_unique_id(void *out, int len);
 /* Joins the nranks-process communicator (one process per GPU).  Required before world = 1. */
 compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, int len);
 
+/* Copy-engine chain broadcast of B for world = 1, instead of NCCL: slab j of B travels
+ * root -> rank 1 -> ... -> rank P-1, each hop one cudaMemcpyAsync from the upstream rank's buffer
+ * (CUDA IPC; NVLink between GPUs), started by a GPU-side wait (cuStreamWaitValue32) on the
+ * upstream's "slab j ready" word and followed by "slab j consumed" (cuStreamWriteValue32) in the
+ * upstream's flags, so the hops are pipelined slab by slab, no host round trip and no SM is used
+ * (the slab GEMMs keep all SMs).  Setup, on every rank: compar_ce_export allocates the chain
+ * buffer (B up to max_b_bytes) and the flag words and writes an opaque blob
+ * (len >= COMPAR_CE_BLOB_BYTES); the caller all-gathers the blobs (rank-major) and passes them to
+ * compar_ce_import.  Without an NCCL communicator, world-mode samples need compar_set_reduce_hook.
+ * The ranks may share one GPU (separate processes), which is how the tests exercise it. */
+#define COMPAR_CE_BLOB_BYTES 256
+compar_status compar_ce_export(void *ctx, int nranks, int rank, uint64_t max_b_bytes, void *blob, int len);
+compar_status compar_ce_import(void *ctx, const void *blobs, int len);
+
 /* Replace the NCCL max-all-reduce that makes world-mode samples rank-consistent by a caller
  * hook (in-place max of *value over all ranks).  Used by the host-only SPMD tests (gloo) in
  * virtual-clock mode; fn = NULL restores the default. */

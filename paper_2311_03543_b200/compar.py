@@ -38,6 +38,7 @@ MEM_DEVICE, MEM_HOST = 0, 1
 TASK_ALL = (1 << 64) - 1
 MAX_PANELS = 8
 UNIQUE_ID_BYTES = 128
+CE_BLOB_BYTES = 256
 
 
 class Config(C.Structure):
@@ -93,7 +94,8 @@ EXPORTS = ["compar_config_default", "compar_init", "compar_terminate", "compar_r
            "compar_variant_count", "compar_variant_info", "compar_gemm_submit", "compar_sync", "compar_select",
            "compar_register_sort_variant", "compar_sort_submit",
            "compar_perf_save", "compar_perf_load", "compar_history_get", "compar_partition_rows",
-           "compar_comm_unique_id", "compar_comm_init", "compar_set_reduce_hook", "compar_set_reduce_n_hook",
+           "compar_comm_unique_id", "compar_comm_init", "compar_ce_export", "compar_ce_import",
+           "compar_set_reduce_hook", "compar_set_reduce_n_hook",
            "compar_stats_get",
            "compar_last_error", "compar_debug_spin"]
 
@@ -121,6 +123,8 @@ def _load():
         "compar_partition_rows": (st, [i64, i, C.POINTER(i64)]),
         "compar_comm_unique_id": (st, [vp, i]),
         "compar_comm_init": (st, [vp, i, i, vp, i]),
+        "compar_ce_export": (st, [vp, i, i, C.c_uint64, vp, i]),
+        "compar_ce_import": (st, [vp, vp, i]),
         "compar_set_reduce_hook": (st, [vp, REDUCE_FN, vp]),
         "compar_set_reduce_n_hook": (st, [vp, REDUCE_N_FN, vp]),
         "compar_stats_get": (st, [vp, C.POINTER(Stats)]),
@@ -331,6 +335,16 @@ class Compar:
     def comm_init(self, nranks: int, rank: int, uid: bytes):
         buf = C.create_string_buffer(uid, UNIQUE_ID_BYTES)
         _check(lib.compar_comm_init(self.ctx, nranks, rank, buf, UNIQUE_ID_BYTES), self.ctx)
+
+    def ce_init(self, nranks: int, rank: int, max_b_bytes: int, allgather):
+        """Copy-engine chain broadcast for world mode (compar_ce_export / _import).  `allgather(b)`
+        returns the list of every rank's bytes `b`, rank-major (e.g. torch.distributed
+        all_gather_object)."""
+        blob = C.create_string_buffer(CE_BLOB_BYTES)
+        _check(lib.compar_ce_export(self.ctx, nranks, rank, max_b_bytes, blob, CE_BLOB_BYTES), self.ctx)
+        blobs = allgather(bytes(blob.raw))
+        allb = C.create_string_buffer(b"".join(blobs), nranks * CE_BLOB_BYTES)
+        _check(lib.compar_ce_import(self.ctx, allb, nranks * CE_BLOB_BYTES), self.ctx)
 
     def set_reduce_hook(self, fn):
         cfn = REDUCE_FN(fn) if fn is not None else REDUCE_FN()

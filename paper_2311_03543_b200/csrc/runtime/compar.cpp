@@ -12,6 +12,7 @@
 //                                placement in dmda.{h,cpp}.
 #include "compar.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -114,6 +115,15 @@ struct Ctx {
     size_t bpacked_bytes = 0;
     bool bcast_loopback = false;  // 1 rank: emulate the broadcast with D2D copies (tests the slab path)
     int bcast_reserve_sms = 16;   // SMs left free for NCCL while a slab GEMM overlaps a broadcast
+    // copy-engine chain broadcast (compar_ce_export / compar_ce_import): no NCCL, no SMs
+    bool ce = false;
+    void *ce_buf = nullptr;        // own chain buffer (root: packed slabs; others: the replica)
+    size_t ce_cap = 0;
+    uint32_t *ce_flags = nullptr;  // [0, kCeMax): ready (written by self); [kCeMax, 2 kCeMax): consumed
+                                   // (written by the downstream rank after copying a chunk out)
+    void *ce_up_buf = nullptr;     // upstream rank's buffer and flags (IPC-mapped; ranks > 0)
+    uint32_t *ce_up_flags = nullptr;
+    uint32_t ce_seq = 0;           // world broadcasts issued (identical on every rank: SPMD)
     // host-memory pipeline
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     int host_chunks = 8;
@@ -614,8 +624,102 @@ compar_status run_scale(Ctx *c, const compar_gemm_desc *d, const compar_panel &p
 // with its own B (one launch).  Slab GEMMs that overlap a pending broadcast leave
 // bcast_reserve_sms SMs free so NCCL's kernels are never starved by the persistent GEMM.
 template <class F>
+compar_status world_gemms(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *replica,
+                          bool slabbed, int nslab, int64_t w, const std::vector<cudaEvent_t> &landed,
+                          int reserve_sms, F &&launch_on);
+
+// ---------------------------------------------------------------- copy-engine chain broadcast
+// Stream memory operations on IPC-mapped flag words (driver entry points; no SM involvement).
+using PfnWaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PfnWriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PfnWaitValue32 g_wait32 = nullptr;
+PfnWriteValue32 g_write32 = nullptr;
+bool resolve_stream_memops() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_wait32 = reinterpret_cast<PfnWaitValue32>(fn);
+        fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_write32 = reinterpret_cast<PfnWriteValue32>(fn);
+    });
+    return g_wait32 && g_write32;
+}
+constexpr int kCeMax = 64;                      // chunks per broadcast
+inline CUdeviceptr dptr(const uint32_t *p) { return static_cast<CUdeviceptr>(reinterpret_cast<uintptr_t>(p)); }
+
+// World task with the copy-engine chain: slab j travels root -> 1 -> ... -> P-1, each hop a
+// cudaMemcpyAsync from the upstream rank's IPC-mapped buffer, started by a GPU-side wait on the
+// upstream's ready[j] >= seq and followed by consumed[j] = seq in the upstream's flags (it may
+// then overwrite slab j for the next broadcast) and ready[j] = seq in our own.  Every rank runs
+// the same broadcast sequence (SPMD), so seq agrees everywhere; nothing runs on the SMs.
+template <class F>
+compar_status ce_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *Bloc,
+                          size_t b_bytes, F &&launch_on) {
+    const int eb = elem_bytes(d->in_dtype);
+    const bool root = c->rank == 0;
+    const bool has_down = c->rank + 1 < c->nranks;
+    const int64_t K = d->k, N = d->n;
+    int chunks = std::min(kCeMax, c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1);
+    int64_t w = ((N + chunks - 1) / chunks + 255) / 256 * 256;
+    if (w >= N) w = N;
+    int nslab = static_cast<int>((N + w - 1) / w);
+    const bool packable = d->transB ? ((K * eb) % 16 == 0) : ((w * eb) % 16 == 0 && ((N - (nslab - 1) * w) * eb) % 16 == 0);
+    if (!packable) nslab = 1;
+    const bool slabbed = nslab > 1;
+    const size_t total = slabbed ? static_cast<size_t>(K) * N * eb : b_bytes;
+    if (total > c->ce_cap) return fail(COMPAR_E_INVALID, "B larger than the copy-engine chain buffer (max_b_bytes)");
+    const uint32_t seq = ++c->ce_seq;
+    cudaStream_t cs = c->comm_stream;
+    CUstream cus = reinterpret_cast<CUstream>(cs);
+    t.bc0 = get_event(c);
+    t.bc1 = get_event(c);
+    cudaEvent_t ready = get_event(c);
+    t.extra.push_back(ready);
+    cudaEventRecord(ready, st);
+    cudaStreamWaitEvent(cs, ready, 0);
+    cudaEventRecord(t.bc0, cs);
+    std::vector<cudaEvent_t> landed;
+    for (int j = 0; j < nslab; ++j) {
+        const int64_t col0 = slabbed ? j * w : 0, wj = slabbed ? std::min(w, N - col0) : N;
+        const size_t off = static_cast<size_t>(K) * col0 * eb;
+        const size_t bytes = slabbed ? static_cast<size_t>(K) * wj * eb : b_bytes;
+        char *mine = static_cast<char *>(c->ce_buf) + off;
+        if (has_down)  // the downstream rank has copied slab j of the previous broadcast out
+            g_wait32(cus, dptr(c->ce_flags + kCeMax + j), seq - 1, CU_STREAM_WAIT_VALUE_GEQ);
+        if (root) {
+            const char *src = static_cast<const char *>(Bloc);
+            if (!slabbed)
+                cudaMemcpyAsync(mine, src, bytes, cudaMemcpyDeviceToDevice, cs);
+            else if (d->transB)
+                cudaMemcpy2DAsync(mine, K * eb, src + col0 * d->ldb * eb, d->ldb * eb, K * eb, wj,
+                                  cudaMemcpyDeviceToDevice, cs);
+            else
+                cudaMemcpy2DAsync(mine, wj * eb, src + col0 * eb, d->ldb * eb, wj * eb, K, cudaMemcpyDeviceToDevice,
+                                  cs);
+        } else {
+            g_wait32(cus, dptr(c->ce_up_flags + j), seq, CU_STREAM_WAIT_VALUE_GEQ);
+            cudaMemcpyAsync(mine, static_cast<const char *>(c->ce_up_buf) + off, bytes, cudaMemcpyDefault, cs);
+            g_write32(cus, dptr(c->ce_up_flags + kCeMax + j), seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+        }
+        g_write32(cus, dptr(c->ce_flags + j), seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+        cudaEvent_t ev = get_event(c);
+        t.extra.push_back(ev);
+        landed.push_back(ev);
+        cudaEventRecord(ev, cs);
+    }
+    cudaEventRecord(t.bc1, cs);
+    return world_gemms(c, d, t, st, c->ce_buf, slabbed, nslab, w, landed, 0, launch_on);   // no SMs to spare
+}
+
+template <class F>
 compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *Bloc,
                              size_t b_bytes, F &&launch_on) {
+    if (c->ce && c->nranks > 1) return ce_pipeline(c, d, t, st, Bloc, b_bytes, launch_on);
     const int eb = elem_bytes(d->in_dtype);
     const bool loop = c->nranks == 1;              // loopback emulation on one GPU
     const bool root = !loop && c->rank == 0;
@@ -683,7 +787,19 @@ compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStr
     }
     cudaEventRecord(t.bc1, c->comm_stream);
     if (nr != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclBroadcast: ") + ncclGetErrorString(nr));
-    const int reserve_sms = std::max(2, c->num_sms - c->bcast_reserve_sms);
+    return world_gemms(c, d, t, st, replica, slabbed, nslab, w, landed,
+                       std::max(2, c->num_sms - c->bcast_reserve_sms), launch_on);
+}
+
+// Slab GEMMs of a world task (shared by the NCCL and copy-engine broadcasts).  The root multiplies
+// with its own B in one launch; other ranks multiply slab j of the replica once slab j landed.
+template <class F>
+compar_status world_gemms(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *replica,
+                          bool slabbed, int nslab, int64_t w, const std::vector<cudaEvent_t> &landed,
+                          int reserve_sms, F &&launch_on) {
+    const int eb = elem_bytes(d->in_dtype);
+    const bool root = c->nranks > 1 && c->rank == 0;
+    const int64_t K = d->k, N = d->n;
     for (auto &pr : t.panels) {
         pr.start = get_event(c);
         pr.stop = get_event(c);
@@ -939,6 +1055,10 @@ compar_status compar_terminate(void *ctx) {
             if (b) cudaFree(b);
         if (c->breplica) cudaFree(c->breplica);
         if (c->bpacked) cudaFree(c->bpacked);
+        if (c->ce_up_buf) cudaIpcCloseMemHandle(c->ce_up_buf);
+        if (c->ce_up_flags) cudaIpcCloseMemHandle(c->ce_up_flags);
+        if (c->ce_buf) cudaFree(c->ce_buf);
+        if (c->ce_flags) cudaFree(c->ce_flags);
         if (c->scratch) cudaFree(c->scratch);
         if (c->sort_scratch) cudaFree(c->sort_scratch);
         if (c->sort_done) cudaEventDestroy(c->sort_done);
@@ -1617,6 +1737,54 @@ compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, 
     if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     c->nranks = nranks;
     c->rank = rank;
+    return COMPAR_OK;
+}
+
+compar_status compar_ce_export(void *ctx, int nranks, int rank, uint64_t max_b_bytes, void *blob, int len) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (nranks < 2 || rank < 0 || rank >= nranks || !blob || len < COMPAR_CE_BLOB_BYTES || max_b_bytes == 0)
+        return fail(COMPAR_E_INVALID, "bad copy-engine broadcast arguments");
+    if (c->virt) return fail(COMPAR_E_INVALID, "the copy-engine broadcast needs CUDA");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->comm || c->ce_buf) return fail(COMPAR_E_STATE, "a world communicator is already set up");
+    if (!resolve_stream_memops()) return fail(COMPAR_E_CUDA, "cuStreamWaitValue32 / WriteValue32 unavailable");
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaMalloc(&c->ce_buf, max_b_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->ce_flags, 2 * kCeMax * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(c->ce_flags, 0, 2 * kCeMax * sizeof(uint32_t));
+    cudaIpcMemHandle_t hb{}, hf{};
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hb, c->ce_buf);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hf, c->ce_flags);
+    if (e != cudaSuccess) return cuda_fail(e, "copy-engine chain buffers");
+    std::memset(blob, 0, len);
+    std::memcpy(blob, &hb, sizeof(hb));
+    std::memcpy(static_cast<char *>(blob) + sizeof(hb), &hf, sizeof(hf));
+    c->ce_cap = max_b_bytes;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->placer_ready = false;
+    return COMPAR_OK;
+}
+
+compar_status compar_ce_import(void *ctx, const void *blobs, int len) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->ce_buf) return fail(COMPAR_E_STATE, "compar_ce_export first");
+    if (!blobs || len < c->nranks * COMPAR_CE_BLOB_BYTES) return fail(COMPAR_E_INVALID, "need nranks blobs");
+    if (c->rank > 0) {
+        const char *up = static_cast<const char *>(blobs) + static_cast<size_t>(c->rank - 1) * COMPAR_CE_BLOB_BYTES;
+        cudaIpcMemHandle_t hb, hf;
+        std::memcpy(&hb, up, sizeof(hb));
+        std::memcpy(&hf, up + sizeof(hb), sizeof(hf));
+        cudaError_t e = cudaIpcOpenMemHandle(&c->ce_up_buf, hb, cudaIpcMemLazyEnablePeerAccess);
+        void *f = nullptr;
+        if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&f, hf, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle (upstream rank)");
+        c->ce_up_flags = static_cast<uint32_t *>(f);
+    }
+    c->ce = true;
     return COMPAR_OK;
 }
 

@@ -1,0 +1,134 @@
+"""Copy-engine chain broadcast (compar_ce_export / compar_ce_import) with 3 processes sharing one GPU
+(-m gpu): a gloo process group exchanges the IPC blobs and max-reduces the world samples; world-mode
+row panels then receive B slab by slab along root -> 1 -> 2 (cudaMemcpyAsync from the upstream
+rank's IPC-mapped buffer, GPU-side ready / consumed flag words).  Three consecutive tasks with
+different B check the slab-reuse protocol; every rank's C panel must be BITWISE equal to the same
+rows of the plain single-process call (each C element sums its full K in order)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+WORLD = 3
+CASES = [("tc_bf16_2sm", "bf16", 1000, 1536, 768, 0, 1536, 4),
+         ("tc_tf32_2sm", "f32", 700, 1280, 512, 1, 512, 3),
+         ("tc_bf16", "bf16", 900, 1001, 640, 0, 1008, 4)]     # N slabs not packable: one raw chunk
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, port, case, outdir):
+    import torch.distributed as dist
+
+    import gen
+    from gen.device import fill
+    from paper_2311_03543_b200 import compar as cm
+
+    name, dt, m, n, k, tb, ldb, chunks = case
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=WORLD)
+    torch.cuda.set_device(0)
+    ctx = cm.Compar(bcast_chunks=chunks)
+
+    def allgather(b):
+        out = [None] * WORLD
+        dist.all_gather_object(out, b)
+        return out
+
+    def red(p, _user):
+        t = torch.tensor([p[0]], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        p[0] = int(t.item())
+
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    brows, bcols = (n, k) if tb else (k, n)
+    ctx.ce_init(WORLD, rank, brows * ldb * (2 if dt == "bf16" else 4), allgather)
+    ctx.set_reduce_hook(red)
+    offs = cm.partition_rows(m, WORLD)
+    r0, r1 = offs[rank], offs[rank + 1]
+    mloc = r1 - r0
+    names = [v for v, _ in ctx.variants()]
+    sp = torch.cuda.current_stream().cuda_stream
+    A = torch.empty((max(mloc, 1), k), dtype=tdt, device="cuda")
+    if mloc:
+        fill(A.data_ptr(), dt, mloc, k, k, gen.TAG_A, row0=r0, stream=sp)
+    B = torch.zeros((brows, ldb), dtype=tdt, device="cuda") if rank == 0 else None
+    kw = dict(alpha=1.5, beta=0.5, in_dtype=cm.BF16 if dt == "bf16" else cm.F32,
+              compute=cm.COMPUTE_BF16 if dt == "bf16" else cm.COMPUTE_TF32, transB=tb, stream=sp,
+              variant_hint=names.index(name))
+    for it in range(3):                      # a different B each time: slab buffers are reused
+        Cl = torch.empty((max(mloc, 1), n), dtype=torch.float32, device="cuda")
+        if mloc:
+            fill(Cl.data_ptr(), "f32", mloc, n, n, gen.TAG_C, row0=r0, stream=sp)
+        if rank == 0:
+            fill(B.data_ptr(), dt, brows, bcols, ldb, gen.TAG_B, seed=gen.SEED_DATA + it, stream=sp)
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cl, C_out=Cl, lda=k, ldb=ldb, ldc_in=n, ldc_out=n, world=1, **kw)
+        rep = ctx.run(d)
+        assert rep.status == 0
+        np.save(os.path.join(outdir, f"c{it}_r{rank}.npy"), Cl[:mloc].cpu().numpy())
+    dist.barrier()
+    ctx.terminate()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] + f"-n{c[3]}-t{c[5]}" for c in CASES])
+def test_ce_chain_broadcast_three_processes_bitwise(tmp_path, case):
+    import torch.multiprocessing as mp
+
+    import gen
+    from gen.device import fill
+    from paper_2311_03543_b200 import compar as cm
+
+    mp.spawn(_worker, args=(_port(), case, str(tmp_path)), nprocs=WORLD, join=True)
+    name, dt, m, n, k, tb, ldb, chunks = case
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    brows, bcols = (n, k) if tb else (k, n)
+    offs = cm.partition_rows(m, WORLD)
+    with cm.Compar() as ctx:
+        names = [v for v, _ in ctx.variants()]
+        sp = torch.cuda.current_stream().cuda_stream
+        A = torch.empty((m, k), dtype=tdt, device="cuda")
+        fill(A.data_ptr(), dt, m, k, k, gen.TAG_A, stream=sp)
+        B = torch.zeros((brows, ldb), dtype=tdt, device="cuda")
+        for it in range(3):
+            fill(B.data_ptr(), dt, brows, bcols, ldb, gen.TAG_B, seed=gen.SEED_DATA + it, stream=sp)
+            C = torch.empty((m, n), dtype=torch.float32, device="cuda")
+            fill(C.data_ptr(), "f32", m, n, n, gen.TAG_C, stream=sp)
+            d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, lda=k, ldb=ldb, ldc_in=n, ldc_out=n, alpha=1.5,
+                             beta=0.5, in_dtype=cm.BF16 if dt == "bf16" else cm.F32,
+                             compute=cm.COMPUTE_BF16 if dt == "bf16" else cm.COMPUTE_TF32, transB=tb, stream=sp,
+                             variant_hint=names.index(name))
+            assert ctx.run(d).status == 0
+            ref = C.cpu().numpy()
+            for r in range(WORLD):
+                got = np.load(tmp_path / f"c{it}_r{r}.npy")
+                np.testing.assert_array_equal(got, ref[offs[r]:offs[r + 1]])
+
+
+def test_bench_world_path_shared_gpu():
+    """bench.py's N > 1 path end to end (torchrun, 2 ranks, copy-engine broadcast) with both ranks on
+    the one GPU (COMPAR_BENCH_SHARED_GPU=1, gloo process group): it must print one JSON line from
+    rank 0 with n_gpus = 2.  A functional check only — two processes share the GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, COMPAR_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--size", "2048", "--bcast", "ce", "--e2e-steps", "0", "--no-targets"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["config"]["bcast"] == "ce" and out["value"] > 0
