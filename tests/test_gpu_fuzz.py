@@ -34,6 +34,20 @@ def ctx():
        transB=st.integers(0, 1), pad=st.sampled_from([0, 8, 24]), beta=st.sampled_from([0.0, 0.5, -1.0]),
        integer=st.booleans(), seed=st.integers(0, 10 ** 6), pick=st.integers(0, 10))
 def test_fuzz_parity(m, n, k, compute, transB, pad, beta, integer, seed, pick):
+    _fuzz_case(m, n, k, compute, transB, pad, beta, integer, seed, pick)
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+@given(m=st.integers(1, 300), n=st.integers(1, 300), k=st.integers(2000, 12000),
+       compute=st.sampled_from([cm.COMPUTE_TF32, cm.COMPUTE_BF16]),
+       transB=st.integers(0, 1), pad=st.sampled_from([0, 8]), beta=st.sampled_from([0.0, 0.5]),
+       integer=st.booleans(), seed=st.integers(0, 10 ** 6), pick=st.integers(0, 10))
+def test_fuzz_parity_deep_k(m, n, k, compute, transB, pad, beta, integer, seed, pick):
+    """Deep K (where the split-K variant becomes eligible), small M x N."""
+    _fuzz_case(m, n, k, compute, transB, pad, beta, integer, seed, pick)
+
+
+def _fuzz_case(m, n, k, compute, transB, pad, beta, integer, seed, pick):
     c = ctx()
     dtype_id = cm.BF16 if compute == cm.COMPUTE_BF16 else cm.F32
     dt = "bf16" if dtype_id == cm.BF16 else "f32"
