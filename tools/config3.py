@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import gen  # noqa: E402
-from bench import ClockSampler, load_peaks  # noqa: E402
+from bench import ClockSampler, fair_medians, load_peaks  # noqa: E402
 from gen.device import device_matrix  # noqa: E402
 from paper_2311_03543_b200 import compar as cm  # noqa: E402
 
@@ -82,19 +82,13 @@ def main(out_path, secs):
             per = {}
             tc = [v for v in E if names[v].startswith("tc_")]
             ffma = [v for v in E if v not in tc]
-            # burst, interleaved: R rounds, each round one launch of every tensor-core variant
-            # (after one untimed round), so clock / power drift hits all variants alike
+            # per-variant burst time: bench.fair_medians (idle gap + warm-up before each variant's
+            # timed launches, rotated order; median over rounds of the per-round mean)
             descs = {v: mk(v) for v in E}
+            fm = fair_medians(ctx, {v: descs[v] for v in tc}, rounds=5, per_round=3)
             for v in tc:
-                ctx.run(descs[v])
-            samples = {v: [] for v in tc}
-            for _ in range(R):
-                for v in tc:
-                    samples[v].append(ctx.run(descs[v]).ns)
-            for v in tc:
-                b, m = min(samples[v]), statistics.median(samples[v])
-                per[names[v]] = {"best_ns": b, "median_ns": m, "tflops_best": flops / b / 1e3,
-                                 "tflops_median": flops / m / 1e3, "frac_best": flops / b / 1e3 / peak,
+                m = fm[v]
+                per[names[v]] = {"median_ns": m, "tflops_median": flops / m / 1e3,
                                  "frac_median": flops / m / 1e3 / peak}
             for v in ffma:   # FFMA variants: 10-50x slower here, 3 launches are enough for the regret
                 b, m = burst(lambda: ctx.run(descs[v]).ns, R=3)
