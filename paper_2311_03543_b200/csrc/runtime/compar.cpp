@@ -664,7 +664,8 @@ compar_status ce_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream
     const bool root = c->rank == 0;
     const bool has_down = c->rank + 1 < c->nranks;
     const int64_t K = d->k, N = d->n;
-    int chunks = std::min(kCeMax, c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1);
+    // the last rank's first slab arrives after P - 1 hops: use at least 4 slabs per hop
+    int chunks = std::min(kCeMax, std::max(c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1, 4 * (c->nranks - 1)));
     int64_t w = ((N + chunks - 1) / chunks + 255) / 256 * 256;
     if (w >= N) w = N;
     int nslab = static_cast<int>((N + w - 1) / w);
