@@ -181,6 +181,12 @@ typedef struct {
                                    receives B (its layout afterwards is the library's slab layout,
                                    unspecified to the caller); NULL: a library-owned buffer       */
     int variant_hint;           /* -1: run the selector; >= 0: force that registry index          */
+    uint64_t handles[4];        /* task-parallel world: caller ids of the A, B, C_in, C_out data
+                                   (StarPU-style data handles, R21); a non-zero id makes
+                                   dependency tracking use that id instead of the pointer's byte
+                                   range — required for rank-consistent placement when the
+                                   processes' allocations differ (pointers are per process); the
+                                   same id on C_in and C_out marks an in-place update.  0: range */
 } compar_gemm_desc;
 
 /* ---- the "sort" interface ----
@@ -313,6 +319,11 @@ compar_status compar_partition_rows(int64_t m, int p, int64_t *offsets);
 compar_status compar_comm_unique_id(void *out, int len);
 /* Joins the nranks-process communicator (one process per GPU).  Required before world = 1. */
 compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, int len);
+
+/* Joins an nranks-process SPMD world WITHOUT an NCCL communicator: the task-parallel world's sample
+ * exchange then goes through compar_set_reduce_n_hook (and world = 1 needs compar_ce_* for B and
+ * compar_set_reduce_hook).  E_STATE if a communicator is already set up. */
+compar_status compar_world_init(void *ctx, int nranks, int rank);
 
 /* Copy-engine chain broadcast of B for world = 1, instead of NCCL: slab j of B travels
  * root -> rank 1 -> ... -> rank P-1, each hop one cudaMemcpyAsync from the upstream rank's buffer

@@ -54,7 +54,7 @@ class GemmDesc(C.Structure):
                 ("A", C.c_void_p), ("lda", C.c_int64), ("B", C.c_void_p), ("ldb", C.c_int64),
                 ("C_in", C.c_void_p), ("ldc_in", C.c_int64), ("C_out", C.c_void_p), ("ldc_out", C.c_int64),
                 ("mem", C.c_int), ("stream", C.c_void_p), ("panels", C.c_int), ("world", C.c_int),
-                ("B_replica", C.c_void_p), ("variant_hint", C.c_int)]
+                ("B_replica", C.c_void_p), ("variant_hint", C.c_int), ("handles", C.c_uint64 * 4)]
 
 
 class SortDesc(C.Structure):
@@ -94,7 +94,7 @@ EXPORTS = ["compar_config_default", "compar_init", "compar_terminate", "compar_r
            "compar_variant_count", "compar_variant_info", "compar_gemm_submit", "compar_sync", "compar_select",
            "compar_register_sort_variant", "compar_sort_submit",
            "compar_perf_save", "compar_perf_load", "compar_history_get", "compar_partition_rows",
-           "compar_comm_unique_id", "compar_comm_init", "compar_ce_export", "compar_ce_import",
+           "compar_comm_unique_id", "compar_comm_init", "compar_world_init", "compar_ce_export", "compar_ce_import",
            "compar_set_reduce_hook", "compar_set_reduce_n_hook",
            "compar_stats_get",
            "compar_last_error", "compar_debug_spin"]
@@ -123,6 +123,7 @@ def _load():
         "compar_partition_rows": (st, [i64, i, C.POINTER(i64)]),
         "compar_comm_unique_id": (st, [vp, i]),
         "compar_comm_init": (st, [vp, i, i, vp, i]),
+        "compar_world_init": (st, [vp, i, i]),
         "compar_ce_export": (st, [vp, i, i, C.c_uint64, vp, i]),
         "compar_ce_import": (st, [vp, vp, i]),
         "compar_set_reduce_hook": (st, [vp, REDUCE_FN, vp]),
@@ -191,7 +192,7 @@ def make_sort_desc(keys, n=None, key_type=None, stream=None, variant_hint=-1) ->
 
 def make_desc(m, n, k, *, A=None, B=None, C_in=None, C_out=None, lda=None, ldb=None, ldc_in=None, ldc_out=None,
               alpha=1.0, beta=0.0, in_dtype=F32, compute=COMPUTE_F32_STRICT, transB=0, mem=MEM_DEVICE, stream=None,
-              panels=0, world=0, B_replica=None, variant_hint=-1) -> GemmDesc:
+              panels=0, world=0, B_replica=None, variant_hint=-1, handles=None) -> GemmDesc:
     d = GemmDesc()
     d.m, d.n, d.k = int(m), int(n), int(k)
     d.alpha, d.beta = float(alpha), float(beta)
@@ -206,6 +207,9 @@ def make_desc(m, n, k, *, A=None, B=None, C_in=None, C_out=None, lda=None, ldb=N
     d.panels, d.world = int(panels), int(world)
     d.B_replica = _ptr(B_replica)
     d.variant_hint = int(variant_hint)
+    if handles is not None:          # (A, B, C_in, C_out) data-handle ids, 0 = byte range
+        for i, h in enumerate(handles):
+            d.handles[i] = int(h)
     return d
 
 
@@ -335,6 +339,10 @@ class Compar:
     def comm_init(self, nranks: int, rank: int, uid: bytes):
         buf = C.create_string_buffer(uid, UNIQUE_ID_BYTES)
         _check(lib.compar_comm_init(self.ctx, nranks, rank, buf, UNIQUE_ID_BYTES), self.ctx)
+
+    def world_init(self, nranks: int, rank: int):
+        """SPMD world without NCCL (exchanges through the reduce hooks): compar_world_init."""
+        _check(lib.compar_world_init(self.ctx, nranks, rank), self.ctx)
 
     def ce_init(self, nranks: int, rank: int, max_b_bytes: int, allgather):
         """Copy-engine chain broadcast for world mode (compar_ce_export / _import).  `allgather(b)`

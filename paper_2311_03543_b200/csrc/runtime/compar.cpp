@@ -1379,10 +1379,18 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             const uintptr_t lo = reinterpret_cast<uintptr_t>(p);
             return Span{lo, lo + bytes};
         };
-        if (gemm && d->A && a_bytes) acc.reads.push_back(span(d->A, a_bytes));
-        if (gemm && d->B && b_bytes) acc.reads.push_back(span(d->B, b_bytes));
-        if (d->C_in && cin_bytes) acc.reads.push_back(span(d->C_in, cin_bytes));
-        if (d->C_out && cout_bytes) acc.writes.push_back(span(d->C_out, cout_bytes));
+        // a caller data handle (non-zero id) maps to its own disjoint range of a synthetic space,
+        // identical on every rank; otherwise the operand's byte range (per-process pointers)
+        auto span_h = [&](int i, const void *p, size_t bytes) {
+            if (d->handles[i] == 0) return span(p, bytes);
+            const uintptr_t lo = (uintptr_t(1) << 63) + static_cast<uintptr_t>(d->handles[i] % (uint64_t(1) << 22)) *
+                                                            (uintptr_t(1) << 40);
+            return Span{lo, lo + bytes};
+        };
+        if (gemm && (d->A || d->handles[0]) && a_bytes) acc.reads.push_back(span_h(0, d->A, a_bytes));
+        if (gemm && (d->B || d->handles[1]) && b_bytes) acc.reads.push_back(span_h(1, d->B, b_bytes));
+        if ((d->C_in || d->handles[2]) && cin_bytes) acc.reads.push_back(span_h(2, d->C_in, cin_bytes));
+        if ((d->C_out || d->handles[3]) && cout_bytes) acc.writes.push_back(span_h(3, d->C_out, cout_bytes));
         int64_t exec = 0;  // predicted ns: the variant's measured mean for the key, else unknown (0)
         if (gemm) {
             const Record *r = c->hist.find(c->variants[t.variant].hid, plan.key);
@@ -1738,6 +1746,18 @@ compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, 
     if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     c->nranks = nranks;
     c->rank = rank;
+    return COMPAR_OK;
+}
+
+compar_status compar_world_init(void *ctx, int nranks, int rank) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COMPAR_E_INVALID, "bad world arguments");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->comm || c->ce_buf) return fail(COMPAR_E_STATE, "a world communicator is already set up");
+    c->nranks = nranks;
+    c->rank = rank;
+    c->placer_ready = false;
     return COMPAR_OK;
 }
 

@@ -132,3 +132,74 @@ def test_bench_world_path_shared_gpu():
     assert len(lines) == 1
     out = json.loads(lines[0])
     assert out["n_gpus"] == 2 and out["config"]["bcast"] == "ce" and out["value"] > 0
+
+
+TASK_SHAPES = [(64, 64, 64), (300, 520, 256), (1000, 777, 333), (512, 1024, 512), (129, 257, 70), (2048, 256, 512)]
+
+
+def _tasks_worker(rank, port, outdir):
+    import torch.distributed as dist
+
+    import gen
+    from paper_2311_03543_b200 import compar as cm
+    from tests._gpu_util import to_device
+
+    world = 2
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ctx = cm.Compar(lanes=2)
+    ctx.world_init(world, rank)
+
+    def red_n(buf, n, _user):
+        t = torch.tensor([buf[i] for i in range(n)], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        for i in range(n):
+            buf[i] = int(t[i])
+    ctx.set_reduce_n_hook(red_n)
+    reps, tids, bufs = [], [], []
+    for rnd in range(2):                     # round 0 trains the selector; round 1 is placed by dmda
+        for t, (m, n, k) in enumerate(TASK_SHAPES * 4):
+            A = to_device(gen.matrix(gen.TAG_A, m, k, gen.DIST_I, "f32", seed=t))
+            B = to_device(gen.matrix(gen.TAG_B, k, n, gen.DIST_I, "f32", seed=t))
+            C = to_device(gen.matrix(gen.TAG_C, m, n, gen.DIST_I, "f32", seed=t))
+            h = 3 * (len(TASK_SHAPES) * 4 * rnd + t) + 1     # data handles: identical on both ranks
+            d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=2.0, beta=-1.0, compute=cm.COMPUTE_TF32,
+                             world=cm.WORLD_TASKS, stream=torch.cuda.current_stream().cuda_stream,
+                             handles=(h, h + 1, h + 2, h + 2))
+            tids.append((rnd, t, ctx.submit(d)))
+            bufs.append((A, B, C))
+        for (r_, t, tid), (_, _, C) in zip(tids, bufs):    # collective syncs, in submission order
+            r = ctx.sync(tid)
+            assert r.status == 0
+            if r_ == 1:
+                reps.append((r.variant, r.rank, r.lane))
+                if r.rank == rank:
+                    np.save(os.path.join(outdir, f"t{t}.npy"), C.cpu().numpy())
+        tids, bufs = [], []
+    np.save(os.path.join(outdir, f"reps_r{rank}.npy"), np.array(reps))
+    ctx.terminate()
+    dist.destroy_process_group()
+
+
+def test_task_world_two_processes_real_kernels(tmp_path):
+    """NEXT-1 (task-parallel world) with two processes on the one GPU, real kernels, lanes = 2, the
+    sample exchange through a gloo reduce_n hook (compar_world_init: no NCCL) and caller data
+    handles (the processes' pointers differ): both ranks take identical (variant, rank, lane)
+    decisions, each task runs exactly on the rank its report names, and that rank's C is bitwise
+    the oracle's (integer inputs)."""
+    import torch.multiprocessing as mp
+
+    import gen
+    from oracle import gemm as og
+
+    mp.spawn(_tasks_worker, args=(_port(), str(tmp_path)), nprocs=2, join=True)
+    r0, r1 = np.load(tmp_path / "reps_r0.npy"), np.load(tmp_path / "reps_r1.npy")
+    bad = [(i, r0[i].tolist(), r1[i].tolist()) for i in range(len(r0)) if (r0[i] != r1[i]).any()]
+    assert not bad, bad
+    assert set(r0[:, 1].tolist()) == {0, 1}                  # both ranks got work
+    for t, (m, n, k) in enumerate(TASK_SHAPES * 4):
+        A = gen.matrix(gen.TAG_A, m, k, gen.DIST_I, "f32", seed=t)
+        B = gen.matrix(gen.TAG_B, k, n, gen.DIST_I, "f32", seed=t)
+        C0 = gen.matrix(gen.TAG_C, m, n, gen.DIST_I, "f32", seed=t)
+        np.testing.assert_array_equal(np.load(tmp_path / f"t{t}.npy").astype(np.float64),
+                                      og.gemm(A, B, C0, alpha=2.0, beta=-1.0))
