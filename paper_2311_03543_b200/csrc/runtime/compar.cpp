@@ -287,6 +287,8 @@ bool admits(compar_target t, compar_dtype dt, compar_compute cp) {
         case COMPAR_TGT_TCW_BF16:
         case COMPAR_TGT_TCS_BF16:
         case COMPAR_TGT_SIMT_BF16: return dt == COMPAR_BF16 && cp == COMPAR_COMPUTE_BF16;
+        case COMPAR_TGT_SORT_RADIX:
+        case COMPAR_TGT_SORT_BITONIC: return false;   // the sort interface's variants
     }
     return false;
 }
