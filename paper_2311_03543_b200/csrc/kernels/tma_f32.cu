@@ -16,6 +16,7 @@
 // Eligibility: 16-byte aligned A/B and lda, ldb multiples of 4 (TMA stride rule).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -36,10 +37,19 @@ __device__ __forceinline__ void ffma2(float &c0, float &c1, float a, float b0, f
     asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
 }
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 4;
-constexpr int kConsumers = 256, kThreads = kConsumers + 32;
-constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BK * BN * 4, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 128;
+// Tile TB x TB (128, or 64 for grids that would not fill the GPU: 4x the CTAs of a small problem,
+// each (TB/8)^2 consumer threads with the same 8 x 8 micro-tile and k order, so C is bitwise the
+// same for either tile), K-step BK = 32 (one 128-byte swizzle row), 4-stage TMA ring.
+constexpr int BK = 32, STAGES = 4;
+template <int TB>
+struct TmaCfg {
+    static constexpr int TY = TB / 8;                       // consumer threads per tile dimension
+    static constexpr int kConsumers = TY * TY;
+    static constexpr int kThreads = kConsumers + 32;
+    static constexpr uint32_t A_BYTES = TB * BK * 4, B_BYTES = BK * TB * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 128;
+    static constexpr int kMinBlocks = TB == 128 ? 1 : 3;
+};
 
 struct TmaParams {
     int64_t m, n, k;
@@ -55,9 +65,12 @@ struct TmaParams {
 // byte offset of the float4 holding (row, k4*4 .. k4*4+3) in a 128-byte-swizzled [rows][32] FP32 tile
 __device__ __forceinline__ uint32_t sw128_off(int row, int k4) { return row * 128 + ((k4 ^ (row & 7)) << 4); }
 
-template <bool kTransB>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kTransB, int TB>
+__global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     tma_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TmaParams p) {
+    using Cf = TmaCfg<TB>;
+    constexpr int BM = TB, BN = TB, TY = Cf::TY, kConsumers = Cf::kConsumers;
+    constexpr uint32_t A_BYTES = Cf::A_BYTES, STAGE_BYTES = Cf::STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
@@ -96,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ---------------- consumer warps
-    const int tx = tid & 15, ty = tid >> 4;
+    const int tx = tid % TY, ty = tid / TY;
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -112,11 +125,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k4 = 0; k4 < BK / 4; ++k4) {
             float4 a[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + 16 * i, k4));
+            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + TY * i, k4));
             if (kTransB) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float4 b = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + 16 * j, k4));
+                    const float4 b = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + TY * j, k4));
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < 4; ++kk) {
                     const float *brow = reinterpret_cast<const float *>(sb + (k4 * 4 + kk) * (BN * 4));
                     const float4 b0 = *reinterpret_cast<const float4 *>(brow + tx * 4);
-                    const float4 b1 = *reinterpret_cast<const float4 *>(brow + 64 + tx * 4);
+                    const float4 b1 = *reinterpret_cast<const float4 *>(brow + BN / 2 + tx * 4);
                     const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -148,14 +161,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int64_t r = m0 + ty + 16 * i;
+        const int64_t r = m0 + ty + TY * i;
         if (r >= p.m) continue;
         float *crow = p.C_out + r * p.ldc_out;
         const float *cin = p.C_in + r * p.ldc_in;
         if (kTransB) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const int64_t c = n0 + tx + 16 * j;
+                const int64_t c = n0 + tx + TY * j;
                 if (c < p.n) {
                     float o = p.alpha * acc[i][j];
                     if (p.beta != 0.f) o = fmaf(p.beta, cin[c], o);
@@ -165,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t c = n0 + h * 64 + tx * 4;
+                const int64_t c = n0 + h * (BN / 2) + tx * 4;
                 float o[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) o[j] = p.alpha * acc[i][h * 4 + j];
@@ -192,18 +205,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <bool kTransB>
+template <bool kTransB, int TB>
 cudaError_t launch_t(const GemmLaunch &g) {
+    using Cf = TmaCfg<TB>;
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [] {
-        attr = cudaFuncSetAttribute(tma_f32_kernel<kTransB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        attr = cudaFuncSetAttribute(tma_f32_kernel<kTransB, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
     });
     if (attr != cudaSuccess) return attr;
     CUtensorMap ta, tb;
-    if (!get_tmap_2d(&ta, g.A, 4, g.m, g.k, g.lda, BM, BK, Swz::B128)) return cudaErrorInvalidValue;
-    bool ok = kTransB ? get_tmap_2d(&tb, g.B, 4, g.n, g.k, g.ldb, BN, BK, Swz::B128)
-                      : get_tmap_2d(&tb, g.B, 4, g.k, g.n, g.ldb, BK, BN, Swz::None);
+    if (!get_tmap_2d(&ta, g.A, 4, g.m, g.k, g.lda, TB, BK, Swz::B128)) return cudaErrorInvalidValue;
+    bool ok = kTransB ? get_tmap_2d(&tb, g.B, 4, g.n, g.k, g.ldb, TB, BK, Swz::B128)
+                      : get_tmap_2d(&tb, g.B, 4, g.k, g.n, g.ldb, BK, TB, Swz::None);
     if (!ok) return cudaErrorInvalidValue;
     TmaParams p;
     p.m = g.m, p.n = g.n, p.k = g.k, p.alpha = g.alpha, p.beta = g.beta;
@@ -211,22 +225,32 @@ cudaError_t launch_t(const GemmLaunch &g) {
     p.num_kb = static_cast<int>((g.k + BK - 1) / BK);
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
-    dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM));
-    tma_f32_kernel<kTransB><<<grid, kThreads, SMEM, g.stream>>>(ta, tb, p);
+    dim3 grid(static_cast<unsigned>((g.n + TB - 1) / TB), static_cast<unsigned>((g.m + TB - 1) / TB));
+    tma_f32_kernel<kTransB, TB><<<grid, Cf::kThreads, Cf::SMEM, g.stream>>>(ta, tb, p);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_tma_f32(const GemmLaunch &g) {
-    if ((g.m + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
-    return g.transB ? launch_t<true>(g) : launch_t<false>(g);
+    if ((g.m + 127) / 128 > 65535) return cudaErrorInvalidValue;
+    // 64 x 64 tiles when 128 x 128 tiles would fill at most a quarter of the SMs (measured: 256^3
+    // 36 -> 27 us, 512^3 58 -> 40 us; at 1024^3+ the 128 tile's 8 consumer warps per CTA win).
+    // COMPAR_TMA_TILE=128 / 64 forces one.
+    const int64_t tiles128 = ((g.m + 127) / 128) * ((g.n + 127) / 128);
+    const char *e = std::getenv("COMPAR_TMA_TILE");
+    const int force = e ? std::atoi(e) : 0;
+    const bool small = force == 64 || (force != 128 && 4 * tiles128 <= g.num_sms);
+    if (small) return g.transB ? launch_t<true, 64>(g) : launch_t<false, 64>(g);
+    return g.transB ? launch_t<true, 128>(g) : launch_t<false, 128>(g);
 }
 
 cudaError_t preload_tma_kernels() {
     cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, tma_f32_kernel<false>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tma_f32_kernel<true>);
+    cudaError_t e = cudaFuncGetAttributes(&a, tma_f32_kernel<false, 128>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tma_f32_kernel<true, 128>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tma_f32_kernel<false, 64>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tma_f32_kernel<true, 64>);
     return e;
 }
 
