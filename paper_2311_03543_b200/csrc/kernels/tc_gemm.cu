@@ -35,9 +35,10 @@ constexpr int kThreads = 192;
 constexpr int kGroupM = 16;
 constexpr int kTileRing = 4;
 
-template <bool kBF16, bool kTransB>
+template <bool kBF16, bool kTransB, int kBN>
 struct TcCfg {
-    static constexpr int BM = 128, BN = 256;
+    static constexpr int BM = 128, BN = kBN;       // 256, or 64 for grids that leave most SMs idle
+    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;   // two accumulators
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / ELEM;       // K per tcgen05.mma (16 bf16 / 8 tf32)
@@ -86,10 +87,10 @@ __device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, i
     nb = r / gm;
 }
 
-template <bool kBF16, bool kTransB>
+template <bool kBF16, bool kTransB, int kBN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
-    using C = TcCfg<kBF16, kTransB>;
+    using C = TcCfg<kBF16, kTransB, kBN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc<512>(ptx::smem_u32(tmem_slot));
+    if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -276,17 +277,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     __syncthreads();
-    if (warp == 1) ptx::tmem_dealloc<512>(tmem_base);
+    if (warp == 1) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
 // ---------------------------------------------------------------- host side
-template <bool kBF16, bool kTransB>
+template <bool kBF16, bool kTransB, int kBN>
 cudaError_t launch_tc_t(const GemmLaunch &g) {
-    using C = TcCfg<kBF16, kTransB>;
+    using C = TcCfg<kBF16, kTransB, kBN>;
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<kBF16, kTransB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<kBF16, kTransB, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         C::SMEM);
     });
     if (attr_err != cudaSuccess) return attr_err;
@@ -319,23 +320,42 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
     p.serp = serp_env;
     const int tiles = p.m_blocks * p.n_blocks;
     const int grid = tiles < g.num_sms ? tiles : g.num_sms;
-    tc_gemm_kernel<kBF16, kTransB><<<grid, kThreads, C::SMEM, g.stream>>>(ta, tb, p);
+    tc_gemm_kernel<kBF16, kTransB, kBN><<<grid, kThreads, C::SMEM, g.stream>>>(ta, tb, p);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16) {
-    if (bf16) return g.transB ? launch_tc_t<true, true>(g) : launch_tc_t<true, false>(g);
-    return g.transB ? launch_tc_t<false, true>(g) : launch_tc_t<false, false>(g);
+    // 128 x 64 tiles when 128 x 256 tiles would fill at most a quarter of the SMs (latency-bound
+    // small problems: 4x the CTAs, each a quarter of the work); same k order per element, so C is
+    // bitwise the same.  COMPAR_TC1_BN=256 / 64 forces one.
+    const int64_t tiles256 = ((g.m + 127) / 128) * ((g.n + 255) / 256);
+    const char *e = std::getenv("COMPAR_TC1_BN");
+    const int force = e ? std::atoi(e) : 0;
+    const bool small = force == 64 || (force != 256 && 4 * tiles256 <= g.num_sms);
+    if (small) {
+        if (bf16) return g.transB ? launch_tc_t<true, true, 64>(g) : launch_tc_t<true, false, 64>(g);
+        return g.transB ? launch_tc_t<false, true, 64>(g) : launch_tc_t<false, false, 64>(g);
+    }
+    if (bf16) return g.transB ? launch_tc_t<true, true, 256>(g) : launch_tc_t<true, false, 256>(g);
+    return g.transB ? launch_tc_t<false, true, 256>(g) : launch_tc_t<false, false, 256>(g);
 }
 
 cudaError_t preload_tc_kernels() {
     cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, tc_gemm_kernel<true, false>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<true, true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<false, false>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<false, true>);
+    cudaError_t e = cudaSuccess;
+#define COMPAR_PRELOAD_TC(B, T, N) \
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_kernel<B, T, N>);
+    COMPAR_PRELOAD_TC(true, false, 256)
+    COMPAR_PRELOAD_TC(true, true, 256)
+    COMPAR_PRELOAD_TC(false, false, 256)
+    COMPAR_PRELOAD_TC(false, true, 256)
+    COMPAR_PRELOAD_TC(true, false, 64)
+    COMPAR_PRELOAD_TC(true, true, 64)
+    COMPAR_PRELOAD_TC(false, false, 64)
+    COMPAR_PRELOAD_TC(false, true, 64)
+#undef COMPAR_PRELOAD_TC
     return e;
 }
 
