@@ -37,7 +37,7 @@ constexpr int kTileRing = 4;
 
 template <bool kBF16, bool kTransB, int kBN>
 struct TcCfg {
-    static constexpr int BM = 128, BN = kBN;       // 256, or 64 for grids that leave most SMs idle
+    static constexpr int BM = 128, BN = kBN;       // 256, or 128 / 64 for grids that leave SMs idle
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;   // two accumulators
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K
@@ -327,16 +327,29 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
 }  // namespace
 
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16) {
-    // 128 x 64 tiles when 128 x 256 tiles would fill at most a quarter of the SMs (latency-bound
-    // small problems: 4x the CTAs, each a quarter of the work); same k order per element, so C is
-    // bitwise the same.  COMPAR_TC1_BN=256 / 64 forces one.
-    const int64_t tiles256 = ((g.m + 127) / 128) * ((g.n + 255) / 256);
+    // Tile width: 128 x 256 unless that leaves many SMs idle — then 128 x 128 or 128 x 64 (N = 128
+    // / 64 MMAs), whichever first gives at least half as many tiles as SMs: latency-bound small
+    // and mid-size problems get up to 4x the CTAs.  Every element keeps its k order, so C is
+    // bitwise the same for any width.  COMPAR_TC1_BN=256 / 128 / 64 forces one.
+    const int64_t mb = (g.m + 127) / 128;
     const char *e = std::getenv("COMPAR_TC1_BN");
-    const int force = e ? std::atoi(e) : 0;
-    const bool small = force == 64 || (force != 256 && 4 * tiles256 <= g.num_sms);
-    if (small) {
+    int bn = e ? std::atoi(e) : 0;
+    if (bn != 256 && bn != 128 && bn != 64) {
+        bn = 64;
+        for (int w : {256, 128}) {
+            if (2 * mb * ((g.n + w - 1) / w) >= g.num_sms) {
+                bn = w;
+                break;
+            }
+        }
+    }
+    if (bn == 64) {
         if (bf16) return g.transB ? launch_tc_t<true, true, 64>(g) : launch_tc_t<true, false, 64>(g);
         return g.transB ? launch_tc_t<false, true, 64>(g) : launch_tc_t<false, false, 64>(g);
+    }
+    if (bn == 128) {
+        if (bf16) return g.transB ? launch_tc_t<true, true, 128>(g) : launch_tc_t<true, false, 128>(g);
+        return g.transB ? launch_tc_t<false, true, 128>(g) : launch_tc_t<false, false, 128>(g);
     }
     if (bf16) return g.transB ? launch_tc_t<true, true, 256>(g) : launch_tc_t<true, false, 256>(g);
     return g.transB ? launch_tc_t<false, true, 256>(g) : launch_tc_t<false, false, 256>(g);
@@ -355,6 +368,10 @@ cudaError_t preload_tc_kernels() {
     COMPAR_PRELOAD_TC(true, true, 64)
     COMPAR_PRELOAD_TC(false, false, 64)
     COMPAR_PRELOAD_TC(false, true, 64)
+    COMPAR_PRELOAD_TC(true, false, 128)
+    COMPAR_PRELOAD_TC(true, true, 128)
+    COMPAR_PRELOAD_TC(false, false, 128)
+    COMPAR_PRELOAD_TC(false, true, 128)
 #undef COMPAR_PRELOAD_TC
     return e;
 }
