@@ -203,6 +203,23 @@ def test_splitk_parity(ctx, name, shape, transB, beta, dist):
         assert og.rel_fro(got, ref) <= tol
 
 
+@pytest.mark.parametrize("name", ["tc_tf32", "tc_bf16", "tma_f32"])
+@pytest.mark.parametrize("transB", [0, 1])
+def test_small_tile_instantiations_bitwise(ctx, monkeypatch, name, transB):
+    """tc_* (1-SM) at tile widths 256 / 128 / 64 and tma_f32 at tiles 128 / 64 — the launcher
+    picks one from the grid size — give BITWISE the same C (same k order per element), within
+    tolerance of the oracle."""
+    env, widths = ("COMPAR_TMA_TILE", ("128", "64")) if name == "tma_f32" else ("COMPAR_TC1_BN", ("256", "128", "64"))
+    outs = []
+    for w in widths:
+        monkeypatch.setenv(env, w)
+        got, ref, tol = run_case(ctx, name, 700, 900, 333, transB=transB)
+        outs.append(got)
+        assert og.rel_fro(got, ref) <= tol
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+
+
 @pytest.mark.parametrize("name", list(VARIANTS))
 def test_transB_and_beta0_nan(ctx, name):
     got, ref, tol = run_case(ctx, name, 190, 300, 260, transB=1, beta=0.0)
