@@ -42,10 +42,12 @@ constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;   // producer, MMA, 4 epilogue, 
 constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
 constexpr int kRingM = 4;
 
-template <bool kBF16, bool kTransB, int kPairs>
+template <bool kBF16, bool kTransB, int kPairs, int kBN>
 struct TcMCfg {
     static constexpr int BM = 128;              // A rows per CTA (UMMA_M = 256 per pair)
-    static constexpr int BN = 256;              // UMMA_N; each CTA holds BN/2 columns of B
+    static constexpr int BN = kBN;              // UMMA_N (256, or 128 for grids that leave pairs idle);
+                                                // each CTA holds BN/2 columns of B
+    static constexpr uint32_t TMEM_COLS = 2 * BN;   // two accumulators
     static constexpr int BN_CTA = BN / 2;
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;
@@ -106,12 +108,13 @@ __device__ __forceinline__ void tile_coords_m(int t, int m_blocks, int n_blocks,
     nb = r / gm;
 }
 
-template <bool kBF16, bool kTransB, int kPairs>
+template <bool kBF16, bool kTransB, int kPairs, int kBN>
 __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 1)
     tc_gemm_2sm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmCo, const __grid_constant__ CUtensorMap tmCi,
                           TcMParams p) {
-    using C = TcMCfg<kBF16, kTransB, kPairs>;
+    using C = TcMCfg<kBF16, kTransB, kPairs, kBN>;
+    static_assert(kPairs == 1 || kBN == 256, "the B-multicast form splits a 256-wide tile");
     constexpr int kCluster = 2 * kPairs;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -161,7 +164,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         ptx::mbar_init(tload, 2 * kEpiWarpsM);
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc_2sm<512>(ptx::smem_u32(tmem_slot));
+    if (warp == 1) ptx::tmem_alloc_2sm<C::TMEM_COLS>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();
     ptx::cluster_sync();
     ptx::tc_fence_after();
@@ -503,7 +506,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     ptx::cluster_sync();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc_2sm<512>(tmem_base);
+        ptx::tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
     }
 }
 
@@ -546,15 +549,15 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
     }
 }
 
-template <bool kBF16, bool kTransB, int kPairs>
+template <bool kBF16, bool kTransB, int kPairs, int kBN = 256>
 cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
-    using C = TcMCfg<kBF16, kTransB, kPairs>;
+    using C = TcMCfg<kBF16, kTransB, kPairs, kBN>;
     constexpr int kCluster = 2 * kPairs;
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs>,
+        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs, kBN>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (attr_err != cudaSuccess) return;
         cudaLaunchConfig_t cfg = {};
@@ -563,7 +566,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         at.val.clusterDim.x = kCluster, at.val.clusterDim.y = 1, at.val.clusterDim.z = 1;
         cfg.gridDim = dim3(kCluster * 64), cfg.blockDim = dim3(kThreadsM), cfg.dynamicSmemBytes = C::SMEM;
         cfg.attrs = &at, cfg.numAttrs = 1;
-        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs>, &cfg);
+        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs, kBN>, &cfg);
         if (std::getenv("COMPAR_VERBOSE")) std::fprintf(stderr, "tc_gemm_2sm_mc: max active %d-CTA clusters = %d\n", kCluster, max_clusters);
     });
     if (attr_err != cudaSuccess) return attr_err;
@@ -629,7 +632,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         if (!w) return cudaErrorMemoryAllocation;
         p.flags = w->flags, p.partial = w->partial, p.epoch = ++w->epoch;
     }
-    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
+    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs, kBN><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     if (p.splits > 1) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -649,6 +652,17 @@ cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16, int pairs) {
         if (bf16) return g.transB ? launch_tcm_t<true, true, 2>(g) : launch_tcm_t<true, false, 2>(g);
         return g.transB ? launch_tcm_t<false, true, 2>(g) : launch_tcm_t<false, false, 2>(g);
     }
+    // 256 x 128 pair tiles (N = 128 MMAs) when 256 x 256 ones would give fewer tiles than half the
+    // CTA pairs (e.g. 1536^3: 36 tiles for 74 pairs); same k order per element, bitwise-same C.
+    // COMPAR_TC2_BN=256 / 128 forces one.
+    const char *e = std::getenv("COMPAR_TC2_BN");
+    const int force = e ? std::atoi(e) : 0;
+    const int64_t tiles256 = ((g.m + 255) / 256) * ((g.n + 255) / 256);
+    const bool narrow = force == 128 || (force != 256 && 2 * tiles256 < g.num_sms / 2);   // tiles < pairs / 2
+    if (narrow) {
+        if (bf16) return g.transB ? launch_tcm_t<true, true, 1, 128>(g) : launch_tcm_t<true, false, 1, 128>(g);
+        return g.transB ? launch_tcm_t<false, true, 1, 128>(g) : launch_tcm_t<false, false, 1, 128>(g);
+    }
     if (bf16) return g.transB ? launch_tcm_t<true, true, 1>(g) : launch_tcm_t<true, false, 1>(g);
     return g.transB ? launch_tcm_t<false, true, 1>(g) : launch_tcm_t<false, false, 1>(g);
 }
@@ -662,14 +676,22 @@ cudaError_t launch_tc_gemm_splitk(const GemmLaunch &g, bool bf16) {
 
 cudaError_t preload_tcm_kernels() {
     cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, false, 2>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, true, 2>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, false, 2>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, true, 2>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, false, 1>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, true, 1>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, false, 1>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, true, 1>);
+    cudaError_t e = cudaSuccess;
+#define COMPAR_PRELOAD_TCM(B, T, P, N) \
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, P, N>);
+    COMPAR_PRELOAD_TCM(true, false, 2, 256)
+    COMPAR_PRELOAD_TCM(true, true, 2, 256)
+    COMPAR_PRELOAD_TCM(false, false, 2, 256)
+    COMPAR_PRELOAD_TCM(false, true, 2, 256)
+    COMPAR_PRELOAD_TCM(true, false, 1, 256)
+    COMPAR_PRELOAD_TCM(true, true, 1, 256)
+    COMPAR_PRELOAD_TCM(false, false, 1, 256)
+    COMPAR_PRELOAD_TCM(false, true, 1, 256)
+    COMPAR_PRELOAD_TCM(true, false, 1, 128)
+    COMPAR_PRELOAD_TCM(true, true, 1, 128)
+    COMPAR_PRELOAD_TCM(false, false, 1, 128)
+    COMPAR_PRELOAD_TCM(false, true, 1, 128)
+#undef COMPAR_PRELOAD_TCM
     return e;
 }
 

@@ -203,13 +203,15 @@ def test_splitk_parity(ctx, name, shape, transB, beta, dist):
         assert og.rel_fro(got, ref) <= tol
 
 
-@pytest.mark.parametrize("name", ["tc_tf32", "tc_bf16", "tma_f32"])
+@pytest.mark.parametrize("name", ["tc_tf32", "tc_bf16", "tma_f32", "tc_tf32_2sm", "tc_bf16_2sm"])
 @pytest.mark.parametrize("transB", [0, 1])
 def test_small_tile_instantiations_bitwise(ctx, monkeypatch, name, transB):
     """tc_* (1-SM) at tile widths 256 / 128 / 64 and tma_f32 at tiles 128 / 64 — the launcher
     picks one from the grid size — give BITWISE the same C (same k order per element), within
     tolerance of the oracle."""
-    env, widths = ("COMPAR_TMA_TILE", ("128", "64")) if name == "tma_f32" else ("COMPAR_TC1_BN", ("256", "128", "64"))
+    env, widths = {"tma_f32": ("COMPAR_TMA_TILE", ("128", "64")),
+                   "tc_tf32_2sm": ("COMPAR_TC2_BN", ("256", "128")),
+                   "tc_bf16_2sm": ("COMPAR_TC2_BN", ("256", "128"))}.get(name, ("COMPAR_TC1_BN", ("256", "128", "64")))
     outs = []
     for w in widths:
         monkeypatch.setenv(env, w)
