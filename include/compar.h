@@ -277,6 +277,29 @@ compar_status compar_register_variant(void *ctx, const char *iface, const char *
  * USER with fn.  Same registry (indices, names, mask) as the GEMM variants. */
 compar_status compar_register_sort_variant(void *ctx, const char *name, compar_target target,
                                            compar_sort_fn fn, void *user, int *out_id);
+/* ---- generic interfaces (the target of the #pragma compar pre-compiler) ----
+ * An interface declared with `#pragma compar method_declare interface(I) ...`: its
+ * variants are user functions that enqueue GPU work on the task's stream, which they obtain with
+ * compar_current_stream() while the runtime calls them (like StarPU's
+ * starpu_cuda_get_local_stream).  args[i] points at the i-th interface argument; sizes[] are the
+ * values of the size clauses ("size"), the history key is (I, sizes[0], sizes[1], product of
+ * the rest).  Selection, calibration, history, tasks and reports are those of the GEMM interface. */
+typedef compar_status (*compar_generic_fn)(void *const *args, const int64_t *sizes, int nsizes, void *user);
+typedef struct {
+    const char *iface;          /* interface name (variants registered under it compete)          */
+    int nargs;
+    void *const *args;          /* args[i]: address of the i-th argument value                     */
+    int nsizes;                 /* 0..8 */
+    const int64_t *sizes;
+    void *stream;               /* cudaStream_t the variant's work is ordered on (NULL: default)   */
+    int variant_hint;           /* -1: selector; >= 0: that registry index                          */
+} compar_generic_desc;
+compar_status compar_register_generic_variant(void *ctx, const char *iface, const char *name, compar_generic_fn fn,
+                                              void *user, int *out_id);
+compar_status compar_generic_submit(void *ctx, const compar_generic_desc *d, uint64_t *task);
+/* The stream of the task whose variant the calling thread is running (NULL outside a variant). */
+void *compar_current_stream(void);
+
 compar_status compar_variant_count(void *ctx, int *n);
 compar_status compar_variant_info(void *ctx, int id, char *name, int name_len, int *target);
 

@@ -84,10 +84,23 @@ def build_gen(force: bool = False) -> str:
     return GEN_LIB
 
 
+COMPARCC = os.path.join(PKG, "bin", "comparcc")
+
+
+def build_precompiler(force: bool = False) -> str:
+    """comparcc, the #pragma compar pre-compiler (host C++)."""
+    src = os.path.join(PKG, "csrc", "precompiler", "comparcc.cpp")
+    if force or _stale(COMPARCC, [src]):
+        os.makedirs(os.path.dirname(COMPARCC), exist_ok=True)
+        _run(["g++", "-O2", "-std=c++17", "-Wall", "-Wextra", "-o", COMPARCC + ".tmp", src])
+        os.replace(COMPARCC + ".tmp", COMPARCC)
+    return COMPARCC
+
+
 def build_all(force: bool = False, verbose: bool = False):
-    """Product library + the input-generator twin.  (The oracle is compiled by
+    """Product library + the input-generator twin + the pre-compiler.  (The oracle is compiled by
     __graft_entry__.build() / the tests; the product package never touches oracle/.)"""
-    return [build_compar(force, verbose), build_gen(force)]
+    return [build_compar(force, verbose), build_gen(force), build_precompiler(force)]
 
 
 if __name__ == "__main__":

@@ -88,11 +88,18 @@ GEMM_FN = C.CFUNCTYPE(C.c_int, C.POINTER(GemmDesc), C.POINTER(Panel), C.c_void_p
                       C.POINTER(C.c_int64))
 SORT_FN = C.CFUNCTYPE(C.c_int, C.POINTER(SortDesc), C.c_void_p, C.c_void_p, C.POINTER(C.c_int64))
 REDUCE_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_void_p)
+GENERIC_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int, C.c_void_p)
+
+
+class GenericDesc(C.Structure):
+    _fields_ = [("iface", C.c_char_p), ("nargs", C.c_int), ("args", C.POINTER(C.c_void_p)), ("nsizes", C.c_int),
+                ("sizes", C.POINTER(C.c_int64)), ("stream", C.c_void_p), ("variant_hint", C.c_int)]
 REDUCE_N_FN = C.CFUNCTYPE(None, C.POINTER(C.c_int64), C.c_int, C.c_void_p)
 
 EXPORTS = ["compar_config_default", "compar_init", "compar_terminate", "compar_register_variant",
            "compar_variant_count", "compar_variant_info", "compar_gemm_submit", "compar_sync", "compar_select",
            "compar_register_sort_variant", "compar_sort_submit",
+           "compar_register_generic_variant", "compar_generic_submit", "compar_current_stream",
            "compar_perf_save", "compar_perf_load", "compar_history_get", "compar_partition_rows",
            "compar_comm_unique_id", "compar_comm_init", "compar_world_init", "compar_ce_export", "compar_ce_import",
            "compar_set_reduce_hook", "compar_set_reduce_n_hook",
@@ -115,6 +122,9 @@ def _load():
         "compar_gemm_submit": (st, [vp, C.POINTER(GemmDesc), C.POINTER(C.c_uint64)]),
         "compar_register_sort_variant": (st, [vp, C.c_char_p, i, SORT_FN, vp, C.POINTER(i)]),
         "compar_sort_submit": (st, [vp, C.POINTER(SortDesc), C.POINTER(C.c_uint64)]),
+        "compar_register_generic_variant": (st, [vp, C.c_char_p, C.c_char_p, GENERIC_FN, vp, C.POINTER(i)]),
+        "compar_generic_submit": (st, [vp, C.POINTER(GenericDesc), C.POINTER(C.c_uint64)]),
+        "compar_current_stream": (vp, []),
         "compar_sync": (st, [vp, C.c_uint64, C.POINTER(Report)]),
         "compar_select": (st, [vp, C.POINTER(GemmDesc), C.POINTER(i), C.POINTER(i)]),
         "compar_perf_save": (st, [vp, C.c_char_p]),
@@ -152,6 +162,11 @@ def _check(status, ctx=None):
         msg = lib.compar_last_error(ctx)
         raise ComparError(status, msg.decode() if msg else "")
     return status
+
+
+def current_stream() -> int:
+    """compar_current_stream(): the running generic variant's stream (inside a variant call)."""
+    return lib.compar_current_stream() or 0
 
 
 def partition_rows(m: int, p: int) -> list[int]:
@@ -261,6 +276,24 @@ class Compar:
         _check(lib.compar_register_sort_variant(self.ctx, name.encode() if name is not None else None, target, cfn,
                                                 None, C.byref(out)), self.ctx)
         return out.value
+
+    def register_generic_variant(self, iface: str, name: str, fn) -> int:
+        """A variant of a user interface (what the #pragma compar pre-compiler generates):
+        fn(args, sizes, nsizes, user) enqueues GPU work on current_stream()."""
+        cfn = GENERIC_FN(fn)
+        self._callbacks.append(cfn)
+        out = C.c_int()
+        _check(lib.compar_register_generic_variant(self.ctx, iface.encode(), name.encode(), cfn, None, C.byref(out)),
+               self.ctx)
+        return out.value
+
+    def generic_submit(self, iface: str, args_ptrs, sizes, stream=None, variant_hint=-1) -> int:
+        arr = (C.c_void_p * max(1, len(args_ptrs)))(*args_ptrs)
+        sz = (C.c_int64 * max(1, len(sizes)))(*[int(x) for x in sizes])
+        d = GenericDesc(iface.encode(), len(args_ptrs), arr, len(sizes), sz, stream, variant_hint)
+        t = C.c_uint64()
+        _check(lib.compar_generic_submit(self.ctx, C.byref(d), C.byref(t)), self.ctx)
+        return t.value
 
     def variants(self) -> list[tuple[str, int]]:
         n = C.c_int()

@@ -47,7 +47,7 @@ compar_status cuda_fail(cudaError_t e, const char *what) {
     return fail(COMPAR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-enum Iface { kGemm = 0, kSort = 1 };
+enum Iface { kGemm = 0, kSort = 1, kGeneric = 2 };
 
 struct Variant {
     std::string name;
@@ -57,7 +57,11 @@ struct Variant {
     int hid;  // interned history id of `name`
     int iface = kGemm;
     compar_sort_fn sfn = nullptr;
+    std::string giface;               // generic interface name
+    compar_generic_fn gfn = nullptr;
 };
+
+thread_local void *t_current_stream = nullptr;   // compar_current_stream() inside a generic variant
 
 struct PanelRun {
     compar_panel p{};
@@ -1605,6 +1609,87 @@ compar_status compar_sort_submit(void *ctx, const compar_sort_desc *d, uint64_t 
     } else {
         t.mode = kNoop;
     }
+    if (task_out) *task_out = t.id;
+    c->tasks.emplace(t.id, std::move(t));
+    return COMPAR_OK;
+}
+
+compar_status compar_register_generic_variant(void *ctx, const char *iface, const char *name, compar_generic_fn fn,
+                                              void *user, int *out_id) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    if (!iface || !*iface || std::strlen(iface) > 63) return fail(COMPAR_E_INVALID, "bad interface name");
+    if (!std::strcmp(iface, "gemm") || !std::strcmp(iface, "sort"))
+        return fail(COMPAR_E_INVALID, "gemm / sort are built-in interfaces (compar_register_variant / _sort_variant)");
+    if (!name || !*name || std::strlen(name) > 63) return fail(COMPAR_E_INVALID, "bad variant name");
+    if (!fn) return fail(COMPAR_E_INVALID, "a generic variant needs a function");
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (const auto &v : c->variants)
+        if (v.name == name) return fail(COMPAR_E_DUPLICATE, std::string("duplicate variant ") + name);
+    if (c->variants.size() >= 64) return fail(COMPAR_E_INVALID, "too many variants");
+    Variant v{name, COMPAR_TGT_USER, nullptr, user, c->hist.intern(name)};
+    v.iface = kGeneric;
+    v.giface = iface;
+    v.gfn = fn;
+    c->variants.push_back(v);
+    if (out_id) *out_id = static_cast<int>(c->variants.size()) - 1;
+    return COMPAR_OK;
+}
+
+void *compar_current_stream(void) { return t_current_stream; }
+
+compar_status compar_generic_submit(void *ctx, const compar_generic_desc *d, uint64_t *task_out) {
+    Ctx *c = as_ctx(ctx);
+    if (!c) return fail(COMPAR_E_STATE, "not an initialised context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!d || !d->iface) return fail(COMPAR_E_INVALID, "desc / interface is NULL");
+    if (d->nargs < 0 || (d->nargs > 0 && !d->args)) return fail(COMPAR_E_INVALID, "bad args");
+    if (d->nsizes < 0 || d->nsizes > 8 || (d->nsizes > 0 && !d->sizes)) return fail(COMPAR_E_INVALID, "bad sizes");
+    if (d->variant_hint < -1 || d->variant_hint >= static_cast<int>(c->variants.size()))
+        return fail(COMPAR_E_INVALID, "variant_hint out of range");
+    if (c->virt) return fail(COMPAR_E_INVALID, "generic interfaces need CUDA");
+    int64_t sz[3] = {1, 1, 1};
+    for (int i = 0; i < d->nsizes; ++i) {
+        if (d->sizes[i] < 0) return fail(COMPAR_E_INVALID, "negative size");
+        if (i < 2) sz[i] = d->sizes[i];
+        else sz[2] *= d->sizes[i];
+    }
+    c->stats.submits++;
+    Task t;
+    t.id = c->next_task++;
+    // key: the sizes plus the interface (its name's history id in the dtype slot, apart from the
+    // GEMM / sort keys)
+    t.key = Key{sz[0], sz[1], sz[2], 1000 + c->hist.intern(std::string("iface:") + d->iface), -3, 0, 0};
+    cudaStream_t st = static_cast<cudaStream_t>(d->stream);
+    std::vector<int> idx, names;
+    for (size_t v = 0; v < c->variants.size(); ++v) {
+        if (v < 63 && (c->cfg.variant_mask >> v) & 1) continue;
+        const Variant &var = c->variants[v];
+        if (var.iface != kGeneric || var.giface != d->iface) continue;
+        idx.push_back(static_cast<int>(v));
+        names.push_back(var.hid);
+    }
+    if (idx.empty()) return fail(COMPAR_E_NO_VARIANT, std::string("no variant of interface ") + d->iface);
+    bool warm = false;
+    compar_status s = choose_core(c, idx, names, t.key, d->variant_hint, true, &t.variant, &t.mode, &warm);
+    if (s != COMPAR_OK) {
+        c->stats.failed++;
+        return s;
+    }
+    t.warm = warm;
+    t.history = (t.mode == kWarmup || t.mode == kCalib || t.mode == kModel || t.mode == kPredict);
+    const Variant &var = c->variants[t.variant];
+    PanelRun pr;
+    pr.p.rows = sz[0];
+    pr.start = get_event(c);
+    pr.stop = get_event(c);
+    cudaEventRecord(pr.start, st);
+    t_current_stream = d->stream;
+    if (var.gfn(d->args, d->sizes, d->nsizes, var.user) != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
+    t_current_stream = nullptr;
+    c->stats.launches++;
+    cudaEventRecord(pr.stop, st);
+    t.panels.push_back(pr);
     if (task_out) *task_out = t.id;
     c->tasks.emplace(t.id, std::move(t));
     return COMPAR_OK;
