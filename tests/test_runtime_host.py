@@ -336,3 +336,28 @@ def test_sort_interface_selector_virtual(golden):
     with pytest.raises(cm.ComparError):
         ctx.register_sort_variant("bad", cm.TGT_TC_BF16, None)
     ctx.terminate()
+
+
+def test_generic_world_and_ce_argument_errors():
+    """ABI argument / state errors of the generic-interface, world and copy-engine calls (host side,
+    virtual clock: no GPU needed)."""
+    ctx = cm.Compar(virtual_clock=1)
+    fn = lambda args, sizes, nsizes, user: 0  # noqa: E731
+    with pytest.raises(cm.ComparError) as e:                         # built-in interface names are reserved
+        ctx.register_generic_variant("gemm", "g1", fn)
+    assert e.value.status == 1
+    v = ctx.register_generic_variant("axpy", "axpy_a", fn)
+    with pytest.raises(cm.ComparError) as e:                         # variant names are unique registry-wide
+        ctx.register_generic_variant("axpy", "axpy_a", fn)
+    assert e.value.status == 3
+    with pytest.raises(cm.ComparError) as e:                         # no CUDA in virtual-clock mode
+        ctx.generic_submit("axpy", [], [10])
+    assert e.value.status == 1
+    assert ctx.variants()[v][0] == "axpy_a"
+    with pytest.raises(cm.ComparError):                              # bad world arguments
+        ctx.world_init(2, 5)
+    ctx.world_init(2, 1)
+    with pytest.raises(cm.ComparError):                              # copy engines need CUDA
+        ctx.ce_init(2, 1, 1 << 20, lambda b: [b, b])
+    ctx.terminate()
+    assert cm.current_stream() == 0                                  # outside a variant call
