@@ -129,3 +129,43 @@ def test_batched_calibration_timing(compute, dt):
     assert any(r.batch > 1 for r in cal)
     assert ctx.stats().launches == sum(r.batch for r in reps)
     ctx.terminate()
+
+
+def test_long_stream_no_resource_growth():
+    """5000 submit/sync pairs over mixed tiny keys (GEMM, sort, generic): no device-memory or event
+    growth after the first round (events are pooled, workspaces cached), every task succeeds and
+    the history holds one record per (variant, key) used."""
+    ctx = cm.Compar()
+    names = [v for v, _ in ctx.variants()]
+    A = device_matrix(gen.TAG_A, 64, 64)
+    B = device_matrix(gen.TAG_B, 64, 64)
+    C = device_matrix(gen.TAG_C, 64, 64)
+    keys = torch.randn(3000, device="cuda")
+    calls = {"n": 0}
+
+    def gfn(args, sizes, nsizes, user):
+        calls["n"] += 1
+        return 0
+    ctx.register_generic_variant("noop", "noop_v", gfn)
+    ds = [cm.make_desc(s, s, s, A=A, B=B, C_in=C, C_out=C, compute=cm.COMPUTE_TF32) for s in (16, 32, 48, 64)]
+
+    def round_():
+        for i in range(1000):
+            r = ctx.run(ds[i % 4])
+            assert r.status == 0
+            if i % 10 == 0:
+                assert ctx.sort(keys).status == 0
+            if i % 10 == 5:
+                t = ctx.generic_submit("noop", [], [i % 3 + 1])
+                assert ctx.sync(t).status == 0
+    round_()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(4):
+        round_()
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] >= free0 - (4 << 20)
+    st = ctx.stats()
+    assert st.failed == 0 and st.submits >= 5000
+    assert calls["n"] == 500
+    ctx.terminate()
