@@ -390,7 +390,9 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
         const char *s = std::getenv("COMPAR_TCW_GROUP");
         return s ? std::atoi(s) : 0;
     }();
-    p.group_m = group_env > 0 ? group_env : kGroupW;
+    // raster bands of 4 pair-rows; 8 when K <= 8192, where a band's A rows plus the B columns a
+    // wave touches then fit in L2 (8192^3: 741 vs 752 us; 32768^3 keeps 4: 52.3 vs 53.7 ms)
+    p.group_m = group_env > 0 ? group_env : (g.k <= 8192 ? 2 * kGroupW : kGroupW);
     const char *cp_s = std::getenv("COMPAR_CIN_PREFETCH");
     p.cin_prefetch = cp_s ? std::atoi(cp_s) : 0;   // measured slower (8192^3 763 vs 737 us): opt-in
     const char *dl = std::getenv("COMPAR_TCW_DELAY");     // read per launch (tests compare D = 0)
