@@ -593,7 +593,8 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         const char *s = std::getenv("COMPAR_TCM_GROUP");
         return s ? std::atoi(s) : 0;
     }();
-    p.group_m = group_env > 0 ? group_env : kGroupM4;
+    // bands of 4 cluster tiles; 8 when K <= 8192 (8192^3: 729 vs 743 us; 32768^3 keeps 4)
+    p.group_m = group_env > 0 ? group_env : (g.k <= 8192 ? 2 * kGroupM4 : kGroupM4);
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
