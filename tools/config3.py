@@ -122,6 +122,24 @@ def main(out_path, secs):
                 if secs > 0:
                     time.sleep(1.0)
                     case["cublas"]["sustained"] = sustained(lambda: torch.matmul(A, B), flops, secs)
+                # the same operation through cuBLAS: C_out = 1.5 AB + 0.5 C_in, FP32 C in and out
+                # (BF16 inputs: addmm with out_dtype=float32; F32 inputs: TF32 addmm)
+                kw = {"out_dtype": torch.float32} if dt == "bf16" else {}
+
+                def mm_same():
+                    e0.record()
+                    torch.addmm(C, A, B, beta=0.5, alpha=1.5, **kw)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    return int(e0.elapsed_time(e1) * 1e6)
+                time.sleep(1.0)
+                b, m = burst(mm_same)
+                case["cublas_same_op"] = {"best_ns": b, "median_ns": m, "tflops_best": flops / b / 1e3,
+                                          "tflops_median": flops / m / 1e3}
+                if secs > 0:
+                    time.sleep(1.0)
+                    case["cublas_same_op"]["sustained"] = sustained(
+                        lambda: torch.addmm(C, A, B, beta=0.5, alpha=1.5, **kw), flops, secs)
             res["cases"].append(case)
             print(json.dumps({k: v for k, v in case.items() if k != "variants"}), flush=True)
             for n, p in per.items():

@@ -44,7 +44,7 @@ if __name__ == "__main__":
     secs = float(sys.argv[1]) if len(sys.argv) > 1 else 3.0
     ctx = cm.Compar()
     names = [v for v, _ in ctx.variants()]
-    for s in (8192, 16384, 32768):
+    for s in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else (8192, 16384, 32768))]:
         A = device_matrix(gen.TAG_A, s, s, dtype="bf16")
         B = device_matrix(gen.TAG_B, s, s, dtype="bf16")
         Cd = device_matrix(gen.TAG_C, s, s)
@@ -61,6 +61,11 @@ if __name__ == "__main__":
         ctx.sync()
         out = torch.empty((s, s), dtype=torch.bfloat16, device="cuda")
         res["torch.matmul(bf16->bf16)"] = sustained(lambda: torch.matmul(A, B, out=out), flops, secs)
+        del out
+        # the same operation as ours: C = 1.5 AB + 0.5 C, FP32 C in and out
+        out = torch.empty((s, s), dtype=torch.float32, device="cuda")
+        res["torch.addmm(same op, f32 C)"] = sustained(
+            lambda: torch.addmm(Cd, A, B, beta=0.5, alpha=1.5, out_dtype=torch.float32, out=out), flops, secs)
         print(f"{s}^3 sustained {secs:.0f}s: " + "  ".join(f"{k}={v}" for k, v in res.items()), flush=True)
         del A, B, Cd, out
         torch.cuda.empty_cache()
