@@ -152,33 +152,52 @@ __global__ void __launch_bounds__(THREADS, 2) simt_f32_kernel(GemmLaunch g) {
     // Epilogue: C_out = alpha*acc + beta*C_in (C_in unread when beta == 0).
     const bool cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
                       (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
+    // C_in is gathered kRows rows at a time before their stores: C_in may alias C_out, so the
+    // compiler cannot hoist a load above an earlier store, and load/store pairs issued in turn
+    // would serialise 16 memory round trips (kRows = 2 keeps the epilogue within 128 registers).
+    constexpr int kRows = 2;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-        if (r >= g.m) continue;
+    for (int i0 = 0; i0 < 8; i0 += kRows) {
+        float ci[kRows][8];
+        if (g.beta != 0.f) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int64_t c = n0 + h * 64 + tx * 4;
-            float o[4];
+            for (int ii = 0; ii < kRows; ++ii) {
+                const int i = i0 + ii;
+                const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
 #pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] = g.alpha * acc[i][h * 4 + j];
-            if (cvec && c + 3 < g.n) {
-                if (g.beta != 0.f) {
-                    const float4 ci = *reinterpret_cast<const float4 *>(g.C_in + r * g.ldc_in + c);
-                    o[0] = fmaf(g.beta, ci.x, o[0]);
-                    o[1] = fmaf(g.beta, ci.y, o[1]);
-                    o[2] = fmaf(g.beta, ci.z, o[2]);
-                    o[3] = fmaf(g.beta, ci.w, o[3]);
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t c = n0 + h * 64 + tx * 4;
+                    const float *src = g.C_in + r * g.ldc_in + c;
+                    if (r < g.m && cvec && c + 3 < g.n) {
+                        const float4 v = *reinterpret_cast<const float4 *>(src);
+                        ci[ii][h * 4 + 0] = v.x, ci[ii][h * 4 + 1] = v.y, ci[ii][h * 4 + 2] = v.z, ci[ii][h * 4 + 3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) ci[ii][h * 4 + j] = r < g.m && c + j < g.n ? src[j] : 0.f;
+                    }
                 }
-                *reinterpret_cast<float4 *>(g.C_out + r * g.ldc_out + c) = make_float4(o[0], o[1], o[2], o[3]);
-            } else {
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < kRows; ++ii) {
+            const int i = i0 + ii;
+            const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+            if (r >= g.m) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = n0 + h * 64 + tx * 4;
+                float o[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    if (c + j < g.n) {
-                        float v = o[j];
-                        if (g.beta != 0.f) v = fmaf(g.beta, g.C_in[r * g.ldc_in + c + j], v);
-                        g.C_out[r * g.ldc_out + c + j] = v;
-                    }
+                    o[j] = g.alpha * acc[i][h * 4 + j];
+                    if (g.beta != 0.f) o[j] = fmaf(g.beta, ci[ii][h * 4 + j], o[j]);
+                }
+                if (cvec && c + 3 < g.n) {
+                    *reinterpret_cast<float4 *>(g.C_out + r * g.ldc_out + c) = make_float4(o[0], o[1], o[2], o[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (c + j < g.n) g.C_out[r * g.ldc_out + c + j] = o[j];
                 }
             }
         }

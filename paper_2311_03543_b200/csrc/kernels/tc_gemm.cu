@@ -230,46 +230,63 @@ __global__ void __launch_bounds__(kThreads, 1)
             tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
-            ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
-            ptx::tc_fence_after();
             const int64_t row = static_cast<int64_t>(mb) * C::BM + q * 32 + lane;
             const bool row_ok = row < p.m;
             float *crow = p.C_out + row * p.ldc_out;
             const float *cin = p.C_in + row * p.ldc_in;
+            const int64_t colb = static_cast<int64_t>(nb) * C::BN;
+            // C_in one 32-column chunk ahead in registers: chunk 0 is loaded before the accumulator
+            // is ready, so its latency hides under the mainloop (small grids are otherwise bound by
+            // the serial C_in round trips of the epilogue)
+            const bool pre = p.beta != 0.f && p.cvec && row_ok;
+            auto vec_chunk = [&](int c) { return pre && colb + c * 32 + 32 <= p.n; };
+            float4 cur[8], nxt[8];
+            if (vec_chunk(0)) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) cur[v] = *reinterpret_cast<const float4 *>(cin + colb + 4 * v);
+            }
+            ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < C::BN / 32; ++c) {
+                const int64_t col0 = colb + c * 32;
+                if (c + 1 < C::BN / 32 && vec_chunk(c + 1)) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) nxt[v] = *reinterpret_cast<const float4 *>(cin + col0 + 32 + 4 * v);
+                }
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + c * 32, r);
                 ptx::tmem_ld_wait();
-                const int64_t col0 = static_cast<int64_t>(nb) * C::BN + c * 32;
-                if (!row_ok || col0 >= p.n) continue;
-                if (p.cvec && col0 + 32 <= p.n) {
+                if (row_ok && col0 < p.n) {
+                    if (p.cvec && col0 + 32 <= p.n) {
 #pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        float4 o;
-                        o.x = p.alpha * __uint_as_float(r[4 * v + 0]);
-                        o.y = p.alpha * __uint_as_float(r[4 * v + 1]);
-                        o.z = p.alpha * __uint_as_float(r[4 * v + 2]);
-                        o.w = p.alpha * __uint_as_float(r[4 * v + 3]);
-                        if (p.beta != 0.f) {
-                            const float4 ci = *reinterpret_cast<const float4 *>(cin + col0 + 4 * v);
-                            o.x = fmaf(p.beta, ci.x, o.x);
-                            o.y = fmaf(p.beta, ci.y, o.y);
-                            o.z = fmaf(p.beta, ci.z, o.z);
-                            o.w = fmaf(p.beta, ci.w, o.w);
+                        for (int v = 0; v < 8; ++v) {
+                            float4 o;
+                            o.x = p.alpha * __uint_as_float(r[4 * v + 0]);
+                            o.y = p.alpha * __uint_as_float(r[4 * v + 1]);
+                            o.z = p.alpha * __uint_as_float(r[4 * v + 2]);
+                            o.w = p.alpha * __uint_as_float(r[4 * v + 3]);
+                            if (pre) {
+                                o.x = fmaf(p.beta, cur[v].x, o.x);
+                                o.y = fmaf(p.beta, cur[v].y, o.y);
+                                o.z = fmaf(p.beta, cur[v].z, o.z);
+                                o.w = fmaf(p.beta, cur[v].w, o.w);
+                            }
+                            *reinterpret_cast<float4 *>(crow + col0 + 4 * v) = o;
                         }
-                        *reinterpret_cast<float4 *>(crow + col0 + 4 * v) = o;
-                    }
-                } else {
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        if (col0 + e < p.n) {
-                            float o = p.alpha * __uint_as_float(r[e]);
-                            if (p.beta != 0.f) o = fmaf(p.beta, cin[col0 + e], o);
-                            crow[col0 + e] = o;
+                        for (int e = 0; e < 32; ++e) {
+                            if (col0 + e < p.n) {
+                                float o = p.alpha * __uint_as_float(r[e]);
+                                if (p.beta != 0.f) o = fmaf(p.beta, cin[col0 + e], o);
+                                crow[col0 + e] = o;
+                            }
                         }
                     }
                 }
+#pragma unroll
+                for (int v = 0; v < 8; ++v) cur[v] = nxt[v];
             }
             ptx::tc_fence_before();
             __syncwarp();

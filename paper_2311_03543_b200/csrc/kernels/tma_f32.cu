@@ -159,19 +159,49 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     }
 
     // ---------------- epilogue
+    // C_in is gathered for the whole 8 x 8 micro-tile before the first store: C_in may alias C_out,
+    // so the compiler cannot hoist a load above an earlier store, and load/store pairs issued in
+    // turn would serialise 16 (or 64) memory round trips.
+    float ci[8][8];
+    const bool has_cin = p.beta != 0.f;
+    if (has_cin) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t r = m0 + ty + TY * i;
+            const float *cin = p.C_in + r * p.ldc_in;
+            if (kTransB) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t c = n0 + tx + TY * j;
+                    ci[i][j] = r < p.m && c < p.n ? cin[c] : 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t c = n0 + h * (BN / 2) + tx * 4;
+                    if (r < p.m && p.cvec && c + 3 < p.n) {
+                        const float4 v = *reinterpret_cast<const float4 *>(cin + c);
+                        ci[i][h * 4 + 0] = v.x, ci[i][h * 4 + 1] = v.y, ci[i][h * 4 + 2] = v.z, ci[i][h * 4 + 3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) ci[i][h * 4 + j] = r < p.m && c + j < p.n ? cin[c + j] : 0.f;
+                    }
+                }
+            }
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int64_t r = m0 + ty + TY * i;
         if (r >= p.m) continue;
         float *crow = p.C_out + r * p.ldc_out;
-        const float *cin = p.C_in + r * p.ldc_in;
         if (kTransB) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int64_t c = n0 + tx + TY * j;
                 if (c < p.n) {
                     float o = p.alpha * acc[i][j];
-                    if (p.beta != 0.f) o = fmaf(p.beta, cin[c], o);
+                    if (has_cin) o = fmaf(p.beta, ci[i][j], o);
                     crow[c] = o;
                 }
             }
@@ -181,24 +211,16 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
                 const int64_t c = n0 + h * (BN / 2) + tx * 4;
                 float o[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) o[j] = p.alpha * acc[i][h * 4 + j];
+                for (int j = 0; j < 4; ++j) {
+                    o[j] = p.alpha * acc[i][h * 4 + j];
+                    if (has_cin) o[j] = fmaf(p.beta, ci[i][h * 4 + j], o[j]);
+                }
                 if (p.cvec && c + 3 < p.n) {
-                    if (p.beta != 0.f) {
-                        const float4 ci = *reinterpret_cast<const float4 *>(cin + c);
-                        o[0] = fmaf(p.beta, ci.x, o[0]);
-                        o[1] = fmaf(p.beta, ci.y, o[1]);
-                        o[2] = fmaf(p.beta, ci.z, o[2]);
-                        o[3] = fmaf(p.beta, ci.w, o[3]);
-                    }
                     *reinterpret_cast<float4 *>(crow + c) = make_float4(o[0], o[1], o[2], o[3]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if (c + j < p.n) {
-                            float v = o[j];
-                            if (p.beta != 0.f) v = fmaf(p.beta, cin[c + j], v);
-                            crow[c + j] = v;
-                        }
+                        if (c + j < p.n) crow[c + j] = o[j];
                 }
             }
         }

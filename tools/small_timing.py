@@ -35,4 +35,24 @@ for s in (64, 256, 1024):
         batch = e0.elapsed_time(e1) * 1e6 / 200
         print(f"{s}^3 {v:12s} synced-one-by-one median {statistics.median(one)/1e3:7.1f} us | back-to-back "
               f"median {statistics.median(many)/1e3:7.1f} us | batch avg {batch/1e3:7.1f} us", flush=True)
+        # cuBLAS beside (torch.addmm, TF32), same batch protocol
+    torch.backends.cuda.matmul.allow_tf32 = True
+    for _ in range(3):
+        torch.addmm(Cd, A, B)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(200):
+        torch.addmm(Cd, A, B)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{s}^3 cublas addmm batch avg {e0.elapsed_time(e1) * 1e3 / 200:7.1f} us", flush=True)
+x = torch.zeros(1, device="cuda")
+torch.cuda.synchronize()
+e0.record()
+for _ in range(200):
+    x.add_(1)
+e1.record()
+torch.cuda.synchronize()
+print(f"one-element torch kernel (launch floor) batch avg {e0.elapsed_time(e1) * 1e3 / 200:7.2f} us", flush=True)
 ctx.terminate()
