@@ -130,9 +130,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int num_tiles = p.m_blocks * p.n_blocks;
     // Consumer side of the tile ring: returns the i-th tile of this CTA (>= num_tiles: done).
+    // tile 0 of CTA b is tile b (no ring round trip, no atomic before the first loads); tile
+    // i >= 1 comes through ring index i - 1 from the global counter, offset by the grid size
     auto next_tile = [&](int i) -> int {
-        const int slot = i % kTileRing;
-        ptx::mbar_wait(rfull0 + 8 * slot, (i / kTileRing) & 1);
+        if (i == 0) return static_cast<int>(blockIdx.x);
+        const int slot = (i - 1) % kTileRing;
+        ptx::mbar_wait(rfull0 + 8 * slot, ((i - 1) / kTileRing) & 1);
         const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(rempty0 + 8 * slot);
@@ -144,11 +147,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int i = 0;; ++i) {
-                const int slot = i % kTileRing;
-                ptx::mbar_wait(rempty0 + 8 * slot, ((i / kTileRing) & 1) ^ 1);
-                const int t = atomicAdd(&p.sched[0], 1);
-                ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
-                ptx::mbar_arrive(rfull0 + 8 * slot);
+                int t = static_cast<int>(blockIdx.x);
+                if (i > 0) {
+                    const int slot = (i - 1) % kTileRing;
+                    ptx::mbar_wait(rempty0 + 8 * slot, (((i - 1) / kTileRing) & 1) ^ 1);
+                    t = static_cast<int>(gridDim.x) + atomicAdd(&p.sched[0], 1);
+                    ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
+                    ptx::mbar_arrive(rfull0 + 8 * slot);
+                }
                 if (t >= num_tiles) break;
                 int mb, nb;
                 tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);

@@ -64,7 +64,10 @@ struct TcMCfg {
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
     static constexpr uint32_t B_LBO = kTransB ? 16 : BK * 128;   // MN-major: stride between N atoms
-    static constexpr uint32_t EPI_BYTES = kEpiWarpsM * 2 * 4096;
+    // C_in / C_out staging chunks (32 x 32 FP32) per epilogue warp: all four chunks of a 128-wide
+    // tile are loaded before its accumulator is ready; the 256-wide tile cycles two
+    static constexpr int EPI_BUFS = kBN == 128 ? 4 : 2;
+    static constexpr uint32_t EPI_BYTES = kEpiWarpsM * EPI_BUFS * 4096;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
                                       ((kTransB ? 0u : 1u) << 16) | ((uint32_t(BN) >> 3) << 17) |
@@ -128,7 +131,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     const uint32_t rfull0 = tempty0 + 16;
     const uint32_t rempty0 = rfull0 + 8 * kRingM;
     const uint32_t cbar0 = rempty0 + 8 * kRingM;
-    const uint32_t ring0 = cbar0 + 16 * kEpiWarpsM;
+    const uint32_t ring0 = cbar0 + 8 * C::EPI_BUFS * kEpiWarpsM;
     const uint32_t tload = ring0 + 4 * kRingM;                    // stream-K partial loaded (pair leader)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
 
@@ -160,7 +163,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             ptx::mbar_init(rfull0 + 8 * r, 1);
             ptx::mbar_init(rempty0 + 8 * r, kConsumers);
         }
-        for (int b = 0; b < 2 * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
+        for (int b = 0; b < C::EPI_BUFS * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
         ptx::mbar_init(tload, 2 * kEpiWarpsM);
         ptx::fence_mbar_init();
     }
@@ -204,10 +207,18 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         }
         return true;
     };
+    // Dynamic mode: item 0 of cluster cl is item cl (no ring round trip, no atomic on the
+    // critical path of the first tile); item j >= 1 comes through ring index j - 1 from the
+    // global counter, offset by the number of clusters.
+    const int n_cl = static_cast<int>(gridDim.x) / kCluster;
     auto next_item = [&](int j, Item &it) -> bool {  // whole-warp consumer (MMA and epilogue warps)
         if (p.sk) return sk_item(j, it);
-        const int slot = j % kRingM;
-        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (j / kRingM) & 1);
+        if (j == 0) {
+            it = dyn_item(cl);
+            return true;
+        }
+        const int slot = (j - 1) % kRingM;
+        ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((j - 1) / kRingM) & 1);
         const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
@@ -226,12 +237,14 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 Item it;
                 if (p.sk) {
                     if (!sk_item(i, it)) break;
+                } else if (i == 0) {
+                    it = dyn_item(cl);
                 } else {
                     int t;
-                    const int slot = i % kRingM;
+                    const int slot = (i - 1) % kRingM;
                     if (rank == 0 && me == 0) {
-                        ptx::mbar_wait_cluster(rempty0 + 8 * slot, ((i / kRingM) & 1) ^ 1);
-                        t = atomicAdd(&p.sched[0], 1);
+                        ptx::mbar_wait_cluster(rempty0 + 8 * slot, (((i - 1) / kRingM) & 1) ^ 1);
+                        t = n_cl + atomicAdd(&p.sched[0], 1);
                         ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
                         for (uint32_t q = 1; q < kCluster; ++q)
                             ptx::st_shared_cluster_u32(ptx::mapa_rank(ring0 + 4 * slot, q), static_cast<uint32_t>(t));
@@ -239,7 +252,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                         for (uint32_t q = 1; q < kCluster; ++q)
                             ptx::mbar_arrive_cluster(ptx::mapa_rank(rfull0 + 8 * slot, q));
                     } else {
-                        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingM) & 1);
+                        ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - 1) / kRingM) & 1);
                         t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
                         ptx::mbar_arrive_cluster(rempty_root + 8 * slot);
                     }
@@ -331,9 +344,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, 8 chunks of 32 x 32
         const int q = warp & 3;
         const int ew = warp - 2;
-        const uint32_t buf[2] = {epi0 + (2 * ew) * 4096, epi0 + (2 * ew + 1) * 4096};
-        const uint32_t cbar[2] = {cbar0 + 16 * ew, cbar0 + 16 * ew + 8};
-        uint32_t loads[2] = {0, 0};
+        constexpr int NB = C::EPI_BUFS;
+        // staging chunk b of this warp and its C_in barrier (computed: no local-memory arrays)
+        auto buf = [&](int b) -> uint32_t { return epi0 + static_cast<uint32_t>(NB * ew + b) * 4096; };
+        auto cbar = [&](int b) -> uint32_t { return cbar0 + 8 * static_cast<uint32_t>(NB * ew + b); };
+        uint32_t loads_odd = 0;   // bit b: an odd number of C_in loads issued into chunk b
         const uint32_t tempty_leader = ptx::mapa_rank(tempty0, pleader);
         const bool ldc = p.beta != 0.f;
         const uint32_t swz = lane * 128;
@@ -433,22 +448,22 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             if (lane == 0) {
                 ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
                 if (ldc && p.cin_prefetch) {              // C_in of this tile -> L2 during its mainloop
-                    for (int idx = 2; idx < kChunks; ++idx) ptx::tma_prefetch_2d(&tmCi, col_base + 32 * idx, row_base);
+                    for (int idx = NB; idx < kChunks; ++idx) ptx::tma_prefetch_2d(&tmCi, col_base + 32 * idx, row_base);
                 }
                 if (ldc) {
-                    for (int b = 0; b < 2; ++b) {
-                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
-                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], col_base + 32 * b, row_base);
+                    for (int b = 0; b < NB; ++b) {
+                        ptx::mbar_arrive_expect_tx(cbar(b), 4096);
+                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + 32 * b, row_base);
                     }
                 }
             }
-            if (ldc) ++loads[0], ++loads[1];
+            if (ldc) loads_odd ^= (1u << NB) - 1;
             __syncwarp();
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int idx = 0; idx < kChunks; ++idx) {
-                const int b = idx & 1;
+                const int b = idx % NB;
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx, r);
                 ptx::tmem_ld_wait();
@@ -458,14 +473,14 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                     if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
                 }
                 if (ldc) {
-                    ptx::mbar_wait(cbar[b], (loads[b] - 1) & 1);
-                } else if (idx >= 2) {
-                    if (lane == 0) ptx::bulk_wait_read<1>();
+                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
+                } else if (idx >= NB) {
+                    if (lane == 0) ptx::bulk_wait_read<NB - 1>();
                     __syncwarp();
                 }
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    const uint32_t a = buf[b] + swz + ((g ^ (lane & 7)) << 4);
+                    const uint32_t a = buf(b) + swz + ((g ^ (lane & 7)) << 4);
                     float4 o;
                     o.x = p.alpha * __uint_as_float(r[4 * g + 0]);
                     o.y = p.alpha * __uint_as_float(r[4 * g + 1]);
@@ -483,15 +498,15 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmCo, buf[b], col_base + 32 * idx, row_base);
+                    ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base);
                     ptx::bulk_commit();
-                    if (ldc && idx + 2 < kChunks) {
+                    if (ldc && idx + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
-                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
-                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], col_base + 32 * (idx + 2), row_base);
+                        ptx::mbar_arrive_expect_tx(cbar(b), 4096);
+                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + 32 * (idx + NB), row_base);
                     }
                 }
-                if (ldc && idx + 2 < kChunks) ++loads[b];
+                if (ldc && idx + NB < kChunks) loads_odd ^= 1u << b;
                 __syncwarp();
             }
         }

@@ -137,9 +137,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
 
     const int num_tiles = p.m_blocks * p.n_blocks;
     const uint32_t rempty_leader = ptx::leader_addr(rempty0);
+    // tile 0 of cluster cl is tile cl (no ring round trip, no atomic before the first loads);
+    // tile i >= 1 comes through ring index i - 1 from the global counter, offset by the clusters
+    const int cl = static_cast<int>(blockIdx.x >> 1), n_cl = static_cast<int>(gridDim.x >> 1);
     auto next_tile = [&](int i) -> int {  // whole-warp consumer of the tile ring
-        const int slot = i % kRingW;
-        ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingW) & 1);
+        if (i == 0) return cl;
+        const int slot = (i - 1) % kRingW;
+        ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - 1) / kRingW) & 1);
         const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(rempty_leader + 8 * slot);
@@ -152,16 +156,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             uint32_t phase = 0;
             for (int i = 0;; ++i) {
                 int t;
-                const int slot = i % kRingW;
-                if (leader) {
-                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, ((i / kRingW) & 1) ^ 1);
-                    t = atomicAdd(&p.sched[0], 1);
+                const int slot = (i - 1) % kRingW;
+                if (i == 0) {
+                    t = cl;
+                } else if (leader) {
+                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, (((i - 1) / kRingW) & 1) ^ 1);
+                    t = n_cl + atomicAdd(&p.sched[0], 1);
                     ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
                     ptx::st_shared_cluster_u32(peer_addr_w(ring0 + 4 * slot, 1), static_cast<uint32_t>(t));
                     ptx::mbar_arrive(rfull0 + 8 * slot);
                     ptx::mbar_arrive_cluster(peer_addr_w(rfull0 + 8 * slot, 1));
                 } else {
-                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, (i / kRingW) & 1);
+                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - 1) / kRingW) & 1);
                     t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
                     ptx::mbar_arrive_cluster(rempty_leader + 8 * slot);
                 }
@@ -267,9 +273,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, 16 chunks of 32 x 32
         const int q = warp & 3;
         const int ew = warp - 2;
-        const uint32_t buf[2] = {epi0 + (2 * ew) * 4096, epi0 + (2 * ew + 1) * 4096};
-        const uint32_t cbar[2] = {cbar0 + 16 * ew, cbar0 + 16 * ew + 8};
-        uint32_t loads[2] = {0, 0};                       // C_in loads issued per buffer (parity)
+        // staging chunk b of this warp and its C_in barrier (computed: no local-memory arrays)
+        auto buf = [&](int b) -> uint32_t { return epi0 + static_cast<uint32_t>(2 * ew + b) * 4096; };
+        auto cbar = [&](int b) -> uint32_t { return cbar0 + 16 * ew + 8 * b; };
+        uint32_t loads_odd = 0;                           // bit b: odd number of C_in loads into chunk b
         const uint32_t tempty_leader = ptx::leader_addr(tempty);
         const bool ldc = p.beta != 0.f;
         const uint32_t swz = lane * 128;                  // this thread's row in a chunk buffer
@@ -288,12 +295,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 }
                 if (ldc) {
                     for (int b = 0; b < 2; ++b) {
-                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
-                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], chunk_col(b), row_base);
+                        ptx::mbar_arrive_expect_tx(cbar(b), 4096);
+                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), chunk_col(b), row_base);
                     }
                 }
             }
-            if (ldc) ++loads[0], ++loads[1];              // warp-uniform phase bookkeeping
+            if (ldc) loads_odd ^= 3u;                     // warp-uniform phase bookkeeping
             __syncwarp();
             ptx::mbar_wait(tfull, local & 1);
             ptx::tc_fence_after();
@@ -310,14 +317,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                     if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * (idx >> 3));
                 }
                 if (ldc) {
-                    ptx::mbar_wait(cbar[b], (loads[b] - 1) & 1);
+                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
                 } else if (idx >= 2) {
                     if (lane == 0) ptx::bulk_wait_read<1>();   // store idx-2 has left buf[b]
                     __syncwarp();
                 }
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    const uint32_t a = buf[b] + swz + ((g ^ (lane & 7)) << 4);
+                    const uint32_t a = buf(b) + swz + ((g ^ (lane & 7)) << 4);
                     float4 o;
                     o.x = p.alpha * __uint_as_float(r[4 * g + 0]);
                     o.y = p.alpha * __uint_as_float(r[4 * g + 1]);
@@ -335,15 +342,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmCo, buf[b], chunk_col(idx), row_base);
+                    ptx::tma_store_2d(&tmCo, buf(b), chunk_col(idx), row_base);
                     ptx::bulk_commit();
                     if (ldc && idx + 2 < 16) {            // refill buf[b] with chunk idx+2 once it is read
                         ptx::bulk_wait_read<0>();
-                        ptx::mbar_arrive_expect_tx(cbar[b], 4096);
-                        ptx::tma_load_2d(buf[b], &tmCi, cbar[b], chunk_col(idx + 2), row_base);
+                        ptx::mbar_arrive_expect_tx(cbar(b), 4096);
+                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), chunk_col(idx + 2), row_base);
                     }
                 }
-                if (ldc && idx + 2 < 16) ++loads[b];
+                if (ldc && idx + 2 < 16) loads_odd ^= 1u << b;
                 __syncwarp();
             }
         }
