@@ -96,6 +96,27 @@ struct TcMParams {
     unsigned epoch;
 };
 
+#ifdef COMPAR_TRACE
+// Development-only phase stamps (tools/trace_pair.py builds a separate library with -DCOMPAR_TRACE):
+// clock64 at fixed points of CTAs 0 and 1, globaltimer at entry / exit.
+__device__ unsigned long long g_trace[2][16];
+#define TRACE(i)                                                                              \
+    do {                                                                                      \
+        if (blockIdx.x < 2) g_trace[blockIdx.x][i] = clock64();                               \
+    } while (0)
+#define TRACE_GT(i)                                                                           \
+    do {                                                                                      \
+        if (blockIdx.x < 2) {                                                                 \
+            unsigned long long t;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                           \
+            g_trace[blockIdx.x][i] = t;                                                       \
+        }                                                                                     \
+    } while (0)
+#else
+#define TRACE(i) ((void)0)
+#define TRACE_GT(i) ((void)0)
+#endif
+
 enum { kFull = 0, kHead = 1, kTail = 2, kSplit = 3 };
 struct Item {
     int tile, kb0, kb1, kind;
@@ -136,6 +157,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        TRACE_GT(10);
+        TRACE(0);
+    }
     const uint32_t rank = ptx::cluster_ctarank();   // 0..3
     const uint32_t pr = rank & 1;                    // rank inside the pair
     const uint32_t pair = rank >> 1;                 // 0: rows [0,256) of the tile, 1: [256,512)
@@ -172,6 +197,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TRACE(1);
 
     const int num_tiles = p.m_blocks * p.n_blocks;
     const int num_items = num_tiles * p.splits;                // dynamic mode: ring values are items
@@ -287,6 +313,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                         else
                             ptx::tma_load_2d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1);
                     }
+                    if (kstep == 0 && me == 0) TRACE(2);
                 }
             }
             if (rank == 0 && me == 0) {  // last cluster out re-arms the counters for the next launch on this stream
@@ -313,6 +340,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 const bool carry = it.kind == kTail;
                 for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     ptx::mbar_wait(full0 + 8 * stage, phase);
+                    if (local == 0 && lane == 0) TRACE(3);
                     ptx::tc_fence_after();
                     if (lane == 0) {
                         const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
@@ -338,6 +366,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                     }
                 }
                 if (lane == 0) ptx::tc_commit_2sm_mc(tfull0 + 8 * acc, pair_mask);
+                if (local == 0 && lane == 0) TRACE(4);
                 __syncwarp();
             }
         }
@@ -460,20 +489,21 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             if (ldc) loads_odd ^= (1u << NB) - 1;
             __syncwarp();
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+            if (local == 0 && warp == 2 && lane == 0) TRACE(5);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int idx = 0; idx < kChunks; ++idx) {
                 const int b = idx % NB;
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx, r);
-                ptx::tmem_ld_wait();
+                ptx::tmem_ld_wait(); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(12);
                 if (idx == kChunks - 1) {                 // accumulator drained: free it for tile + 2
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
                 }
                 if (ldc) {
-                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
+                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(13);
                 } else if (idx >= NB) {
                     if (lane == 0) ptx::bulk_wait_read<NB - 1>();
                     __syncwarp();
@@ -495,10 +525,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                     }
                     ptx::sts128(a, o);
                 }
-                ptx::fence_proxy_async_smem();
+                if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(9);
+                ptx::fence_proxy_async_smem(); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(14);
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base);
+                    ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(15);
                     ptx::bulk_commit();
                     if (ldc && idx + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
@@ -509,21 +540,33 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 if (ldc && idx + NB < kChunks) loads_odd ^= 1u << b;
                 __syncwarp();
             }
+            if (local == 0 && warp == 2 && lane == 0) TRACE(6);
         }
         if (p.sk) {  // a cluster without a HEAD item still advances its flag by one launch
             Item h;
             if (!(sk_item(0, h) && h.kind == kHead) && lane == 0) atomicAdd(p.flags + cl, 1u);
         }
         if (lane == 0) ptx::bulk_wait<0>();
+        if (warp == 2 && lane == 0) TRACE(7);
         __syncwarp();
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
+    if (threadIdx.x == 0) {
+        TRACE(8);
+        TRACE_GT(11);
+    }
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
     }
 }
+
+#ifdef COMPAR_TRACE
+int trace_read(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // Split-K epilogue: C_out = alpha * (P_0 + P_1 + ... + P_{S-1}) + beta * C_in, the planes summed in
 // split order; 4 consecutive columns per thread (16-byte C accesses: the variant requires TMA-style
@@ -712,3 +755,7 @@ cudaError_t preload_tcm_kernels() {
 }
 
 }  // namespace compar
+
+#ifdef COMPAR_TRACE
+extern "C" int compar_trace_read(unsigned long long *out) { return compar::trace_read(out); }
+#endif

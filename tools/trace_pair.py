@@ -1,0 +1,56 @@
+"""Phase stamps of the CTA-pair kernel (tc_gemm_2sm_mc) on small grids: where the fixed per-launch
+time goes.  Development aid.
+
+  python tools/trace_pair.py build          # (CPU) library with -DCOMPAR_TRACE -> build_trace/
+  python tools/trace_pair.py run M N K ...  # (GPU) stamps of CTAs 0 / 1, in SM cycles from entry
+
+Stamps: 0 entry, 1 init done (barriers, TMEM, cluster sync), 2 first TMA issued, 3 first stage
+landed (MMA warp), 4 tile 0 committed, 5 epilogue sees the accumulator, 6 tile 0 stored,
+7 stores drained, 8 exit sync; 10 / 11 globaltimer at entry / exit.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+TRACE_DIR = os.path.join(ROOT, "build_trace")
+
+if __name__ == "__main__" and sys.argv[1] == "build":
+    from paper_2311_03543_b200 import build as b
+    b.ARCH = b.ARCH + ["-DCOMPAR_TRACE"]
+    b.BUILD = os.path.join(TRACE_DIR, "obj")
+    b.LIB = os.path.join(TRACE_DIR, "libcompar.so")
+    print(b.build_compar(force=True))
+    sys.exit(0)
+
+os.environ["COMPAR_LIB"] = os.path.join(TRACE_DIR, "libcompar.so")
+import ctypes  # noqa: E402
+
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+from gen.device import device_matrix  # noqa: E402
+from paper_2311_03543_b200 import compar as cm  # noqa: E402
+
+lib = ctypes.CDLL(os.environ["COMPAR_LIB"])
+ctx = cm.Compar()
+names = [v for v, _ in ctx.variants()]
+args = [int(x) for x in sys.argv[2:]] or [256, 128, 64]
+for i in range(0, len(args), 3):
+    m, n, k = args[i:i + 3]
+    for beta in (0.5, 0.0):
+        A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
+        B = device_matrix(gen.TAG_B, k, n, dtype="bf16")
+        C = device_matrix(gen.TAG_C, m, n)
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=beta, in_dtype=cm.BF16,
+                         compute=cm.COMPUTE_BF16, variant_hint=names.index("tc_bf16_2sm"))
+        for _ in range(5):
+            rep = ctx.run(d)
+        buf = (ctypes.c_ulonglong * 32)()
+        assert lib.compar_trace_read(buf) == 0
+        for cta in (0, 1):
+            t = list(buf[cta * 16:(cta + 1) * 16])
+            st = " ".join(f"{j}:{t[j] - t[0]:6d}" for j in list(range(10)) + [12, 13, 14, 15])
+            print(f"{m}x{n}x{k} beta={beta} cta{cta}: {st} | wall {(t[11] - t[10]) / 1e3:.2f} us | event {rep.ns / 1e3:.2f} us",
+                  flush=True)
+ctx.terminate()
