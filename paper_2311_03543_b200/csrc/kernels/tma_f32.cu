@@ -37,14 +37,19 @@ __device__ __forceinline__ void ffma2(float &c0, float &c1, float a, float b0, f
     asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
 }
 
-// Tile TB x TB (128, or 64 for grids that would not fill the GPU: 4x the CTAs of a small problem,
-// each (TB/8)^2 consumer threads with the same 8 x 8 micro-tile and k order, so C is bitwise the
-// same for either tile), K-step BK = 32 (one 128-byte swizzle row), 4-stage TMA ring.
+// Tile TB x TB (128, or 64 for grids that would not fill the GPU: 4x the CTAs of a small problem),
+// K-step BK = 32 (one 128-byte swizzle row), 4-stage TMA ring.  Each consumer thread owns an 8-row x
+// MJ-column micro-tile: 8 x 8 for TB = 128 (256 threads), 8 x 4 for TB = 64 (128 threads: one warp
+// per SM sub-partition even when a small grid leaves one CTA per SM).  Every element accumulates its
+// k in the same order with the same FMA, so C is bitwise the same for either tile.
 constexpr int BK = 32, STAGES = 4;
 template <int TB>
 struct TmaCfg {
-    static constexpr int TY = TB / 8;                       // consumer threads per tile dimension
-    static constexpr int kConsumers = TY * TY;
+    static constexpr int MJ4 = TB == 128 ? 2 : 1;            // float4 column groups per thread
+    static constexpr int MJ = 4 * MJ4;                       // micro-tile columns
+    static constexpr int TY = TB / 8;                        // consumer threads along M
+    static constexpr int TX = TB / MJ;                       // consumer threads along N
+    static constexpr int kConsumers = TX * TY;
     static constexpr int kThreads = kConsumers + 32;
     static constexpr uint32_t A_BYTES = TB * BK * 4, B_BYTES = BK * TB * 4, STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 128;
@@ -69,7 +74,7 @@ template <bool kTransB, int TB>
 __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     tma_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TmaParams p) {
     using Cf = TmaCfg<TB>;
-    constexpr int BM = TB, BN = TB, TY = Cf::TY, kConsumers = Cf::kConsumers;
+    constexpr int BM = TB, BN = TB, TY = Cf::TY, TX = Cf::TX, MJ = Cf::MJ, MJ4 = Cf::MJ4, kConsumers = Cf::kConsumers;
     constexpr uint32_t A_BYTES = Cf::A_BYTES, STAGE_BYTES = Cf::STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -109,12 +114,12 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     }
 
     // ---------------- consumer warps
-    const int tx = tid % TY, ty = tid / TY;
-    float acc[8][8];
+    const int tx = tid % TX, ty = tid / TX;
+    float acc[8][MJ];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < MJ; ++j) acc[i][j] = 0.f;
 
     for (int kb = 0; kb < p.num_kb; ++kb) {
         const int s = kb % STAGES;
@@ -128,8 +133,8 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
             for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + TY * i, k4));
             if (kTransB) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float4 b = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + TY * j, k4));
+                for (int j = 0; j < MJ; ++j) {
+                    const float4 b = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + TX * j, k4));
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
@@ -142,14 +147,17 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     const float *brow = reinterpret_cast<const float *>(sb + (k4 * 4 + kk) * (BN * 4));
-                    const float4 b0 = *reinterpret_cast<const float4 *>(brow + tx * 4);
-                    const float4 b1 = *reinterpret_cast<const float4 *>(brow + BN / 2 + tx * 4);
-                    const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    float b[MJ];
+#pragma unroll
+                    for (int h = 0; h < MJ4; ++h) {
+                        const float4 bh = *reinterpret_cast<const float4 *>(brow + h * (BN / MJ4) + tx * 4);
+                        b[4 * h + 0] = bh.x, b[4 * h + 1] = bh.y, b[4 * h + 2] = bh.z, b[4 * h + 3] = bh.w;
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
 #pragma unroll
-                        for (int j = 0; j < 8; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
+                        for (int j = 0; j < MJ; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
                     }
                 }
             }
@@ -159,10 +167,10 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     }
 
     // ---------------- epilogue
-    // C_in is gathered for the whole 8 x 8 micro-tile before the first store: C_in may alias C_out,
-    // so the compiler cannot hoist a load above an earlier store, and load/store pairs issued in
-    // turn would serialise 16 (or 64) memory round trips.
-    float ci[8][8];
+    // C_in is gathered for the whole micro-tile before the first store: C_in may alias C_out, so
+    // the compiler cannot hoist a load above an earlier store, and load/store pairs issued in turn
+    // would serialise 8 * MJ4 (or 8 * MJ) memory round trips.
+    float ci[8][MJ];
     const bool has_cin = p.beta != 0.f;
     if (has_cin) {
 #pragma unroll
@@ -171,14 +179,14 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
             const float *cin = p.C_in + r * p.ldc_in;
             if (kTransB) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int64_t c = n0 + tx + TY * j;
+                for (int j = 0; j < MJ; ++j) {
+                    const int64_t c = n0 + tx + TX * j;
                     ci[i][j] = r < p.m && c < p.n ? cin[c] : 0.f;
                 }
             } else {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int64_t c = n0 + h * (BN / 2) + tx * 4;
+                for (int h = 0; h < MJ4; ++h) {
+                    const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
                     if (r < p.m && p.cvec && c + 3 < p.n) {
                         const float4 v = *reinterpret_cast<const float4 *>(cin + c);
                         ci[i][h * 4 + 0] = v.x, ci[i][h * 4 + 1] = v.y, ci[i][h * 4 + 2] = v.z, ci[i][h * 4 + 3] = v.w;
@@ -197,8 +205,8 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
         float *crow = p.C_out + r * p.ldc_out;
         if (kTransB) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int64_t c = n0 + tx + TY * j;
+            for (int j = 0; j < MJ; ++j) {
+                const int64_t c = n0 + tx + TX * j;
                 if (c < p.n) {
                     float o = p.alpha * acc[i][j];
                     if (has_cin) o = fmaf(p.beta, ci[i][j], o);
@@ -207,8 +215,8 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
             }
         } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t c = n0 + h * (BN / 2) + tx * 4;
+            for (int h = 0; h < MJ4; ++h) {
+                const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
                 float o[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -256,13 +264,14 @@ cudaError_t launch_t(const GemmLaunch &g) {
 
 cudaError_t launch_tma_f32(const GemmLaunch &g) {
     if ((g.m + 127) / 128 > 65535) return cudaErrorInvalidValue;
-    // 64 x 64 tiles when 128 x 128 tiles would fill at most a quarter of the SMs (measured: 256^3
-    // 36 -> 27 us, 512^3 58 -> 40 us; at 1024^3+ the 128 tile's 8 consumer warps per CTA win).
+    // 64 x 64 tiles (8 x 4 micro-tiles, 128 consumer threads) when 128 x 128 tiles would fill at
+    // most three quarters of the SMs (measured: 768^3 81.5 -> 37.1 us, 1024^3 105 -> 72 us,
+    // 1280^3 130 -> 120 us; from 1536^3 (144 tiles) the 128 tile's 8 x 8 micro-tiles win).
     // COMPAR_TMA_TILE=128 / 64 forces one.
     const int64_t tiles128 = ((g.m + 127) / 128) * ((g.n + 127) / 128);
     const char *e = std::getenv("COMPAR_TMA_TILE");
     const int force = e ? std::atoi(e) : 0;
-    const bool small = force == 64 || (force != 128 && 4 * tiles128 <= g.num_sms);
+    const bool small = force == 64 || (force != 128 && 4 * tiles128 <= 3 * static_cast<int64_t>(g.num_sms));
     if (small) return g.transB ? launch_t<true, 64>(g) : launch_t<false, 64>(g);
     return g.transB ? launch_t<true, 128>(g) : launch_t<false, 128>(g);
 }
