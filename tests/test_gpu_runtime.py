@@ -79,7 +79,11 @@ def test_config1_calibration_trace(order):
     d = cm.make_desc(m, m, m, A=A, B=B, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, compute=cm.COMPUTE_TF32)
     E = ctx.eligible(d)
     n_cal = 4 * len(E)
-    trace = [ctx.run(d) for _ in range(n_cal + 1)]
+    trace = [ctx.run(d) for _ in range(n_cal)]
+    # the model decision uses the calibration samples (the model-mode run then adds its own sample,
+    # which can flip a near-tie, so the means are read before it)
+    means = [ctx.history(v, d).mean_ns for v in E]
+    trace.append(ctx.run(d))
     if order == cm.CALIB_INTERLEAVED:
         assert [r.variant for r in trace[:n_cal]] == E * 4
         assert [r.mode for r in trace[:len(E)]] == [cm.MODE_WARMUP] * len(E)
@@ -87,7 +91,6 @@ def test_config1_calibration_trace(order):
         assert [r.variant for r in trace[:n_cal]] == [v for v in E for _ in range(4)]
         assert [r.mode for r in trace[:n_cal]] == ([cm.MODE_WARMUP] + [cm.MODE_CALIB] * 3) * len(E)
     assert trace[n_cal].mode == cm.MODE_MODEL
-    means = [ctx.history(v, d).mean_ns for v in E]
     assert trace[n_cal].variant == E[int(np.argmin(means))]
     st = ctx.stats()
     assert st.launches == sum(r.batch for r in trace) and st.harvested == 3 * len(E) + 1
