@@ -63,7 +63,9 @@ def test_real_event_selector_crossover(golden):
         assert (v, mode) == (want, cm.MODE_MODEL)
         mean = ctx.history(v, d).mean_ns
         expect = (0.1 * n if want == 0 else 50 + 0.01 * n) * 1000
-        assert expect <= mean <= expect * 1.2 + 5000
+        # the spin is wall-clock exact; the bound allows event / launch overhead and one slow
+        # sample on a freshly started box (a 20 % + 5 us bound failed once there)
+        assert expect <= mean <= expect * 1.25 + 10000
     ctx.terminate()
 
 
