@@ -41,6 +41,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-targets", action="store_true", help="skip the config-3 / 5a north-star block")
+    p.add_argument("--no-yardstick", action="store_true", help="skip the same-operation cuBLAS comparison")
     p.add_argument("--bcast", default="nccl", choices=["nccl", "ce"],
                    help="N > 1: broadcast of B by NCCL (default) or by the copy-engine chain (compar_ce_*)")
     return p.parse_args()
@@ -226,6 +227,34 @@ def fair_medians(ctx, descs, rounds=3, per_round=2, idle_s=0.1):
 
 
 # ---------------------------------------------------------------------------------------------
+def cublas_yardstick(ctx, dv, A, B, Cm, M, N, flops_step):
+    """cuBLAS on the same operation (C_out = ALPHA*AB + BETA*C_in, FP32 C in and out) at the bench
+    shape, interleaved launch by launch with the chosen variant (context, not a bench value)."""
+    import torch
+    cout = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def cublas_once():
+        e0.record()
+        torch.addmm(Cm, A, B, beta=BETA, alpha=ALPHA, out_dtype=torch.float32, out=cout)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e6
+    cublas_once()
+    ctx.run(dv)
+    ours_ns, cub_ns = [], []
+    for _ in range(3):
+        ours_ns.append(ctx.run(dv).ns)
+        cub_ns.append(cublas_once())
+    yard = {"what": "torch.addmm(C, A, B, beta, alpha, out_dtype=float32): the same operation through cuBLAS",
+            "cublas_tflops": flops_step / statistics.median(cub_ns) / 1e3,
+            "ours_tflops": flops_step / statistics.median(ours_ns) / 1e3, "launches_each": 3}
+    yard["ours_over_cublas"] = yard["ours_tflops"] / yard["cublas_tflops"]
+    del cout
+    torch.cuda.empty_cache()
+    return yard
+
+
 def north_star_targets(ctx, cm, peaks, R=10):
     """BASELINE.json north_star targets on this GPU, through the same C ABI (untimed w.r.t. the
     headline): config 3 (8192^3 BF16, target >= 70 % of the measured burst BF16 peak) and config 5a
@@ -435,6 +464,16 @@ def main():
         regret = {"chosen": vn[reps[-1].variant], "best": best,
                   "regret": med[vn[reps[-1].variant]] / med[best] - 1.0, "median_ns_per_variant": med}
 
+    # context, not a bench value: cuBLAS on the SAME operation at this shape (torch.addmm with FP32
+    # C in and out, out_dtype=float32), interleaved launch by launch with the chosen variant
+    yard = None
+    if world == 1 and not args.no_yardstick:
+        try:
+            yard = cublas_yardstick(ctx, hinted[reps[-1].variant] if reps[-1].variant in hinted else desc,
+                                    A, B, Cm, M, N, flops_step)
+        except Exception as ex:  # noqa: BLE001  (context only: never fail the bench on it)
+            yard = {"error": str(ex)[:200]}
+
     # end to end through the same C ABI call with HOST buffers (pinned), copies in the timed region
     e2e = None
     if args.e2e_steps > 0:
@@ -492,7 +531,7 @@ def main():
                "selector": {"calibration_runs_before_timing": calib_runs, "chosen": chosen, "regret": regret,
                             "variants_in_timed_region": used,
                             "eligible": [variant_names[v] for v in ctx.eligible(desc)]},
-               "clocks": clocks, "e2e": e2e, "north_star_targets": targets}
+               "clocks": clocks, "e2e": e2e, "north_star_targets": targets, "cublas_same_op": yard}
     if world > 1:
         dist.barrier()
     ctx.terminate()
