@@ -9,6 +9,9 @@ key, select, partition, broadcast, tcgen05 kernel, events) + compar_sync (harves
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--size S]
 
+--gpus N > 1 without torchrun re-executes itself under torch.distributed.run with N ranks; under
+torchrun, WORLD_SIZE must equal N.
+
 value = total FLOPs of all ranks / max-over-ranks device time (CUDA events on the launch
 stream); inputs (2 GiB + 2 GiB + 4 GiB) are larger than L2, so no flush is needed.
 """
@@ -45,6 +48,29 @@ def parse():
     p.add_argument("--bcast", default="nccl", choices=["nccl", "ce"],
                    help="N > 1: broadcast of B by NCCL (default) or by the copy-engine chain (compar_ce_*)")
     return p.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec this script as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) and exit with its code,
+    so the driver's plain command form measures N GPUs.  NCCL's INIT log lines (communicator
+    size per rank) go to stderr."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def dist_env():
@@ -134,6 +160,7 @@ def reference_arm(args, rank, world):
 
     import gen
     from oracle import gemm as og
+    og.set_threads(len(os.sched_getaffinity(0)))   # torchrun exports OMP_NUM_THREADS=1
     M = N = K = args.size
     r = c = 512
     rows = np.linspace(0, M - 1, r).astype(np.int64)
@@ -166,6 +193,7 @@ def cpu_baseline(size):
 
     import gen
     from oracle import gemm as og
+    og.set_threads(len(os.sched_getaffinity(0)))
     K = size
     r = 256
     for _ in range(3):
@@ -255,13 +283,30 @@ def cublas_yardstick(ctx, dv, A, B, Cm, M, N, flops_step):
     return yard
 
 
+def alu_peak_tflops(peaks):
+    """FP32 FFMA ceiling: SMs x 128 FFMA/clk x 2 FLOP x the max SM clock."""
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return sms * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+
+
+# (key, m, n, k, storage, compute class) of the BASELINE.json north-star targets timed after the
+# headline: config 3 in BF16 (target >= 70 % of the burst BF16 peak), config 5a (HBM-bound), and
+# the paper's own arithmetic with FP32 storage (P:78 "float arrays", P:202 SGEMM): TF32 tensor
+# cores at the headline 32768^3 shape and strict FP32 (FFMA variants only) at 8192^3.
+TARGETS = (("config3_8192cube_bf16", 8192, 8192, 8192, "bf16", "bf16"),
+           ("config5a_65536x256x4096_bf16", 65536, 256, 4096, "bf16", "bf16"),
+           ("config4_32768cube_tf32_fp32_storage", 32768, 32768, 32768, "f32", "tf32"),
+           ("config3_8192cube_f32_strict", 8192, 8192, 8192, "f32", "f32"))
+
+
 def north_star_targets(ctx, cm, peaks, R=10):
     """BASELINE.json north_star targets on this GPU, through the same C ABI (untimed w.r.t. the
-    headline): config 3 (8192^3 BF16, target >= 70 % of the measured burst BF16 peak) and config 5a
-    (65536x256x4096 BF16, HBM-bound: % of the measured copy bandwidth).  Each shape: selector trained
-    on the key (calibration), R model-mode runs after an idle gap; then regret = chosen / best - 1
-    over an exhaustive timing of every eligible tensor-core variant under fair_medians (FFMA
-    variants: history mean)."""
+    headline).  Each shape: selector trained on the key (calibration), R model-mode runs after an
+    idle gap; then regret = chosen / best - 1 over an exhaustive timing of every eligible variant
+    of the key's fastest class under fair_medians (the others: their calibration mean).
+    Roofline fractions: BF16 against the measured burst BF16 peak, TF32 against half of it (the
+    guide's nominal TF32:BF16 ratio), FP32 against the FFMA ALU ceiling, bytes against HBM."""
     import statistics
 
     import torch
@@ -270,50 +315,71 @@ def north_star_targets(ctx, cm, peaks, R=10):
     from gen.device import device_matrix
     names = [n for n, _ in ctx.variants()]
     out = {}
-    for key, (m, n, k) in (("config3_8192cube_bf16", (8192, 8192, 8192)),
-                           ("config5a_65536x256x4096_bf16", (65536, 256, 4096))):
-        A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
-        B = device_matrix(gen.TAG_B, k, n, dtype="bf16")
+    alu = alu_peak_tflops(peaks)
+    for key, m, n, k, sdt, cls in TARGETS:
+        A = device_matrix(gen.TAG_A, m, k, dtype=sdt)
+        B = device_matrix(gen.TAG_B, k, n, dtype=sdt)
         C = device_matrix(gen.TAG_C, m, n)
+        compute = {"bf16": cm.COMPUTE_BF16, "tf32": cm.COMPUTE_TF32, "f32": cm.COMPUTE_F32_STRICT}[cls]
+        in_dtype = cm.BF16 if sdt == "bf16" else cm.F32
 
         def mk(hint=-1):
-            return cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=ALPHA, beta=BETA, in_dtype=cm.BF16,
-                                compute=cm.COMPUTE_BF16, variant_hint=hint)
+            return cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=ALPHA, beta=BETA, in_dtype=in_dtype,
+                                compute=compute, variant_hint=hint)
         d = mk()
         calib = 0
+        t_cal = time.perf_counter()
         while ctx.select(d)[1] != cm.MODE_MODEL and calib < 64:
             ctx.run(d)
             calib += 1
+        t_cal = time.perf_counter() - t_cal
         torch.cuda.synchronize()
         time.sleep(0.5)                      # same starting power state for every target
-        sel = [ctx.run(d) for _ in range(R)]
+        reps = R if m * n * k <= 8192 ** 3 else max(3, R // 2)
+        sel = [ctx.run(d) for _ in range(reps)]
         chosen = sel[-1].variant
         E = ctx.eligible(d)
-        tc = [v for v in E if names[v].startswith("tc_")]
-        fm = fair_medians(ctx, {v: mk(v) for v in tc}, rounds=3, per_round=3)
-        med = {names[v]: fm[v] for v in tc}
+        fast = [v for v in E if names[v].startswith("tc_")] or list(E)
+        fm = fair_medians(ctx, {v: mk(v) for v in fast}, rounds=3, per_round=2 if m * n * k > 8192 ** 3 else 3)
+        med = {names[v]: fm[v] for v in fast}
         for v in E:
-            if v not in tc:
+            if v not in fast:
                 med[names[v]] = ctx.history(v, d).mean_ns
         best = min(med, key=med.get)
         t_sel = statistics.median(r.ns for r in sel)
         flops = 2.0 * m * n * k
-        nbytes = 2 * (m * k + k * n) + 4 * m * n * 2
-        out[key] = {"variant": names[chosen], "ms": t_sel / 1e6, "tflops": flops / t_sel / 1e3,
-                    "frac_of_bf16_burst_peak": flops / t_sel / 1e3 / peaks["bf16_tflops"],
+        eb = 2 if sdt == "bf16" else 4
+        nbytes = eb * (m * k + k * n) + 4 * m * n * 2
+        tflops = flops / t_sel / 1e3
+        peak = {"bf16": peaks["bf16_tflops"], "tf32": peaks["bf16_tflops"] / 2.0, "f32": alu}[cls]
+        out[key] = {"variant": names[chosen], "ms": t_sel / 1e6, "tflops": tflops,
+                    "peak_tflops": peak, "frac_of_peak": tflops / peak,
+                    "peak_kind": {"bf16": "measured burst BF16 (MEASURED_PEAKS.bf16_tflops)",
+                                  "tf32": "half the measured burst BF16 peak (nominal TF32 = BF16 / 2)",
+                                  "f32": "FFMA ceiling: SMs x 128 x 2 x sm_max_mhz"}[cls],
                     "hbm_gbs": nbytes / t_sel, "frac_of_hbm_peak": nbytes / t_sel / peaks["hbm_gbs"],
                     "best_variant": best, "regret": med[names[chosen]] / med[best] - 1.0,
-                    "median_ns_per_variant": med, "calibration_runs": calib}
+                    "median_ns_per_variant": med, "calibration_runs": calib, "calibration_s": t_cal}
+        if cls == "bf16":
+            out[key]["frac_of_bf16_burst_peak"] = tflops / peaks["bf16_tflops"]
+        if cls == "tf32":
+            out[key]["frac_of_tf32_sustained"] = tflops / (peaks.get("bf16_tflops_sustained", peak * 2) / 2.0)
+        if cls == "f32":
+            out[key]["fp32_alu_peak_tflops"] = alu
         del A, B, C
         torch.cuda.empty_cache()
-    out["selector_regret_max"] = max(v["regret"] for v in out.values())
+    out["selector_regret_max"] = max(v["regret"] for v in out.values() if isinstance(v, dict))
     return out
 
 
 # ---------------------------------------------------------------------------------------------
 def main():
     args = parse()
+    self_launch(args)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU"}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
@@ -328,6 +394,13 @@ def main():
     # the N > 1 path (with --bcast ce) runs end to end on a one-GPU box; never a performance number
     shared = os.environ.get("COMPAR_BENCH_SHARED_GPU") == "1"
     coll_dev = "cpu" if shared else "cuda"
+    if not shared and torch.cuda.device_count() < world:
+        print(json.dumps({"error": f"{world} ranks but {torch.cuda.device_count()} visible GPU(s)"}), flush=True)
+        sys.exit(2)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator size per rank (INIT lines)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     torch.cuda.set_device(0 if shared else local)
     if world > 1:
         if shared:

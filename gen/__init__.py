@@ -7,7 +7,8 @@ one importing the other (DESIGN.md §"Input recipe").
 
 * `gen.inputs`   — the canonical host (numpy) generator.
 * `gen/gen.cu`   — the device twin (libcompar_gen.so), which must match the host
-                   generator bit for bit (checked by tests/test_gpu_gen.py).
+                   generator bit for bit (checked by
+                   tests/test_gpu_runtime.py::test_device_generator_matches_host_bitwise).
 """
 from .inputs import (  # noqa: F401
     DIST_U, DIST_P, DIST_I, TAG_A, TAG_B, TAG_C, SEED_DATA, SEED_STREAM,

@@ -4,7 +4,8 @@
  * Not part of the GEMM method: it only materialises the synthetic inputs of SURVEY.md §8(d)
  * ("Inputs") on the GPU so that full-size workloads (e.g. 32768^3) need no host->device copy
  * of generated data.  It implements the same counter-based recipe as the canonical host
- * generator gen/inputs.py and must match it bit for bit (tests/test_gpu_gen.py):
+ * generator gen/inputs.py and must match it bit for bit
+ * (tests/test_gpu_runtime.py::test_device_generator_matches_host_bitwise):
  *
  *     h = splitmix64(seed ^ (tag << 56) ^ (i << 28) ^ j)        (i, j) = LOGICAL row, column
  *     U = ((h >> 40) - 2^23) * 2^-23,  P = (h >> 40) * 2^-24,  I = h mod 5 - 2

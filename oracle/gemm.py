@@ -91,6 +91,51 @@ def set_threads(n: int) -> None:
     _load().compar_oracle_set_threads(int(n))
 
 
+U_F32 = 2.0 ** -24       # unit roundoff of FP32 round-to-nearest
+DELTA_TF32 = 2.0 ** -10  # relative error of truncating an FP32 value to TF32 (10 explicit mantissa bits)
+
+
+def elementwise_bound(A, B, C_in=None, alpha: float = 1.0, beta: float = 0.0, dtype: str = "f32",
+                      tf32: bool = False, c: float = 2.0) -> np.ndarray:
+    """Componentwise forward-error bound of C_out = alpha*A@B + beta*C_in computed with FP32
+    accumulation in ANY summation order (the classical dot-product bound |fl(x.y) - x.y| <=
+    gamma_K |x|.|y|, gamma_K ~ K*u; Higham, Accuracy and Stability of Numerical Algorithms §3.1):
+
+        |C - C_exact| <= |alpha| * (e_op + c*K*u) * (1 + e_op + c*K*u) * (|A| @ |B|)
+                         + 2u * (|alpha| * (1 + ...) * (|A| @ |B|) + |beta| * |C_in|)
+
+    u = 2^-24.  Products of the consumed operands are exact in FP32 (FP32 x FP32 in an FMA, BF16 x
+    BF16 and TF32 x TF32 fit 24 bits), so the operand term e_op is 0 except for TF32, whose
+    hardware truncation of each operand (R6) perturbs every product by at most
+    e_op = 2*2^-10 + 2^-20 relative.  c >= 1 widens K*u for accumulators that are not round-to-
+    nearest (tensor-core block sums truncate after alignment); c = 2 by default.  The trailing 2u
+    terms are the two roundings of the alpha/beta epilogue.  Returns the FP64 bound array.
+    |A| @ |B| is this module's own FP64 GEMM of the absolute values."""
+    A64, B64 = np.abs(widen(A, dtype)), np.abs(widen(B, dtype))
+    K = A64.shape[1]
+    e_op = (2.0 * DELTA_TF32 + DELTA_TF32 ** 2) if tf32 else 0.0
+    acc = e_op + c * K * U_F32
+    absab = gemm(A64.astype(np.float64), B64.astype(np.float64)) if K > 0 else np.zeros((A64.shape[0], B64.shape[1]))
+    grow = abs(alpha) * (1.0 + acc) * absab
+    bound = abs(alpha) * acc * (1.0 + acc) * absab + 2.0 * U_F32 * grow
+    if beta != 0.0:
+        bound = bound + 2.0 * U_F32 * abs(beta) * np.abs(np.asarray(C_in, dtype=np.float64))
+    return bound
+
+
+def elementwise_violation(c_test, c_ref, bound) -> float:
+    """max_ij |C - C_ref| / bound_ij (<= 1 means every element is inside its bound; a zero bound
+    requires an exact match)."""
+    diff = np.abs(np.asarray(c_test, dtype=np.float64) - np.asarray(c_ref, dtype=np.float64))
+    bound = np.asarray(bound, dtype=np.float64)
+    if diff.size == 0:
+        return 0.0
+    exact = bound == 0.0
+    if np.any(diff[exact] != 0.0) or not np.all(np.isfinite(diff)):
+        return float("inf")
+    return float(np.max(np.where(exact, 0.0, diff / np.where(exact, 1.0, bound))))
+
+
 def rel_fro(c_test, c_ref) -> float:
     """max-relative-Frobenius metric of BASELINE.json: ||C - C_ref||_F / ||C_ref||_F (FP64).
 

@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from gen.device import device_matrix  # noqa: E402
 from oracle import gemm as og  # noqa: E402
+from tests._gpu_util import assert_parity  # noqa: E402
 
 cm = pytest.importorskip("paper_2311_03543_b200.compar")
 
@@ -67,9 +68,10 @@ def test_loopback_slab_pipeline_bitwise(loop_ctx, chunks, name, m, n, k, tb):
     assert torch.equal(outs[0], outs[1])
     if chunks == 4:   # and the pipeline result matches the oracle
         got = outs[1].double().numpy()
-        ref = og.gemm(gen.matrix(gen.TAG_A, m, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt),
-                      gen.matrix(gen.TAG_C, m, n), alpha=1.5, beta=0.5, dtype=dt)
-        assert og.rel_fro(got, ref) <= (1e-5 if name == "simt_f32" else 5e-3)
+        Ah, Bh, Ch = gen.matrix(gen.TAG_A, m, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt), gen.matrix(gen.TAG_C, m, n)
+        ref = og.gemm(Ah, Bh, Ch, alpha=1.5, beta=0.5, dtype=dt)
+        tf32 = name.startswith("tc_tf32")
+        assert_parity(got, ref, Ah, Bh, Ch, 1.5, 0.5, dt, tf32, 5e-3 if tf32 else 1e-5, name)
 
 
 @pytest.mark.parametrize("tb", [0, 1])
@@ -120,4 +122,4 @@ def test_loopback_world_host_memory(loop_ctx):
                      compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST, world=1)
     ctx.run(d)
     ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5, dtype="bf16")
-    assert og.rel_fro(Ch.double().numpy(), ref) <= 5e-3
+    assert_parity(Ch.double().numpy(), ref, A, B, C0, 1.5, 0.5, "bf16", False, 1e-5, "world host")

@@ -154,3 +154,76 @@ def test_rel_fro_metric():
     assert og.rel_fro(np.zeros(3), np.zeros(3)) == 0.0
     assert og.rel_fro(np.ones(3), np.zeros(3)) == float("inf")
     assert og.rel_fro([3.0, 4.0], [0.0, 5.0]) == pytest.approx(np.sqrt(10.0) / 5.0)
+
+
+def _fp32_sequential(A, B, C0, alpha, beta, tf32=False):
+    """Independent simulation of an FP32 kernel: operands optionally truncated to TF32 (low 13
+    mantissa bits cleared), every k-step one FMA acc = fl32(acc + a*b) (the product of two FP32
+    values is exact in FP64), epilogue fl32(fl32(alpha*acc) + fl32(beta*c))."""
+    def trunc(x):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        return (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32) if tf32 else x
+    a, b = trunc(A).astype(np.float64), trunc(B).astype(np.float64)
+    acc = np.zeros((a.shape[0], b.shape[1]), dtype=np.float32)
+    for k in range(a.shape[1]):
+        acc = (acc.astype(np.float64) + np.outer(a[:, k], b[k, :])).astype(np.float32)
+    out = (np.float32(alpha) * acc).astype(np.float32)
+    if beta != 0.0:
+        out = (out.astype(np.float64) + (np.float32(beta) * C0.astype(np.float32)).astype(np.float64)).astype(np.float32)
+    return out.astype(np.float64)
+
+
+@pytest.mark.parametrize("dist", [gen.DIST_U, gen.DIST_P])
+def test_elementwise_bound_holds_for_fp32_accumulation(dist):
+    """Error bound (Higham §3.1 dot-product bound, oracle/gemm.elementwise_bound): a simulated FP32
+    sequential-FMA GEMM stays inside the componentwise bound at c = 1 (round-to-nearest), with the
+    P distribution (all terms positive: the bound's worst case for bias)."""
+    M, N, K = 12, 10, 2048
+    A = gen.matrix(1, M, K, dist, "f32", seed=21)
+    B = gen.matrix(2, K, N, dist, "f32", seed=21)
+    C0 = gen.matrix(3, M, N, dist, "f32", seed=21)
+    sim = _fp32_sequential(A, B, C0, 1.5, 0.5)
+    ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5)
+    v = og.elementwise_violation(sim, ref, og.elementwise_bound(A, B, C0, 1.5, 0.5, c=1.0))
+    assert 0.0 < v <= 1.0
+
+
+def test_elementwise_bound_tf32_operand_term():
+    """TF32 truncation (R6): the simulated TF32 GEMM is inside the bound only WITH the operand term
+    e_op = 2*2^-10 + 2^-20 (catches a dropped e_op)."""
+    M, N, K = 8, 9, 256
+    A = gen.matrix(1, M, K, gen.DIST_P, "f32", seed=4)
+    B = gen.matrix(2, K, N, gen.DIST_P, "f32", seed=4)
+    sim = _fp32_sequential(A, B, None, 1.0, 0.0, tf32=True)
+    ref = og.gemm(A, B)
+    assert og.elementwise_violation(sim, ref, og.elementwise_bound(A, B, tf32=True, c=1.0)) <= 1.0
+    assert og.elementwise_violation(sim, ref, og.elementwise_bound(A, B, tf32=False, c=1.0)) > 1.0
+
+
+def test_elementwise_bound_catches_dropped_term_and_wrong_element():
+    """A plausible kernel bug — one k-term dropped from one element, or one garbage element —
+    fails the componentwise check although the Frobenius ratio of the whole matrix stays small."""
+    M, N, K = 64, 64, 512
+    A = gen.matrix(1, M, K, gen.DIST_U, "f32", seed=8)
+    B = gen.matrix(2, K, N, gen.DIST_U, "f32", seed=8)
+    ref = og.gemm(A, B)
+    bound = og.elementwise_bound(A, B)
+    bad = ref.copy()
+    big = int(np.argmax(np.abs(A[5].astype(np.float64) * B[:, 7].astype(np.float64))))
+    bad[5, 7] -= float(A[5, big]) * float(B[big, 7])       # dropped k-term
+    assert og.elementwise_violation(bad, ref, bound) > 1.0
+    bad2 = ref.copy()
+    bad2[10, 3] = 0.0                                         # one unwritten element
+    assert og.elementwise_violation(bad2, ref, bound) > 1.0
+    assert og.rel_fro(bad2, ref) < 0.05
+    assert og.elementwise_violation(ref, ref, bound) == 0.0
+
+
+def test_elementwise_bound_k_zero_and_exact_zero():
+    """K = 0: C = beta*C_in, the bound is the epilogue rounding only; a zero bound demands exactness."""
+    C0 = _u(3, 4, 5)
+    b = og.elementwise_bound(np.zeros((4, 0), np.float32), np.zeros((0, 5), np.float32), C0, 1.5, -2.0)
+    np.testing.assert_allclose(b, 2.0 ** -23 * 2.0 * np.abs(C0.astype(np.float64)))
+    z = np.zeros((2, 2))
+    assert og.elementwise_violation(z, z, z) == 0.0
+    assert og.elementwise_violation(z + 1e-30, z, z) == float("inf")
