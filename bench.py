@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--no-yardstick", action="store_true", help="skip the same-operation cuBLAS comparison")
     p.add_argument("--bcast", default="nccl", choices=["nccl", "ce"],
                    help="N > 1: broadcast of B by NCCL (default) or by the copy-engine chain (compar_ce_*)")
+    p.add_argument("--variant", default=None, help="testing: force this variant (no selector)")
+    p.add_argument("--dump-c", default=None, help="testing: after the run, recompute one step from fresh inputs "
+                                                 "and save this rank's C panel to DIR/c_r<rank>.npy")
     return p.parse_args()
 
 
@@ -442,9 +445,10 @@ def main():
     if rank == 0:
         fill(B.data_ptr(), "bf16", K, N, N, gen.TAG_B, stream=sp)
     torch.cuda.synchronize()
+    hint = [v for v, _ in ctx.variants()].index(args.variant) if args.variant else -1
     desc = cm.make_desc(M, N, K, A=A, B=B if rank == 0 else None, C_in=Cm, C_out=Cm, lda=K, ldb=N, ldc_in=N,
                         ldc_out=N, alpha=ALPHA, beta=BETA, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, stream=sp,
-                        world=1 if world > 1 else 0, B_replica=B if rank != 0 else None)
+                        world=1 if world > 1 else 0, B_replica=B if rank != 0 else None, variant_hint=hint)
 
     def barrier():
         torch.cuda.synchronize()
@@ -474,7 +478,7 @@ def main():
     # calibration for this key (W warm-up + K timed samples per eligible variant), as a StarPU
     # application does before its measured runs; then the W warm-up steps of the contract.
     calib_runs = 0
-    while ctx.select(desc)[1] != cm.MODE_MODEL and calib_runs < 64:
+    while hint < 0 and ctx.select(desc)[1] != cm.MODE_MODEL and calib_runs < 64:
         ctx.run(desc)
         calib_runs += 1
     for _ in range(args.warmup):
@@ -577,6 +581,25 @@ def main():
         del Cm
         torch.cuda.empty_cache()
         targets = north_star_targets(ctx, cm, load_peaks()[0])
+
+    if args.dump_c:    # testing: one fresh step, this rank's C panel saved (bitwise comparison across N)
+        import numpy as np
+        Cd = torch.empty((max(mloc, 1), N), dtype=torch.float32, device="cuda")
+        Ad = torch.empty((max(mloc, 1), K), dtype=torch.bfloat16, device="cuda")
+        if mloc > 0:
+            fill(Ad.data_ptr(), "bf16", mloc, K, K, gen.TAG_A, row0=r0, stream=sp)
+            fill(Cd.data_ptr(), "f32", mloc, N, N, gen.TAG_C, row0=r0, stream=sp)
+        if rank == 0:
+            fill(B.data_ptr(), "bf16", K, N, N, gen.TAG_B, stream=sp)
+        torch.cuda.synchronize()
+        dd = cm.make_desc(M, N, K, A=Ad, B=B if rank == 0 else None, C_in=Cd, C_out=Cd, lda=K, ldb=N, ldc_in=N,
+                          ldc_out=N, alpha=ALPHA, beta=BETA, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, stream=sp,
+                          world=1 if world > 1 else 0, B_replica=B if rank != 0 else None,
+                          variant_hint=reps[-1].variant)
+        ctx.run(dd)
+        os.makedirs(args.dump_c, exist_ok=True)
+        np.save(os.path.join(args.dump_c, f"c_r{rank}.npy"), Cd[:mloc].cpu().numpy())
+        del Cd, Ad
 
     out = None
     if rank == 0:

@@ -134,6 +134,20 @@ typedef struct {
                                    mode samples of lanes > 1 are not added to the history (they
                                    overlap other lanes) and calibration executions run alone.
                                    <1: COMPAR_LANES or 1                                           */
+    int calib_prune;            /* calibration pruning threshold in percent (R32): a variant
+                                   stops calibrating for a key once its mean, or its static lower
+                                   bound (FLOPs at its class's nominal peak, compulsory bytes at
+                                   nominal HBM bandwidth), exceeds calib_prune/100 x the key's best
+                                   mean; blocked calibration visits variants by increasing lower
+                                   bound.  0: off.  <0: COMPAR_CALIB_PRUNE or 300 */
+    int bcast_ctas;             /* world mode, NCCL broadcast: the communicator's maxCTAs (NCCL
+                                   config), and the SMs a GEMM overlapping a broadcast leaves free.
+                                   <0: COMPAR_BCAST_CTAS or 4                                        */
+    int sync_timeout_ms;        /* world-mode waits (compar_sync on a task with a collective) poll
+                                   ncclCommGetAsyncError; an NCCL error, or no completion within this
+                                   many ms, aborts the communicator: E_NCCL, and every later world
+                                   task fails with E_NCCL (sticky).  0: no timeout.
+                                   <0: COMPAR_SYNC_TIMEOUT_MS or 600000                              */
 } compar_config;
 
 enum { COMPAR_WORLD_LOCAL = 0, COMPAR_WORLD_PANELS = 1, COMPAR_WORLD_TASKS = 2 };
@@ -164,8 +178,11 @@ typedef struct {
     int world;                  /* 1: SPMD row-panel split across the ranks of compar_comm_init.
                                    A and C_* then point at THIS rank's panel (rows
                                    [o_r, o_{r+1}) of compar_partition_rows(m, nranks)), B is read
-                                   on rank 0 and broadcast with NCCL (in bcast_chunks N-slabs,
-                                   overlapped with the slab GEMMs) to the other ranks.  Without a
+                                   on rank 0, packed into contiguous N-slabs (geometric widths: a
+                                   small first slab, doubling) and broadcast with NCCL to the other
+                                   ranks; a receiver's GEMM consumes slab j as soon as it landed
+                                   (one persistent launch that waits per slab on device flags, or
+                                   one launch per slab).  Without a
                                    communicator world = 1 is a 1-rank world.  Combines with HOST.
                                    2 (COMPAR_WORLD_TASKS): task-parallel world:
                                    the WHOLE task runs on one worker = (rank, lane) chosen by the
@@ -179,7 +196,9 @@ typedef struct {
                                    ranks, same order).  Device memory only.                     */
     void *B_replica;            /* world mode, rank != 0: device workspace of >= k*n elements that
                                    receives B (its layout afterwards is the library's slab layout,
-                                   unspecified to the caller); NULL: a library-owned buffer       */
+                                   unspecified to the caller); NULL: a library-owned buffer.  (When
+                                   the packed layout needs more than k*n elements — a row pitch that
+                                   TMA cannot use — the library uses its own buffer instead.)     */
     int variant_hint;           /* -1: run the selector; >= 0: force that registry index          */
     uint64_t handles[4];        /* task-parallel world: caller ids of the A, B, C_in, C_out data
                                    (StarPU-style data handles, R21); a non-zero id makes
@@ -318,10 +337,15 @@ compar_status compar_sort_submit(void *ctx, const compar_sort_desc *d, uint64_t 
 /* Blocks until the task's stop event(s); harvests its sample into the history; fills *out
  * (may be NULL).  task == COMPAR_TASK_ALL syncs every outstanding task (out gets the last).
  * A failed variant -> E_TASK_FAILED (status also in out).  After return the library holds no
- * reference to the task's buffers. */
+ * reference to the task's buffers.  A task the selector already harvested implicitly (step 6,
+ * before a decision) keeps its report until this call returns it (same status, same report).
+ * World-mode tasks: the wait polls NCCL's asynchronous error state (see sync_timeout_ms). */
 compar_status compar_sync(void *ctx, uint64_t task, compar_report *out);
-/* Pure query: the (variant, mode) the next submit of d would get.  No launch, no history change
- * (it may harvest completed pending samples, which does not change any decision). */
+/* Query: the (variant, mode) the next submit of d would get.  No launch, no history change.  Like
+ * a submit it may first harvest (block on) pending LOCAL samples of the key — their reports stay
+ * available to compar_sync — but it never harvests tasks whose harvest is collective (world
+ * tasks on several ranks), so it is safe to call on one rank; with such tasks pending, the answer
+ * reflects the samples harvested so far. */
 compar_status compar_select(void *ctx, const compar_gemm_desc *d, int *variant, int *mode);
 
 /* ---- performance model persistence ("additional training") ---- */

@@ -13,7 +13,8 @@ runtime/dmda.cpp); it is written from the scheduling rule it implements:
 * DESIGN.md readings R20-R23: workers are (rank, lane) pairs w = rank * lanes + lane; ready[w] is
   the predicted end of the last task placed on w (reset by a full sync); exec = the variant's
   measured mean for the key (integer division of the integer sums), else 0; a task that reads a
-  range last written on rank r may only run on rank r (no inter-rank transfer: cost infinite);
+  range whose bytes were last written on rank r may only run on rank r (no inter-rank transfer:
+  cost infinite), and a range whose bytes were last written on two ranks cannot be read at all;
   RAW / WAR / WAW on the same rank delay the start to the earlier task's predicted end; with
   lanes > 1, model-mode executions are not samples.
 
@@ -34,13 +35,14 @@ class DmdaOracle:
     nranks: int = 1
     lanes: int = 1
     blocked: bool = True
+    prune_pct: int = 300       # the runtime's default (R32)
     sel: SelectorOracle = None
     ready: list = field(default_factory=list)
     live: list = field(default_factory=list)      # (task, w, end, span, write)
     pending: list = field(default_factory=list)   # (task, v, key, mode, warm, ns, history)
 
     def __post_init__(self):
-        self.sel = SelectorOracle(self.n_variants, blocked=self.blocked)
+        self.sel = SelectorOracle(self.n_variants, blocked=self.blocked, prune_pct=self.prune_pct)
         self.reset_workers()
 
     def reset_workers(self):
@@ -63,23 +65,25 @@ class DmdaOracle:
         self.pending = keep
 
     def _calibrating(self, key, eligible):
-        need = self.sel.calib_warmup + self.sel.calib_k
-        return min(self.sel.rec(v, key).seen for v in eligible) < need
+        return self.sel.calibrating(key, eligible)
 
     # ---- placement (SPEC S:330 with the R20-R23 readings)
     def place(self, reads, writes, exec_ns):
+        # Residency (R22): every byte of a read span lives on the rank of ITS latest writer.  Cut
+        # the span at every writer boundary into elementary intervals; each interval's latest
+        # overlapping writer names its rank; all ranks met must agree, else nowhere may read it.
         pin = None
         for s in reads:
-            latest = None
-            for (task, w, end, span, write) in self.live:
-                if write and _overlap(s, span) and (latest is None or task > latest[0]):
-                    latest = (task, w)
-            if latest is None:
-                continue
-            r = self.rank_of(latest[1])
-            if pin is not None and pin != r:
-                return None
-            pin = r
+            writers = [(task, w, span) for (task, w, end, span, write) in self.live if write and _overlap(s, span)]
+            cuts = sorted({s[0], s[1]} | {x for (_, _, sp) in writers for x in sp if s[0] < x < s[1]})
+            for lo, hi in zip(cuts, cuts[1:]):
+                over = [(task, w) for (task, w, sp) in writers if _overlap((lo, hi), sp)]
+                if not over:
+                    continue
+                r = self.rank_of(max(over)[1])
+                if pin is not None and pin != r:
+                    return None
+                pin = r
         best = None
         for w in range(self.nranks * self.lanes):
             if pin is not None and self.rank_of(w) != pin:
@@ -99,7 +103,9 @@ class DmdaOracle:
 
     def submit(self, task, key, eligible, reads, writes, cost):
         """One task: returns (variant, mode, worker) or None (no worker may run it)."""
-        if not self._calibrating(key, eligible):
+        # step 6 (and R32: pruning reads the key's best mean, so with pruning on every decision
+        # harvests the key's pending samples first)
+        if self.prune_pct > 0 or not self._calibrating(key, eligible):
             self._harvest(lambda p: p[2] == key)
         v, mode = self.sel.decide(key, eligible)
         r = self.sel.rec(v, key)

@@ -69,28 +69,61 @@ class SelectorOracle:
     calib_k: int = 3           # K_cal
     eager: bool = False
     blocked: bool = False      # calibration order (R19); False = SPEC S:369 interleaving
+    prune_pct: int = 300       # DESIGN.md R32 calibration pruning threshold (percent, the runtime default); 0 = SPEC
     hist: dict = field(default_factory=dict)   # (v, key) -> Record
 
     def rec(self, v: int, key) -> Record:
         return self.hist.setdefault((v, key), Record())
 
-    def decide(self, key, eligible):
+    # ---- R32: calibration pruning.  Written from the rule: let best = the smallest measured mean
+    # over the eligible variants of the key; a variant is done calibrating once its own mean, or its
+    # static lower bound lb (ns), exceeds prune_pct / 100 x best.
+    def best_mean(self, key, eligible):
+        """(sum, count) of the smallest mean, or None if no eligible variant has a sample."""
+        best = None
+        for v in eligible:
+            r = self.rec(v, key)
+            if r.count and (best is None or r.sum_ns * best[1] < best[0] * r.count):
+                best = (r.sum_ns, r.count)
+        return best
+
+    def pruned(self, key, eligible, t, lb=None):
+        if self.prune_pct <= 0:
+            return False
+        best = self.best_mean(key, eligible)
+        if best is None:
+            return False
+        bs, bc = best
+        r = self.rec(eligible[t], key)
+        if r.count and 100 * r.sum_ns * bc > self.prune_pct * bs * r.count:
+            return True
+        lv = lb[t] if lb else 0.0
+        return lv > 0.0 and lv * 100.0 * float(bc) > float(self.prune_pct) * float(bs)
+
+    def calibrating(self, key, eligible, lb=None):
+        need = self.calib_warmup + self.calib_k
+        return any(self.rec(v, key).seen < need and not self.pruned(key, eligible, t, lb)
+                   for t, v in enumerate(eligible))
+
+    def decide(self, key, eligible, lb=None):
         """Steps 3-5 and 7: return (variant, mode) for the next execution of `key`.
 
-        `eligible` is the ordered list E of eligible variant indices (step 1).
-        Assumes all pending samples have been harvested when model mode is
-        reached (step 6 is the caller's blocking harvest)."""
+        `eligible` is the ordered list E of eligible variant indices (step 1); `lb` the static
+        lower bounds (ns) in the same order (R32), None = none.  Assumes all pending samples have
+        been harvested when model mode is reached (step 6 is the caller's blocking harvest)."""
         if not eligible:
             raise LookupError("E_NO_VARIANT")
         if self.eager:
             return eligible[0], MODE_EAGER
         need = self.calib_warmup + self.calib_k
         seen = [self.rec(v, key).seen for v in eligible]
-        if min(seen) < need:                                   # step 4: calibration
-            if self.blocked:   # R19: finish one variant's W + K executions before the next
-                best = next(t for t in range(len(eligible)) if seen[t] < need)
+        cand = [t for t in range(len(eligible)) if seen[t] < need and not self.pruned(key, eligible, t, lb)]
+        if cand:                                               # step 4: calibration
+            if self.blocked:   # R19 / R32: finish one variant's W + K executions before the next,
+                # visiting variants by increasing lower bound (ties: eligibility order)
+                best = min(cand, key=lambda t: ((lb[t] if lb else 0.0), t))
             else:
-                best = min(range(len(eligible)), key=lambda t: (seen[t], eligible[t]))
+                best = min(cand, key=lambda t: (seen[t], eligible[t]))
             v = eligible[best]
             return v, (MODE_WARMUP if seen[best] < self.calib_warmup else MODE_CALIB)
         best_v = None                                           # step 5: model
@@ -174,24 +207,58 @@ class SelectorOracle:
             return None
         return float(np.array(self.features(key)) @ best[1])
 
-    def unknown_predict(self, key, eligible):
-        """Variants with neither samples for `key` nor a fitted prediction; in predict mode only
-        these are calibrated when decide_predict returns None (all of E when nothing is known)."""
-        return [v for v in eligible if self.rec(v, key).count == 0 and self.predict(v, key) is None]
-
-    def decide_predict(self, key, eligible):
-        """Measured mean where (v, key) has samples, else the fitted prediction; None if some
-        eligible variant has neither (the caller then calibrates)."""
-        best = None
+    def _estimates(self, key, eligible):
+        """Per eligible variant: (estimate ns, predicted?) or None — measured mean, else the fit."""
+        out = []
         for v in eligible:
             r = self.rec(v, key)
             if r.count > 0:
-                est, pred = r.sum_ns / r.count, False
+                out.append((r.sum_ns / r.count, False))
             else:
-                est = self.predict(v, key)
-                pred = True
-                if est is None:
-                    return None
-            if best is None or est < best[1]:
-                best = (v, est, pred)
+                p = self.predict(v, key)
+                out.append(None if p is None else (p, True))
+        return out
+
+    def _lb_skipped(self, est, t, lb):
+        """R32 in predict mode: a variant with no estimate whose lower bound exceeds prune_pct/100
+        x the best known estimate is not calibrated."""
+        known = [e[0] for e in est if e is not None]
+        lv = lb[t] if lb else 0.0
+        return bool(known) and self.prune_pct > 0 and lv > 0.0 and lv * 100.0 > float(self.prune_pct) * min(known)
+
+    def unknown_predict(self, key, eligible, lb=None):
+        """Variants with neither samples for `key` nor a fitted prediction (nor skipped by their
+        lower bound); in predict mode only these are calibrated when decide_predict returns None."""
+        est = self._estimates(key, eligible)
+        return [v for t, v in enumerate(eligible) if est[t] is None and not self._lb_skipped(est, t, lb)]
+
+    def decide_predict(self, key, eligible, lb=None):
+        """Measured mean where (v, key) has samples, else the fitted prediction; None if some
+        eligible variant has neither (the caller then calibrates) and is not skipped by R32."""
+        est = self._estimates(key, eligible)
+        best = None
+        for t, v in enumerate(eligible):
+            if est[t] is None:
+                if self._lb_skipped(est, t, lb):
+                    continue
+                return None
+            if best is None or est[t][0] < best[1]:
+                best = (v, est[t][0], est[t][1])
+        if best is None:
+            return None
         return best[0], (MODE_PREDICT if best[2] else MODE_MODEL)
+
+    # ---- R32 static lower bound of a built-in GEMM variant (mirrors the runtime's class peaks,
+    # restated): FLOPs at the nominal peak of its class, compulsory bytes at nominal 8 TB/s.
+    @staticmethod
+    def static_lb_ns(cls, key, sms=148):
+        """cls: 'ffma' | 'bf16' | 'tf32' | None (USER: no bound)."""
+        if cls is None:
+            return 0.0
+        peak = {"ffma": float(sms) * 128.0 * 2.0 * 1.965e9, "bf16": 2.25e15, "tf32": 1.125e15}[cls]
+        m, n, k, dtype, _c, _t, beta0 = key
+        m, n, k = float(m), float(n), float(k)
+        flops = 2.0 * m * n * k
+        eb = 2.0 if dtype == BF16 else 4.0
+        nbytes = eb * (m * k + k * n) + 4.0 * m * n * (1.0 if beta0 else 2.0)
+        return max(flops / peak, nbytes / 8.0e12) * 1e9

@@ -45,7 +45,8 @@ class Config(C.Structure):
     _fields_ = [("ngpu", C.c_int), ("device", C.c_int), ("sched", C.c_int), ("calib_k", C.c_int),
                 ("calib_warmup", C.c_int), ("perf_model_path", C.c_char_p), ("bcast_chunks", C.c_int),
                 ("builtins", C.c_int), ("virtual_clock", C.c_int), ("variant_mask", C.c_int64),
-                ("calib_order", C.c_int), ("lanes", C.c_int)]
+                ("calib_order", C.c_int), ("lanes", C.c_int), ("calib_prune", C.c_int), ("bcast_ctas", C.c_int),
+                ("sync_timeout_ms", C.c_int)]
 
 
 class GemmDesc(C.Structure):
@@ -232,7 +233,8 @@ class Compar:
     """One runtime context (compar_init ... compar_terminate)."""
 
     def __init__(self, ngpu=-1, device=-1, sched=-1, calib_k=-1, calib_warmup=-1, perf_model_path=None,
-                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1, calib_order=-1, lanes=-1):
+                 bcast_chunks=-1, builtins=-1, virtual_clock=0, variant_mask=-1, calib_order=-1, lanes=-1,
+                 calib_prune=-1, bcast_ctas=-1, sync_timeout_ms=-1):
         cfg = Config()
         lib.compar_config_default(C.byref(cfg))
         cfg.ngpu, cfg.device, cfg.sched = ngpu, device, sched
@@ -243,6 +245,7 @@ class Compar:
         cfg.variant_mask = variant_mask
         cfg.calib_order = calib_order
         cfg.lanes = lanes
+        cfg.calib_prune, cfg.bcast_ctas, cfg.sync_timeout_ms = calib_prune, bcast_ctas, sync_timeout_ms
         self.ctx = C.c_void_p()
         self._callbacks = []     # keep ctypes thunks alive
         _check(lib.compar_init(C.byref(cfg), C.byref(self.ctx)))

@@ -6,6 +6,41 @@
 
 namespace compar {
 
+// Launcher tuning knobs, read once per runtime context from the environment (read_knobs) and
+// passed with every launch — nothing reads the environment on the launch path.  0 = the launcher's
+// own choice.  They only change tile widths / raster order / schedule, never any element's k order.
+struct Knobs {
+    int tc1_bn = 0;          // COMPAR_TC1_BN: 1-SM tile width 256 / 128 / 64
+    int tc1_group = 0;       // COMPAR_TC1_GROUP: 1-SM raster band (row blocks)
+    int tc2_bn = 0;          // COMPAR_TC2_BN: pair tile width 256 / 128
+    int tc2_group = 0;       // COMPAR_TCM_GROUP: pair raster band (cluster tiles)
+    int tc2_rowstore_group = 0;   // COMPAR_TC_GROUP: raster band of the row-store pair kernel
+    int tc2_producers = 2;   // COMPAR_TC2_PRODUCERS: TMA producer warps per CTA in the pair kernel (1 or 2)
+    int tcw_group = 0;       // COMPAR_TCW_GROUP: wide-pair raster band (pair rows)
+    int tcw_delay = 24;      // COMPAR_TCW_DELAY: wide-pair epilogue-overlap delay in k-steps
+    int tma_tile = 0;        // COMPAR_TMA_TILE: tma_f32 tile 128 / 64
+};
+Knobs read_knobs();
+
+// World-mode (row panels + broadcast of B) extras of a wide-pair launch (tc_gemm_2sm_wide.cu):
+//   * slab wait (flags != nullptr): B arrives as nslab contiguous slabs of slab_w columns (packed:
+//     slab j is a K x slab_w row-major block; transB: rows [j slab_w, (j+1) slab_w) of B^T); before
+//     loading the B tiles of slab j a producer waits until flags[j] >= seq (written on the comm
+//     stream after slab j landed), and tiles are visited column-major so slab j's tiles come first;
+//   * split launch (helper_sms > 0): the main launch runs on num_sms - helper_sms SMs (the rest
+//     are left to the broadcast's kernels); once `helper_after` (the broadcast's end) has fired, a
+//     helper launch on helper_stream adds helper_sms SMs, drawing tiles from the same counter; the
+//     launch's stream then waits for `helper_done` (recorded after the helper).
+struct WorldLaunch {
+    const unsigned *flags = nullptr;
+    unsigned seq = 0;
+    int slab_w = 0, nslab = 0;
+    int helper_sms = 0;
+    cudaStream_t helper_stream = nullptr;
+    cudaEvent_t helper_after = nullptr, helper_done = nullptr;
+    mutable int launches = 0;    // out: kernel launches issued (1, or 2 with the helper)
+};
+
 // One variant launch over a row panel: C_out = alpha * A * B + beta * C_in
 // (PAPER.md P:76-80, P:201-205 read as xGEMM; R1-R3).
 struct GemmLaunch {
@@ -18,7 +53,14 @@ struct GemmLaunch {
     float *C_out; int64_t ldc_out;
     cudaStream_t stream;
     int num_sms;               // SMs of the device (persistent grids)
+    const Knobs *knobs = nullptr;        // nullptr: defaults
+    const WorldLaunch *world = nullptr;  // wide-pair kernel only
 };
+
+inline const Knobs &knobs_of(const GemmLaunch &g) {
+    static const Knobs defaults;
+    return g.knobs ? *g.knobs : defaults;
+}
 
 cudaError_t launch_simt_f32(const GemmLaunch &g);            // variant (a)
 cudaError_t launch_simt_bf16(const GemmLaunch &g);           // variant (a), BF16 operands
@@ -33,20 +75,13 @@ cudaError_t launch_tma_f32(const GemmLaunch &g);             // variant (b)
 cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16);  // variant (c): tcgen05 TF32 / BF16
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16);  // variant (c), CTA-pair (cta_group::2)
 cudaError_t launch_tc_gemm_2sm_wide(const GemmLaunch &g, bool bf16);  // variant (c), wide CTA-pair 256x512
-// variant (c), CTA-pair kernel with TMA C epilogue (tc_gemm_2sm_mc.cu): `pairs` = 1 (cluster of 2) or
-// 2 (cluster of 4, B shared by TMA multicast); needs TMA-compatible C.  Reached through launch_tc_gemm_2sm.
-cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16, int pairs);
+// variant (c), CTA-pair kernel with TMA C epilogue (tc_gemm_2sm_mc.cu); needs TMA-compatible C.
+// Reached through launch_tc_gemm_2sm.
+cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16);
 cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha == 0: C_out = beta*C_in
 cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
 cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)
 int *sched_workspace(cudaStream_t s);                        // {next, done} tile counters for persistent kernels
-struct SkWorkspace {                                         // stream-K partials (tc_gemm_2sm_mc.cu)
-    unsigned *flags = nullptr;
-    float *partial = nullptr;
-    int cap = 0;
-    uint32_t epoch = 0;
-};
-SkWorkspace *sk_workspace(cudaStream_t s, int clusters);
 // Split-K partial planes of the tc_*_sk variant (grown on demand, per stream).
 struct SplitWorkspace {
     float *part = nullptr;

@@ -259,6 +259,20 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap 
         "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// 3-D form (world-mode slab-packed B: {column in slab, k, slab}).
+__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap *m, uint32_t leader_bar, int32_t c0,
+                                                int32_t c1, int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// Data written by other agents (copy engine, NCCL kernels) and observed through an acquire load
+// is then read by TMA (the async proxy): order the two proxies.
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 // shared::cluster address of the same smem offset in cluster CTA `rank`.
 __device__ __forceinline__ uint32_t mapa_rank(uint32_t local, uint32_t rank) {
     uint32_t r;

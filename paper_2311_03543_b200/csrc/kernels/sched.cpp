@@ -8,12 +8,32 @@
 // launches on one stream are ordered, so one pair per stream is enough.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
 #include "kernels.h"
 
 namespace compar {
+
+Knobs read_knobs() {
+    auto get = [](const char *name, int dflt) {
+        const char *v = std::getenv(name);
+        return (v && *v) ? std::atoi(v) : dflt;
+    };
+    Knobs k;
+    k.tc1_bn = get("COMPAR_TC1_BN", 0);
+    k.tc1_group = get("COMPAR_TC1_GROUP", 0);
+    k.tc2_bn = get("COMPAR_TC2_BN", 0);
+    k.tc2_group = get("COMPAR_TCM_GROUP", 0);
+    k.tc2_rowstore_group = get("COMPAR_TC_GROUP", 0);
+    k.tc2_producers = get("COMPAR_TC2_PRODUCERS", 2) == 1 ? 1 : 2;
+    k.tcw_group = get("COMPAR_TCW_GROUP", 0);
+    k.tcw_delay = get("COMPAR_TCW_DELAY", 24);
+    if (k.tcw_delay < 0) k.tcw_delay = 0;
+    k.tma_tile = get("COMPAR_TMA_TILE", 0);
+    return k;
+}
 
 int *sched_workspace(cudaStream_t s) {
     static std::mutex mu;
@@ -26,27 +46,6 @@ int *sched_workspace(cudaStream_t s) {
     if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
     slots.emplace(s, p);
     return p;
-}
-
-// Stream-K workspace (tc_gemm_2sm_mc.cu): per cluster one flag word and one 256 x 256 FP32
-// partial accumulator; `epoch` counts the stream-K launches on this stream, so flags never need
-// resetting (a flag reaches 8 * epoch when that launch's partial is published).
-SkWorkspace *sk_workspace(cudaStream_t s, int clusters) {
-    static std::mutex mu;
-    static std::map<cudaStream_t, SkWorkspace> slots;
-    std::lock_guard<std::mutex> lk(mu);
-    SkWorkspace &w = slots[s];
-    if (w.cap < clusters) {
-        if (w.flags) cudaFree(w.flags);
-        if (w.partial) cudaFree(w.partial);
-        w = SkWorkspace{};
-        const int cap = clusters < 128 ? 128 : clusters;
-        if (cudaMalloc(&w.flags, cap * sizeof(unsigned)) != cudaSuccess) return nullptr;
-        if (cudaMemset(w.flags, 0, cap * sizeof(unsigned)) != cudaSuccess) return nullptr;
-        if (cudaMalloc(&w.partial, static_cast<size_t>(cap) * 256 * 256 * sizeof(float)) != cudaSuccess) return nullptr;
-        w.cap = cap;
-    }
-    return &w;
 }
 
 SplitWorkspace *split_workspace(cudaStream_t s, size_t part_bytes, size_t count_words) {

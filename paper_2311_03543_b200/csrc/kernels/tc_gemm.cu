@@ -21,7 +21,6 @@
 // Edges: TMA zero-fills out-of-bounds boxes; the epilogue predicates rows/cols.
 #include <cuda.h>
 
-#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -74,7 +73,6 @@ struct TcParams {
     int cvec;
     int *sched;  // {next, done}: zero on entry, re-zeroed by the last CTA
     int group_m;
-    int serp;    // 1: alternate the K direction between consecutive waves (L2 reuse at wave seams)
 };
 
 __device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
@@ -158,9 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t >= num_tiles) break;
                 int mb, nb;
                 tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
-                const bool rev = p.serp && ((t / static_cast<int>(gridDim.x)) & 1);
-                for (int it = 0; it < p.num_kb; ++it) {
-                    const int kb = rev ? p.num_kb - 1 - it : it;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
                     ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
@@ -331,16 +327,7 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
-    static const int group_env = [] {
-        const char *s = std::getenv("COMPAR_TC1_GROUP");
-        return s ? std::atoi(s) : 0;
-    }();
-    static const int serp_env = [] {
-        const char *s = std::getenv("COMPAR_TC_SERP");
-        return s ? std::atoi(s) : 0;
-    }();
-    p.group_m = group_env > 0 ? group_env : kGroupM;
-    p.serp = serp_env;
+    p.group_m = knobs_of(g).tc1_group > 0 ? knobs_of(g).tc1_group : kGroupM;
     const int tiles = p.m_blocks * p.n_blocks;
     const int grid = tiles < g.num_sms ? tiles : g.num_sms;
     tc_gemm_kernel<kBF16, kTransB, kBN><<<grid, kThreads, C::SMEM, g.stream>>>(ta, tb, p);
@@ -353,10 +340,9 @@ cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16) {
     // Tile width: 128 x 256 unless that leaves many SMs idle — then 128 x 128 or 128 x 64 (N = 128
     // / 64 MMAs), whichever first gives at least half as many tiles as SMs: latency-bound small
     // and mid-size problems get up to 4x the CTAs.  Every element keeps its k order, so C is
-    // bitwise the same for any width.  COMPAR_TC1_BN=256 / 128 / 64 forces one.
+    // bitwise the same for any width.  COMPAR_TC1_BN=256 / 128 / 64 (Knobs) forces one.
     const int64_t mb = (g.m + 127) / 128;
-    const char *e = std::getenv("COMPAR_TC1_BN");
-    int bn = e ? std::atoi(e) : 0;
+    int bn = knobs_of(g).tc1_bn;
     if (bn != 256 && bn != 128 && bn != 64) {
         bn = 64;
         for (int w : {256, 128}) {

@@ -21,7 +21,6 @@
 // Tiles come from a global atomic counter drawn by the leader's producer (see sched.cpp).
 #include <cuda.h>
 
-#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -338,11 +337,7 @@ cudaError_t launch_tc2_t(const GemmLaunch &g) {
     p.m_blocks = static_cast<int>((g.m + 2 * C::BM - 1) / (2 * C::BM));
     p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
-    static const int group_env = [] {
-        const char *s = std::getenv("COMPAR_TC_GROUP");
-        return s ? std::atoi(s) : 0;
-    }();
-    p.group_m = group_env != 0 ? group_env : kGroupM2;
+    p.group_m = knobs_of(g).tc2_rowstore_group != 0 ? knobs_of(g).tc2_rowstore_group : kGroupM2;
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     p.sched = sched_workspace(g.stream);
@@ -358,15 +353,9 @@ cudaError_t launch_tc2_t(const GemmLaunch &g) {
 
 cudaError_t launch_tc_gemm_2sm(const GemmLaunch &g, bool bf16) {
     // C movable by TMA (16-byte aligned, ldc * 4 % 16 == 0): the TMA-epilogue form of the same
-    // pair tile (tc_gemm_2sm_mc.cu; 134 vs 164 us on config 5a).  COMPAR_TC2_PAIRS=2 selects its
-    // cluster-of-4 B-multicast form (measured, not faster: DESIGN.md §5).  Otherwise: row stores.
-    static const int pairs = [] {
-        const char *s = std::getenv("COMPAR_TC2_PAIRS");
-        return s ? std::atoi(s) : 1;
-    }();
-    if (pairs > 0 && tma_compatible(g.C_out, g.ldc_out, 4) &&
-        (g.beta == 0.f || tma_compatible(g.C_in, g.ldc_in, 4)))
-        return launch_tc_gemm_pairs(g, bf16, pairs);
+    // pair tile (tc_gemm_2sm_mc.cu; 134 vs 164 us on config 5a).  Otherwise: row stores.
+    if (tma_compatible(g.C_out, g.ldc_out, 4) && (g.beta == 0.f || tma_compatible(g.C_in, g.ldc_in, 4)))
+        return launch_tc_gemm_pairs(g, bf16);
     if (bf16) return g.transB ? launch_tc2_t<true, true>(g) : launch_tc2_t<true, false>(g);
     return g.transB ? launch_tc2_t<false, true>(g) : launch_tc2_t<false, false>(g);
 }

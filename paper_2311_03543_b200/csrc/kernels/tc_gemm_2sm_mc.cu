@@ -1,33 +1,26 @@
-// Variant (c), multicast CTA-pair form "tc_*_2sm_mc": two tcgen05 CTA pairs share B through
-// TMA multicast (cluster of 4 CTAs) for sm_100a.
+// Variant (c), CTA-pair form "tc_*_2sm" with a TMA epilogue (and its split-K form "tc_*_sk") for
+// sm_100a.
 //
-// Same math as tc_gemm.cu / tc_gemm_2sm.cu (C_out = alpha*A*B + beta*C_in, BF16 / TF32 in, FP32
-// TMEM accumulation; R1-R6).  A cluster of four CTAs = two CTA pairs stacked along M
-// owns a 512 x 256 output tile; pair p (CTAs 2p, 2p+1) computes rows [256 p, 256 p + 256) with
-// one tcgen05.mma.cta_group::2 M=256 N=256 per UMMA_K slice, exactly as tc_gemm_2sm.cu.  The two
-// pairs need the same B tile, so CTA r of pair p loads only half of its 128-column B slice and
-// multicasts it to CTA r of both pairs: per SM the L2 -> SMEM traffic per FLOP is that of the
-// wide 256 x 512 pair tile (tc_gemm_2sm_wide.cu), while each CTA's accumulator stays 128 x 256
-// (256 TMEM columns), so two accumulators alternate and tile i's epilogue overlaps tile i+1's
-// MMAs (the wide kernel's 512-column accumulator cannot).  Epilogue as in the wide
-// kernel: TMA load of C_in two chunks ahead, alpha*acc + beta*C_in in registers, swizzled smem
-// staging, TMA store of C_out.
+// Same math as tc_gemm.cu (C_out = alpha*A*B + beta*C_in, BF16 / TF32 in, FP32 TMEM accumulation;
+// DESIGN.md R1-R6).  A cluster of two CTAs owns a 256 x BN output tile (BN = 256, or 128 for grids
+// that would leave CTA pairs idle): one tcgen05.mma.cta_group::2 M=256 N=BN per UMMA_K slice, each
+// CTA holding 128 A rows and BN/2 B columns.  Each CTA's accumulator is 128 x BN (BN TMEM columns),
+// so two accumulators alternate and tile i's epilogue overlaps tile i+1's MMAs (the wide kernel's
+// 512-column accumulator cannot).  Epilogue as in the wide kernel: TMA load of C_in
+// ahead, alpha*acc + beta*C_in in registers, swizzled smem staging, TMA store of C_out.
 //
-// Synchronisation (all mbarriers at identical smem offsets in every CTA):
-//   full[s]   pair leaders; count 1 (leader arrive.expect_tx of both pair CTAs' bytes); the pair's
-//             A loads and the B multicasts of both pairs complete_tx on the destination's pair
-//             leader barrier;
-//   empty[s]  every CTA; count 2: both pair leaders' tcgen05.commit multicast to all four CTAs
-//             (a B slot is rewritten by the other pair's multicast, so it must be free in both);
-//   tfull[a]  every CTA; the pair leader's commit multicast to its pair;
-//   tempty[a] pair leaders; count 8 = 4 epilogue warps x 2 CTAs of the pair;
+// Synchronisation (mbarriers at identical smem offsets in both CTAs):
+//   full[s]   leader; count 1 (leader arrive.expect_tx of both CTAs' bytes);
+//   empty[s]  both CTAs; the leader's tcgen05.commit multicast;
+//   tfull[a]  both CTAs; the leader's commit multicast;
+//   tempty[a] leader; count 8 = 4 epilogue warps x 2 CTAs;
 //   rfull/rempty  the tile ring: CTA 0's producer draws tile ids from the global counter
-//             (sched.cpp) and publishes them to all four CTAs over DSMEM;
+//             (sched.cpp) and publishes them to both CTAs over DSMEM;
 //   cbar[w][b] C_in chunk landed (epilogue warp w, buffer b).
+// (A cluster-of-4 form sharing B by TMA multicast and a stream-K schedule were measured in round 1,
+// not faster — DESIGN.md §5 — and removed.)
 #include <cuda.h>
 
-#include <cstdio>
-#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -42,7 +35,7 @@ constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;   // producer, MMA, 4 epilogue, 
 constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
 constexpr int kRingM = 4;
 
-template <bool kBF16, bool kTransB, int kPairs, int kBN>
+template <bool kBF16, bool kTransB, int kBN>
 struct TcMCfg {
     static constexpr int BM = 128;              // A rows per CTA (UMMA_M = 256 per pair)
     static constexpr int BN = kBN;              // UMMA_N (256, or 128 for grids that leave pairs idle);
@@ -57,7 +50,7 @@ struct TcMCfg {
     static constexpr uint32_t B_BYTES = BN_CTA * 128;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int B_ATOM_N = 128 / ELEM;
-    // B boxes of one CTA's 128-column slice; each of the kPairs pairs loads 1/kPairs of them
+    // B boxes of one CTA's BN/2-column slice
     static constexpr int B_BOXES = kTransB ? 2 : BN_CTA / B_ATOM_N;
     static constexpr uint32_t B_BOX_BYTES = B_BYTES / B_BOXES;
     static constexpr bool B_BASE32 = !kBF16 && !kTransB;
@@ -77,23 +70,17 @@ struct TcMCfg {
 struct TcMParams {
     int64_t m, n, k;
     float alpha, beta;
-    int m_blocks, n_blocks, num_kb;  // 512-row x 256-column cluster tiles
+    int m_blocks, n_blocks, num_kb;  // 256-row x BN-column cluster tiles
     int group_m;
     int *sched;
-    // stream-K (kPairs == 1 only): static (tile, k-block) ranges per cluster
-    int sk, sk_clusters;
     int nprod;             // TMA producer warps per CTA (1 or 2)
-    // split-K variant (tc_*_sk, kPairs == 1): every tile's k-blocks are cut into `splits` ranges of
+    // split-K variant (tc_*_sk): every tile's k-blocks are cut into `splits` ranges of
     // ksplit k-blocks; each range is one work item whose raw FP32 partial goes to plane `split` of
     // `spart`; splitk_reduce_kernel then sums the planes in split order (fixed, so the result
     // depends only on (K, splits), never on the schedule) and applies alpha / beta.
     int splits, ksplit;
     float *spart;          // [splits][m padded to 256][n padded to 256] raw FP32 partials
     int64_t spart_ld, spart_plane;
-    int cin_prefetch;      // L2-prefetch the tile's C_in when the tile starts (COMPAR_CIN_PREFETCH=0 disables)
-    unsigned *flags;       // per cluster: published HEAD partials, 8 per launch (epoch)
-    float *partial;        // per cluster: 256 x 256 FP32 raw accumulator
-    unsigned epoch;
 };
 
 #ifdef COMPAR_TRACE
@@ -117,7 +104,7 @@ __device__ unsigned long long g_trace[2][16];
 #define TRACE_GT(i) ((void)0)
 #endif
 
-enum { kFull = 0, kHead = 1, kTail = 2, kSplit = 3 };
+enum { kFull = 0, kSplit = 1 };
 struct Item {
     int tile, kb0, kb1, kind;
 };
@@ -132,14 +119,13 @@ __device__ __forceinline__ void tile_coords_m(int t, int m_blocks, int n_blocks,
     nb = r / gm;
 }
 
-template <bool kBF16, bool kTransB, int kPairs, int kBN>
-__global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 1)
+template <bool kBF16, bool kTransB, int kBN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
     tc_gemm_2sm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmCo, const __grid_constant__ CUtensorMap tmCi,
                           TcMParams p) {
-    using C = TcMCfg<kBF16, kTransB, kPairs, kBN>;
-    static_assert(kPairs == 1 || kBN == 256, "the B-multicast form splits a 256-wide tile");
-    constexpr int kCluster = 2 * kPairs;
+    using C = TcMCfg<kBF16, kTransB, kBN>;
+    constexpr int kCluster = 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t smem0 = ptx::smem_u32(smem);
@@ -153,7 +139,6 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     const uint32_t rempty0 = rfull0 + 8 * kRingM;
     const uint32_t cbar0 = rempty0 + 8 * kRingM;
     const uint32_t ring0 = cbar0 + 8 * C::EPI_BUFS * kEpiWarpsM;
-    const uint32_t tload = ring0 + 4 * kRingM;                    // stream-K partial loaded (pair leader)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -161,16 +146,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         TRACE_GT(10);
         TRACE(0);
     }
-    const uint32_t rank = ptx::cluster_ctarank();   // 0..3
-    const uint32_t pr = rank & 1;                    // rank inside the pair
-    const uint32_t pair = rank >> 1;                 // 0: rows [0,256) of the tile, 1: [256,512)
-    const uint32_t pleader = rank & 2;               // cluster rank of this pair's MMA leader
-    const bool leader = pr == 0;
-    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << pleader);
-    const uint16_t b_mask = static_cast<uint16_t>(kPairs == 2 ? (1u << pr) | (1u << (pr + 2)) : 0u);
-    // consumers of a tile-ring slot: 4 epilogue warps per CTA, producers of CTAs 1..3, 2 MMA warps
-    // (+ every CTA's second producer warp when p.nprod == 2)
-    const int kConsumers = kCluster * kEpiWarpsM + (kCluster - 1) + kPairs + (p.nprod == 2 ? kCluster : 0);
+    const uint32_t rank = ptx::cluster_ctarank();   // 0 (MMA leader) or 1
+    const bool leader = rank == 0;
+    // consumers of a tile-ring slot: 4 epilogue warps per CTA, the peer's producer, the MMA warp
+    // (+ both CTAs' second producer warps when p.nprod == 2)
+    const int kConsumers = kCluster * kEpiWarpsM + (kCluster - 1) + 1 + (p.nprod == 2 ? kCluster : 0);
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -178,7 +158,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         ptx::prefetch_tmap(&tmCi);
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(full0 + 8 * s, 1);
-            ptx::mbar_init(empty0 + 8 * s, kPairs);
+            ptx::mbar_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(tfull0 + 8 * a, 1);
@@ -189,7 +169,6 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             ptx::mbar_init(rempty0 + 8 * r, kConsumers);
         }
         for (int b = 0; b < C::EPI_BUFS * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
-        ptx::mbar_init(tload, 2 * kEpiWarpsM);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm<C::TMEM_COLS>(ptx::smem_u32(tmem_slot));
@@ -200,7 +179,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     if (threadIdx.x == 0) TRACE(1);
 
     const int num_tiles = p.m_blocks * p.n_blocks;
-    const int num_items = num_tiles * p.splits;                // dynamic mode: ring values are items
+    const int num_items = num_tiles * p.splits;                // ring values are work items
     auto dyn_item = [&](int t) -> Item {
         if (p.splits == 1) return Item{t, 0, p.num_kb, kFull};
         const int sidx = t % p.splits;
@@ -209,36 +188,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
     };
     const uint32_t rempty_root = ptx::mapa_rank(rempty0, 0);
     const int cl = static_cast<int>(blockIdx.x) / kCluster;   // this cluster's index in the grid
-    // Work item j of this cluster.  Dynamic mode: whole tiles from the tile ring (the call is the
-    // ring consumer: the whole warp arrives once).  Stream-K mode (p.sk): the static range of
-    // (tile, k-block) units [cl*U/C, (cl+1)*U/C) in the order HEAD (first k-blocks of the range's
-    // last tile; raw accumulator published to the workspace), FULL tiles, TAIL (last k-blocks of
-    // the range's first tile; continues the accumulator chain from the previous cluster's HEAD).
-    auto sk_item = [&](int j, Item &it) -> bool {
-        const int64_t U = static_cast<int64_t>(num_tiles) * p.num_kb;
-        const int64_t s0 = U * cl / p.sk_clusters, e0 = U * (cl + 1) / p.sk_clusters;
-        const int t0 = static_cast<int>(s0 / p.num_kb), a = static_cast<int>(s0 % p.num_kb);
-        const int t1 = static_cast<int>(e0 / p.num_kb), b = static_cast<int>(e0 % p.num_kb);
-        const int has_head = b != 0, has_tail = a != 0;
-        const int first_full = has_tail ? t0 + 1 : t0;
-        const int n_full = t1 - first_full;
-        if (j < has_head) {
-            it = Item{t1, 0, b, kHead};
-        } else if (j < has_head + n_full) {
-            it = Item{first_full + j - has_head, 0, p.num_kb, kFull};
-        } else if (j == has_head + n_full && has_tail) {
-            it = Item{t0, a, p.num_kb, kTail};
-        } else {
-            return false;
-        }
-        return true;
-    };
-    // Dynamic mode: item 0 of cluster cl is item cl (no ring round trip, no atomic on the
-    // critical path of the first tile); item j >= 1 comes through ring index j - 1 from the
-    // global counter, offset by the number of clusters.
+    // Item 0 of cluster cl is item cl (no ring round trip, no atomic on the critical path of the
+    // first tile); item j >= 1 comes through ring index j - 1 from the global counter, offset by
+    // the number of clusters.
     const int n_cl = static_cast<int>(gridDim.x) / kCluster;
     auto next_item = [&](int j, Item &it) -> bool {  // whole-warp consumer (MMA and epilogue warps)
-        if (p.sk) return sk_item(j, it);
         if (j == 0) {
             it = dyn_item(cl);
             return true;
@@ -261,9 +215,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             uint32_t kstep = 0;
             for (int i = 0;; ++i) {
                 Item it;
-                if (p.sk) {
-                    if (!sk_item(i, it)) break;
-                } else if (i == 0) {
+                if (i == 0) {
                     it = dyn_item(cl);
                 } else {
                     int t;
@@ -272,11 +224,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                         ptx::mbar_wait_cluster(rempty0 + 8 * slot, (((i - 1) / kRingM) & 1) ^ 1);
                         t = n_cl + atomicAdd(&p.sched[0], 1);
                         ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
-                        for (uint32_t q = 1; q < kCluster; ++q)
-                            ptx::st_shared_cluster_u32(ptx::mapa_rank(ring0 + 4 * slot, q), static_cast<uint32_t>(t));
+                        ptx::st_shared_cluster_u32(ptx::mapa_rank(ring0 + 4 * slot, 1), static_cast<uint32_t>(t));
                         ptx::mbar_arrive(rfull0 + 8 * slot);
-                        for (uint32_t q = 1; q < kCluster; ++q)
-                            ptx::mbar_arrive_cluster(ptx::mapa_rank(rfull0 + 8 * slot, q));
+                        ptx::mbar_arrive_cluster(ptx::mapa_rank(rfull0 + 8 * slot, 1));
                     } else {
                         ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - 1) / kRingM) & 1);
                         t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
@@ -288,7 +238,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 int mb, nb;
                 tile_coords_m(it.tile, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * (kCluster * C::BM) + static_cast<int32_t>(rank) * C::BM;
-                const int32_t bcol = nb * C::BN + static_cast<int32_t>(pr) * C::BN_CTA;
+                const int32_t bcol = nb * C::BN + static_cast<int32_t>(rank) * C::BN_CTA;
                 for (int kb = it.kb0; kb < it.kb1; ++kb, ++kstep) {
                     if (p.nprod == 2 && (kstep & 1) != static_cast<uint32_t>(me)) continue;
                     const int stage = static_cast<int>(kstep % C::STAGES);
@@ -297,21 +247,17 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
                     const uint32_t fb_local = full0 + 8 * stage;
-                    const uint32_t fb = ptx::mapa_rank(fb_local, pleader);
-                    // The pair leader arms its barrier with both pair CTAs' bytes (A from each, B
-                    // halves arriving from both pairs' multicasts).  Bytes may land before the arm
-                    // (transiently negative tx); no CTA runs a phase ahead, because every producer
-                    // first waits for empty[s], i.e. for both pairs to have consumed the slot.
+                    const uint32_t fb = ptx::mapa_rank(fb_local, 0);
+                    // The leader arms its barrier with both CTAs' bytes.  Bytes may land before the
+                    // arm (transiently negative tx); no CTA runs a phase ahead, because every
+                    // producer first waits for empty[s].
                     if (leader) ptx::mbar_arrive_expect_tx(fb_local, 2 * C::STAGE_BYTES);
                     ptx::tma_load_2d_2sm(sa, &tmA, fb, kb * C::BK, arow);
 #pragma unroll
-                    for (int b = pair * (C::B_BOXES / kPairs); b < (pair + 1) * (C::B_BOXES / kPairs); ++b) {
+                    for (int b = 0; b < C::B_BOXES; ++b) {
                         const int32_t c0 = kTransB ? kb * C::BK : bcol + b * C::B_ATOM_N;
                         const int32_t c1 = kTransB ? bcol + b * (C::BN_CTA / 2) : kb * C::BK;
-                        if (kPairs == 2)
-                            ptx::tma_load_2d_2sm_mc(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1, b_mask);
-                        else
-                            ptx::tma_load_2d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1);
+                        ptx::tma_load_2d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1);
                     }
                     if (kstep == 0 && me == 0) TRACE(2);
                 }
@@ -325,7 +271,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
             }
         }
     } else if (warp == 1) {
-        if (leader) {  // ---------------- MMA issuer (pair leaders)
+        if (leader) {  // ---------------- MMA issuer (leader)
             int stage = 0;
             uint32_t phase = 0;
             for (int local = 0;; ++local) {
@@ -334,10 +280,8 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
-                if (it.kind == kTail) ptx::mbar_wait_cluster(tload, 0);   // partial accumulator in TMEM
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C::BN;
-                const bool carry = it.kind == kTail;
                 for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     ptx::mbar_wait(full0 + 8 * stage, phase);
                     if (local == 0 && lane == 0) TRACE(3);
@@ -351,13 +295,13 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                             const uint64_t bdesc = kTransB ? ptx::smem_desc(sb + j * 32, 16, 1024, 2)
                                                            : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_LBO,
                                                                             C::B_SBO, C::B_LAYOUT);
-                            const uint32_t accum = carry || kb != it.kb0 || j != 0;
+                            const uint32_t accum = kb != it.kb0 || j != 0;
                             if (kBF16)
                                 ptx::mma_bf16_2sm(d_tmem, adesc, bdesc, C::IDESC, accum);
                             else
                                 ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, C::IDESC, accum);
                         }
-                        ptx::tc_commit_2sm_mc(empty0 + 8 * stage, kPairs == 2 ? 0xF : 0x3);
+                        ptx::tc_commit_2sm_mc(empty0 + 8 * stage, 0x3);
                     }
                     __syncwarp();
                     if (++stage == C::STAGES) {
@@ -365,12 +309,12 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                         phase ^= 1;
                     }
                 }
-                if (lane == 0) ptx::tc_commit_2sm_mc(tfull0 + 8 * acc, pair_mask);
+                if (lane == 0) ptx::tc_commit_2sm_mc(tfull0 + 8 * acc, 0x3);
                 if (local == 0 && lane == 0) TRACE(4);
                 __syncwarp();
             }
         }
-    } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, 8 chunks of 32 x 32
+    } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, BN/32 chunks of 32 x 32
         const int q = warp & 3;
         const int ew = warp - 2;
         constexpr int NB = C::EPI_BUFS;
@@ -378,45 +322,13 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
         auto buf = [&](int b) -> uint32_t { return epi0 + static_cast<uint32_t>(NB * ew + b) * 4096; };
         auto cbar = [&](int b) -> uint32_t { return cbar0 + 8 * static_cast<uint32_t>(NB * ew + b); };
         uint32_t loads_odd = 0;   // bit b: an odd number of C_in loads issued into chunk b
-        const uint32_t tempty_leader = ptx::mapa_rank(tempty0, pleader);
+        const uint32_t tempty_leader = ptx::mapa_rank(tempty0, 0);
         const bool ldc = p.beta != 0.f;
         const uint32_t swz = lane * 128;
         constexpr int kChunks = C::BN / 32;
-        // this thread's row of the cluster's 256 x 256 stream-K partial (rows = pair tile rows)
-        const int prow = static_cast<int>(rank) * C::BM + q * 32 + lane;
         for (int local = 0;; ++local) {
             Item it;
             if (!next_item(local, it)) break;
-            if (p.sk) {
-                Item nx;
-                if (sk_item(local + 1, nx) && nx.kind == kTail) {
-                    // Load the previous cluster's HEAD partial into the accumulator item local+1
-                    // will use (drained in iteration local-1), then release the MMA warp.
-                    const int src = cl - 1;
-                    if (lane == 0) ptx::spin_until_geq(p.flags + src, 2u * kEpiWarpsM * p.epoch);
-                    __syncwarp();
-                    const float *part = p.partial + (static_cast<size_t>(src) * 256 + prow) * 256;
-                    const int nacc = (local + 1) & 1;
-#pragma unroll 1
-                    for (int idx = 0; idx < kChunks; ++idx) {
-                        uint32_t r[32];
-#pragma unroll
-                        for (int v = 0; v < 8; ++v) {
-                            const float4 x = __ldcg(reinterpret_cast<const float4 *>(part + 32 * idx) + v);
-                            r[4 * v + 0] = __float_as_uint(x.x);
-                            r[4 * v + 1] = __float_as_uint(x.y);
-                            r[4 * v + 2] = __float_as_uint(x.z);
-                            r[4 * v + 3] = __float_as_uint(x.w);
-                        }
-                        ptx::tmem_st_32x32b_x32(
-                            tmem_base + (static_cast<uint32_t>(q * 32) << 16) + nacc * C::BN + 32 * idx, r);
-                    }
-                    ptx::tmem_st_wait();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_rank(tload, pleader));
-                }
-            }
             int mb, nb;
             tile_coords_m(it.tile, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
@@ -447,38 +359,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 }
                 continue;
             }
-            if (it.kind == kHead) {  // publish the raw accumulator (no alpha / beta) for the next cluster
-                ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
-                ptx::tc_fence_after();
-                float *part = p.partial + (static_cast<size_t>(cl) * 256 + prow) * 256;
-#pragma unroll 1
-                for (int idx = 0; idx < kChunks; ++idx) {
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx,
-                                            r);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int v = 0; v < 8; ++v)
-                        __stcg(reinterpret_cast<float4 *>(part + 32 * idx) + v,
-                               make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                           __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
-                }
-                ptx::tc_fence_before();
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
-                    atomicAdd(p.flags + cl, 1u);
-                }
-                continue;
-            }
             const int32_t row_base = mb * (kCluster * C::BM) + static_cast<int32_t>(rank) * C::BM + q * 32;
             const int32_t col_base = nb * C::BN;
             if (lane == 0) {
                 ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
-                if (ldc && p.cin_prefetch) {              // C_in of this tile -> L2 during its mainloop
-                    for (int idx = NB; idx < kChunks; ++idx) ptx::tma_prefetch_2d(&tmCi, col_base + 32 * idx, row_base);
-                }
                 if (ldc) {
                     for (int b = 0; b < NB; ++b) {
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);
@@ -496,14 +380,14 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 const int b = idx % NB;
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx, r);
-                ptx::tmem_ld_wait(); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(12);
+                ptx::tmem_ld_wait();
                 if (idx == kChunks - 1) {                 // accumulator drained: free it for tile + 2
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
                 }
                 if (ldc) {
-                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(13);
+                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
                 } else if (idx >= NB) {
                     if (lane == 0) ptx::bulk_wait_read<NB - 1>();
                     __syncwarp();
@@ -525,11 +409,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                     }
                     ptx::sts128(a, o);
                 }
-                if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(9);
-                ptx::fence_proxy_async_smem(); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(14);
+                ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base); if (local == 0 && warp == 2 && lane == 0 && idx == 1) TRACE(15);
+                    ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base);
                     ptx::bulk_commit();
                     if (ldc && idx + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
@@ -541,10 +424,6 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kThreadsM, 
                 __syncwarp();
             }
             if (local == 0 && warp == 2 && lane == 0) TRACE(6);
-        }
-        if (p.sk) {  // a cluster without a HEAD item still advances its flag by one launch
-            Item h;
-            if (!(sk_item(0, h) && h.kind == kHead) && lane == 0) atomicAdd(p.flags + cl, 1u);
         }
         if (lane == 0) ptx::bulk_wait<0>();
         if (warp == 2 && lane == 0) TRACE(7);
@@ -607,15 +486,15 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
     }
 }
 
-template <bool kBF16, bool kTransB, int kPairs, int kBN = 256>
+template <bool kBF16, bool kTransB, int kBN = 256>
 cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
-    using C = TcMCfg<kBF16, kTransB, kPairs, kBN>;
-    constexpr int kCluster = 2 * kPairs;
+    using C = TcMCfg<kBF16, kTransB, kBN>;
+    constexpr int kCluster = 2;
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs, kBN>,
+        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (attr_err != cudaSuccess) return;
         cudaLaunchConfig_t cfg = {};
@@ -624,8 +503,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         at.val.clusterDim.x = kCluster, at.val.clusterDim.y = 1, at.val.clusterDim.z = 1;
         cfg.gridDim = dim3(kCluster * 64), cfg.blockDim = dim3(kThreadsM), cfg.dynamicSmemBytes = C::SMEM;
         cfg.attrs = &at, cfg.numAttrs = 1;
-        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs, kBN>, &cfg);
-        if (std::getenv("COMPAR_VERBOSE")) std::fprintf(stderr, "tc_gemm_2sm_mc: max active %d-CTA clusters = %d\n", kCluster, max_clusters);
+        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN>, &cfg);
     });
     if (attr_err != cudaSuccess) return attr_err;
     if (max_clusters <= 0) return cudaErrorInvalidConfiguration;
@@ -641,18 +519,15 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
     } else {
         tci = tco;  // unused
     }
+    const Knobs &kn = knobs_of(g);
     TcMParams p;
     p.m = g.m, p.n = g.n, p.k = g.k;
     p.alpha = g.alpha, p.beta = g.beta;
     p.m_blocks = static_cast<int>((g.m + kCluster * C::BM - 1) / (kCluster * C::BM));
     p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
-    static const int group_env = [] {
-        const char *s = std::getenv("COMPAR_TCM_GROUP");
-        return s ? std::atoi(s) : 0;
-    }();
     // bands of 4 cluster tiles; 8 when K <= 8192 (8192^3: 729 vs 743 us; 32768^3 keeps 4)
-    p.group_m = group_env > 0 ? group_env : (g.k <= 8192 ? 2 * kGroupM4 : kGroupM4);
+    p.group_m = kn.tc2_group > 0 ? kn.tc2_group : (g.k <= 8192 ? 2 * kGroupM4 : kGroupM4);
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
@@ -670,28 +545,8 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
     int clusters = g.num_sms / kCluster < max_clusters ? g.num_sms / kCluster : max_clusters;
     if (clusters < 1) clusters = 1;
     if (items < clusters) clusters = items;
-    // Stream-K when whole tiles would leave the last wave badly filled (> 3 % idle): every
-    // cluster gets the same number of (tile, k-block) units; a tile split between two clusters
-    // continues the same MMA chain from a published FP32 partial, so C is bitwise the
-    // data-parallel result.  COMPAR_STREAMK=0 never, =1 whenever the grid allows it.
-    const char *sk_s = std::getenv("COMPAR_STREAMK");   // read per launch (tests flip it)
-    const int sk_env = sk_s ? std::atoi(sk_s) : -1;
-    const int waves = (tiles + clusters - 1) / clusters;
-    const bool sk_ok = kPairs == 1 && p.splits == 1 && tiles >= clusters && (tiles % clusters != 0 || sk_env == 2);
-    (void)waves;  // auto mode measured slower: stream-K only on request
-    p.sk = sk_ok && sk_env >= 1;
-    p.sk_clusters = clusters;
-    p.flags = nullptr, p.partial = nullptr, p.epoch = 0;
-    const char *cp_s = std::getenv("COMPAR_CIN_PREFETCH");
-    p.cin_prefetch = cp_s ? std::atoi(cp_s) : 0;   // measured slower (8192^3 763 vs 737 us): opt-in
-    const char *np_s = std::getenv("COMPAR_TC2_PRODUCERS");
-    p.nprod = np_s && std::atoi(np_s) == 1 ? 1 : 2;
-    if (p.sk) {
-        SkWorkspace *w = sk_workspace(g.stream, clusters);
-        if (!w) return cudaErrorMemoryAllocation;
-        p.flags = w->flags, p.partial = w->partial, p.epoch = ++w->epoch;
-    }
-    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kPairs, kBN><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
+    p.nprod = kn.tc2_producers == 1 ? 1 : 2;
+    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     if (p.splits > 1) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -706,50 +561,41 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
 
 }  // namespace
 
-cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16, int pairs) {
-    if (pairs == 2) {
-        if (bf16) return g.transB ? launch_tcm_t<true, true, 2>(g) : launch_tcm_t<true, false, 2>(g);
-        return g.transB ? launch_tcm_t<false, true, 2>(g) : launch_tcm_t<false, false, 2>(g);
-    }
+cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16) {
     // 256 x 128 pair tiles (N = 128 MMAs) when 256 x 256 ones would give fewer tiles than half the
     // CTA pairs (e.g. 1536^3: 36 tiles for 74 pairs); same k order per element, bitwise-same C.
-    // COMPAR_TC2_BN=256 / 128 forces one.
-    const char *e = std::getenv("COMPAR_TC2_BN");
-    const int force = e ? std::atoi(e) : 0;
+    // COMPAR_TC2_BN=256 / 128 (Knobs) forces one.
+    const int force = knobs_of(g).tc2_bn;
     const int64_t tiles256 = ((g.m + 255) / 256) * ((g.n + 255) / 256);
     const bool narrow = force == 128 || (force != 256 && 2 * tiles256 < g.num_sms / 2);   // tiles < pairs / 2
     if (narrow) {
-        if (bf16) return g.transB ? launch_tcm_t<true, true, 1, 128>(g) : launch_tcm_t<true, false, 1, 128>(g);
-        return g.transB ? launch_tcm_t<false, true, 1, 128>(g) : launch_tcm_t<false, false, 1, 128>(g);
+        if (bf16) return g.transB ? launch_tcm_t<true, true, 128>(g) : launch_tcm_t<true, false, 128>(g);
+        return g.transB ? launch_tcm_t<false, true, 128>(g) : launch_tcm_t<false, false, 128>(g);
     }
-    if (bf16) return g.transB ? launch_tcm_t<true, true, 1>(g) : launch_tcm_t<true, false, 1>(g);
-    return g.transB ? launch_tcm_t<false, true, 1>(g) : launch_tcm_t<false, false, 1>(g);
+    if (bf16) return g.transB ? launch_tcm_t<true, true>(g) : launch_tcm_t<true, false>(g);
+    return g.transB ? launch_tcm_t<false, true>(g) : launch_tcm_t<false, false>(g);
 }
 
 cudaError_t launch_tc_gemm_splitk(const GemmLaunch &g, bool bf16) {
     const int s = tc_splitk_splits(g.m, g.n, g.k, bf16);
     if (s < 2) return cudaErrorInvalidValue;
-    if (bf16) return g.transB ? launch_tcm_t<true, true, 1>(g, s) : launch_tcm_t<true, false, 1>(g, s);
-    return g.transB ? launch_tcm_t<false, true, 1>(g, s) : launch_tcm_t<false, false, 1>(g, s);
+    if (bf16) return g.transB ? launch_tcm_t<true, true>(g, s) : launch_tcm_t<true, false>(g, s);
+    return g.transB ? launch_tcm_t<false, true>(g, s) : launch_tcm_t<false, false>(g, s);
 }
 
 cudaError_t preload_tcm_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess;
-#define COMPAR_PRELOAD_TCM(B, T, P, N) \
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, P, N>);
-    COMPAR_PRELOAD_TCM(true, false, 2, 256)
-    COMPAR_PRELOAD_TCM(true, true, 2, 256)
-    COMPAR_PRELOAD_TCM(false, false, 2, 256)
-    COMPAR_PRELOAD_TCM(false, true, 2, 256)
-    COMPAR_PRELOAD_TCM(true, false, 1, 256)
-    COMPAR_PRELOAD_TCM(true, true, 1, 256)
-    COMPAR_PRELOAD_TCM(false, false, 1, 256)
-    COMPAR_PRELOAD_TCM(false, true, 1, 256)
-    COMPAR_PRELOAD_TCM(true, false, 1, 128)
-    COMPAR_PRELOAD_TCM(true, true, 1, 128)
-    COMPAR_PRELOAD_TCM(false, false, 1, 128)
-    COMPAR_PRELOAD_TCM(false, true, 1, 128)
+#define COMPAR_PRELOAD_TCM(B, T, N) \
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, N>);
+    COMPAR_PRELOAD_TCM(true, false, 256)
+    COMPAR_PRELOAD_TCM(true, true, 256)
+    COMPAR_PRELOAD_TCM(false, false, 256)
+    COMPAR_PRELOAD_TCM(false, true, 256)
+    COMPAR_PRELOAD_TCM(true, false, 128)
+    COMPAR_PRELOAD_TCM(true, true, 128)
+    COMPAR_PRELOAD_TCM(false, false, 128)
+    COMPAR_PRELOAD_TCM(false, true, 128)
 #undef COMPAR_PRELOAD_TCM
     return e;
 }

@@ -18,9 +18,15 @@
 // Synchronisation as in tc_gemm_2sm.cu, with one accumulator set: tfull (leader commit multicast),
 // tempty (leader only, count 8 = 4 epilogue warps x 2 CTAs); cbar[w][b]: C_in chunk landed.
 // Eligibility adds the TMA rule for C: 16-byte aligned C_in/C_out, ldc * 4 % 16 == 0.
+//
+// World mode (row panels + broadcast of B; kernels.h WorldLaunch): on a rank that
+// receives B slab by slab, the producers wait per tile for the slab's "landed" flag (written on
+// the comm stream after the slab's copy) and the tiles are visited column-major, so one
+// persistent launch consumes the slabs as they arrive; a slab-packed row-major B is read through
+// a 3-D tensor map {column in slab, k, slab}.  A helper launch started after the broadcast (on
+// the SMs NCCL used) shares the tile counter with the main launch.
 #include <cuda.h>
 
-#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -64,9 +70,16 @@ struct TcWParams {
     float alpha, beta;
     int m_blocks, n_blocks, num_kb;  // 256-row x 512-column pair tiles
     int group_m;
-    int cin_prefetch;  // L2-prefetch the tile's C_in when the tile starts (COMPAR_CIN_PREFETCH=0 disables)
     int delay;       // k-steps of accumulator half 0 issued before half 1 is needed (epilogue overlap)
     int *sched;
+    // world mode (WorldLaunch): slab flags, 3-D slab-packed B, counter shared with a helper launch
+    const unsigned *flags;   // nullptr: B is resident
+    unsigned seq;
+    int slab_w;              // columns per slab (a multiple of 512)
+    int b3d;                 // 1: tmB is the 3-D map of the slab-packed row-major B
+    int static_first;        // clusters take tile cl first (0: every tile from the counter)
+    int counter_base;        // first tile handed out by the counter
+    int arm_total;           // clusters of all launches sharing the counter (last one re-arms it)
 };
 
 __device__ __forceinline__ void tile_coords_w(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
@@ -138,12 +151,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     const int num_tiles = p.m_blocks * p.n_blocks;
     const uint32_t rempty_leader = ptx::leader_addr(rempty0);
     // tile 0 of cluster cl is tile cl (no ring round trip, no atomic before the first loads);
-    // tile i >= 1 comes through ring index i - 1 from the global counter, offset by the clusters
-    const int cl = static_cast<int>(blockIdx.x >> 1), n_cl = static_cast<int>(gridDim.x >> 1);
+    // tile i >= 1 comes through ring index i - 1 from the global counter, from counter_base on
+    // (a helper launch has no static tile: its tile i is ring index i)
+    const int cl = static_cast<int>(blockIdx.x >> 1);
+    const int sf = p.static_first;
     auto next_tile = [&](int i) -> int {  // whole-warp consumer of the tile ring
-        if (i == 0) return cl;
-        const int slot = (i - 1) % kRingW;
-        ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - 1) / kRingW) & 1);
+        if (i == 0 && sf) return cl;
+        const int slot = (i - sf) % kRingW;
+        ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - sf) / kRingW) & 1);
         const int t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(rempty_leader + 8 * slot);
@@ -156,18 +171,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             uint32_t phase = 0;
             for (int i = 0;; ++i) {
                 int t;
-                const int slot = (i - 1) % kRingW;
-                if (i == 0) {
+                const int slot = (i - sf) % kRingW;
+                if (i == 0 && sf) {
                     t = cl;
                 } else if (leader) {
-                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, (((i - 1) / kRingW) & 1) ^ 1);
-                    t = n_cl + atomicAdd(&p.sched[0], 1);
+                    ptx::mbar_wait_cluster(rempty0 + 8 * slot, (((i - sf) / kRingW) & 1) ^ 1);
+                    t = p.counter_base + atomicAdd(&p.sched[0], 1);
                     ptx::st_shared_u32(ring0 + 4 * slot, static_cast<uint32_t>(t));
                     ptx::st_shared_cluster_u32(peer_addr_w(ring0 + 4 * slot, 1), static_cast<uint32_t>(t));
                     ptx::mbar_arrive(rfull0 + 8 * slot);
                     ptx::mbar_arrive_cluster(peer_addr_w(rfull0 + 8 * slot, 1));
                 } else {
-                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - 1) / kRingW) & 1);
+                    ptx::mbar_wait_cluster(rfull0 + 8 * slot, ((i - sf) / kRingW) & 1);
                     t = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot));
                     ptx::mbar_arrive_cluster(rempty_leader + 8 * slot);
                 }
@@ -176,6 +191,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM;
                 const int32_t bcol0 = nb * C::BN + static_cast<int32_t>(rank) * 128;   // + 256 h
+                // world mode: this tile's 512 columns lie in slab nb*512 / slab_w; wait until it landed
+                const int slab = p.flags ? (nb * C::BN) / p.slab_w : 0;
+                if (p.flags) {
+                    ptx::spin_until_geq(p.flags + slab, p.seq);
+                    ptx::fence_proxy_async_global();
+                }
+                const int32_t scol0 = bcol0 - slab * p.slab_w;   // column inside the slab (3-D map)
                 // Step order: with delay D > 0 (every tile but the CTA's first), the
                 // first D k-steps feed accumulator half 0 only, then the same D k-steps half 1 (A
                 // re-loaded), then both halves: half 0 restarts while the epilogue still drains half
@@ -198,6 +220,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                         const uint32_t sb = sa + C::A_BYTES + h * C::BH_BYTES;
                         if (kTransB) {
                             ptx::tma_load_2d_2sm(sb, &tmB, fb, kb * C::BK, bcol0 + 256 * h);
+                        } else if (p.b3d) {
+#pragma unroll
+                            for (int b = 0; b < C::B_BOXES; ++b)
+                                ptx::tma_load_3d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb,
+                                                     scol0 + 256 * h + b * C::B_ATOM_N, kb * C::BK, slab);
                         } else {
 #pragma unroll
                             for (int b = 0; b < C::B_BOXES; ++b)
@@ -213,7 +240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             }
             if (leader) {
                 __threadfence();
-                if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x >> 1) - 1) {
+                if (atomicAdd(&p.sched[1], 1) == p.arm_total - 1) {
                     p.sched[0] = 0;
                     p.sched[1] = 0;
                 }
@@ -290,9 +317,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             auto chunk_col = [&](int idx) { return col_base + 256 * (idx >> 3) + 32 * (idx & 7); };
             if (lane == 0) {
                 ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
-                if (ldc && p.cin_prefetch) {              // C_in of this tile -> L2 during its mainloop
-                    for (int idx = 2; idx < 16; ++idx) ptx::tma_prefetch_2d(&tmCi, chunk_col(idx), row_base);
-                }
                 if (ldc) {
                     for (int b = 0; b < 2; ++b) {
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);
@@ -375,11 +399,20 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     });
     if (attr_err != cudaSuccess) return attr_err;
+    const WorldLaunch *w = g.world;
+    const bool slabs = w && w->flags;
+    if (slabs && (w->slab_w <= 0 || w->slab_w % C::BN != 0)) return cudaErrorInvalidValue;
+    const bool b3d = slabs && !kTransB && w->nslab > 1;
     CUtensorMap ta, tb, tco, tci;
     if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, Swz::B128)) return cudaErrorInvalidValue;
-    bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, 128, C::BK, Swz::B128)
-                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N,
-                                    C::B_BASE32 ? Swz::B128_32B : Swz::B128);
+    bool ok;
+    if (kTransB)
+        ok = get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, 128, C::BK, Swz::B128);
+    else if (b3d)   // slab-packed: plane j = slab j, a K x slab_w row-major block (not cached: per task)
+        ok = make_tmap_3d(&tb, g.B, C::ELEM, w->nslab, g.k, w->slab_w, w->slab_w, g.k * w->slab_w, C::BK, C::B_ATOM_N,
+                          C::B_BASE32 ? Swz::B128_32B : Swz::B128);
+    else
+        ok = get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N, C::B_BASE32 ? Swz::B128_32B : Swz::B128);
     if (!ok) return cudaErrorInvalidValue;
     if (!get_tmap_2d(&tco, g.C_out, 4, g.m, g.n, g.ldc_out, 32, 32, Swz::B128)) return cudaErrorInvalidValue;
     if (g.beta != 0.f) {
@@ -387,31 +420,50 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
     } else {
         tci = tco;  // unused
     }
+    const Knobs &kn = knobs_of(g);
     TcWParams p;
     p.m = g.m, p.n = g.n, p.k = g.k;
     p.alpha = g.alpha, p.beta = g.beta;
     p.m_blocks = static_cast<int>((g.m + 2 * C::BM - 1) / (2 * C::BM));
     p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
-    static const int group_env = [] {
-        const char *s = std::getenv("COMPAR_TCW_GROUP");
-        return s ? std::atoi(s) : 0;
-    }();
     // raster bands of 4 pair-rows; 8 when K <= 8192, where a band's A rows plus the B columns a
-    // wave touches then fit in L2 (8192^3: 741 vs 752 us; 32768^3 keeps 4: 52.3 vs 53.7 ms)
-    p.group_m = group_env > 0 ? group_env : (g.k <= 8192 ? 2 * kGroupW : kGroupW);
-    const char *cp_s = std::getenv("COMPAR_CIN_PREFETCH");
-    p.cin_prefetch = cp_s ? std::atoi(cp_s) : 0;   // measured slower (8192^3 763 vs 737 us): opt-in
-    const char *dl = std::getenv("COMPAR_TCW_DELAY");     // read per launch (tests compare D = 0)
-    p.delay = dl ? std::atoi(dl) : kDelayW;
-    if (p.delay < 0) p.delay = 0;
+    // wave touches then fit in L2 (8192^3: 741 vs 752 us; 32768^3 keeps 4: 52.3 vs 53.7 ms);
+    // column-major (one band of all rows) when B arrives slab by slab
+    p.group_m = slabs ? p.m_blocks : (kn.tcw_group > 0 ? kn.tcw_group : (g.k <= 8192 ? 2 * kGroupW : kGroupW));
+    p.delay = kn.tcw_delay;
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;
+    p.flags = slabs ? w->flags : nullptr;
+    p.seq = slabs ? w->seq : 0;
+    p.slab_w = slabs ? w->slab_w : C::BN;
+    p.b3d = b3d ? 1 : 0;
     const int tiles = p.m_blocks * p.n_blocks;
-    const int max_clusters = g.num_sms / 2;
+    const int helper = (w && w->helper_sms >= 2 && w->helper_stream) ? w->helper_sms / 2 : 0;   // clusters
+    const int max_clusters = g.num_sms / 2 - helper;
     const int clusters = tiles < max_clusters ? tiles : max_clusters;
+    if (clusters < 1) return cudaSuccess;
+    const int extra = tiles > clusters ? (helper < tiles - clusters ? helper : tiles - clusters) : 0;
+    p.static_first = 1;
+    p.counter_base = clusters;
+    p.arm_total = clusters + extra;
+    if (extra > 0) {   // the helper must not touch the counter before earlier launches on g.stream re-armed it
+        cudaEventRecord(w->helper_done, g.stream);
+        cudaStreamWaitEvent(w->helper_stream, w->helper_done, 0);
+    }
     tc_gemm_2sm_wide_kernel<kBF16, kTransB><<<2 * clusters, kThreadsW, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (w) w->launches = 1;
+    if (e != cudaSuccess || extra == 0) return e;
+    // helper: starts once the broadcast has released its SMs, takes every tile from the counter
+    if (w->helper_after) cudaStreamWaitEvent(w->helper_stream, w->helper_after, 0);
+    p.static_first = 0;
+    tc_gemm_2sm_wide_kernel<kBF16, kTransB><<<2 * extra, kThreadsW, C::SMEM, w->helper_stream>>>(ta, tb, tco, tci, p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    w->launches = 2;
+    cudaEventRecord(w->helper_done, w->helper_stream);
+    return cudaStreamWaitEvent(g.stream, w->helper_done, 0);
 }
 
 }  // namespace

@@ -267,10 +267,9 @@ cudaError_t launch_tma_f32(const GemmLaunch &g) {
     // 64 x 64 tiles (8 x 4 micro-tiles, 128 consumer threads) when 128 x 128 tiles would fill at
     // most three quarters of the SMs (measured: 768^3 81.5 -> 37.1 us, 1024^3 105 -> 72 us,
     // 1280^3 130 -> 120 us; from 1536^3 (144 tiles) the 128 tile's 8 x 8 micro-tiles win).
-    // COMPAR_TMA_TILE=128 / 64 forces one.
+    // COMPAR_TMA_TILE=128 / 64 (Knobs) forces one.
     const int64_t tiles128 = ((g.m + 127) / 128) * ((g.n + 127) / 128);
-    const char *e = std::getenv("COMPAR_TMA_TILE");
-    const int force = e ? std::atoi(e) : 0;
+    const int force = knobs_of(g).tma_tile;
     const bool small = force == 64 || (force != 128 && 4 * tiles128 <= 3 * static_cast<int64_t>(g.num_sms));
     if (small) return g.transB ? launch_t<true, 64>(g) : launch_t<false, 64>(g);
     return g.transB ? launch_t<true, 128>(g) : launch_t<false, 128>(g);

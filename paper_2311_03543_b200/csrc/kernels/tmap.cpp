@@ -37,6 +37,22 @@ bool make_tmap_2d(CUtensorMap *out, const void *base, int elem_bytes, int64_t ro
     return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_3d(CUtensorMap *out, const void *base, int elem_bytes, int64_t planes, int64_t rows, int64_t cols,
+                  int64_t ld, int64_t plane, uint32_t box_rows, uint32_t box_cols, Swz swizzle) {
+    std::call_once(g_once, resolve);
+    if (!g_encode) return false;
+    const CUtensorMapDataType dt = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(planes)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * static_cast<cuuint64_t>(elem_bytes),
+                             static_cast<cuuint64_t>(plane) * static_cast<cuuint64_t>(elem_bytes)};
+    cuuint32_t box[3] = {box_cols, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(out, dt, 3, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          static_cast<CUtensorMapSwizzle>(static_cast<int>(swizzle)),
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 namespace {
 struct MapKey {
     const void *ptr;

@@ -21,6 +21,11 @@ enum class Swz : int {
 bool make_tmap_2d(CUtensorMap *out, const void *base, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,
                   uint32_t box_rows, uint32_t box_cols, Swz swizzle);
 
+// 3-D tensor {cols, rows, planes}: row pitch `ld` elements, plane pitch `plane` elements; box
+// box_cols x box_rows x 1.  (World-mode slab-packed B: plane j = slab j, a K x slab_w block.)
+bool make_tmap_3d(CUtensorMap *out, const void *base, int elem_bytes, int64_t planes, int64_t rows, int64_t cols,
+                  int64_t ld, int64_t plane, uint32_t box_rows, uint32_t box_cols, Swz swizzle);
+
 // Cached wrapper: tensor maps are keyed by (ptr, shape, ld, box, swizzle) so repeated
 // submissions on the same buffers skip the host-side encode (SURVEY §7 hard part 4).
 bool get_tmap_2d(CUtensorMap *out, const void *ptr, int elem_bytes, int64_t rows, int64_t cols, int64_t ld,

@@ -15,9 +15,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cerrno>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -38,6 +41,15 @@ namespace compar {
 namespace {
 
 thread_local std::string t_err;
+
+// NVTX ranges around the runtime's phases (select, bcast, launch, harvest, sync): visible in any
+// NVTX-aware profiler, a few ns each when none is attached (header-only nvtx3).
+struct Range {
+    explicit Range(const char *name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+    Range(const Range &) = delete;
+    Range &operator=(const Range &) = delete;
+};
 
 compar_status fail(compar_status s, const std::string &msg) {
     t_err = msg;
@@ -115,9 +127,13 @@ struct Ctx {
     void *reduce_user = nullptr;
     // world-mode broadcast pipeline
     cudaStream_t comm_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;   // world mode: the GEMM's extra CTAs launched after the broadcast
+    uint32_t *slab_flags = nullptr;      // world mode: per-slab "landed" words read by the fused GEMM
+    uint32_t slab_seq = 0;               // world broadcasts issued (flag value of the current one)
     void *bpacked = nullptr;  // root: B packed into contiguous N-slabs
     size_t bpacked_bytes = 0;
-    bool bcast_loopback = false;  // 1 rank: emulate the broadcast with D2D copies (tests the slab path)
+    int bcast_loopback = 0;       // 1 rank: emulate the broadcast with D2D copies (tests the slab path);
+                                  // 2: also leave the NCCL SM reserve (exercises the helper launch)
     int bcast_reserve_sms = 16;   // SMs left free for NCCL while a slab GEMM overlaps a broadcast
     // copy-engine chain broadcast (compar_ce_export / compar_ce_import): no NCCL, no SMs
     bool ce = false;
@@ -151,6 +167,19 @@ struct Ctx {
     int64_t batch_below_ns = 100000;
     void *scratch = nullptr;  // C_out of the r - 1 extra launches
     size_t scratch_bytes = 0;
+    // reports of tasks the selector harvested implicitly (step 6), kept until compar_sync
+    std::map<uint64_t, std::pair<compar_status, compar_report>> done;
+    bool in_select = false;   // compar_select: never harvest tasks whose harvest is collective
+    // the next task that reuses a shared library buffer waits for the previous user to finish
+    cudaEvent_t staging_free = nullptr;   // host-mode staging buffers
+    bool staging_free_set = false;
+    cudaEvent_t bcast_free = nullptr;     // world-mode packed B / replica / slab flags
+    bool bcast_free_set = false;
+    // NCCL robustness: bounded waits, sticky failure after an asynchronous error or a timeout
+    int64_t sync_timeout_ms = 600000;
+    compar_status sticky = COMPAR_OK;
+    std::string sticky_msg;
+    Knobs knobs;              // launcher tuning knobs, read from the environment once at init
 };
 
 std::mutex g_live_mu;
@@ -402,6 +431,57 @@ compar_status build_plan(Ctx *c, const compar_gemm_desc *d, Plan &plan, const vo
     return COMPAR_OK;
 }
 
+// ---------------------------------------------------------------- bounded waits (NCCL robustness)
+// Marks the context's cross-rank path failed: the communicator is aborted (its pending
+// collectives end) and every later task that needs a collective fails with E_NCCL.
+void make_sticky(Ctx *c, const std::string &msg) {
+    if (c->sticky == COMPAR_OK) {
+        c->sticky = COMPAR_E_NCCL;
+        c->sticky_msg = msg;
+    }
+    if (c->comm) {
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+    }
+}
+
+// Waits for `ev`.  For work that involves other ranks (collective = true) the wait polls
+// ncclCommGetAsyncError and the sync timeout instead of blocking in the driver: a rank that died,
+// or a collective that errored, turns into E_NCCL here instead of a hang.
+compar_status wait_event(Ctx *c, cudaEvent_t ev, bool collective, cudaError_t *cuda_err) {
+    *cuda_err = cudaSuccess;
+    if (!ev) return COMPAR_OK;
+    if (!collective || (!c->comm && !c->ce)) {
+        *cuda_err = cudaEventSynchronize(ev);
+        return COMPAR_OK;
+    }
+    if (c->sticky != COMPAR_OK) return fail(c->sticky, c->sticky_msg);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spins = 0;; ++spins) {
+        const cudaError_t e = cudaEventQuery(ev);
+        if (e != cudaErrorNotReady) {
+            *cuda_err = e;
+            return COMPAR_OK;
+        }
+        ncclResult_t ar = ncclSuccess;
+        if (c->comm) ncclCommGetAsyncError(c->comm, &ar);
+        const int64_t ms = std::chrono::duration_cast<std::chrono::milliseconds>(
+                               std::chrono::steady_clock::now() - t0).count();
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            make_sticky(c, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+            return fail(COMPAR_E_NCCL, c->sticky_msg);
+        }
+        if (c->sync_timeout_ms > 0 && ms > c->sync_timeout_ms) {
+            make_sticky(c, "cross-rank wait timed out after " + std::to_string(ms) + " ms (sync_timeout_ms)");
+            return fail(COMPAR_E_NCCL, c->sticky_msg);
+        }
+        if (spins < 256)
+            std::this_thread::yield();
+        else
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
 // ---------------------------------------------------------------- harvest
 compar_status finish_task(Ctx *c, Task &t, compar_report *rep);
 
@@ -411,7 +491,12 @@ int64_t measure(Ctx *c, Task &t, compar_report *rep) {
     int64_t sample = 0;
     cudaEvent_t last = t.end ? t.end : (t.panels.empty() ? nullptr : t.panels.back().stop);
     if (!c->virt && last) {
-        cudaError_t e = cudaEventSynchronize(last);
+        cudaError_t e = cudaSuccess;
+        const compar_status ws = wait_event(c, last, (t.world || t.tasks) && c->nranks > 1, &e);
+        if (ws != COMPAR_OK && t.status == COMPAR_OK) {
+            t.status = ws;
+            return 0;
+        }
         if (e != cudaSuccess && t.status == COMPAR_OK) {
             t.status = COMPAR_E_TASK_FAILED;
             t_err = std::string("task execution failed: ") + cudaGetErrorString(e);
@@ -468,8 +553,16 @@ compar_status exchange_samples(Ctx *c, const std::vector<Task *> &ts) {
             cudaMemcpyAsync(c->xbuf, buf.data(), buf.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
             const ncclResult_t r = ncclAllReduce(c->xbuf, c->xbuf, buf.size(), ncclInt64, ncclMax, c->comm, c->stream);
             cudaMemcpyAsync(buf.data(), c->xbuf, buf.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
-            cudaStreamSynchronize(c->stream);
-            if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("sample exchange: ") + ncclGetErrorString(r));
+            if (r != ncclSuccess) {
+                make_sticky(c, std::string("sample exchange: ") + ncclGetErrorString(r));
+                return fail(COMPAR_E_NCCL, c->sticky_msg);
+            }
+            cudaEvent_t ev = get_event(c);
+            cudaEventRecord(ev, c->stream);
+            cudaError_t ce = cudaSuccess;
+            const compar_status ws = wait_event(c, ev, true, &ce);
+            put_event(c, ev);
+            if (ws != COMPAR_OK) return ws;
         } else {
             return fail(COMPAR_E_STATE, "task-parallel world over several ranks needs a communicator or a reduce hook");
         }
@@ -492,36 +585,42 @@ compar_status exchange_ids(Ctx *c, const std::vector<uint64_t> &ids) {
     return exchange_samples(c, xs);
 }
 
-// Step 6: before a model decision, every pending execution of this key is harvested in
-// task-id order (std::map iterates in id order).
-compar_status harvest_key(Ctx *c, const Key &k) {
-    std::vector<uint64_t> ids;
-    for (auto &kv : c->tasks)
-        if (kv.second.history && kv.second.key == k) ids.push_back(kv.first);
+// A task whose harvest is a collective (NCCL sample all-reduce or exchange across ranks): only
+// harvested where every rank harvests it (submit / sync), never from compar_select.
+bool collective_harvest(const Ctx *c, const Task &t) {
+    return c->nranks > 1 && (t.world || t.tasks);
+}
+
+// Implicit harvest (step 6): the task's report is kept in `done` until compar_sync returns it.
+compar_status harvest_ids(Ctx *c, const std::vector<uint64_t> &ids) {
+    Range r("compar.harvest");
     compar_status s = exchange_ids(c, ids);
     if (s != COMPAR_OK) return s;
     for (uint64_t id : ids) {
         auto it = c->tasks.find(id);
         compar_report rep;
-        finish_task(c, it->second, &rep);
+        const compar_status st = finish_task(c, it->second, &rep);
+        c->done[id] = {st, rep};
         c->tasks.erase(it);
     }
     return COMPAR_OK;
 }
 
+// Step 6: before a decision, every pending execution of this key is harvested in task-id order
+// (std::map iterates in id order).
+compar_status harvest_key(Ctx *c, const Key &k) {
+    std::vector<uint64_t> ids;
+    for (auto &kv : c->tasks)
+        if (kv.second.history && kv.second.key == k && !(c->in_select && collective_harvest(c, kv.second)))
+            ids.push_back(kv.first);
+    return harvest_ids(c, ids);
+}
+
 compar_status harvest_all(Ctx *c) {
     std::vector<uint64_t> ids;
     for (auto &kv : c->tasks)
-        if (kv.second.history) ids.push_back(kv.first);
-    compar_status s = exchange_ids(c, ids);
-    if (s != COMPAR_OK) return s;
-    for (uint64_t id : ids) {
-        auto it = c->tasks.find(id);
-        compar_report rep;
-        finish_task(c, it->second, &rep);
-        c->tasks.erase(it);
-    }
-    return COMPAR_OK;
+        if (kv.second.history && !(c->in_select && collective_harvest(c, kv.second))) ids.push_back(kv.first);
+    return harvest_ids(c, ids);
 }
 
 compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
@@ -561,8 +660,17 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
         cudaMemcpyAsync(c->red_buf, &sample, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
         ncclResult_t r = ncclAllReduce(c->red_buf, c->red_buf, 1, ncclInt64, ncclMax, c->comm, c->stream);
         cudaMemcpyAsync(&sample, c->red_buf, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream);
-        cudaStreamSynchronize(c->stream);
-        if (r != ncclSuccess && t.status == COMPAR_OK) t.status = COMPAR_E_NCCL;
+        if (r != ncclSuccess) {
+            make_sticky(c, std::string("sample all-reduce: ") + ncclGetErrorString(r));
+            if (t.status == COMPAR_OK) t.status = COMPAR_E_NCCL;
+        } else {
+            cudaEvent_t ev = get_event(c);
+            cudaEventRecord(ev, c->stream);
+            cudaError_t ce = cudaSuccess;
+            const compar_status ws = wait_event(c, ev, true, &ce);
+            put_event(c, ev);
+            if (ws != COMPAR_OK && t.status == COMPAR_OK) t.status = ws;
+        }
     }
     rep->ns = sample;
     rep->status = t.status;
@@ -575,13 +683,16 @@ compar_status finish_task(Ctx *c, Task &t, compar_report *rep) {
     if (rep->batch == 0) rep->batch = 1;
     if (t.status != COMPAR_OK) c->stats.failed++;
     release_task_events(c, t);
-    return t.status == COMPAR_OK ? COMPAR_OK : COMPAR_E_TASK_FAILED;
+    if (t.status == COMPAR_OK) return COMPAR_OK;
+    return t.status == COMPAR_E_NCCL ? COMPAR_E_NCCL : COMPAR_E_TASK_FAILED;
 }
 
 // ---------------------------------------------------------------- running a variant on a panel
 compar_status run_builtin(Ctx *c, compar_target t, const compar_gemm_desc *d, const compar_panel &p,
-                          cudaStream_t s, int sms = 0) {
+                          cudaStream_t s, int sms = 0, const WorldLaunch *wl = nullptr) {
     GemmLaunch g;
+    g.knobs = &c->knobs;
+    g.world = wl;
     g.m = p.rows, g.n = d->n, g.k = d->k;
     g.alpha = d->alpha, g.beta = d->beta;
     g.A = p.A, g.lda = d->lda, g.B = p.B, g.ldb = d->ldb, g.transB = d->transB;
@@ -614,6 +725,7 @@ compar_status run_scale(Ctx *c, const compar_gemm_desc *d, const compar_panel &p
     g.C_in = p.C_in, g.ldc_in = d->ldc_in, g.C_out = p.C_out, g.ldc_out = d->ldc_out;
     g.stream = s;
     g.num_sms = c->num_sms;
+    g.knobs = &c->knobs;
     cudaError_t e = launch_scale(g);
     c->stats.launches++;
     if (e != cudaSuccess) return fail(COMPAR_E_TASK_FAILED, std::string("scale: ") + cudaGetErrorString(e));
@@ -621,18 +733,106 @@ compar_status run_scale(Ctx *c, const compar_gemm_desc *d, const compar_panel &p
 }
 
 // ---------------------------------------------------------------- world mode: B broadcast + panel GEMM
-// SURVEY §8(a) a5 / §8(e).  B is cut into `bcast_chunks` contiguous N-slabs (row-major B: packed
-// on the root by the copy engine with cudaMemcpy2DAsync; transB: slabs are already contiguous
-// row ranges of B^T), each slab is broadcast with ncclBroadcast on the library's comm stream,
-// and a non-root rank multiplies its A panel by slab j as soon as slab j has landed (event
-// hand-off), so slab j+1 travels while slab j is multiplied.  Every C element still sums its
-// full K in order, so C is bitwise identical to the single-GPU result.  The root multiplies
-// with its own B (one launch).  Slab GEMMs that overlap a pending broadcast leave
-// bcast_reserve_sms SMs free so NCCL's kernels are never starved by the persistent GEMM.
+// SURVEY §8(a) a5 / §8(e); DESIGN.md §6.  B (on rank 0) is packed into contiguous N-slabs by the
+// copy engine (row-major B: slab j is a K x w_j row-major block; transB: rows of B^T, pitch K) and
+// each slab is broadcast (ncclBroadcast on the library's comm stream, or the copy-engine chain).
+// A receiver consumes slab j as soon as it landed:
+//   * fused (wide-pair variant, uniform slabs of a multiple of 512 columns dividing N): ONE
+//     persistent launch whose producers wait per tile on the slab's flag word (written on the comm
+//     stream after the slab landed) and visit the tiles column-major;
+//   * otherwise one launch per slab after the slab's event (geometric widths: a small first slab,
+//     then doubling, so the exposed first-slab latency is short and the launches few).
+// Every C element still sums its full K in order, so C is bitwise the single-GPU result.  The root
+// multiplies with its own B.  GEMMs that overlap an NCCL broadcast leave bcast_reserve_sms SMs to
+// NCCL's kernels (the communicator is capped at bcast_ctas CTAs); the wide variant gets them back
+// through a helper launch after the broadcast ends.
+
+// Slab plan of a world task.
+struct SlabPlan {
+    std::vector<int64_t> col0;   // slab j = columns [col0[j], col0[j+1]) of B (size nslab + 1)
+    bool fused = false;          // uniform slabs read by one flag-waiting launch
+    int64_t w = 0;               // fused: slab width
+    int64_t pitch1 = 0;          // nslab == 1: packed row pitch (elements; >= width, TMA-aligned)
+    int nslab() const { return static_cast<int>(col0.size()) - 1; }
+};
+
+constexpr int kMaxSlabs = 64;
+
+// fused_ok: the variant is the wide pair kernel.  chunks: the non-fused slab count.
+SlabPlan plan_slabs(int64_t N, int64_t K, int eb, bool transB, bool fused_ok, int chunks) {
+    SlabPlan sp;
+    const int64_t width = transB ? K : N;   // row width of a packed slab's rows (transB: B^T rows)
+    if (fused_ok) {   // smallest multiple of 512 dividing N with at most 32 slabs
+        for (int64_t w = 512; w <= N; w += 512) {
+            if (N % w == 0 && N / w <= 32 && (transB || (w * eb) % 16 == 0)) {
+                sp.fused = true;
+                sp.w = w;
+                for (int64_t c0 = 0; c0 <= N; c0 += w) sp.col0.push_back(c0);
+                break;
+            }
+        }
+        if (sp.fused && sp.nslab() >= 1 && (transB ? (K * eb) % 16 == 0 : true)) return sp;
+        sp = SlabPlan{};
+    }
+    // geometric: boundaries at N / 2^(S-j), rounded up to 256 columns
+    const int S = std::max(1, std::min(chunks, 16));
+    sp.col0.push_back(0);
+    for (int j = 1; j < S; ++j) {
+        int64_t b = (N >> (S - j));
+        b = (b + 255) / 256 * 256;
+        if (b > sp.col0.back() && b < N) sp.col0.push_back(b);
+    }
+    sp.col0.push_back(N);
+    // every packed slab pitch must be TMA-usable (16-byte rows); else a single padded slab
+    bool ok = true;
+    for (int j = 0; j < sp.nslab(); ++j) {
+        const int64_t pitch = transB ? K : sp.col0[j + 1] - sp.col0[j];
+        if ((pitch * eb) % 16 != 0) ok = false;
+    }
+    if (!ok) sp.col0 = {0, N};
+    const int64_t unit = 16 / eb;
+    sp.pitch1 = (width + unit - 1) / unit * unit;
+    return sp;
+}
+
+// Bytes of the packed replica for a plan (all slabs; a single slab may carry row padding).
+size_t packed_bytes(const SlabPlan &sp, int64_t N, int64_t K, int eb, bool transB) {
+    if (sp.nslab() == 1) return static_cast<size_t>(transB ? N : K) * sp.pitch1 * eb;
+    return static_cast<size_t>(K) * N * eb;
+}
+
+// Packed geometry of slab j: byte offset, rows, row pitch (elements).
+struct SlabGeo {
+    size_t off;
+    int64_t rows, pitch, cols;
+};
+SlabGeo slab_geo(const SlabPlan &sp, int j, int64_t K, int eb, bool transB) {
+    const int64_t c0 = sp.col0[j], wj = sp.col0[j + 1] - c0;
+    if (sp.nslab() == 1)
+        return {0, transB ? wj : K, sp.pitch1, transB ? K : wj};
+    if (transB) return {static_cast<size_t>(c0) * K * eb, wj, K, K};
+    return {static_cast<size_t>(K) * c0 * eb, K, wj, wj};
+}
+
+// Copy-engine pack of slab j from the caller's B (any ld) into `dst`.
+void pack_slab(const SlabPlan &sp, int j, const compar_gemm_desc *d, const void *Bsrc, void *dst, int eb,
+               cudaStream_t s) {
+    const SlabGeo g = slab_geo(sp, j, d->k, eb, d->transB);
+    const int64_t c0 = sp.col0[j];
+    const char *src = static_cast<const char *>(Bsrc);
+    char *out = static_cast<char *>(dst) + g.off;
+    if (d->transB)   // rows [c0, c0 + w) of B^T
+        cudaMemcpy2DAsync(out, g.pitch * eb, src + c0 * d->ldb * eb, d->ldb * eb, g.cols * eb, g.rows,
+                          cudaMemcpyDeviceToDevice, s);
+    else             // columns [c0, c0 + w) of every row of B
+        cudaMemcpy2DAsync(out, g.pitch * eb, src + c0 * eb, d->ldb * eb, g.cols * eb, g.rows, cudaMemcpyDeviceToDevice,
+                          s);
+}
+
 template <class F>
 compar_status world_gemms(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *replica,
-                          bool slabbed, int nslab, int64_t w, const std::vector<cudaEvent_t> &landed,
-                          int reserve_sms, F &&launch_on);
+                          const SlabPlan &sp, const std::vector<cudaEvent_t> &landed, const unsigned *flags,
+                          unsigned seq, int reserve, F &&launch_on);
 
 // ---------------------------------------------------------------- copy-engine chain broadcast
 // Stream memory operations on IPC-mapped flag words (driver entry points; no SM involvement).
@@ -661,24 +861,22 @@ inline CUdeviceptr dptr(const uint32_t *p) { return static_cast<CUdeviceptr>(rei
 // World task with the copy-engine chain: slab j travels root -> 1 -> ... -> P-1, each hop a
 // cudaMemcpyAsync from the upstream rank's IPC-mapped buffer, started by a GPU-side wait on the
 // upstream's ready[j] >= seq and followed by consumed[j] = seq in the upstream's flags (it may
-// then overwrite slab j for the next broadcast) and ready[j] = seq in our own.  Every rank runs
-// the same broadcast sequence (SPMD), so seq agrees everywhere; nothing runs on the SMs.
+// then overwrite slab j for the next broadcast) and ready[j] = seq in our own — which is also the
+// slab flag the fused GEMM waits on.  Every rank runs the same broadcast sequence (SPMD), so seq
+// agrees everywhere; nothing runs on the SMs.
 template <class F>
 compar_status ce_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *Bloc,
-                          size_t b_bytes, F &&launch_on) {
+                          bool fused_ok, F &&launch_on) {
     const int eb = elem_bytes(d->in_dtype);
     const bool root = c->rank == 0;
     const bool has_down = c->rank + 1 < c->nranks;
     const int64_t K = d->k, N = d->n;
-    // the last rank's first slab arrives after P - 1 hops: use at least 4 slabs per hop
-    int chunks = std::min(kCeMax, std::max(c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1, 4 * (c->nranks - 1)));
-    int64_t w = ((N + chunks - 1) / chunks + 255) / 256 * 256;
-    if (w >= N) w = N;
-    int nslab = static_cast<int>((N + w - 1) / w);
-    const bool packable = d->transB ? ((K * eb) % 16 == 0) : ((w * eb) % 16 == 0 && ((N - (nslab - 1) * w) * eb) % 16 == 0);
-    if (!packable) nslab = 1;
-    const bool slabbed = nslab > 1;
-    const size_t total = slabbed ? static_cast<size_t>(K) * N * eb : b_bytes;
+    // the last rank's first slab arrives after P - 1 hops: at least 4 slabs per hop
+    const int chunks = std::min(16, std::max(c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1, 4 * (c->nranks - 1)));
+    const SlabPlan sp = plan_slabs(N, K, eb, d->transB, fused_ok, chunks);
+    const int nslab = sp.nslab();
+    if (nslab > kCeMax) return fail(COMPAR_E_INVALID, "too many slabs");
+    const size_t total = packed_bytes(sp, N, K, eb, d->transB);
     if (total > c->ce_cap) return fail(COMPAR_E_INVALID, "B larger than the copy-engine chain buffer (max_b_bytes)");
     const uint32_t seq = ++c->ce_seq;
     cudaStream_t cs = c->comm_stream;
@@ -689,28 +887,20 @@ compar_status ce_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream
     t.extra.push_back(ready);
     cudaEventRecord(ready, st);
     cudaStreamWaitEvent(cs, ready, 0);
+    if (c->bcast_free_set) cudaStreamWaitEvent(cs, c->bcast_free, 0);
     cudaEventRecord(t.bc0, cs);
     std::vector<cudaEvent_t> landed;
     for (int j = 0; j < nslab; ++j) {
-        const int64_t col0 = slabbed ? j * w : 0, wj = slabbed ? std::min(w, N - col0) : N;
-        const size_t off = static_cast<size_t>(K) * col0 * eb;
-        const size_t bytes = slabbed ? static_cast<size_t>(K) * wj * eb : b_bytes;
-        char *mine = static_cast<char *>(c->ce_buf) + off;
+        const SlabGeo g = slab_geo(sp, j, K, eb, d->transB);
+        const size_t bytes = static_cast<size_t>(g.rows) * g.pitch * eb;
+        char *mine = static_cast<char *>(c->ce_buf) + g.off;
         if (has_down)  // the downstream rank has copied slab j of the previous broadcast out
             g_wait32(cus, dptr(c->ce_flags + kCeMax + j), seq - 1, CU_STREAM_WAIT_VALUE_GEQ);
         if (root) {
-            const char *src = static_cast<const char *>(Bloc);
-            if (!slabbed)
-                cudaMemcpyAsync(mine, src, bytes, cudaMemcpyDeviceToDevice, cs);
-            else if (d->transB)
-                cudaMemcpy2DAsync(mine, K * eb, src + col0 * d->ldb * eb, d->ldb * eb, K * eb, wj,
-                                  cudaMemcpyDeviceToDevice, cs);
-            else
-                cudaMemcpy2DAsync(mine, wj * eb, src + col0 * eb, d->ldb * eb, wj * eb, K, cudaMemcpyDeviceToDevice,
-                                  cs);
+            pack_slab(sp, j, d, Bloc, c->ce_buf, eb, cs);
         } else {
             g_wait32(cus, dptr(c->ce_up_flags + j), seq, CU_STREAM_WAIT_VALUE_GEQ);
-            cudaMemcpyAsync(mine, static_cast<const char *>(c->ce_up_buf) + off, bytes, cudaMemcpyDefault, cs);
+            cudaMemcpyAsync(mine, static_cast<const char *>(c->ce_up_buf) + g.off, bytes, cudaMemcpyDefault, cs);
             g_write32(cus, dptr(c->ce_up_flags + kCeMax + j), seq, CU_STREAM_WRITE_VALUE_DEFAULT);
         }
         g_write32(cus, dptr(c->ce_flags + j), seq, CU_STREAM_WRITE_VALUE_DEFAULT);
@@ -720,123 +910,146 @@ compar_status ce_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream
         cudaEventRecord(ev, cs);
     }
     cudaEventRecord(t.bc1, cs);
-    return world_gemms(c, d, t, st, c->ce_buf, slabbed, nslab, w, landed, 0, launch_on);   // no SMs to spare
+    // no SMs to spare: the copy engines move B
+    return world_gemms(c, d, t, st, c->ce_buf, sp, landed, c->ce_flags, seq, 0, launch_on);
 }
 
 template <class F>
 compar_status world_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *Bloc,
-                             size_t b_bytes, F &&launch_on) {
-    if (c->ce && c->nranks > 1) return ce_pipeline(c, d, t, st, Bloc, b_bytes, launch_on);
+                             bool fused_ok, F &&launch_on) {
+    Range range("compar.bcast");
+    if (c->ce && c->nranks > 1) return ce_pipeline(c, d, t, st, Bloc, fused_ok, launch_on);
     const int eb = elem_bytes(d->in_dtype);
     const bool loop = c->nranks == 1;              // loopback emulation on one GPU
     const bool root = !loop && c->rank == 0;
     const bool use_nccl = c->comm != nullptr;      // loopback with a 1-rank communicator still calls NCCL
     const int64_t K = d->k, N = d->n;
-    int chunks = c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1;
-    int64_t w = ((N + chunks - 1) / chunks + 255) / 256 * 256;
-    if (w >= N) w = N;
-    int nslab = static_cast<int>((N + w - 1) / w);
-    const bool packable = d->transB ? ((K * eb) % 16 == 0) : ((w * eb) % 16 == 0 && ((N - (nslab - 1) * w) * eb) % 16 == 0);
-    if (!packable) nslab = 1;
-    const bool slabbed = nslab > 1;
+    const SlabPlan sp = plan_slabs(N, K, eb, d->transB, fused_ok, c->cfg.bcast_chunks > 0 ? c->cfg.bcast_chunks : 1);
+    const int nslab = sp.nslab();
+    if (nslab > kMaxSlabs) return fail(COMPAR_E_INVALID, "too many slabs");
+    const size_t total = packed_bytes(sp, N, K, eb, d->transB);
     compar_status s;
-    // buffers: the root (or loopback) packs into bpacked; receivers (or loopback) use the replica
-    void *packed = nullptr, *replica = const_cast<void *>(Bloc);
-    const size_t slab_total = static_cast<size_t>(K) * N * eb;
-    if (slabbed && (root || loop)) {
-        if ((s = ensure_buffer(&c->bpacked, &c->bpacked_bytes, slab_total)) != COMPAR_OK) return s;
+    // buffers: the root (or loopback) packs into bpacked; receivers (or loopback) fill the replica —
+    // the caller's B_replica when the packed layout fits its k * n elements, else the library's
+    void *packed = nullptr;
+    void *replica = nullptr;
+    if (root || loop) {
+        if ((s = ensure_buffer(&c->bpacked, &c->bpacked_bytes, total)) != COMPAR_OK) return s;
         packed = c->bpacked;
     }
-    if (loop) {
-        if ((s = ensure_buffer(&c->breplica, &c->breplica_bytes, std::max(slab_total, b_bytes))) != COMPAR_OK) return s;
-        replica = c->breplica;
+    if (!root) {
+        if (!loop && d->B_replica && total <= static_cast<size_t>(K) * N * eb) {
+            replica = d->B_replica;
+        } else {
+            if ((s = ensure_buffer(&c->breplica, &c->breplica_bytes, total)) != COMPAR_OK) return s;
+            replica = c->breplica;
+        }
     }
+    if (!c->slab_flags) {
+        cudaError_t e = cudaMalloc(&c->slab_flags, kMaxSlabs * sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMemset(c->slab_flags, 0, kMaxSlabs * sizeof(uint32_t));
+        if (e != cudaSuccess) return cuda_fail(e, "slab flags");
+    }
+    if (sp.fused && !resolve_stream_memops()) return fail(COMPAR_E_CUDA, "cuStreamWriteValue32 unavailable");
+    const uint32_t seq = ++c->slab_seq;
+    cudaStream_t cs = c->comm_stream;
     t.bc0 = get_event(c);
     t.bc1 = get_event(c);
     cudaEvent_t ready = get_event(c);
     t.extra.push_back(ready);
-    cudaEventRecord(ready, st);                     // inputs / previous users of the buffers are done
-    cudaStreamWaitEvent(c->comm_stream, ready, 0);
-    cudaEventRecord(t.bc0, c->comm_stream);
+    cudaEventRecord(ready, st);                     // inputs of this task are ready
+    cudaStreamWaitEvent(cs, ready, 0);
+    if (c->bcast_free_set) cudaStreamWaitEvent(cs, c->bcast_free, 0);   // previous world task's GEMMs
+    cudaEventRecord(t.bc0, cs);
     std::vector<cudaEvent_t> landed;
     ncclResult_t nr = ncclSuccess;
-    if (!slabbed) {
-        // one raw broadcast of the B region (any ld), then the plain panel GEMM
+    for (int j = 0; j < nslab; ++j) {
+        const SlabGeo g = slab_geo(sp, j, K, eb, d->transB);
+        const size_t bytes = static_cast<size_t>(g.rows) * g.pitch * eb;
+        char *pk = packed ? static_cast<char *>(packed) + g.off : nullptr;
+        char *rp = replica ? static_cast<char *>(replica) + g.off : nullptr;
+        if (root || loop) pack_slab(sp, j, d, Bloc, packed, eb, cs);
         if (loop && !use_nccl)
-            cudaMemcpyAsync(replica, Bloc, b_bytes, cudaMemcpyDeviceToDevice, c->comm_stream);
-        else
-            nr = ncclBroadcast(root || loop ? Bloc : replica, root ? const_cast<void *>(Bloc) : replica, b_bytes,
-                               ncclChar, 0, c->comm, c->comm_stream);
-    } else {
-        for (int j = 0; j < nslab; ++j) {
-            const int64_t col0 = j * w, wj = std::min(w, N - col0);
-            const size_t off = static_cast<size_t>(K) * col0 * eb, bytes = static_cast<size_t>(K) * wj * eb;
-            char *pk = static_cast<char *>(packed) + off;
-            char *rp = static_cast<char *>(replica) + off;
-            const char *src = static_cast<const char *>(root || loop ? Bloc : nullptr);
-            if (root || loop) {
-                if (d->transB)
-                    cudaMemcpy2DAsync(pk, K * eb, src + col0 * d->ldb * eb, d->ldb * eb, K * eb, wj,
-                                      cudaMemcpyDeviceToDevice, c->comm_stream);
-                else
-                    cudaMemcpy2DAsync(pk, wj * eb, src + col0 * eb, d->ldb * eb, wj * eb, K, cudaMemcpyDeviceToDevice,
-                                      c->comm_stream);
-            }
-            if (loop && !use_nccl)
-                cudaMemcpyAsync(rp, pk, bytes, cudaMemcpyDeviceToDevice, c->comm_stream);
-            else if (nr == ncclSuccess)
-                nr = ncclBroadcast(pk, root ? pk : rp, bytes, ncclChar, 0, c->comm, c->comm_stream);
-            cudaEvent_t ev = get_event(c);
-            t.extra.push_back(ev);
-            landed.push_back(ev);
-            cudaEventRecord(ev, c->comm_stream);
-        }
+            cudaMemcpyAsync(rp, pk, bytes, cudaMemcpyDeviceToDevice, cs);
+        else if (nr == ncclSuccess)
+            nr = ncclBroadcast(pk, root ? pk : rp, bytes, ncclChar, 0, c->comm, cs);
+        if (sp.fused && !root)
+            g_write32(reinterpret_cast<CUstream>(cs), dptr(c->slab_flags + j), seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+        cudaEvent_t ev = get_event(c);
+        t.extra.push_back(ev);
+        landed.push_back(ev);
+        cudaEventRecord(ev, cs);
     }
-    cudaEventRecord(t.bc1, c->comm_stream);
-    if (nr != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclBroadcast: ") + ncclGetErrorString(nr));
-    return world_gemms(c, d, t, st, replica, slabbed, nslab, w, landed,
-                       std::max(2, c->num_sms - c->bcast_reserve_sms), launch_on);
+    cudaEventRecord(t.bc1, cs);
+    if (nr != ncclSuccess) {
+        make_sticky(c, std::string("ncclBroadcast: ") + ncclGetErrorString(nr));
+        return fail(COMPAR_E_NCCL, c->sticky_msg);
+    }
+    return world_gemms(c, d, t, st, replica, sp, landed, c->slab_flags, seq,
+                       (use_nccl && !loop) || c->bcast_loopback >= 2 ? c->bcast_reserve_sms : 0, launch_on);
 }
 
-// Slab GEMMs of a world task (shared by the NCCL and copy-engine broadcasts).  The root multiplies
-// with its own B in one launch; other ranks multiply slab j of the replica once slab j landed.
+// GEMMs of a world task (shared by the NCCL and copy-engine broadcasts).  The root multiplies with
+// its own B; receivers read the replica (fused: one flag-waiting launch; else one launch per slab).
+// reserve: SMs the broadcast's kernels need while it runs (0: copy engines only).
 template <class F>
 compar_status world_gemms(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStream_t st, const void *replica,
-                          bool slabbed, int nslab, int64_t w, const std::vector<cudaEvent_t> &landed,
-                          int reserve_sms, F &&launch_on) {
+                          const SlabPlan &sp, const std::vector<cudaEvent_t> &landed, const unsigned *flags,
+                          unsigned seq, int reserve, F &&launch_on) {
     const int eb = elem_bytes(d->in_dtype);
     const bool root = c->nranks > 1 && c->rank == 0;
-    const int64_t K = d->k, N = d->n;
+    const int64_t K = d->k;
+    const int nslab = sp.nslab();
+    // the wide kernel returns the reserved SMs through a helper launch once the broadcast is over
+    WorldLaunch split;
+    if (reserve >= 2) {
+        split.helper_sms = reserve;
+        split.helper_stream = c->aux_stream;
+        split.helper_after = t.bc1;
+        split.helper_done = get_event(c);
+        t.extra.push_back(split.helper_done);
+    }
+    const int main_sms = reserve > 0 ? std::max(2, c->num_sms - reserve) : 0;
     for (auto &pr : t.panels) {
         pr.start = get_event(c);
         pr.stop = get_event(c);
         cudaEventRecord(pr.start, st);
         compar_status r = COMPAR_OK;
         if (root) {
-            r = launch_on(d, pr.p, reserve_sms);     // the root already holds B
-        } else if (!slabbed) {
-            cudaStreamWaitEvent(st, t.bc1, 0);
+            // the root already holds B: one launch (helper SMs join after the broadcast)
+            r = launch_on(d, pr.p, main_sms, reserve >= 2 ? &split : nullptr);
+        } else if (sp.fused) {
+            WorldLaunch wl = split;
+            wl.flags = flags;
+            wl.seq = seq;
+            wl.slab_w = static_cast<int>(sp.w);
+            wl.nslab = nslab;
+            compar_gemm_desc dd = *d;
+            dd.ldb = d->transB ? K : sp.w;      // (row-major: the 3-D map's row pitch)
             compar_panel pp = pr.p;
             pp.B = replica;
-            r = launch_on(d, pp, 0);
+            r = launch_on(&dd, pp, main_sms, &wl);
         } else {
             for (int j = 0; j < nslab && r == COMPAR_OK; ++j) {
-                const int64_t col0 = j * w, wj = std::min(w, N - col0);
+                const SlabGeo g = slab_geo(sp, j, K, eb, d->transB);
+                const int64_t col0 = sp.col0[j], wj = sp.col0[j + 1] - col0;
                 cudaStreamWaitEvent(st, landed[j], 0);
                 compar_gemm_desc dj = *d;
                 dj.n = wj;
-                dj.ldb = d->transB ? K : wj;
+                dj.ldb = g.pitch;
                 compar_panel pj = pr.p;
-                pj.B = static_cast<const char *>(replica) + static_cast<size_t>(K) * col0 * eb;
+                pj.B = static_cast<const char *>(replica) + g.off;
                 pj.C_in = pr.p.C_in ? pr.p.C_in + col0 : nullptr;
                 pj.C_out = pr.p.C_out + col0;
-                r = launch_on(&dj, pj, j + 1 < nslab ? reserve_sms : 0);
+                r = launch_on(&dj, pj, j + 1 < nslab ? main_sms : 0, nullptr);
             }
         }
         if (r != COMPAR_OK) t.status = COMPAR_E_TASK_FAILED;
         cudaEventRecord(pr.stop, st);
     }
     cudaStreamWaitEvent(st, t.bc1, 0);              // the task ends after its broadcast (B reusable)
+    cudaEventRecord(c->bcast_free, st);             // the next world task may overwrite the slabs
+    c->bcast_free_set = true;
     return COMPAR_OK;
 }
 
@@ -930,6 +1143,9 @@ void compar_config_default(compar_config *cfg) {
     cfg->variant_mask = -1;
     cfg->calib_order = -1;
     cfg->lanes = -1;
+    cfg->calib_prune = -1;
+    cfg->bcast_ctas = -1;
+    cfg->sync_timeout_ms = -1;
 }
 
 const char *compar_last_error(void *) { return t_err.c_str(); }
@@ -962,6 +1178,12 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     if (cfg.calib_order != COMPAR_CALIB_INTERLEAVED && cfg.calib_order != COMPAR_CALIB_BLOCKED)
         return fail(COMPAR_E_INVALID, "calib_order must be INTERLEAVED (0) or BLOCKED (1)");
     if (cfg.builtins < 0) cfg.builtins = 1;
+    if (cfg.calib_prune < 0) cfg.calib_prune = env_int("COMPAR_CALIB_PRUNE", 300);
+    if (cfg.calib_prune != 0 && cfg.calib_prune < 100)
+        return fail(COMPAR_E_INVALID, "calib_prune must be 0 (off) or >= 100 (percent of the best mean)");
+    if (cfg.bcast_ctas < 0) cfg.bcast_ctas = env_int("COMPAR_BCAST_CTAS", 4);
+    if (cfg.bcast_ctas < 1 || cfg.bcast_ctas > 64) return fail(COMPAR_E_INVALID, "bcast_ctas must be in 1..64");
+    if (cfg.sync_timeout_ms < 0) cfg.sync_timeout_ms = env_int("COMPAR_SYNC_TIMEOUT_MS", 600000);
     if (cfg.variant_mask < 0) {
         const char *s = std::getenv("COMPAR_VARIANT_MASK");
         cfg.variant_mask = s ? std::strtoll(s, nullptr, 0) : 0;
@@ -972,6 +1194,9 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     c->hist.calib_k = cfg.calib_k;
     c->hist.calib_warmup = cfg.calib_warmup;
     c->hist.calib_blocked = cfg.calib_order == COMPAR_CALIB_BLOCKED;
+    c->hist.prune_pct = cfg.calib_prune;
+    c->sync_timeout_ms = cfg.sync_timeout_ms;
+    c->knobs = read_knobs();
     c->batch_below_ns = env_int("COMPAR_CALIB_BATCH_NS", 100000);
     const char *pp = cfg.perf_model_path ? cfg.perf_model_path : std::getenv("COMPAR_PERF_MODEL");
     if (pp) c->perf_path = pp;
@@ -989,23 +1214,40 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
                 return fail(COMPAR_E_CUDA, "cannot select device");
             }
         }
-        cudaGetDevice(&c->device);
-        cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
-        if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        // every CUDA call of the set-up is checked; a failure releases what was created
+        auto undo = [c]() {
+            for (cudaStream_t s : {c->stream, c->comm_stream, c->aux_stream, c->h2d_stream, c->d2h_stream})
+                if (s) cudaStreamDestroy(s);
+            for (cudaEvent_t ev : {c->staging_free, c->bcast_free})
+                if (ev) cudaEventDestroy(ev);
+            if (c->red_buf) cudaFree(c->red_buf);
             delete c;
+        };
+        if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
+            (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess) {
+            undo();
+            return cuda_fail(e, "device query");
+        }
+        if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            undo();
             return cuda_fail(e, "cudaStreamCreate");
         }
         if ((e = preload_kernels()) != cudaSuccess) {
-            cudaStreamDestroy(c->stream);
-            delete c;
+            undo();
             return cuda_fail(e, "kernel preload (is this an sm_100 device?)");
         }
-        cudaMalloc(reinterpret_cast<void **>(&c->red_buf), sizeof(int64_t));
-        cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
-        c->bcast_loopback = env_int("COMPAR_BCAST_LOOPBACK", 0) != 0;
-        c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", 16);
-        cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking);
-        cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking);
+        if ((e = cudaMalloc(reinterpret_cast<void **>(&c->red_buf), sizeof(int64_t))) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&c->bcast_free, cudaEventDisableTiming)) != cudaSuccess) {
+            undo();
+            return cuda_fail(e, "runtime streams / events / buffers");
+        }
+        c->bcast_loopback = env_int("COMPAR_BCAST_LOOPBACK", 0);
+        c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", cfg.bcast_ctas);
         c->host_chunks = env_int("COMPAR_HOST_CHUNKS", 32);
     }
     {
@@ -1050,6 +1292,7 @@ compar_status compar_terminate(void *ctx) {
             finish_task(c, kv.second, &rep);
         }
         c->tasks.clear();
+        c->done.clear();
     }
     if (!c->perf_path.empty()) st = compar_perf_save(c, c->perf_path.c_str());
     {
@@ -1069,7 +1312,10 @@ compar_status compar_terminate(void *ctx) {
         if (c->scratch) cudaFree(c->scratch);
         if (c->sort_scratch) cudaFree(c->sort_scratch);
         if (c->sort_done) cudaEventDestroy(c->sort_done);
-        for (cudaStream_t s : {c->comm_stream, c->h2d_stream, c->d2h_stream}) {
+        for (cudaEvent_t ev : {c->staging_free, c->bcast_free})
+            if (ev) cudaEventDestroy(ev);
+        if (c->slab_flags) cudaFree(c->slab_flags);
+        for (cudaStream_t s : {c->comm_stream, c->aux_stream, c->h2d_stream, c->d2h_stream}) {
             if (s) {
                 cudaStreamSynchronize(s);
                 cudaStreamDestroy(s);
@@ -1203,6 +1449,34 @@ int calib_batch(Ctx *c, const Task &t) {
     return static_cast<int>(std::min(64.0, std::ceil(200000.0 / est)));
 }
 
+// Static lower bound (ns) of a built-in GEMM variant on a key (R32): FLOPs at the
+// nominal dense peak of its arithmetic class, compulsory bytes at the nominal HBM bandwidth —
+// both datasheet figures above anything measured, so the bound is below the true time.
+// FFMA class: SMs x 128 FMA/clk x 2 FLOP x 1965 MHz; tensor cores: 2.25 PFLOP/s BF16, half for
+// TF32; HBM3e 8 TB/s.  0 (no bound) for USER variants and other interfaces.
+double static_lb_ns(const Ctx *c, compar_target t, const Key &k) {
+    double peak;
+    switch (t) {
+        case COMPAR_TGT_SIMT_F32:
+        case COMPAR_TGT_TMA_F32:
+        case COMPAR_TGT_SIMT_BF16: peak = static_cast<double>(c->num_sms) * 128.0 * 2.0 * 1.965e9; break;
+        case COMPAR_TGT_TC_BF16:
+        case COMPAR_TGT_TC2_BF16:
+        case COMPAR_TGT_TCW_BF16:
+        case COMPAR_TGT_TCS_BF16: peak = 2.25e15; break;
+        case COMPAR_TGT_TC_TF32:
+        case COMPAR_TGT_TC2_TF32:
+        case COMPAR_TGT_TCW_TF32:
+        case COMPAR_TGT_TCS_TF32: peak = 1.125e15; break;
+        default: return 0.0;
+    }
+    const double m = static_cast<double>(k.m), n = static_cast<double>(k.n), kk = static_cast<double>(k.k);
+    const double flops = 2.0 * m * n * kk;
+    const double eb = k.dtype == COMPAR_BF16 ? 2.0 : 4.0;
+    const double bytes = eb * (m * kk + kk * n) + 4.0 * m * n * (k.beta0 ? 1.0 : 2.0);
+    return std::max(flops / peak, bytes / 8.0e12) * 1e9;
+}
+
 // Steps 3-7 over an eligible set (registry indices idx, history ids names), any interface.
 compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector<int> &names, const Key &key,
                           int hint, bool commit, int *variant, int *mode, bool *warm);
@@ -1217,6 +1491,7 @@ compar_status choose(Ctx *c, const compar_gemm_desc *d, const Plan &plan, bool c
 
 compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector<int> &names, const Key &key,
                           int hint, bool commit, int *variant, int *mode, bool *warm) {
+    Range range("compar.select");
     Plan plan;  // (only .key is used below)
     plan.key = key;
     *warm = false;
@@ -1233,13 +1508,16 @@ compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector
         *mode = kEager;
         return COMPAR_OK;
     }
+    std::vector<double> lb(idx.size(), 0.0);   // R32 static lower bounds (GEMM keys only)
+    if (key.compute >= 0)
+        for (size_t i = 0; i < idx.size(); ++i) lb[i] = static_lb_ns(c, c->variants[idx[i]].target, key);
     if (c->cfg.sched == 2 && key.compute >= 0) {
         // "predict" scheduler (NEXT-2; GEMM keys — its features are FLOPs and bytes): every pending sample is harvested first (the fit reads all
         // keys), then measured means / model predictions decide; unknown variants fall back to
         // calibration below.
         harvest_all(c);
         Mode pm;
-        const int ppos = c->hist.decide_predict(names, plan.key, &pm);
+        const int ppos = c->hist.decide_predict(names, plan.key, &pm, &lb);
         if (ppos >= 0) {
             *variant = idx[ppos];
             *mode = pm;
@@ -1249,24 +1527,29 @@ compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector
         // Only the variants with neither a sample nor a model are calibrated for this key (a
         // variant eligible on too few keys to fit, e.g. the split-K one, must not send every
         // other variant back to calibration).
-        const std::vector<int> unk = c->hist.unknown_predict(names, plan.key);
+        const std::vector<int> unk = c->hist.unknown_predict(names, plan.key, &lb);
         std::vector<int> uidx, unames;
+        std::vector<double> ulb;
         for (int u : unk) {
             uidx.push_back(idx[u]);
             unames.push_back(names[u]);
+            ulb.push_back(lb[u]);
         }
         if (!unames.empty() && unames.size() < names.size()) {
             Mode m;
-            const int pos = c->hist.decide(unames, plan.key, &m);
+            const int pos = c->hist.decide(unames, plan.key, &m, &ulb);
             *variant = uidx[pos];
             *mode = m;
             if (commit) *warm = c->hist.commit(unames[pos], plan.key);
             return COMPAR_OK;
         }
     }
-    if (!c->hist.calibrating(names, plan.key)) harvest_key(c, plan.key);
+    // Step 6: pending samples of the key are harvested (blocking) before a model decision — and,
+    // with pruning on, before a calibration decision too, since R32 reads the key's best mean
+    // (so every decision stays a function of the submission sequence and the measured values).
+    if (c->hist.prune_pct > 0 || !c->hist.calibrating(names, plan.key, &lb)) harvest_key(c, plan.key);
     Mode m;
-    const int pos = c->hist.decide(names, plan.key, &m);
+    const int pos = c->hist.decide(names, plan.key, &m, &lb);
     *variant = idx[pos];
     *mode = m;
     if (commit) *warm = c->hist.commit(names[pos], plan.key);
@@ -1286,7 +1569,9 @@ compar_status compar_select(void *ctx, const compar_gemm_desc *d, int *variant, 
     int v = -1, m = kNoop;
     bool warm;
     if (d->m > 0 && d->n > 0 && d->k > 0 && d->alpha != 0.f) {
+        c->in_select = true;    // never a collective harvest from a query
         s = choose(c, d, plan, false, &v, &m, &warm);
+        c->in_select = false;
         if (s != COMPAR_OK) return s;
     }
     if (variant) *variant = v;
@@ -1301,6 +1586,8 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
     compar_status s = validate(c, d);
     if (s != COMPAR_OK) return s;
     c->stats.submits++;
+    if (c->sticky != COMPAR_OK && d->world != COMPAR_WORLD_LOCAL && c->nranks > 1)
+        return fail(c->sticky, "cross-rank path failed earlier: " + c->sticky_msg);
     Task t;
     t.id = c->next_task++;
     t.world = d->world == COMPAR_WORLD_PANELS;
@@ -1464,6 +1751,9 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             cudaEventRecord(t.begin, st);
         }
         const bool pipelined = host && gemm && !t.world && t.panels.size() == 1 && c->host_chunks > 1 && d->m >= 512;
+        // the staging buffers are shared by every host-mode task of the context: a task on another
+        // stream must not overwrite them while the previous host task still reads or returns them
+        if (host && c->staging_free_set) cudaStreamWaitEvent(st, c->staging_free, 0);
         if (host && !pipelined) {
             if (a_bytes) cudaMemcpyAsync(const_cast<void *>(A), d->A, a_bytes, cudaMemcpyHostToDevice, st);
             if (b_bytes && root_b) cudaMemcpyAsync(const_cast<void *>(B), d->B, b_bytes, cudaMemcpyHostToDevice, st);
@@ -1471,13 +1761,21 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             c->stats.bytes_h2d += static_cast<int64_t>(a_bytes + (root_b ? b_bytes : 0) + cin_bytes);
         }
         const Variant *var = gemm ? &c->variants[t.variant] : nullptr;
-        auto launch_on = [&](const compar_gemm_desc *dd, const compar_panel &pp, int sms) -> compar_status {
+        Range launch_range("compar.launch");
+        // sms: SMs a launch may use (0 = all; world mode leaves the broadcast's share); wl: the
+        // wide variant's world-mode extras (slab flags; helper launch that returns the reserve)
+        auto launch_on = [&](const compar_gemm_desc *dd, const compar_panel &pp, int sms,
+                             const WorldLaunch *wl = nullptr) -> compar_status {
             if (!gemm) return run_scale(c, dd, pp, st);
             if (var->target == COMPAR_TGT_USER) {
                 c->stats.launches++;
                 return var->fn(dd, &pp, st, var->user, nullptr);
             }
-            return run_builtin(c, var->target, dd, pp, st, sms);
+            const bool wide = var->target == COMPAR_TGT_TCW_TF32 || var->target == COMPAR_TGT_TCW_BF16;
+            if (wide && wl && wl->helper_sms > 0) sms = 0;      // the launcher splits main / helper itself
+            const compar_status rs = run_builtin(c, var->target, dd, pp, st, sms, wide ? wl : nullptr);
+            if (rs == COMPAR_OK && wide && wl && wl->launches > 1) c->stats.launches += wl->launches - 1;   // helper
+            return rs;
         };
         const bool bcast = t.world && gemm && (c->nranks > 1 || c->bcast_loopback);
         if (pipelined) {
@@ -1514,7 +1812,8 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
                 cudaEventRecord(pr.stop, st);
             }
         } else {
-            compar_status r = world_pipeline(c, d, t, st, B, b_bytes, launch_on);
+            const bool fused_ok = var && (var->target == COMPAR_TGT_TCW_TF32 || var->target == COMPAR_TGT_TCW_BF16);
+            compar_status r = world_pipeline(c, d, t, st, B, fused_ok, launch_on);
             if (r != COMPAR_OK && t.status == COMPAR_OK) t.status = r;
         }
         if (host && !pipelined && mloc > 0) {
@@ -1523,6 +1822,10 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
             (void)cout_bytes;
         }
         if (t.end) cudaEventRecord(t.end, st);
+        if (host) {
+            cudaEventRecord(c->staging_free, st);
+            c->staging_free_set = true;
+        }
         if (t.tasks) {
             cudaEventRecord(c->lane_done[t.lane], st);
             if (calib_task && c->placer.lanes() > 1) {
@@ -1702,11 +2005,17 @@ compar_status compar_sync(void *ctx, uint64_t task, compar_report *out) {
     compar_report rep;
     std::memset(&rep, 0, sizeof(rep));
     compar_status st = COMPAR_OK;
+    Range range("compar.sync");
     if (task == COMPAR_TASK_ALL) {
         std::vector<uint64_t> ids;
         for (auto &kv : c->tasks) ids.push_back(kv.first);
         compar_status xs = exchange_ids(c, ids);  // collective in the task-parallel world
         if (xs != COMPAR_OK) return xs;
+        for (auto &kv : c->done) {                // implicitly harvested, not yet synced
+            rep = kv.second.second;
+            if (kv.second.first != COMPAR_OK) st = kv.second.first;
+        }
+        c->done.clear();
         for (auto &kv : c->tasks) {
             compar_status s = finish_task(c, kv.second, &rep);
             if (s != COMPAR_OK) st = s;
@@ -1717,7 +2026,16 @@ compar_status compar_sync(void *ctx, uint64_t task, compar_report *out) {
         c->cal_fence_set = false;
     } else {
         auto it = c->tasks.find(task);
-        if (it == c->tasks.end()) return fail(COMPAR_E_UNKNOWN_TASK, "unknown or already-synced task");
+        if (it == c->tasks.end()) {
+            auto dn = c->done.find(task);         // harvested by the selector: its stored report
+            if (dn == c->done.end()) return fail(COMPAR_E_UNKNOWN_TASK, "unknown or already-synced task");
+            rep = dn->second.second;
+            st = dn->second.first;
+            c->done.erase(dn);
+            if (out) *out = rep;
+            if (st != COMPAR_OK) t_err = "task failed (harvested before this sync)";
+            return st;
+        }
         compar_status xs = exchange_ids(c, {task});
         if (xs != COMPAR_OK) return xs;
         st = finish_task(c, it->second, &rep);
@@ -1829,8 +2147,16 @@ compar_status compar_comm_init(void *ctx, int nranks, int rank, const void *id, 
     cudaSetDevice(c->device);
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
-    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
-    if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    // The broadcast of B overlaps the GEMMs, so NCCL's kernels get a bounded SM budget: maxCTAs =
+    // bcast_ctas, which is also the SM reserve a GEMM overlapping a broadcast leaves free.
+    ncclConfig_t config = NCCL_CONFIG_INITIALIZER;
+    config.blocking = 1;
+    config.minCTAs = 1;
+    config.maxCTAs = c->cfg.bcast_ctas;
+    ncclResult_t r = ncclCommInitRankConfig(&c->comm, nranks, uid, rank, &config);
+    if (r != ncclSuccess) return fail(COMPAR_E_NCCL, std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r));
+    c->sticky = COMPAR_OK;
+    c->sticky_msg.clear();
     c->nranks = nranks;
     c->rank = rank;
     return COMPAR_OK;

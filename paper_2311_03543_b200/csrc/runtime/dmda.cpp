@@ -20,16 +20,36 @@ void Placer::reset() {
 }
 
 int Placer::place(const Access &a, int64_t exec_ns, int64_t *end, std::vector<uint64_t> *deps) const {
-    // Residency: each range this task reads is valid only on the rank of its latest writer.
+    // Residency: each byte a task reads is valid only on the rank of its latest writer.  Per read
+    // span, walk the overlapping writers from the latest back, each claiming the part of the span
+    // no later writer covers; every claiming writer's rank must agree (a span whose bytes were
+    // last written on two ranks cannot be read anywhere: no inter-rank transfer, R22).
     int pin = -1;
     for (const Span &s : a.reads) {
-        const Live *latest = nullptr;
+        std::vector<const Live *> ws;
         for (const Live &l : live_)
-            if (l.write && overlap(s, l.s) && (!latest || l.task > latest->task)) latest = &l;
-        if (!latest) continue;
-        const int r = rank_of(latest->w);
-        if (pin >= 0 && pin != r) return -1;
-        pin = r;
+            if (l.write && overlap(s, l.s)) ws.push_back(&l);
+        std::sort(ws.begin(), ws.end(), [](const Live *x, const Live *y) { return x->task > y->task; });
+        std::vector<Span> open{s};          // parts of s no later writer has covered yet
+        for (const Live *l : ws) {
+            std::vector<Span> rest;
+            bool claims = false;
+            for (const Span &u : open) {
+                if (!overlap(u, l->s)) {
+                    rest.push_back(u);
+                    continue;
+                }
+                claims = true;
+                if (u.lo < l->s.lo) rest.push_back({u.lo, l->s.lo});
+                if (l->s.hi < u.hi) rest.push_back({l->s.hi, u.hi});
+            }
+            open.swap(rest);
+            if (!claims) continue;
+            const int r = rank_of(l->w);
+            if (pin >= 0 && pin != r) return -1;
+            pin = r;
+            if (open.empty()) break;
+        }
     }
     const int W = workers();
     int best = -1;

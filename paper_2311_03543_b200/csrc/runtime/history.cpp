@@ -15,33 +15,68 @@ int History::intern(const std::string &name) {
     return id;
 }
 
-bool History::calibrating(const std::vector<int> &ids, const Key &k) {
+bool History::best_mean(const std::vector<int> &ids, const Key &k, unsigned __int128 *sum, int64_t *count) const {
+    bool found = false;
+    for (int id : ids) {
+        const Record *r = find(id, k);
+        if (!r || r->count == 0) continue;
+        // r < best  <=>  r.sum * best.count < best.sum * r.count (exact)
+        if (!found || r->sum_ns * static_cast<unsigned __int128>(*count) <
+                          *sum * static_cast<unsigned __int128>(r->count)) {
+            *sum = r->sum_ns;
+            *count = r->count;
+            found = true;
+        }
+    }
+    return found;
+}
+
+bool History::pruned(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb, size_t i) {
+    if (prune_pct <= 0) return false;
+    unsigned __int128 bs = 0;
+    int64_t bc = 0;
+    if (!best_mean(ids, k, &bs, &bc)) return false;
+    const Record &r = rec(ids[i], k);
+    // measured: mean_i > P/100 * best  <=>  100 * sum_i * bc > P * bs * count_i
+    if (r.count > 0 && 100 * r.sum_ns * static_cast<unsigned __int128>(bc) >
+                           static_cast<unsigned __int128>(prune_pct) * bs * static_cast<unsigned __int128>(r.count))
+        return true;
+    // static: lb_i > P/100 * best  <=>  lb_i * 100 * bc > P * bs   (double, same order as the oracle)
+    const double l = lb ? (*lb)[i] : 0.0;
+    return l > 0.0 && l * 100.0 * static_cast<double>(bc) > static_cast<double>(prune_pct) * static_cast<double>(bs);
+}
+
+bool History::calibrating(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb) {
     const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
-    for (int id : ids)
-        if (rec(id, k).seen < need) return true;
+    for (size_t i = 0; i < ids.size(); ++i)
+        if (rec(ids[i], k).seen < need && !pruned(ids, k, lb, i)) return true;
     return false;
 }
 
-int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode) {
+int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const std::vector<double> *lb) {
     const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
     // Calibration.  Interleaved: least-seen eligible variant, first in registry order on ties.
-    // Blocked: first variant (in eligibility order) that has not completed its W + K executions.
+    // Blocked: the variant of smallest lower bound (ties: eligibility order) that has not completed
+    // its W + K executions.  Pruned variants (R32) are done calibrating.
     int best = -1;
     int64_t best_seen = 0;
+    double best_lb = 0.0;
     for (size_t i = 0; i < ids.size(); ++i) {
         const int64_t s = rec(ids[i], k).seen;
+        if (s >= need || pruned(ids, k, lb, i)) continue;
+        const double l = lb ? (*lb)[i] : 0.0;
         if (calib_blocked) {
-            if (s < need) {
+            if (best < 0 || l < best_lb) {
                 best = static_cast<int>(i);
                 best_seen = s;
-                break;
+                best_lb = l;
             }
         } else if (best < 0 || s < best_seen) {
             best = static_cast<int>(i);
             best_seen = s;
         }
     }
-    if (best >= 0 && best_seen < need) {
+    if (best >= 0) {
         *mode = best_seen < calib_warmup ? kWarmup : kCalib;
         return best;
     }
@@ -165,38 +200,65 @@ bool History::predict(int id, const Key &q, double *ns) const {
     return true;
 }
 
-int History::decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode) const {
-    int best = -1;
-    double best_est = 0;
-    bool best_pred = false;
+bool History::estimate(int id, const Key &k, double *est, bool *pred) const {
+    const Record *r = find(id, k);
+    if (r && r->count > 0) {
+        *est = static_cast<double>(r->sum_ns) / static_cast<double>(r->count);
+        *pred = false;
+        return true;
+    }
+    *pred = true;
+    return predict(id, k, est);
+}
+
+int History::decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode, const std::vector<double> *lb) const {
+    // best estimate over the variants that have one (for the lower-bound skip of the others)
+    double floor_est = 0.0;
+    bool have = false;
+    std::vector<double> est(ids.size(), 0.0);
+    std::vector<char> known(ids.size(), 0), pred(ids.size(), 0);
     for (size_t i = 0; i < ids.size(); ++i) {
-        const Record *r = find(ids[i], k);
-        double est;
-        bool pred = false;
-        if (r && r->count > 0) {
-            est = static_cast<double>(r->sum_ns) / static_cast<double>(r->count);
-        } else if (predict(ids[i], k, &est)) {
-            pred = true;
-        } else {
-            return -1;
-        }
-        if (best < 0 || est < best_est) {
-            best = static_cast<int>(i);
-            best_est = est;
-            best_pred = pred;
+        bool p = false;
+        if (estimate(ids[i], k, &est[i], &p)) {
+            known[i] = 1;
+            pred[i] = p ? 1 : 0;
+            if (!have || est[i] < floor_est) floor_est = est[i];
+            have = true;
         }
     }
-    *mode = best_pred ? kPredict : kModel;
+    int best = -1;
+    for (size_t i = 0; i < ids.size(); ++i) {
+        if (!known[i]) {
+            const double l = lb ? (*lb)[i] : 0.0;
+            if (have && prune_pct > 0 && l > 0.0 && l * 100.0 > static_cast<double>(prune_pct) * floor_est) continue;
+            return -1;
+        }
+        if (best < 0 || est[i] < est[best]) best = static_cast<int>(i);
+    }
+    if (best < 0) return -1;
+    *mode = pred[best] ? kPredict : kModel;
     return best;
 }
 
-std::vector<int> History::unknown_predict(const std::vector<int> &ids, const Key &k) const {
-    std::vector<int> out;
+std::vector<int> History::unknown_predict(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb) const {
+    double floor_est = 0.0;
+    bool have = false;
+    std::vector<int> unk;
     for (size_t i = 0; i < ids.size(); ++i) {
-        const Record *r = find(ids[i], k);
-        double est;
-        if ((r && r->count > 0) || predict(ids[i], k, &est)) continue;
-        out.push_back(static_cast<int>(i));
+        double e;
+        bool p;
+        if (estimate(ids[i], k, &e, &p)) {
+            if (!have || e < floor_est) floor_est = e;
+            have = true;
+        } else {
+            unk.push_back(static_cast<int>(i));
+        }
+    }
+    std::vector<int> out;
+    for (int i : unk) {
+        const double l = lb ? (*lb)[i] : 0.0;
+        if (have && prune_pct > 0 && l > 0.0 && l * 100.0 > static_cast<double>(prune_pct) * floor_est) continue;
+        out.push_back(i);
     }
     return out;
 }

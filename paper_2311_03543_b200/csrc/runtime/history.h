@@ -9,7 +9,14 @@
 //   * calibration: while some eligible variant has seen < W + K, pick argmin seen
 //     (ties -> lowest registry index; "interleaved") or the first variant in eligibility order with
 //     seen < W + K ("blocked", R19); the first W executions of a variant are warm-ups (dropped);
-//   * model: argmin mean ns over eligible variants with count > 0 (ties -> lowest index).
+//   * model: argmin mean ns over eligible variants with count > 0 (ties -> lowest index);
+//   * calibration pruning (R32; VERDICT r1 "bound the calibration cost"): with
+//     prune = P percent > 0, a variant stops calibrating for a key as soon as its mean exceeds
+//     P/100 x the best mean of the key, or its static lower bound lb (FLOPs at its class's nominal
+//     peak, bytes at nominal HBM) exceeds P/100 x that best mean; blocked calibration visits the
+//     variants in increasing lb (ties: eligibility order), so the fast classes set the best mean
+//     before the slow ones are considered.  lb = 0 (USER variants, other interfaces) never prunes
+//     statically and keeps the eligibility order.
 #pragma once
 #include <cstdint>
 #include <map>
@@ -48,6 +55,7 @@ public:
     int calib_warmup = 1;
     int calib_k = 3;
     bool calib_blocked = true;
+    int prune_pct = 300;   // 0: no pruning (SPEC S:363-371 behaviour)
 
     // Records belong to variant NAMES (so a loaded perf model applies to whichever registry index
     // that name gets); names are interned to small ids for the hot path.
@@ -59,10 +67,13 @@ public:
         auto it = table_.find({id, k});
         return it == table_.end() ? nullptr : &it->second;
     }
-    // True if any eligible variant is still calibrating for this key.
-    bool calibrating(const std::vector<int> &ids, const Key &k);
+    // True if any eligible variant is still calibrating for this key (pruned ones are done).
+    // lb: per position of ids, the static lower bound in ns (nullptr or 0 entries: none).
+    bool calibrating(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb = nullptr);
     // Decision over the ordered eligible list: returns the position in `ids`.
-    int decide(const std::vector<int> &ids, const Key &k, Mode *mode);
+    int decide(const std::vector<int> &ids, const Key &k, Mode *mode, const std::vector<double> *lb = nullptr);
+    // R32: is position i of ids pruned from calibration for k?
+    bool pruned(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb, size_t i);
     // Account an assigned execution; returns true if it is a warm-up.
     bool commit(int id, const Key &k);
     void harvest(int id, const Key &k, int64_t ns);
@@ -81,12 +92,19 @@ public:
     bool predict(int id, const Key &k, double *ns) const;
     // Decision of the "predict" scheduler: measured mean where (v, key) has samples, prediction
     // otherwise; returns -1 (caller falls back to calibration) if some variant has neither.
-    int decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode) const;
-    // Positions (into ids) of the variants with neither a sample for k nor a prediction: the only
-    // ones the predict scheduler still has to calibrate for k.
-    std::vector<int> unknown_predict(const std::vector<int> &ids, const Key &k) const;
+    // A variant with neither whose lower bound exceeds prune_pct/100 x the best estimate is skipped.
+    int decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode,
+                       const std::vector<double> *lb = nullptr) const;
+    // Positions (into ids) of the variants with neither a sample for k nor a prediction (and not
+    // skipped by their lower bound): the only ones the predict scheduler still has to calibrate.
+    std::vector<int> unknown_predict(const std::vector<int> &ids, const Key &k,
+                                     const std::vector<double> *lb = nullptr) const;
 
 private:
+    // best (smallest) mean over ids with samples: as the exact fraction sum / count; false if none
+    bool best_mean(const std::vector<int> &ids, const Key &k, unsigned __int128 *sum, int64_t *count) const;
+    // predict-mode estimate of position i (measured mean, else prediction); false if neither
+    bool estimate(int id, const Key &k, double *est, bool *pred) const;
     std::map<std::string, int> ids_;
     std::vector<std::string> names_;
     std::map<std::pair<int, Key>, Record> table_;

@@ -23,14 +23,25 @@ def to_host_f64(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def assert_parity(got, ref, A, B, C0, alpha, beta, dtype, tf32, tol, what=""):
+def tc_accum_tol(k):
+    """rel-Fro tolerance of a tensor-core variant whose operands the oracle consumes exactly (BF16):
+    the tcgen05 FP32 accumulator is not round-to-nearest — measured 3.7e-5 at K = 32768 on
+    U(-1,1) against 3.2e-6 for a simulated round-to-nearest FP32 sum (R33) — so the
+    bound grows like one truncation of 2^-23 per K = 16 MMA step: K/16 * 2^-23 = K * 2^-27, and
+    never below the strict-FP32 1e-5."""
+    return max(1e-5, k * 2.0 ** -27)
+
+
+def assert_parity(got, ref, A, B, C0, alpha, beta, dtype, tf32, tol, what="", tc=False):
     """The two parity checks against the FP64 oracle: the BASELINE max relative Frobenius error
-    (<= tol) AND the componentwise FP32-accumulation bound of oracle.gemm.elementwise_bound on
-    every element (so a handful of wrong elements cannot hide inside a small norm ratio)."""
+    (<= tol; for tensor-core variants without TF32 truncation at least tc_accum_tol(K)) AND the
+    componentwise FP32-accumulation bound of oracle.gemm.elementwise_bound on every element (so a
+    handful of wrong elements cannot hide inside a small norm ratio)."""
     from oracle import gemm as og
+    if tc and not tf32:
+        tol = max(tol, tc_accum_tol(np.asarray(A).shape[1]))
     err = og.rel_fro(got, ref)
-    assert err <= tol, (what, "rel_fro", err, tol)
     bound = og.elementwise_bound(A, B, C0, alpha, beta, dtype=dtype, tf32=tf32)
     v = og.elementwise_violation(got, ref, bound)
-    assert v <= 1.0, (what, "elementwise bound exceeded by", v)
+    assert err <= tol and v <= 1.0, (what, "rel_fro", err, "tol", tol, "elementwise violation", v)
     return err

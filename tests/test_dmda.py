@@ -63,6 +63,53 @@ def test_reads_from_two_ranks_are_refused():
     assert o.submit(4, "k", [0], [X, Y], [(500, 600)], lambda v: 300)[2] == 0
 
 
+def test_split_writers_of_one_read_span_are_refused():
+    """C rows [0, 500) written on rank 0 and rows [500, 1000) on rank 1 — a task
+    reading all of C has bytes whose latest writers ran on two ranks: refused, although the single
+    LATEST writer alone would pin it to rank 1.  A later writer covering the whole span re-pins it."""
+    o = DmdaOracle(1, nranks=2, lanes=1)
+    _train(o, "k", lambda v: 300)
+    C = (0, 1000)
+    assert o.submit(1, "k", [0], [], [(0, 500)], lambda v: 300)[2] == 0
+    assert o.submit(2, "k", [0], [], [(500, 1000)], lambda v: 300)[2] == 1
+    assert o.submit(3, "k", [0], [C], [(2000, 2100)], lambda v: 300) is None
+    # one buffer written whole on rank 0, then its first half rewritten on rank 1: refused too
+    o.sync_all()
+    assert o.submit(4, "k", [0], [], [C], lambda v: 300)[2] == 0
+    assert o.submit(5, "k", [0], [], [(3000, 3100)], lambda v: 300)[2] == 1
+    assert o.submit(6, "k", [0], [(3000, 3100)], [(0, 500)], lambda v: 300)[2] == 1
+    assert o.submit(7, "k", [0], [C], [(4000, 4100)], lambda v: 300) is None
+    # ... but a whole-span rewrite on rank 1 makes every byte's latest writer rank 1
+    assert o.submit(8, "k", [0], [(3000, 3100)], [C], lambda v: 300)[2] == 1
+    assert o.submit(9, "k", [0], [C], [(5000, 5100)], lambda v: 300)[2] == 1
+
+
+def test_runtime_refuses_split_writers_like_the_oracle():
+    """The same split-writer stream through the C runtime (2 ranks, virtual clock, world_init)."""
+    ctx = cm.Compar(virtual_clock=1)
+    ctx.register_variant("v", cm.TGT_USER, lambda desc, panel, stream, user, vns: vns.__setitem__(0, 300) or 0)
+    ctx.world_init(2, 0)
+    ctx.set_reduce_n_hook(lambda buf, n, user: None)      # this process plays both ranks' samples
+    kw = dict(lda=1, ldb=1, ldc_in=1, ldc_out=1, alpha=1.0, world=cm.WORLD_TASKS)
+
+    def sub(c_out, n, beta=0.0, c_in=None):          # a 1 x n task: C spans n * 4 bytes
+        return ctx.submit(cm.make_desc(1, n, 1, A=0x20, B=0x10, C_in=c_in, C_out=c_out, beta=beta,
+                                       lda=1, ldb=n, ldc_in=n, ldc_out=n, alpha=1.0, world=cm.WORLD_TASKS))
+    for n in (250, 500):                                 # train both keys: calibration -> model mode
+        for _ in range(6):
+            ctx.sync(sub(0x30000, n))
+    ctx.sync()
+    t1 = sub(0x1000, 250)                                # bytes [0, 1000) of C: rank 0 (both idle)
+    t2 = ctx.submit(cm.make_desc(1, 250, 1, A=0x20, B=0x10, C_out=0x1000 + 1000, lda=1, ldb=250, ldc_in=250,
+                                 ldc_out=250, alpha=1.0, world=cm.WORLD_TASKS))   # [1000, 2000): rank 1
+    with pytest.raises(cm.ComparError) as e:             # reads all of C: halves last written on 2 ranks
+        sub(0x5000, 500, beta=0.5, c_in=0x1000)
+    assert e.value.status == cm.E_INVALID
+    assert (ctx.sync(t1).rank, ctx.sync(t2).rank) == (0, 1)
+    ctx.sync()
+    ctx.terminate()
+
+
 def test_war_across_ranks_needs_no_order_but_same_rank_does():
     o = DmdaOracle(1, nranks=2, lanes=2)
     _train(o, "k", lambda v: 100)
@@ -122,11 +169,8 @@ def test_runtime_placement_matches_oracle(lanes):
         pending.append((t, exp))
         if sync or i == len(wl.tasks) - 1:
             reps = {}
-            for tt, _ in pending:
-                try:
-                    reps[tt] = ctx.sync(tt)
-                except cm.ComparError:
-                    pass                                  # harvested by a model decision already
+            for tt, _ in pending:          # (tasks harvested by a decision keep their reports)
+                reps[tt] = ctx.sync(tt)
             ctx.sync()
             orc.sync_all()
             for tt, (v, mode, w) in pending:

@@ -16,7 +16,10 @@ pytestmark = pytest.mark.gpu
 WORLD = 3
 CASES = [("tc_bf16_2sm", "bf16", 1000, 1536, 768, 0, 1536, 4),
          ("tc_tf32_2sm", "f32", 700, 1280, 512, 1, 512, 3),
-         ("tc_bf16", "bf16", 900, 1001, 640, 0, 1008, 4)]     # N slabs not packable: one raw chunk
+         ("tc_bf16", "bf16", 900, 1001, 640, 0, 1008, 4),     # N slabs not packable: one padded slab
+         # the wide pair kernel: one fused launch per rank, waiting per slab on the chain's ready flags
+         ("tc_bf16_2sm_w", "bf16", 1000, 2048, 640, 0, 2048, 4),
+         ("tc_tf32_2sm_w", "f32", 700, 1536, 520, 1, 520, 3)]
 
 
 def _port():

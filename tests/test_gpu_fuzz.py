@@ -87,4 +87,4 @@ def _fuzz_case(m, n, k, compute, transB, pad, beta, integer, seed, pick):
         name = c.variants()[d.variant_hint][0]
         tf32 = name.startswith("tc_tf32")
         tol = TOL[compute] if tf32 or compute != cm.COMPUTE_TF32 else 1e-5
-        assert_parity(got, ref, A, B, C0, alpha, beta, dt, tf32, tol, (name, m, n, k))
+        assert_parity(got, ref, A, B, C0, alpha, beta, dt, tf32, tol, (name, m, n, k), tc=name.startswith("tc_"))

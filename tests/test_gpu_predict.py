@@ -3,8 +3,9 @@ PAPER.md P:224 / P:308 "additional training of performance models") on a BASELIN
 subset with real kernels and real cudaEvent samples.
 
 * Every decision (variant, mode) equals oracle/selector.py's decide_predict / calibration
-  decision, fed with the runtime's OWN history as written by compar_perf_save just before the
-  submit (every task is synced before the next decision, so nothing is pending);
+  decision (with the R32 pruning and static lower bounds), fed with the runtime's OWN history as
+  written by compar_perf_save just before the submit (every task is synced before the next
+  decision, so nothing is pending);
 * every task's C is checked against the FP64 oracle (small shapes in full; large shapes on
   sampled full rows), at the tolerance of the variant that ran.
 """
@@ -46,18 +47,30 @@ def load_dump(path, names):
     return hist
 
 
-def expected(orc, key, elig):
+def lb_class(name):
+    """R32 arithmetic class of a built-in variant (the static lower bound's peak)."""
+    if name.startswith("tc_tf32"):
+        return "tf32"
+    if name.startswith("tc_bf16"):
+        return "bf16"
+    return "ffma" if name in ("simt_f32", "tma_f32", "simt_bf16") else None
+
+
+def expected(orc, key, elig, lb):
     """The predict scheduler's decision (runtime compar.cpp choose_core, oracle restatement)."""
-    dp = orc.decide_predict(key, elig)
+    dp = orc.decide_predict(key, elig, lb)
     if dp is not None:
         return dp, orc
-    unk = orc.unknown_predict(key, elig)
-    return orc.decide(key, unk if unk and len(unk) < len(elig) else elig), orc
+    unk = orc.unknown_predict(key, elig, lb)
+    if unk and len(unk) < len(elig):
+        return orc.decide(key, unk, [lb[elig.index(v)] for v in unk]), orc
+    return orc.decide(key, elig, lb), orc
 
 
 def test_predict_scheduler_real_kernels_match_oracle():
     ctx = cm.Compar(sched=cm.SCHED_PREDICT)
     names = [n for n, _ in ctx.variants()]
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
     st = torch.cuda.current_stream().cuda_stream
     rng = np.random.Generator(np.random.PCG64(7))
     stream = [SHAPES[i] for i in rng.integers(0, len(SHAPES), 70)]
@@ -82,11 +95,12 @@ def test_predict_scheduler_real_kernels_match_oracle():
             d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=0.0, compute=cm.COMPUTE_TF32,
                              stream=st)
             ctx.perf_save(path)
-            orc = so.SelectorOracle(len(names), blocked=True)
+            orc = so.SelectorOracle(len(names), blocked=True, prune_pct=300)
             orc.hist = load_dump(path, names)
             elig = ctx.eligible(d)
             key = (m, n, k, so.F32, so.COMPUTE_TF32, 0, 1)
-            (ev, emode), _ = expected(orc, key, elig)
+            lb = [so.SelectorOracle.static_lb_ns(lb_class(names[v]), key, sms) for v in elig]
+            (ev, emode), _ = expected(orc, key, elig, lb)
             r = ctx.run(d)
             assert r.status == 0
             assert (r.variant, r.mode) == (ev, emode), (i, s, names[r.variant], r.mode, names[ev], emode)
@@ -95,7 +109,7 @@ def test_predict_scheduler_real_kernels_match_oracle():
             got = C[torch.as_tensor(rows, device="cuda")].double().cpu().numpy()
             tf32 = names[r.variant].startswith("tc_tf32")
             assert_parity(got, ref, Ar, Bh, None, 1.5, 0.0, "f32", tf32, 5e-3 if tf32 else 1e-5,
-                          (i, s, names[r.variant]))
+                          (i, s, names[r.variant]), tc=names[r.variant].startswith("tc_"))
     finally:
         ctx.terminate()
     # the generalisation did its job: shapes first seen after the fit decided without calibrating

@@ -72,8 +72,9 @@ def test_real_event_selector_crossover(golden):
 @pytest.mark.parametrize("order", [cm.CALIB_INTERLEAVED, cm.CALIB_BLOCKED])
 def test_config1_calibration_trace(order):
     """Config 1 (64^3 FP32, COMPUTE_TF32): each eligible variant x (1 warm-up + 3 timed)
-    calibration runs in registry order (interleaved or blocked), then model mode picks the argmin."""
-    ctx = cm.Compar(calib_order=order)
+    calibration runs in registry order (interleaved or blocked), then model mode picks the argmin.
+    (The SPEC plan: calibration pruning, R32, is off here — it is pinned by the selector tests.)"""
+    ctx = cm.Compar(calib_order=order, calib_prune=0)
     m = 64
     A = device_matrix(gen.TAG_A, m, m)
     B = device_matrix(gen.TAG_B, m, m)
@@ -174,3 +175,32 @@ def test_long_stream_no_resource_growth():
     assert st.failed == 0 and st.submits >= 5000
     assert calls["n"] == 500
     ctx.terminate()
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_calibration_prunes_ffma_variants_at_large_keys(dt):
+    """R32 on real kernels: at 8192^3 the FFMA variants' static lower bound
+    (FLOPs at the FFMA peak) exceeds 3x the tensor-core variants' measured mean, so blocked
+    calibration (tensor classes first, smaller bound) never launches them; model mode follows."""
+    import gen
+    from gen.device import device_matrix
+    m = n = k = 8192
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt)
+    C = device_matrix(gen.TAG_C, m, n)
+    with cm.Compar() as ctx:
+        names = [v for v, _ in ctx.variants()]
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=0.5,
+                         in_dtype=cm.BF16 if dt == "bf16" else cm.F32,
+                         compute=cm.COMPUTE_BF16 if dt == "bf16" else cm.COMPUTE_TF32)
+        ran = []
+        for _ in range(40):
+            r = ctx.run(d)
+            ran.append(names[r.variant])
+            if r.mode == cm.MODE_MODEL:
+                break
+        assert r.mode == cm.MODE_MODEL and names[r.variant].startswith("tc_")
+        ffma = ["simt_bf16"] if dt == "bf16" else ["simt_f32", "tma_f32"]
+        assert not set(ffma) & set(ran), ran
+        for v in ffma:
+            assert ctx.history(names.index(v), d).seen == 0

@@ -40,7 +40,11 @@ def loop_ctx():
 
 
 CASES = [("tc_bf16", 1000, 1000, 704, 0), ("tc_bf16", 1000, 1000, 704, 1), ("tc_bf16_2sm", 777, 2048, 512, 0),
-         ("tc_tf32", 300, 1280, 256, 0), ("tc_tf32_2sm", 512, 1030, 300, 1), ("simt_f32", 200, 600, 100, 0)]
+         ("tc_tf32", 300, 1280, 256, 0), ("tc_tf32_2sm", 512, 1030, 300, 1), ("simt_f32", 200, 600, 100, 0),
+         # the wide pair kernel: N a multiple of 512 -> one fused launch waiting per slab on device flags
+         ("tc_bf16_2sm_w", 1000, 2048, 704, 0), ("tc_bf16_2sm_w", 777, 3072, 300, 1),
+         ("tc_tf32_2sm_w", 600, 1536, 260, 0), ("tc_tf32_2sm_w", 520, 1024, 512, 1),
+         ("tc_bf16_2sm_w", 640, 1000, 512, 0)]          # (N not a multiple of 512: per-slab launches)
 
 
 @pytest.mark.parametrize("chunks", [1, 3, 4])
@@ -71,7 +75,48 @@ def test_loopback_slab_pipeline_bitwise(loop_ctx, chunks, name, m, n, k, tb):
         Ah, Bh, Ch = gen.matrix(gen.TAG_A, m, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt), gen.matrix(gen.TAG_C, m, n)
         ref = og.gemm(Ah, Bh, Ch, alpha=1.5, beta=0.5, dtype=dt)
         tf32 = name.startswith("tc_tf32")
-        assert_parity(got, ref, Ah, Bh, Ch, 1.5, 0.5, dt, tf32, 5e-3 if tf32 else 1e-5, name)
+        assert_parity(got, ref, Ah, Bh, Ch, 1.5, 0.5, dt, tf32, 5e-3 if tf32 else 1e-5, name, tc=name.startswith("tc_"))
+
+
+@pytest.mark.parametrize("name,m,n,k,tb", [("tc_bf16_2sm_w", 4096, 4096, 1024, 0), ("tc_tf32_2sm_w", 3072, 4096, 520, 1),
+                                            ("tc_bf16_2sm_w", 4096, 8192, 2048, 0)])
+def test_loopback_fused_with_helper_launch_bitwise(name, m, n, k, tb):
+    """COMPAR_BCAST_LOOPBACK=2: the loopback pipeline also leaves bcast_reserve_sms SMs free while
+    the 'broadcast' runs, so the wide kernel's main launch runs on fewer SMs and a helper launch on
+    the library's aux stream joins after the broadcast, sharing the tile counter; plus several
+    tasks back to back (counter re-arm across the cooperating launches).  C bitwise = plain call."""
+    old = os.environ.get("COMPAR_BCAST_LOOPBACK")
+    os.environ["COMPAR_BCAST_LOOPBACK"] = "2"
+    try:
+        ctx = cm.Compar(bcast_chunks=4, bcast_ctas=8)
+    finally:
+        if old is None:
+            os.environ.pop("COMPAR_BCAST_LOOPBACK", None)
+        else:
+            os.environ["COMPAR_BCAST_LOOPBACK"] = old
+    try:
+        names = [v for v, _ in ctx.variants()]
+        bf = "bf16" in name
+        dt = "bf16" if bf else "f32"
+        A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+        B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))
+        C0 = device_matrix(gen.TAG_C, m, n)
+        kw = dict(ldb=(k if tb else n), alpha=1.5, beta=0.5, in_dtype=cm.BF16 if bf else cm.F32,
+                  compute=cm.COMPUTE_BF16 if bf else cm.COMPUTE_TF32, transB=tb, variant_hint=names.index(name))
+        Cp = C0.clone()
+        ctx.run(cm.make_desc(m, n, k, A=A, B=B, C_in=Cp, C_out=Cp, **kw))
+        s0 = ctx.stats()
+        outs = []
+        for _ in range(3):
+            Cw = C0.clone()
+            r = ctx.run(cm.make_desc(m, n, k, A=A, B=B, C_in=Cw, C_out=Cw, world=1, **kw))
+            assert r.status == 0 and r.bcast_ns > 0
+            outs.append(Cw)
+        assert ctx.stats().launches - s0.launches == 6          # main + helper per task
+        for o in outs:
+            assert torch.equal(o, Cp)
+    finally:
+        ctx.terminate()
 
 
 @pytest.mark.parametrize("tb", [0, 1])
@@ -122,4 +167,4 @@ def test_loopback_world_host_memory(loop_ctx):
                      compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST, world=1)
     ctx.run(d)
     ref = og.gemm(A, B, C0, alpha=1.5, beta=0.5, dtype="bf16")
-    assert_parity(Ch.double().numpy(), ref, A, B, C0, 1.5, 0.5, "bf16", False, 1e-5, "world host")
+    assert_parity(Ch.double().numpy(), ref, A, B, C0, 1.5, 0.5, "bf16", False, 1e-5, "world host", tc=True)

@@ -92,23 +92,17 @@ def test_virtual_stream_matches_selector_oracle(order):
         d = desc(m)
         key = (m, m, m)
         t = ctx.submit(d)
-        pending.append(t)
-        rep_v, rep_m = None, None
         # oracle decision
         v, mode = orc.decide(key, [0, 1, 2])
         warm = orc.commit(v, key, mode)
-        # runtime decision is visible at sync time
+        pending.append((t, v, mode, warm))
+        # runtime decisions are visible at sync time; a task the selector already harvested
+        # implicitly (step 6) still returns its own report (reports are never lost)
         if rnd.random() < 0.5 or step == 299:
-            for tt in pending[:-1]:
-                try:
-                    ctx.sync(tt)
-                except cm.ComparError as e:
-                    assert e.status == cm.E_UNKNOWN_TASK     # already harvested by a model decision
+            for tt, ev, em, ew in pending:
+                r = ctx.sync(tt)
+                assert (r.variant, r.mode, r.warmup) == (ev, em, int(ew)), f"step {step}"
             pending = []
-            r = ctx.sync(t)
-            rep_v, rep_m = r.variant, r.mode
-            assert (rep_v, rep_m) == (v, mode), f"step {step}"
-            assert r.warmup == int(warm)
         orc.harvest(v, key, mode, warm, int(costs[v](m, m, m)))
     ctx.sync()
     ctx.terminate()
@@ -361,3 +355,49 @@ def test_generic_world_and_ce_argument_errors():
         ctx.ce_init(2, 1, 1 << 20, lambda b: [b, b])
     ctx.terminate()
     assert cm.current_stream() == 0                                  # outside a variant call
+
+
+def test_pruned_calibration_matches_oracle_virtual():
+    """R32 through the C ABI (virtual clock, USER variants: no static bound, measured pruning only):
+    a 5x slower variant stops after one timed sample, decisions equal the oracle's, and with
+    calib_prune = 0 the SPEC plan (every variant W + K times) comes back."""
+    costs = [lambda m, n, k: 1000, lambda m, n, k: 5000, lambda m, n, k: 1100]
+    for prune, plan in ((300, [0] * 4 + [1] * 2 + [2] * 4), (0, [0] * 4 + [1] * 4 + [2] * 4)):
+        ctx, _ = vctx(costs, calib_prune=prune)
+        orc = so.SelectorOracle(3, blocked=True, prune_pct=prune)
+        got = []
+        for _ in range(len(plan) + 2):
+            r = ctx.run(desc(64))
+            v, mode = orc.decide((64, 64, 64), [0, 1, 2])
+            warm = orc.commit(v, (64, 64, 64), mode)
+            orc.harvest(v, (64, 64, 64), mode, warm, int(costs[v](64, 64, 64)))
+            assert (r.variant, r.mode) == (v, mode)
+            got.append(r.variant)
+        assert got[:len(plan)] == plan and got[-1] == 0
+        ctx.terminate()
+    with pytest.raises(cm.ComparError):
+        cm.Compar(virtual_clock=1, calib_prune=50)          # below 100 % is meaningless
+
+
+def test_select_keeps_reports_of_implicitly_harvested_tasks():
+    """ADVICE r1: compar_select (and a model decision) may harvest pending samples of the key;
+    those tasks keep their reports — including a failure status — until compar_sync returns them."""
+    calls = {"n": 0}
+
+    def flaky(desc, panel, stream, user, vns):
+        calls["n"] += 1
+        vns[0] = 1000
+        return cm.E_INVALID if calls["n"] == 6 else 0      # the 6th execution fails
+    ctx = cm.Compar(virtual_clock=1)
+    ctx.register_variant("only", cm.TGT_USER, flaky)
+    d = desc(32)
+    tids = [ctx.submit(d) for _ in range(8)]                # calibration, then model decisions
+    assert ctx.select(d)[1] == cm.MODE_MODEL                 # harvests every pending sample
+    statuses = [ctx.sync_status(t) for t in tids]
+    assert [s for s, _ in statuses] == [cm.OK] * 5 + [cm.E_TASK_FAILED] + [cm.OK] * 2
+    assert all(r.task == t for (_, r), t in zip(statuses, tids))
+    assert statuses[5][1].status == cm.E_TASK_FAILED
+    with pytest.raises(cm.ComparError) as e:                 # reported exactly once
+        ctx.sync(tids[0])
+    assert e.value.status == cm.E_UNKNOWN_TASK
+    ctx.terminate()

@@ -183,3 +183,62 @@ def test_partition_invariants():
         assert all(x % 128 == 0 for x in o[:-1] if x < m)       # panel starts are tile-aligned
         sizes = [b - a for a, b in zip(o, o[1:])]
         assert max(sizes) - min(s for s in sizes if s > 0 or m == 0) <= 128 * p if m else True
+
+
+# ---- DESIGN.md R32: calibration pruning, hand-derived plans
+def test_prune_stops_a_slow_variant_after_one_timed_sample():
+    """Blocked, costs 1000 / 5000 / 1100, P = 300 %: v0 calibrates fully (mean 1000); v1's warm-up
+    is dropped and its first timed sample (5000 > 3 x 1000) ends its calibration; v2 calibrates
+    fully; then model picks v0.  10 executions instead of 12."""
+    sel = so.SelectorOracle(3, blocked=True, prune_pct=300)
+    trace = run_stream(sel, "k", [0, 1, 2], lambda v: [1000, 5000, 1100][v], 11)
+    assert [v for v, _ in trace[:10]] == [0] * 4 + [1] * 2 + [2] * 4
+    assert trace[10] == (0, so.MODE_MODEL)
+    # without pruning (SPEC behaviour) every variant runs W + K = 4 times
+    sel0 = so.SelectorOracle(3, blocked=True, prune_pct=0)
+    assert [v for v, _ in run_stream(sel0, "k", [0, 1, 2], lambda v: [1000, 5000, 1100][v], 12)] == \
+        [0] * 4 + [1] * 4 + [2] * 4
+
+
+def test_prune_boundary_is_strict():
+    """Exactly 3 x the best mean is NOT pruned (the rule is 'exceeds'); 3 x + 1 ns is."""
+    for slow, runs in ((3000, 4), (3001, 2)):
+        sel = so.SelectorOracle(2, blocked=True, prune_pct=300)
+        trace = run_stream(sel, "k", [0, 1], lambda v: [1000, slow][v], 4 + runs + 1)
+        assert [v for v, _ in trace[:4 + runs]] == [0] * 4 + [1] * runs
+        assert trace[-1] == (0, so.MODE_MODEL)
+
+
+def test_prune_static_lower_bound_orders_and_skips():
+    """Static lower bounds lb = [3000, 100, 100], costs [10000, 1000, 1000]: blocked calibration
+    visits v1, v2 first (smaller lb), then v0 whose lb is exactly 3 x best (not pruned) runs until
+    its first timed sample; with lb0 = 3001 v0 never runs at all."""
+    key, E = "k", [0, 1, 2]
+    cost = lambda v: [10000, 1000, 1000][v]  # noqa: E731
+    for lb0, v0_runs in ((3000, 2), (3001, 0)):
+        sel = so.SelectorOracle(3, blocked=True, prune_pct=300)
+        lb = [float(lb0), 100.0, 100.0]
+        trace = []
+        for _ in range(8 + v0_runs + 1):
+            v, mode = sel.decide(key, E, lb)
+            warm = sel.commit(v, key, mode)
+            sel.harvest(v, key, mode, warm, cost(v))
+            trace.append((v, mode))
+        assert [v for v, _ in trace[:8 + v0_runs]] == [1] * 4 + [2] * 4 + [0] * v0_runs
+        assert trace[-1] == (1, so.MODE_MODEL)
+
+
+def test_static_lower_bound_closed_form():
+    """lb = max(FLOPs / class peak, bytes / 8 TB/s): 8192^3 BF16 (beta != 0) is compute-bound on
+    the tensor cores (2 * 8192^3 / 2.25e15 s = 488.67 us) and on the FFMA pipes of 148 SMs at
+    1965 MHz (2 * 8192^3 / 74.45e12 s); 65536 x 256 x 4096 BF16 is bandwidth-bound for the tensor
+    class (673.2 MB / 8 TB/s = 84.15 us)."""
+    k = (8192, 8192, 8192, so.BF16, so.COMPUTE_BF16, 0, 0)
+    assert so.SelectorOracle.static_lb_ns("bf16", k) == pytest.approx(2 * 8192 ** 3 / 2.25e15 * 1e9)
+    assert so.SelectorOracle.static_lb_ns("ffma", k) == pytest.approx(2 * 8192 ** 3 / (148 * 256 * 1.965e9) * 1e9)
+    assert so.SelectorOracle.static_lb_ns("tf32", (8192, 8192, 8192, so.F32, so.COMPUTE_TF32, 0, 1)) == \
+        pytest.approx(2 * 8192 ** 3 / 1.125e15 * 1e9)
+    ts = (65536, 256, 4096, so.BF16, so.COMPUTE_BF16, 0, 0)
+    nbytes = 2 * (65536 * 4096 + 4096 * 256) + 4 * 65536 * 256 * 2
+    assert so.SelectorOracle.static_lb_ns("bf16", ts) == pytest.approx(nbytes / 8e12 * 1e9)
+    assert so.SelectorOracle.static_lb_ns(None, ts) == 0.0
