@@ -345,9 +345,14 @@ def north_star_targets(ctx, cm, peaks, R=10):
         fast = [v for v in E if names[v].startswith("tc_")] or list(E)
         fm = fair_medians(ctx, {v: mk(v) for v in fast}, rounds=3, per_round=2 if m * n * k > 8192 ** 3 else 3)
         med = {names[v]: fm[v] for v in fast}
+        pruned = []
         for v in E:
             if v not in fast:
-                med[names[v]] = ctx.history(v, d).mean_ns
+                h = ctx.history(v, d)
+                if h.count:
+                    med[names[v]] = h.mean_ns
+                else:                      # never launched: pruned by its static lower bound (R32)
+                    pruned.append(names[v])
         best = min(med, key=med.get)
         t_sel = statistics.median(r.ns for r in sel)
         flops = 2.0 * m * n * k
@@ -362,7 +367,8 @@ def north_star_targets(ctx, cm, peaks, R=10):
                                   "f32": "FFMA ceiling: SMs x 128 x 2 x sm_max_mhz"}[cls],
                     "hbm_gbs": nbytes / t_sel, "frac_of_hbm_peak": nbytes / t_sel / peaks["hbm_gbs"],
                     "best_variant": best, "regret": med[names[chosen]] / med[best] - 1.0,
-                    "median_ns_per_variant": med, "calibration_runs": calib, "calibration_s": t_cal}
+                    "median_ns_per_variant": med, "pruned_unlaunched": pruned, "calibration_runs": calib,
+                    "calibration_s": t_cal}
         if cls == "bf16":
             out[key]["frac_of_bf16_burst_peak"] = tflops / peaks["bf16_tflops"]
         if cls == "tf32":
@@ -534,12 +540,18 @@ def main():
                                   variant_hint=v) for v in tcv}
         fm = fair_medians(ctx, hinted, rounds=3, per_round=2)
         med = {vn[v]: fm[v] for v in tcv}
+        pruned = []
         for v in elig:
             if v not in tcv:
-                med[vn[v]] = ctx.history(v, desc).mean_ns
+                h = ctx.history(v, desc)
+                if h.count:
+                    med[vn[v]] = h.mean_ns
+                else:                      # never launched: pruned by its static lower bound (R32)
+                    pruned.append(vn[v])
         best = min(med, key=med.get)
         regret = {"chosen": vn[reps[-1].variant], "best": best,
-                  "regret": med[vn[reps[-1].variant]] / med[best] - 1.0, "median_ns_per_variant": med}
+                  "regret": med[vn[reps[-1].variant]] / med[best] - 1.0, "median_ns_per_variant": med,
+                  "pruned_unlaunched": pruned}
 
     # context, not a bench value: cuBLAS on the SAME operation at this shape (torch.addmm with FP32
     # C in and out, out_dtype=float32), interleaved launch by launch with the chosen variant
