@@ -747,6 +747,8 @@ compar_status run_scale(Ctx *c, const compar_gemm_desc *d, const compar_panel &p
 // NCCL's kernels (the communicator is capped at bcast_ctas CTAs); the wide variant gets them back
 // through a helper launch after the broadcast ends.
 
+constexpr int kMaxSlabs = 64;
+
 // Slab plan of a world task.
 struct SlabPlan {
     std::vector<int64_t> col0;   // slab j = columns [col0[j], col0[j+1]) of B (size nslab + 1)
@@ -756,15 +758,13 @@ struct SlabPlan {
     int nslab() const { return static_cast<int>(col0.size()) - 1; }
 };
 
-constexpr int kMaxSlabs = 64;
-
 // fused_ok: the variant is the wide pair kernel.  chunks: the non-fused slab count.
 SlabPlan plan_slabs(int64_t N, int64_t K, int eb, bool transB, bool fused_ok, int chunks) {
     SlabPlan sp;
     const int64_t width = transB ? K : N;   // row width of a packed slab's rows (transB: B^T rows)
-    if (fused_ok) {   // smallest multiple of 512 dividing N with at most 32 slabs
+    if (fused_ok) {   // smallest multiple of 512 dividing N with at most kMaxSlabs slabs
         for (int64_t w = 512; w <= N; w += 512) {
-            if (N % w == 0 && N / w <= 32 && (transB || (w * eb) % 16 == 0)) {
+            if (N % w == 0 && N / w <= kMaxSlabs && (transB || (w * eb) % 16 == 0)) {
                 sp.fused = true;
                 sp.w = w;
                 for (int64_t c0 = 0; c0 <= N; c0 += w) sp.col0.push_back(c0);
@@ -1247,6 +1247,10 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
             return cuda_fail(e, "runtime streams / events / buffers");
         }
         c->bcast_loopback = env_int("COMPAR_BCAST_LOOPBACK", 0);
+        // measurement aid: run the persistent kernels on fewer SMs (e.g. the SMs left beside an
+        // NCCL broadcast), read once here
+        const int sms_cap = env_int("COMPAR_NUM_SMS", 0);
+        if (sms_cap >= 2 && sms_cap < c->num_sms) c->num_sms = sms_cap;
         c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", cfg.bcast_ctas);
         c->host_chunks = env_int("COMPAR_HOST_CHUNKS", 32);
     }

@@ -42,7 +42,7 @@ def loop_ctx():
 CASES = [("tc_bf16", 1000, 1000, 704, 0), ("tc_bf16", 1000, 1000, 704, 1), ("tc_bf16_2sm", 777, 2048, 512, 0),
          ("tc_tf32", 300, 1280, 256, 0), ("tc_tf32_2sm", 512, 1030, 300, 1), ("simt_f32", 200, 600, 100, 0),
          # the wide pair kernel: N a multiple of 512 -> one fused launch waiting per slab on device flags
-         ("tc_bf16_2sm_w", 1000, 2048, 704, 0), ("tc_bf16_2sm_w", 777, 3072, 300, 1),
+         ("tc_bf16_2sm_w", 1000, 2048, 704, 0), ("tc_bf16_2sm_w", 777, 3072, 304, 1),
          ("tc_tf32_2sm_w", 600, 1536, 260, 0), ("tc_tf32_2sm_w", 520, 1024, 512, 1),
          ("tc_bf16_2sm_w", 640, 1000, 512, 0)]          # (N not a multiple of 512: per-slab launches)
 
