@@ -381,6 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx, r);
                 ptx::tmem_ld_wait();
+                const bool tr = local == 0 && warp == 2 && lane == 0 && idx == 1;   // (trace stamps only)
+                if (tr) TRACE(12);
                 if (idx == kChunks - 1) {                 // accumulator drained: free it for tile + 2
                     ptx::tc_fence_before();
                     __syncwarp();
@@ -392,6 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                     if (lane == 0) ptx::bulk_wait_read<NB - 1>();
                     __syncwarp();
                 }
+                if (tr) TRACE(13);
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
                     const uint32_t a = buf(b) + swz + ((g ^ (lane & 7)) << 4);
@@ -409,11 +412,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                     }
                     ptx::sts128(a, o);
                 }
+                if (tr) TRACE(9);
                 ptx::fence_proxy_async_smem();
+                if (tr) TRACE(14);
                 __syncwarp();
                 if (lane == 0) {
                     ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base);
                     ptx::bulk_commit();
+                    if (tr) TRACE(15);
                     if (ldc && idx + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);

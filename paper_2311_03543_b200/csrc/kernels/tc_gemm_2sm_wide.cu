@@ -92,6 +92,29 @@ __device__ __forceinline__ void tile_coords_w(int t, int m_blocks, int n_blocks,
     nb = r / gm;
 }
 
+// World mode (B arriving column slab by column slab): tile columns are visited in groups of
+// 1, 1, 2, 4, 8, 8, ... columns — the first tiles need only the first slabs — and inside a group in
+// bands of `group` pair rows, so a band's A rows are re-read once per group instead of once per
+// column (a plain column-major order re-reads the whole A panel for every 512-column strip).
+__device__ __forceinline__ void tile_coords_world(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
+    int c0 = 0, cw = 1;
+    for (int g = 0;; ++g) {
+        cw = g < 2 ? 1 : min(8, 1 << (g - 1));
+        if (c0 + cw > n_blocks) cw = n_blocks - c0;
+        const int cnt = m_blocks * cw;
+        if (t < cnt || c0 + cw >= n_blocks) break;
+        t -= cnt;
+        c0 += cw;
+    }
+    const int per_band = group * cw;
+    const int band = t / per_band;
+    const int first_m = band * group;
+    const int gm = min(m_blocks - first_m, group);
+    const int r = t - band * per_band;
+    mb = first_m + r % gm;
+    nb = c0 + r / gm;
+}
+
 __device__ __forceinline__ uint32_t peer_addr_w(uint32_t local, uint32_t peer_rank) {
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(peer_rank));
@@ -188,7 +211,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 }
                 if (t >= num_tiles) break;
                 int mb, nb;
-                tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+                if (p.flags)
+                    tile_coords_world(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+                else
+                    tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
                 const int32_t arow = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM;
                 const int32_t bcol0 = nb * C::BN + static_cast<int32_t>(rank) * 128;   // + 256 h
                 // world mode: this tile's 512 columns lie in slab nb*512 / slab_w; wait until it landed
@@ -311,7 +337,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             const int t = next_tile(local);
             if (t >= num_tiles) break;
             int mb, nb;
-            tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+            if (p.flags)
+                    tile_coords_world(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+                else
+                    tile_coords_w(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int32_t row_base = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM + q * 32;
             const int32_t col_base = nb * C::BN;
             auto chunk_col = [&](int idx) { return col_base + 256 * (idx >> 3) + 32 * (idx & 7); };
@@ -429,8 +458,8 @@ cudaError_t launch_tcw_t(const GemmLaunch &g) {
     p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
     // raster bands of 4 pair-rows; 8 when K <= 8192, where a band's A rows plus the B columns a
     // wave touches then fit in L2 (8192^3: 741 vs 752 us; 32768^3 keeps 4: 52.3 vs 53.7 ms);
-    // column-major (one band of all rows) when B arrives slab by slab
-    p.group_m = slabs ? p.m_blocks : (kn.tcw_group > 0 ? kn.tcw_group : (g.k <= 8192 ? 2 * kGroupW : kGroupW));
+    // (world mode: the same bands inside geometric column groups, tile_coords_world)
+    p.group_m = kn.tcw_group > 0 ? kn.tcw_group : (g.k <= 8192 ? 2 * kGroupW : kGroupW);
     p.delay = kn.tcw_delay;
     p.sched = sched_workspace(g.stream);
     if (!p.sched) return cudaErrorMemoryAllocation;

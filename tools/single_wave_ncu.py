@@ -76,12 +76,14 @@ def parse(path, out=None):
     rows = []
     with open(path) as f:
         lines = [ln for ln in f if ln.startswith('"')]
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     for r in csv.DictReader(lines):
-        if r.get("Metric Name") == "gpu__time_duration.sum":
-            rows.append((r["Kernel Name"], float(r["Metric Value"]) / (1e3 if r["Metric Unit"] == "nsecond" else 1)))
+        if r.get("Metric Name") == "gpu__time_duration.sum" and "fill_kernel" not in r["Kernel Name"] \
+                and "FillFunctor" not in r["Kernel Name"]:
+            rows.append((r["Kernel Name"], float(r["Metric Value"]) * scale[r["Metric Unit"]]))
     groups, cur = [], None
     for name, us in rows:
-        if "elementwise" in name or "vectorized" in name:
+        if "CUDAFunctorOnSelf_add" in name:         # the separator (mark.add_(1))
             if cur is not None:
                 groups.append(cur)
             cur = []
