@@ -30,8 +30,11 @@
 namespace compar {
 namespace {
 
-constexpr int kEpiWarpsM = 4;
-constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;   // producer, MMA, 4 epilogue, 2nd producer
+// Warps: 0 producer + scheduler, 1 MMA, 2..5 and 7..10 epilogue (two per TMEM lane quarter, each
+// taking every other 32-column chunk, so a tile's epilogue — exposed on the last tile of every CTA
+// pair — takes half the time), 6 second producer.
+constexpr int kEpiWarpsM = 8;
+constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;
 constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
 constexpr int kRingM = 4;
 
@@ -45,7 +48,8 @@ struct TcMCfg {
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;
     static constexpr int UMMA_K = 32 / ELEM;
-    static constexpr int STAGES = 6;
+    // 256-wide tiles: 5 stages so the 8 epilogue warps' staging (64 KiB) fits beside the ring
+    static constexpr int STAGES = kBN == 256 ? 5 : 6;
     static constexpr uint32_t A_BYTES = BM * 128;
     static constexpr uint32_t B_BYTES = BN_CTA * 128;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -57,9 +61,10 @@ struct TcMCfg {
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
     static constexpr uint32_t B_LBO = kTransB ? 16 : BK * 128;   // MN-major: stride between N atoms
-    // C_in / C_out staging chunks (32 x 32 FP32) per epilogue warp: all four chunks of a 128-wide
-    // tile are loaded before its accumulator is ready; the 256-wide tile cycles two
-    static constexpr int EPI_BUFS = kBN == 128 ? 4 : 2;
+    // C_in / C_out staging chunks (32 x 32 FP32) per epilogue warp: a warp handles BN/64 chunks —
+    // both of a 128-wide tile are loaded before its accumulator is ready; the 256-wide tile's four
+    // cycle through two buffers
+    static constexpr int EPI_BUFS = 2;
     static constexpr uint32_t EPI_BYTES = kEpiWarpsM * EPI_BUFS * 4096;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
@@ -314,9 +319,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 __syncwarp();
             }
         }
-    } else {  // ---------------- epilogue warps 2..5: TMEM lane quarter q, BN/32 chunks of 32 x 32
+    } else {  // ---------------- epilogue warps 2..5, 7..10: TMEM lane quarter q, every other 32 x 32 chunk
         const int q = warp & 3;
-        const int ew = warp - 2;
+        const int ew = warp < 6 ? warp - 2 : warp - 3;   // 0..7
+        const int half = ew >> 2;                        // this warp's chunks: idx = half + 2 j
         constexpr int NB = C::EPI_BUFS;
         // staging chunk b of this warp and its C_in barrier (computed: no local-memory arrays)
         auto buf = [&](int b) -> uint32_t { return epi0 + static_cast<uint32_t>(NB * ew + b) * 4096; };
@@ -325,7 +331,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
         const uint32_t tempty_leader = ptx::mapa_rank(tempty0, 0);
         const bool ldc = p.beta != 0.f;
         const uint32_t swz = lane * 128;
-        constexpr int kChunks = C::BN / 32;
+        constexpr int kChunks = C::BN / 64;              // per warp
+        auto tcol = [&](int j) -> uint32_t { return static_cast<uint32_t>(32 * (half + 2 * j)); };
         for (int local = 0;; ++local) {
             Item it;
             if (!next_item(local, it)) break;
@@ -341,19 +348,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 float *part = p.spart + static_cast<size_t>(sidx) * p.spart_plane + prow_g * p.spart_ld +
                               static_cast<int64_t>(nb) * C::BN;
 #pragma unroll 1
-                for (int idx = 0; idx < kChunks; ++idx) {
+                for (int j = 0; j < kChunks; ++j) {
                     uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx,
-                                            r);
+                    ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + tcol(j), r);
                     ptx::tmem_ld_wait();
-                    if (idx == kChunks - 1) {
+                    if (j == kChunks - 1) {
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
                     }
 #pragma unroll
                     for (int v = 0; v < 8; ++v)
-                        __stcg(reinterpret_cast<float4 *>(part + 32 * idx) + v,
+                        __stcg(reinterpret_cast<float4 *>(part + tcol(j)) + v,
                                make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                                            __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
                 }
@@ -364,9 +370,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
             if (lane == 0) {
                 ptx::bulk_wait_read<0>();                 // previous tile's stores have left smem
                 if (ldc) {
-                    for (int b = 0; b < NB; ++b) {
+                    for (int b = 0; b < NB && b < kChunks; ++b) {
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);
-                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + 32 * b, row_base);
+                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + static_cast<int32_t>(tcol(b)), row_base);
                     }
                 }
             }
@@ -375,58 +381,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             if (local == 0 && warp == 2 && lane == 0) TRACE(5);
             ptx::tc_fence_after();
+            const uint32_t tm = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN;
+            // accumulator chunk j+1 is read from TMEM while chunk j is being finished
+            uint32_t r[32], rn[32];
+            ptx::tmem_ld_32x32b_x32(tm + tcol(0), r);
+            ptx::tmem_ld_wait();
 #pragma unroll 1
-            for (int idx = 0; idx < kChunks; ++idx) {
-                const int b = idx % NB;
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + 32 * idx, r);
-                ptx::tmem_ld_wait();
-                const bool tr = local == 0 && warp == 2 && lane == 0 && idx == 1;   // (trace stamps only)
+            for (int jj = 0; jj < kChunks; ++jj) {
+                const int b = jj % NB;
+                if (jj + 1 < kChunks) ptx::tmem_ld_32x32b_x32(tm + tcol(jj + 1), rn);
+                const bool tr = local == 0 && warp == 2 && lane == 0 && jj == 1;   // (trace stamps only)
                 if (tr) TRACE(12);
-                if (idx == kChunks - 1) {                 // accumulator drained: free it for tile + 2
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
-                }
                 if (ldc) {
                     ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
-                } else if (idx >= NB) {
+                } else if (jj >= NB) {
                     if (lane == 0) ptx::bulk_wait_read<NB - 1>();
                     __syncwarp();
                 }
                 if (tr) TRACE(13);
+                // all eight C_in vectors first, then the eight results (no load waits behind a store)
+                float4 ci[8];
+                if (ldc) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) ci[g] = ptx::lds128(buf(b) + swz + ((g ^ (lane & 7)) << 4));
+                }
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    const uint32_t a = buf(b) + swz + ((g ^ (lane & 7)) << 4);
                     float4 o;
                     o.x = p.alpha * __uint_as_float(r[4 * g + 0]);
                     o.y = p.alpha * __uint_as_float(r[4 * g + 1]);
                     o.z = p.alpha * __uint_as_float(r[4 * g + 2]);
                     o.w = p.alpha * __uint_as_float(r[4 * g + 3]);
                     if (ldc) {
-                        const float4 ci = ptx::lds128(a);
-                        o.x = fmaf(p.beta, ci.x, o.x);
-                        o.y = fmaf(p.beta, ci.y, o.y);
-                        o.z = fmaf(p.beta, ci.z, o.z);
-                        o.w = fmaf(p.beta, ci.w, o.w);
+                        o.x = fmaf(p.beta, ci[g].x, o.x);
+                        o.y = fmaf(p.beta, ci[g].y, o.y);
+                        o.z = fmaf(p.beta, ci[g].z, o.z);
+                        o.w = fmaf(p.beta, ci[g].w, o.w);
                     }
-                    ptx::sts128(a, o);
+                    ptx::sts128(buf(b) + swz + ((g ^ (lane & 7)) << 4), o);
                 }
                 if (tr) TRACE(9);
                 ptx::fence_proxy_async_smem();
                 if (tr) TRACE(14);
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmCo, buf(b), col_base + 32 * idx, row_base);
+                    ptx::tma_store_2d(&tmCo, buf(b), col_base + static_cast<int32_t>(tcol(jj)), row_base);
                     ptx::bulk_commit();
                     if (tr) TRACE(15);
-                    if (ldc && idx + NB < kChunks) {
+                    if (ldc && jj + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);
-                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + 32 * (idx + NB), row_base);
+                        ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + static_cast<int32_t>(tcol(jj + NB)), row_base);
                     }
                 }
-                if (ldc && idx + NB < kChunks) loads_odd ^= 1u << b;
+                if (ldc && jj + NB < kChunks) loads_odd ^= 1u << b;
+                if (jj + 1 < kChunks) {
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) r[e] = rn[e];
+                }
+                if (jj + 2 == kChunks || kChunks == 1) {   // this warp's last TMEM read has completed:
+                    ptx::tc_fence_before();                // free the accumulator for tile + 2
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+                }
                 __syncwarp();
             }
             if (local == 0 && warp == 2 && lane == 0) TRACE(6);
