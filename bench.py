@@ -236,6 +236,51 @@ def cpu_baseline(size):
 
 
 # ---------------------------------------------------------------------------------------------
+def pcie_peaks(nbytes=1 << 30, reps=3):
+    """Measured host<->device copy peaks on this box (pinned host memory, CUDA events, best of
+    `reps`): H2D, D2H, and both directions at once on two streams — the roofline of `e2e`, whose
+    timed region moves A, B, C_in up and C_out down."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        return best
+
+    h2d = nbytes / timed(lambda: d.copy_(h, non_blocking=True)) / 1e6
+    d2h = nbytes / timed(lambda: h.copy_(d, non_blocking=True)) / 1e6
+
+    def both():
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+    bidir = 2 * nbytes / timed(both) / 1e6
+    del h, h2, d, d2
+    torch.cuda.empty_cache()
+    return {"h2d_gbs": h2d, "d2h_gbs": d2h, "bidir_gbs": bidir, "bytes": nbytes,
+            "how": "pinned host <-> device copy of 1 GiB, best of 3, CUDA events; bidir = both at once"}
+
+
+# ---------------------------------------------------------------------------------------------
 def fair_medians(ctx, descs, rounds=3, per_round=2, idle_s=0.1):
     """Per-variant time for the regret comparison, robust to the 1 kW power cap: a kernel that
     follows an idle gap or a lower-power kernel runs at boost clocks for a while, so in every round
@@ -583,6 +628,14 @@ def main():
         e2e = {"value": flops_step * args.e2e_steps / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                "ms_per_step": ems / args.e2e_steps}
+        if world == 1:   # the link's own roofline: the step's bytes at the measured copy peaks
+            pk = pcie_peaks()
+            floor_ms = max((h2d + d2h) / (pk["bidir_gbs"] * 1e9), h2d / (pk["h2d_gbs"] * 1e9),
+                           d2h / (pk["d2h_gbs"] * 1e9)) * 1e3
+            e2e["roofline"] = {"bound": "pcie", "peaks": pk,
+                               "achieved_gbs": (h2d + d2h) / (e2e["ms_per_step"] * 1e-3) / 1e9,
+                               "floor_ms_per_step": floor_ms,
+                               "frac": floor_ms / e2e["ms_per_step"]}
         if world > 1:
             t = torch.tensor([h2d, d2h], device=coll_dev, dtype=torch.float64)
             dist.all_reduce(t)

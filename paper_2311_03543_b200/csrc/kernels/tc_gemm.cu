@@ -75,6 +75,27 @@ struct TcParams {
     int group_m;
 };
 
+#ifdef COMPAR_TRACE
+// Development-only phase stamps (tools/trace_pair.py builds a separate library with -DCOMPAR_TRACE):
+// clock64 at fixed points of CTA 0, globaltimer at entry / exit.
+__device__ unsigned long long g_trace1[16];
+#define TRACE1(i)                                                                             \
+    do {                                                                                      \
+        if (blockIdx.x == 0) g_trace1[i] = clock64();                                        \
+    } while (0)
+#define TRACE1_GT(i)                                                                          \
+    do {                                                                                      \
+        if (blockIdx.x == 0) {                                                                \
+            unsigned long long t;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                           \
+            g_trace1[i] = t;                                                                  \
+        }                                                                                     \
+    } while (0)
+#else
+#define TRACE1(i) ((void)0)
+#define TRACE1_GT(i) ((void)0)
+#endif
+
 __device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
     const int per_group = group * n_blocks;
     const int g = t / per_group;
@@ -103,6 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t smem0 = ptx::smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        TRACE1_GT(10);
+        TRACE1(0);
+    }
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -125,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TRACE1(1);
 
     const int num_tiles = p.m_blocks * p.n_blocks;
     // Consumer side of the tile ring: returns the i-th tile of this CTA (>= num_tiles: done).
@@ -171,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N,
                                              kb * C::BK);
                     }
+                    if (i == 0 && kb == 0) TRACE1(2);
                     if (++stage == C::STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -197,6 +224,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t d_tmem = tmem_base + acc * C::BN;
             for (int kb = 0; kb < p.num_kb; ++kb) {
                 ptx::mbar_wait(full0 + 8 * stage, phase);
+                if (local == 0 && lane == 0) {
+                    if (kb == 0) TRACE1(3);       // first stage landed
+                    TRACE1(4);                    // (last stage landed)
+                }
                 ptx::tc_fence_after();
                 if (lane == 0) {
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
@@ -248,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int v = 0; v < 8; ++v) cur[v] = *reinterpret_cast<const float4 *>(cin + colb + 4 * v);
             }
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+            if (local == 0 && warp == 2 && lane == 0) TRACE1(5);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < C::BN / 32; ++c) {
@@ -293,9 +325,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty0 + 8 * acc);
+            if (local == 0 && warp == 2 && lane == 0) TRACE1(6);
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        TRACE1(8);
+        TRACE1_GT(11);
+    }
     if (warp == 1) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
@@ -364,6 +401,12 @@ cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16) {
     return g.transB ? launch_tc_t<false, true, 256>(g) : launch_tc_t<false, false, 256>(g);
 }
 
+#ifdef COMPAR_TRACE
+int trace1_read(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_trace1, sizeof(g_trace1)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 cudaError_t preload_tc_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess;
@@ -386,3 +429,7 @@ cudaError_t preload_tc_kernels() {
 }
 
 }  // namespace compar
+
+#ifdef COMPAR_TRACE
+extern "C" int compar_trace1_read(unsigned long long *out) { return compar::trace1_read(out); }
+#endif
