@@ -342,6 +342,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     return smem_desc(saddr, lbo, sbo, 2);
 }
+// The descriptor of (saddr + bytes): its start-address field is addr >> 4 in bits [0,14) and shared
+// memory offsets stay below 2^18, so the add never carries out of the field.  The MMA issue loops
+// build descriptors this way from per-kernel bases — one add per tcgen05.mma instead of a re-encode
+// (a chain of ~10 dependent uniform-datapath ops before every UTCHMMA).
+__device__ __forceinline__ uint64_t desc_adv(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 
 }  // namespace ptx
 }  // namespace compar

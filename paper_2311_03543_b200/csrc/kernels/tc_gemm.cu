@@ -41,7 +41,11 @@ struct TcCfg {
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / ELEM;       // K per tcgen05.mma (16 bf16 / 8 tf32)
+#ifdef COMPAR_TC1_DEEP   // (experiment: as many stages as fit 192 KiB)
+    static constexpr int STAGES = (192 * 1024) / (BM * 128 + BN * 128);
+#else
     static constexpr int STAGES = 4;
+#endif
     static constexpr uint32_t A_BYTES = BM * 128;
     static constexpr uint32_t B_BYTES = BN * 128;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -187,7 +191,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
                     const uint32_t fb = full0 + 8 * stage;
+#ifdef COMPAR_TC1_NOLOAD   // (timing experiment: no TMA, the barrier completes on the arrive)
+                    ptx::mbar_arrive(fb);
+                    if (false)
+#endif
                     ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+#ifndef COMPAR_TC1_NOLOAD
                     ptx::tma_load_2d(sa, &tmA, fb, kb * C::BK, mb * C::BM);
                     if (kTransB) {
                         ptx::tma_load_2d(sb, &tmB, fb, kb * C::BK, nb * C::BN);
@@ -197,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N,
                                              kb * C::BK);
                     }
+#endif
                     if (i == 0 && kb == 0) TRACE1(2);
                     if (++stage == C::STAGES) {
                         stage = 0;
@@ -214,6 +224,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {  // ---------------- MMA issuer
         int stage = 0;
         uint32_t phase = 0;
+        const uint64_t adesc0 = ptx::smem_desc_sw128(smem0, 16, 1024);   // stage 0, K-slice 0
+        const uint64_t bdesc0 = kTransB ? ptx::smem_desc_sw128(smem0 + C::A_BYTES, 16, 1024)
+                                        : ptx::smem_desc(smem0 + C::A_BYTES, C::B_BOX_BYTES, C::B_SBO, C::B_LAYOUT);
         for (int local = 0;; ++local) {
             const int t = next_tile(local);
             if (t >= num_tiles) break;
@@ -230,18 +243,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
-                    const uint32_t sb = sa + C::A_BYTES;
+                    const uint32_t so = stage * C::STAGE_BYTES;
+                    const uint64_t as = ptx::desc_adv(adesc0, so), bs = ptx::desc_adv(bdesc0, so);
 #pragma unroll
                     for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
-                        const uint64_t adesc = ptx::smem_desc_sw128(sa + j * 32, 16, 1024);
-                        const uint64_t bdesc = kTransB ? ptx::smem_desc_sw128(sb + j * 32, 16, 1024)
-                                                       : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_BOX_BYTES,
-                                                                        C::B_SBO, C::B_LAYOUT);
+                        const uint64_t adesc = ptx::desc_adv(as, j * 32);
+                        const uint64_t bdesc = ptx::desc_adv(bs, kTransB ? j * 32 : j * C::UMMA_K * 128);
+#ifndef COMPAR_TC1_NOMMA   // (timing experiment: commits without MMAs)
                         if (kBF16)
                             ptx::mma_bf16(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
                         else
                             ptx::mma_tf32(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
+#else
+                        (void)adesc, (void)bdesc;
+#endif
                     }
                     ptx::tc_commit(empty0 + 8 * stage);
                 }

@@ -293,18 +293,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                     ptx::mbar_wait(full0 + 8 * stage, phase);
                     ptx::tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
+                        const uint32_t so = stage * C::STAGE_BYTES;
+                        const uint64_t adesc0 = ptx::smem_desc(smem0, 16, 1024, 2);
+                        const uint64_t bdesc0 = kTransB ? ptx::smem_desc(smem0 + C::A_BYTES, 16, 1024, 2)
+                                                        : ptx::smem_desc(smem0 + C::A_BYTES, C::B_BOX_BYTES, C::B_SBO,
+                                                                         C::B_LAYOUT);
+                        const uint64_t as = ptx::desc_adv(adesc0, so), bs = ptx::desc_adv(bdesc0, so);
 #pragma unroll
                         for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
-                            const uint64_t adesc = ptx::smem_desc(sa + j * 32, 16, 1024, 2);
+                            const uint64_t adesc = ptx::desc_adv(as, j * 32);
 #pragma unroll
                             for (int h = 0; h < 2; ++h) {
                                 if (!((hmask >> h) & 1)) continue;
-                                const uint32_t sb = sa + C::A_BYTES + h * C::BH_BYTES;
-                                const uint64_t bdesc = kTransB
-                                                           ? ptx::smem_desc(sb + j * 32, 16, 1024, 2)
-                                                           : ptx::smem_desc(sb + j * C::UMMA_K * 128, C::B_BOX_BYTES,
-                                                                            C::B_SBO, C::B_LAYOUT);
+                                const uint64_t bdesc = ptx::desc_adv(
+                                    bs, h * C::BH_BYTES + (kTransB ? j * 32 : j * C::UMMA_K * 128));
                                 if (kBF16)
                                     ptx::mma_bf16_2sm(tmem_base + 256 * h, adesc, bdesc, C::IDESC, (kb | j) != 0);
                                 else

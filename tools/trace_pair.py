@@ -16,14 +16,17 @@ sys.path.insert(0, ROOT)
 TRACE_DIR = os.path.join(ROOT, "build_trace")
 
 if __name__ == "__main__" and sys.argv[1] == "build":
+    # python tools/trace_pair.py build [DIR -DFLAG ...]: extra experiment flags into another dir
     from paper_2311_03543_b200 import build as b
-    b.ARCH = b.ARCH + ["-DCOMPAR_TRACE"]
+    if len(sys.argv) > 2:
+        TRACE_DIR = os.path.join(ROOT, sys.argv[2])
+    b.ARCH = b.ARCH + ["-DCOMPAR_TRACE"] + sys.argv[3:]
     b.BUILD = os.path.join(TRACE_DIR, "obj")
     b.LIB = os.path.join(TRACE_DIR, "libcompar.so")
     print(b.build_compar(force=True))
     sys.exit(0)
 
-os.environ["COMPAR_LIB"] = os.path.join(TRACE_DIR, "libcompar.so")
+os.environ["COMPAR_LIB"] = os.environ.get("COMPAR_LIB") or os.path.join(TRACE_DIR, "libcompar.so")
 import ctypes  # noqa: E402
 
 import torch  # noqa: E402
