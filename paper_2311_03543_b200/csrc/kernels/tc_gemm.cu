@@ -41,11 +41,7 @@ struct TcCfg {
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K
     static constexpr int UMMA_K = 32 / ELEM;       // K per tcgen05.mma (16 bf16 / 8 tf32)
-#ifdef COMPAR_TC1_DEEP   // (experiment: as many stages as fit 192 KiB)
-    static constexpr int STAGES = (192 * 1024) / (BM * 128 + BN * 128);
-#else
-    static constexpr int STAGES = 4;
-#endif
+    static constexpr int STAGES = 4;   // (as many as fit 192 KiB measured the same: DESIGN.md §5)
     static constexpr uint32_t A_BYTES = BM * 128;
     static constexpr uint32_t B_BYTES = BN * 128;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -132,6 +128,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         TRACE1_GT(10);
         TRACE1(0);
     }
+    const int num_tiles = p.m_blocks * p.n_blocks;
+    // One k-block of tile (mb, nb) into ring stage `stage` (producer thread only).
+    auto load_stage = [&](int stage, int kb, int mb, int nb) {
+        const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
+        const uint32_t sb = sa + C::A_BYTES;
+        const uint32_t fb = full0 + 8 * stage;
+        ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+        ptx::tma_load_2d(sa, &tmA, fb, kb * C::BK, mb * C::BM);
+        if (kTransB) {
+            ptx::tma_load_2d(sb, &tmB, fb, kb * C::BK, nb * C::BN);
+        } else {
+#pragma unroll
+            for (int b = 0; b < C::B_BOXES; ++b)
+                ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N, kb * C::BK);
+        }
+    };
+    int early = 0;   // k-blocks of the first tile issued before the block-wide barrier
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -148,6 +161,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(rempty0 + 8 * r, 5);
         }
         ptx::fence_mbar_init();
+        // The ring's first STAGES k-blocks of this CTA's static first tile go out right away: the
+        // barriers are this thread's own, the stages are free, and the loads' latency (tensor-map
+        // fetch included) then overlaps the TMEM allocation and the block barrier.
+        if (static_cast<int>(blockIdx.x) < num_tiles) {
+            int mb, nb;
+            tile_coords(static_cast<int>(blockIdx.x), p.m_blocks, p.n_blocks, p.group_m, mb, nb);
+            early = p.num_kb < C::STAGES ? p.num_kb : C::STAGES;
+            for (int kb = 0; kb < early; ++kb) load_stage(kb, kb, mb, nb);
+            TRACE1(2);
+        }
     }
     if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();
@@ -156,7 +179,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) TRACE1(1);
 
-    const int num_tiles = p.m_blocks * p.n_blocks;
     // Consumer side of the tile ring: returns the i-th tile of this CTA (>= num_tiles: done).
     // tile 0 of CTA b is tile b (no ring round trip, no atomic before the first loads); tile
     // i >= 1 comes through ring index i - 1 from the global counter, offset by the grid size
@@ -172,8 +194,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- scheduler + TMA producer
-            int stage = 0;
-            uint32_t phase = 0;
+            int stage = early % C::STAGES;
+            uint32_t phase = early == C::STAGES ? 1u : 0u;
             for (int i = 0;; ++i) {
                 int t = static_cast<int>(blockIdx.x);
                 if (i > 0) {
@@ -186,28 +208,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t >= num_tiles) break;
                 int mb, nb;
                 tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = i == 0 ? early : 0; kb < p.num_kb; ++kb) {
                     ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
-                    const uint32_t sa = smem0 + stage * C::STAGE_BYTES;
-                    const uint32_t sb = sa + C::A_BYTES;
-                    const uint32_t fb = full0 + 8 * stage;
-#ifdef COMPAR_TC1_NOLOAD   // (timing experiment: no TMA, the barrier completes on the arrive)
-                    ptx::mbar_arrive(fb);
-                    if (false)
-#endif
-                    ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
-#ifndef COMPAR_TC1_NOLOAD
-                    ptx::tma_load_2d(sa, &tmA, fb, kb * C::BK, mb * C::BM);
-                    if (kTransB) {
-                        ptx::tma_load_2d(sb, &tmB, fb, kb * C::BK, nb * C::BN);
-                    } else {
-#pragma unroll
-                        for (int b = 0; b < C::B_BOXES; ++b)
-                            ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N,
-                                             kb * C::BK);
-                    }
-#endif
-                    if (i == 0 && kb == 0) TRACE1(2);
+                    load_stage(stage, kb, mb, nb);
                     if (++stage == C::STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -249,14 +252,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
                         const uint64_t adesc = ptx::desc_adv(as, j * 32);
                         const uint64_t bdesc = ptx::desc_adv(bs, kTransB ? j * 32 : j * C::UMMA_K * 128);
-#ifndef COMPAR_TC1_NOMMA   // (timing experiment: commits without MMAs)
                         if (kBF16)
                             ptx::mma_bf16(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
                         else
                             ptx::mma_tf32(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
-#else
-                        (void)adesc, (void)bdesc;
-#endif
                     }
                     ptx::tc_commit(empty0 + 8 * stage);
                 }
