@@ -175,21 +175,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
         }
         for (int b = 0; b < C::EPI_BUFS * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
         ptx::fence_mbar_init();
-        // L2 prefetch of this CTA's first STAGES k-blocks (static first tile): the real loads,
-        // which must wait for the cluster barrier (the peer signals the leader's barriers), then hit
-        // L2 with warm tensor maps
-        if (p.splits == 1 && static_cast<int>(blockIdx.x) / 2 < p.m_blocks * p.n_blocks) {
-            int mb, nb;
-            tile_coords_m(static_cast<int>(blockIdx.x) / 2, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
-            const int32_t arow = mb * (2 * C::BM) + static_cast<int32_t>(rank) * C::BM;
-            const int32_t bcol = nb * C::BN + static_cast<int32_t>(rank) * C::BN_CTA;
-            for (int kb = 0; kb < C::STAGES && kb < p.num_kb; ++kb) {
-                ptx::tma_prefetch_2d(&tmA, kb * C::BK, arow);
-                for (int b = 0; b < C::B_BOXES; ++b)
-                    ptx::tma_prefetch_2d(&tmB, kTransB ? kb * C::BK : bcol + b * C::B_ATOM_N,
-                                         kTransB ? bcol + b * (C::BN_CTA / 2) : kb * C::BK);
-            }
-        }
     }
     if (warp == 1) ptx::tmem_alloc_2sm<C::TMEM_COLS>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();

@@ -164,25 +164,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
         }
         for (int b = 0; b < 2 * kEpiWarpsW; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
         ptx::fence_mbar_init();
-        // L2 prefetch of this CTA's first STAGES k-blocks (static first tile; B resident only):
-        // the real loads must wait for the cluster barrier and then hit L2 with warm tensor maps
-        if (!p.flags && p.static_first && static_cast<int>(blockIdx.x >> 1) < p.m_blocks * p.n_blocks) {
-            int mb, nb;
-            tile_coords_w(static_cast<int>(blockIdx.x >> 1), p.m_blocks, p.n_blocks, p.group_m, mb, nb);
-            const int32_t arow = mb * 2 * C::BM + static_cast<int32_t>(rank) * C::BM;
-            const int32_t bcol0 = nb * C::BN + static_cast<int32_t>(rank) * 128;
-            for (int kb = 0; kb < C::STAGES && kb < p.num_kb; ++kb) {
-                ptx::tma_prefetch_2d(&tmA, kb * C::BK, arow);
-                for (int h = 0; h < 2; ++h) {
-                    if (kTransB) {
-                        ptx::tma_prefetch_2d(&tmB, kb * C::BK, bcol0 + 256 * h);
-                    } else {
-                        for (int b = 0; b < C::B_BOXES; ++b)
-                            ptx::tma_prefetch_2d(&tmB, bcol0 + 256 * h + b * C::B_ATOM_N, kb * C::BK);
-                    }
-                }
-            }
-        }
     }
     if (warp == 1) ptx::tmem_alloc_2sm<512>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();

@@ -104,7 +104,8 @@ def regret_case(ctx, names, prob, compute, targets):
     return {"shape": [prob.m, prob.n, prob.k], "dtype": prob.dt, "compute": compute,
             "eligible": [names[v] for v in E], "chosen": names[chosen], "best": names[best],
             "regret": reg, "median_ns": {names[v]: med[v] for v in E},
-            "calibration_runs": len(trace) - 1, "chosen_stable": len({r.variant for r in model}) == 1}
+            "calibration_runs": len(trace) - 1, "chosen_stable": len({r.variant for r in model}) == 1,
+            "pruned_never_launched": [names[v] for v in E if ctx.history(v, prob.desc(compute)).seen == 0]}
 
 
 def main(out_path):
@@ -202,12 +203,13 @@ def main(out_path):
            "best": {str(list(s)): names[b[0]] for s, b in best.items()}}
     for sched, label in ((0, "history"), (1, "eager"), (2, "predict")):
         c = cm.Compar(sched=sched)
-        chosen, total_ns = [], 0
+        chosen, total_ns, span_ns = [], 0, 0
         t0 = time.perf_counter()
         for s in stream:
             r = c.run(probs[s].desc(cm.COMPUTE_TF32))
             chosen.append((s, r.variant, r.mode))
             total_ns += r.ns
+            span_ns += r.total_ns        # every launch of the task (a batched calibration run: all r)
         wall = time.perf_counter() - t0
         c5b.setdefault("calibration_runs", {})[label] = sum(
             1 for (_, _, mode) in chosen if mode in (cm.MODE_WARMUP, cm.MODE_CALIB))
@@ -221,10 +223,15 @@ def main(out_path):
                 v = max(set(vs), key=vs.count)
                 per_shape[str(list(s))] = {"chosen": names[v],
                                            "regret": best[s][2][names[v]] / best[s][1] - 1.0}
-        c5b[label] = {"kernel_ms_total": total_ns / 1e6, "wall_s": wall, "selection_accuracy_steady": acc,
-                      "per_shape": per_shape}
+        c5b[label] = {"kernel_ms_total": total_ns / 1e6, "task_span_ms_total": span_ns / 1e6, "wall_s": wall,
+                      "selection_accuracy_steady": acc, "per_shape": per_shape,
+                      "pruned_never_launched": {str(list(s)): [names[v] for v in eligible(c, TF32_T, probs[s], cm.COMPUTE_TF32)
+                                                               if c.history(v, probs[s].desc(cm.COMPUTE_TF32)).seen == 0]
+                                                for s in shapes}}
         c.terminate()
     c5b["sum_of_best_ms"] = sum(best[s][1] for s in stream) / 1e6
+    for label in ("history", "eager", "predict"):
+        c5b[label]["span_over_sum_of_best"] = c5b[label]["task_span_ms_total"] / c5b["sum_of_best_ms"]
     res["config5b"] = c5b
     out = json.dumps(res, indent=1)
     if out_path:
