@@ -206,3 +206,73 @@ def test_task_world_two_processes_real_kernels(tmp_path):
         C0 = gen.matrix(gen.TAG_C, m, n, gen.DIST_I, "f32", seed=t)
         np.testing.assert_array_equal(np.load(tmp_path / f"t{t}.npy").astype(np.float64),
                                       og.gemm(A, B, C0, alpha=2.0, beta=-1.0))
+
+
+def _dead_peer_worker(rank, port, outdir):
+    import torch.distributed as dist
+
+    import gen
+    from gen.device import fill
+    from paper_2311_03543_b200 import compar as cm
+
+    world = 2
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ctx = cm.Compar(bcast_chunks=2, sync_timeout_ms=2000)
+
+    def allgather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+    m = n = k = 512
+    ctx.ce_init(world, rank, k * n * 2, allgather)
+    names = [v for v, _ in ctx.variants()]
+    sp = torch.cuda.current_stream().cuda_stream
+    offs = cm.partition_rows(m, world)
+    mloc = offs[rank + 1] - offs[rank]
+    A = torch.empty((mloc, k), dtype=torch.bfloat16, device="cuda")
+    C = torch.empty((mloc, n), dtype=torch.float32, device="cuda")
+    B = torch.empty((k, n), dtype=torch.bfloat16, device="cuda")
+    fill(A.data_ptr(), "bf16", mloc, k, k, gen.TAG_A, row0=offs[rank], stream=sp)
+    fill(C.data_ptr(), "f32", mloc, n, n, gen.TAG_C, row0=offs[rank], stream=sp)
+    fill(B.data_ptr(), "bf16", k, n, n, gen.TAG_B, stream=sp)
+    d = cm.make_desc(m, n, k, A=A, B=B if rank == 0 else None, C_in=C, C_out=C, alpha=1.5, beta=0.5,
+                     in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, stream=sp, world=1, B_replica=B if rank else None,
+                     variant_hint=names.index("tc_bf16"))   # hinted: no sample exchange with the peer
+    assert ctx.run(d).status == 0                         # task 1: both ranks alive
+    dist.barrier()
+    if rank == 1:                                         # the peer dies without a word
+        os._exit(0)
+    out = {}
+    s, r = ctx.sync_status(ctx.submit(d))                 # task 2: rank 1 consumed task 1's slabs
+    out["t2"] = s
+    t3 = ctx.submit(d)                                    # task 3 needs rank 1 to consume task 2's slabs
+    import time
+    t0 = time.perf_counter()
+    s3, r3 = ctx.sync_status(t3)
+    out["t3"], out["t3_s"] = s3, time.perf_counter() - t0
+    out["t3_msg"] = cm.lib.compar_last_error(None).decode()
+    try:
+        ctx.submit(d)
+        out["t4"] = 0
+    except cm.ComparError as e:                           # sticky
+        out["t4"] = e.status
+    np.save(os.path.join(outdir, "dead_peer.npy"), np.array([out["t2"], out["t3"], out["t3_s"], out["t4"]]))
+    with open(os.path.join(outdir, "msg.txt"), "w") as f:
+        f.write(out["t3_msg"])
+    os._exit(0)                                           # the comm stream is stuck on the dead peer
+
+
+def test_dead_peer_wait_times_out_with_sticky_error(tmp_path):
+    """R36: a rank whose peer died does not hang — the wait for the copy-engine chain (or NCCL) polls
+    with sync_timeout_ms, the task fails with E_NCCL within the timeout, and every later cross-rank
+    task fails with E_NCCL at submit (sticky)."""
+    import torch.multiprocessing as mp
+
+    from paper_2311_03543_b200 import compar as cm
+    mp.spawn(_dead_peer_worker, args=(_port(), str(tmp_path)), nprocs=2, join=True)
+    t2, t3, t3_s, t4 = np.load(tmp_path / "dead_peer.npy")
+    assert t2 == cm.OK
+    assert t3 == cm.E_NCCL and 1.5 < t3_s < 30, (t3, t3_s)
+    assert t4 == cm.E_NCCL
+    assert "timed out" in (tmp_path / "msg.txt").read_text()
