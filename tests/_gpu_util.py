@@ -43,5 +43,9 @@ def assert_parity(got, ref, A, B, C0, alpha, beta, dtype, tf32, tol, what="", tc
     err = og.rel_fro(got, ref)
     bound = og.elementwise_bound(A, B, C0, alpha, beta, dtype=dtype, tf32=tf32)
     v = og.elementwise_violation(got, ref, bound)
-    assert err <= tol and v <= 1.0, (what, "rel_fro", err, "tol", tol, "elementwise violation", v)
+    # (R8: below 64 output elements the norm ratio degenerates into a few elements' relative errors,
+    # which cancellation in a dot product can make arbitrarily large — there the componentwise bound
+    # alone is the criterion; found by the fuzz test at m = n = 1, K = 2000: 4.7e-5, bound met)
+    norm_ok = err <= tol or np.size(got) < 64
+    assert norm_ok and v <= 1.0, (what, "rel_fro", err, "tol", tol, "elementwise violation", v)
     return err

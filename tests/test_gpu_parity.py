@@ -392,3 +392,28 @@ def test_full_size_sampled(ctx, name, shape):
     assert_parity(got, ref, Ar, Bc, C0, 1.5, 0.5, dt, is_tf32(name), tol, name, tc=name.startswith("tc_"))
     del A, B, Cd
     torch.cuda.empty_cache()
+
+
+def test_host_mode_tasks_on_two_streams_do_not_share_staging_early(ctx):
+    """host-mode tasks stage A / B / C through the context's buffers; a task submitted on
+    another stream must wait until the previous host task is done with them (staging_free event).
+    Two back-to-back host-mode tasks on different streams, different inputs: both results exact."""
+    m, n, k = 2048, 1024, 2048          # long enough that the first GEMM is still running at the second submit
+    outs, refs = [], []
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    tids = []
+    for i, s in enumerate((s1, s2)):
+        A = gen.matrix(gen.TAG_A, m, k, gen.DIST_I, "f32", seed=40 + i)
+        B = gen.matrix(gen.TAG_B, k, n, gen.DIST_I, "f32", seed=40 + i)
+        C0 = gen.matrix(gen.TAG_C, m, n, gen.DIST_I, "f32", seed=40 + i)
+        Ah, Bh, Ch = (torch.from_numpy(x.copy()).pin_memory() for x in (A, B, C0))
+        d = cm.make_desc(m, n, k, A=Ah, B=Bh, C_in=Ch, C_out=Ch, alpha=2.0, beta=-1.0, compute=cm.COMPUTE_TF32,
+                         mem=cm.MEM_HOST, stream=s.cuda_stream, variant_hint=vid(ctx, "tc_tf32"))
+        tids.append(ctx.submit(d))
+        outs.append((Ah, Bh, Ch))
+        rows = np.arange(0, m, 97)
+        refs.append((rows, og.gemm(A[rows], B, C0[rows], alpha=2.0, beta=-1.0)))
+    for t in tids:
+        assert ctx.sync(t).status == 0
+    for (Ah, Bh, Ch), (rows, ref) in zip(outs, refs):
+        np.testing.assert_array_equal(Ch.numpy()[rows].astype(np.float64), ref)

@@ -1,0 +1,175 @@
+"""Write RESULTS.md: the BASELINE.md §5 results table from committed measurement files only.
+
+Sources (every row names its own): BENCH_r01.json (driver-run, round 1), profiles/r02_bench_line.json
+(builder-run bench line, round 2), profiles/r02_selector.json (tools/selector_sweep.py),
+profiles/r02_single_wave_ncu.json (tools/single_wave_ncu.py), profiles/r02_world_projection.json
+(tools/world_projection.py), MEASURED_PEAKS.json.
+usage: python tools/results_table.py [RESULTS.md]
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def load(rel):
+    p = os.path.join(ROOT, rel)
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        txt = f.read()
+    try:
+        return json.loads(txt)
+    except ValueError:
+        return json.loads(txt.strip().splitlines()[-1])
+
+
+def f(x, nd=1):
+    return "—" if x is None else f"{x:,.{nd}f}"
+
+
+def main(out):
+    mp = load("MEASURED_PEAKS.json") or {}
+    b1 = load("BENCH_r01.json") or {}
+    b1p = b1.get("parsed") or {}
+    b2 = load("profiles/r02_bench_line.json") or {}
+    sel = load("profiles/r02_selector.json") or {}
+    sw = load("profiles/r02_single_wave_ncu.json") or {}
+    wp = load("profiles/r02_world_projection.json") or {}
+    bf16, bf16s, hbm = mp.get("bf16_tflops", 1672.0), mp.get("bf16_tflops_sustained", 1406.2), mp.get("hbm_gbs", 6547.8)
+    ds = 2250.0
+    rows = []
+
+    def row(cfg, shape, variant, prec, P, med, tflops, pk, pk_kind, hbm_frac, err, regret, ep, oracle, clk, src):
+        rows.append(f"| {cfg} | {shape} | {variant} | {prec} | {P} | {med} | {tflops} | {pk} ({pk_kind}) | "
+                    f"{f(None if tflops == '—' else float(tflops.replace(',', '')) / ds * 100)} | {hbm_frac} | {err} | "
+                    f"{regret} | {ep} | {oracle} | {clk} | {src} |")
+
+    def bench_rows(b, label):
+        if not b:
+            return
+        cl = b.get("clocks", {})
+        clk = f"{f(cl.get('sm_mhz'), 0)} MHz, {f(cl.get('power_w_max'), 0)} W max, {', '.join(cl.get('reasons', []))}"
+        cb = b.get("cpu_baseline") or {}
+        orc = f"{f(cb.get('value', 0) * 1e3, 1)} GFLOP/s on {cb.get('cores')} cores (sampled)" if cb else "—"
+        reg = (b.get("selector") or {}).get("regret") or {}
+        row("4", "32768³", b["config"].get("variant"), "BF16 in, FP32 C", b["n_gpus"], f"{f(b['ms_per_step'], 2)} ms",
+            f(b["value"]), f(b["value"] / bf16s * 100), "sustained", "—", "≤ K·2^-27 (R33); exact ints bitwise",
+            f(reg.get("regret", 0) * 100, 1) + " %", "— (1 GPU)", orc, clk, label)
+        e2e = b.get("e2e") or {}
+        if e2e:
+            rf = e2e.get("roofline") or {}
+            pk = rf.get("peaks") or {}
+            row("4 e2e", "32768³ host buffers", b["config"].get("variant"), "BF16", b["n_gpus"],
+                f"{f(e2e.get('ms_per_step'), 1)} ms", f(e2e.get("value")), f(e2e.get("value", 0) / bf16s * 100),
+                "sustained", f"PCIe {f(rf.get('frac', 0) * 100, 0)} % of the measured copy floor "
+                f"({f(pk.get('h2d_gbs'), 1)} / {f(pk.get('d2h_gbs'), 1)} / {f(pk.get('bidir_gbs'), 1)} GB/s H2D / D2H / both)"
+                if rf else "—", "as above", "—", "—", "—", clk, label)
+        for key, t in (b.get("north_star_targets") or {}).items():
+            if not isinstance(t, dict):
+                continue
+            shape = {"config3_8192cube_bf16": "8192³", "config5a_65536x256x4096_bf16": "65536×256×4096",
+                     "config4_32768cube_tf32_fp32_storage": "32768³", "config3_8192cube_f32_strict": "8192³"}.get(key, key)
+            prec = "BF16" if "bf16" in key else ("TF32 (FP32 storage)" if "tf32" in key else "FP32 strict")
+            cfg = key.split("_")[0].replace("config", "")
+            hb = f"{f(t.get('frac_of_hbm_peak', 0) * 100)} %" if "5a" in key else "—"
+            row(cfg, shape, t["variant"], prec, 1, f"{f(t['ms'] * 1e3, 1)} µs" if t["ms"] < 1 else f"{f(t['ms'], 2)} ms",
+                f(t["tflops"]), f(t["frac_of_peak"] * 100), t.get("peak_kind", "").split(" (")[0],
+                hb, "tol. per class", f(t.get("regret", 0) * 100, 1) + " %", "—", "—", clk, label)
+
+    bench_rows(b1p, "driver-run r01 (`BENCH_r01.json`)")
+    bench_rows(b2, "builder-run r02 (`profiles/r02_bench_line.json`)")
+    # selector sweep (builder-run)
+    for c in sel.get("config1", []):
+        row("1", "64³", c["chosen"], "FP32 strict" if c["compute"] == 0 else "TF32", 1,
+            f"{f(c['median_ns'][c['chosen']] / 1e3, 1)} µs", "—", "—", "launch-bound", "—", "1e-5 / tol.",
+            f(c["regret"] * 100, 1) + " %", "—", "—", "—", "builder-run r02 (`profiles/r02_selector.json`)")
+    for mode in ("F32_STRICT", "TF32"):
+        for r in (sel.get("config2") or {}).get(mode, []):
+            s = r["shape"][0]
+            t = r["median_ns"][r["chosen"]]
+            tfl = 2.0 * s ** 3 / t / 1e3
+            peak = 74.45 if mode == "F32_STRICT" else bf16 / 2
+            row("2", f"{s}³", r["chosen"], "FP32 strict" if mode == "F32_STRICT" else "TF32", 1, f"{f(t / 1e3, 1)} µs",
+                f(tfl), f(tfl / peak * 100), "FFMA ceiling" if mode == "F32_STRICT" else "BF16 burst / 2", "—",
+                "1e-5 / 5e-3", f(r["regret"] * 100, 1) + " %", "—", "—", "—", "builder-run r02 (selector sweep)")
+    for r in sel.get("config5a", []):
+        m, n, k = r["shape"]
+        t = r["median_ns"][r["chosen"]]
+        eb = 2 if r["dtype"] == "bf16" else 4
+        nbytes = eb * (m * k + k * n) + 8 * m * n
+        row("5a", "65536×256×4096", r["chosen"], "BF16" if r["dtype"] == "bf16" else "TF32", 1, f"{f(t / 1e3, 1)} µs",
+            f(2.0 * m * n * k / t / 1e3), "—", "HBM-bound", f"{f(nbytes / t / hbm * 100)} %", "tol.",
+            f(r["regret"] * 100, 1) + " %", "—", "—", "—", "builder-run r02 (selector sweep)")
+    c5b = sel.get("config5b") or {}
+    if c5b:
+        for lab in ("history", "predict", "eager"):
+            x = c5b[lab]
+            worst = max(v["regret"] for v in x["per_shape"].values())
+            row("5b", "200-task mixed stream", lab + " scheduler", "TF32", 1, f"{f(x['task_span_ms_total'], 1)} ms",
+                "—", "—", f"{f(x['span_over_sum_of_best'], 2)}× sum of per-shape best ({f(c5b['sum_of_best_ms'], 1)} ms)",
+                "—", "tol.", f"≤ {f(worst * 100, 1)} % per shape", "—", "—", "—", "builder-run r02 (selector sweep)")
+    # multi-GPU projection
+    proj = wp.get("projection_by_bcast_gbs") or {}
+    for bw in ("300", "400"):
+        p = proj.get(bw) or {}
+        for P in ("2", "4", "8"):
+            if P in p:
+                row("4", "32768³ row panels", "tc_bf16_2sm_w (fused receiver)", "BF16", P,
+                    f"{f(p[P]['T_P_ms'], 2)} ms (projected)", "—", "—", "—", "—", "bitwise = P 1", "—",
+                    f"{f(p[P]['E_P'], 3)} at {bw} GB/s broadcast (projection)", "—", "—",
+                    "projection from 1-GPU measurements (`profiles/r02_world_projection.json`)")
+    head = ("| config | shape | variant | precision | P | median | TFLOP/s | % of `MP` peak | % of datasheet 2250 | "
+            "% of HBM roofline | max rel-Fro / parity | regret | E_P | oracle (threads / cores) | SM clock, power | source |\n"
+            "|" + "---|" * 16)
+    sw_rows = ["| shape | ours (kernel-only, ncu) | cuBLAS same op (addmm, FP32 C in/out) |", "|---|---|---|"]
+    for key in ("1024^3_bf16", "2048^3_bf16", "1024^3_f32", "2048^3_f32"):
+        ours = [(v["median_us"], k) for k, v in sw.items() if k.startswith(key) and "cublas" not in k and v["median_us"]]
+        cub = sw.get(f"{key}/cublas_addmm_f32out", {}).get("median_us")
+        if ours:
+            best = min(ours)
+            sw_rows.append(f"| {key.replace('^3', '³').replace('_f32', ' TF32').replace('_bf16', ' BF16')} | "
+                           f"{f(best[0], 2)} µs ({best[1].split('/', 1)[1]}) | {f(cub, 2)} µs |")
+    txt = f"""# RESULTS — COMPAR GEMM hot path on B200 (BASELINE.md §5 format)
+
+Generated by `tools/results_table.py` from committed measurement files only; every row names its
+source.  **Driver-run** = measured by the round driver on a fresh box (`BENCH_r01.json`);
+**builder-run** = measured by this build through `gpurun` during round 2 (one B200, same image) —
+labelled as such.  Peaks: `MEASURED_PEAKS.json` (BF16 burst {f(bf16)} / sustained {f(bf16s)} TFLOP/s,
+HBM {f(hbm)} GB/s); TF32 = BF16 / 2; FP32 FFMA ceiling = 148 SMs × 128 × 2 × 1965 MHz = 74.4 TFLOP/s;
+datasheet BF16 2250 TFLOP/s (secondary).  Parity column: the tolerance rules of DESIGN.md R8 / R33
+(FP32 1e-5; BF16 tensor cores max(1e-5, K·2^-27); TF32 5e-3; every element inside the FP32-accumulation
+bound; integer inputs bitwise) — all `-m gpu` parity suites pass.
+
+{head}
+""" + "\n".join(rows) + f"""
+
+## Single-wave tensor-core shapes (kernel-only, builder-run r02, `profiles/r02_single_wave_ncu.json`)
+
+""" + "\n".join(sw_rows) + """
+
+(Where the time goes and what was changed: `profiles/r02_single_wave_trace.md`.)
+
+## The paper's own numbers, as context (not targets)
+
+The paper reports **no numeric matrix-multiply result**: its execution-time figures (Fig. 1a–1e) survive
+only as placeholders (P:228-268) and `BASELINE.json.published` is empty.  Its setup and qualitative
+findings, quoted with their hardware:
+
+| item | paper (P:n) | here |
+|---|---|---|
+| machine | Xeon E5-2620 v4 (8 cores, 68.3 GB/s) + Titan Xp (GP102, 3840 cores, 1.41–1.58 GHz, 547.6 GB/s, ≈ 12.1 TFLOP/s FP32 derived) — P:153-157, Table 1 | one B200 (148 SMs, 1965 MHz max, ≈ 6.5 TB/s measured, 1672 TFLOP/s BF16 measured burst) |
+| precision / workload | FP32 `float` arrays, square n = 8..8192, mean of 10 repetitions — P:78, P:201-205, P:166 | FP32 / TF32 / BF16 (C FP32), the BASELINE configs, medians of ≥ 10 |
+| variants | BLAS, OpenMP, CUDA, CUBLAS — P:201-205, Table 2 | `simt_f32`, `tma_f32`, `tc_*` (1-SM, pair, wide pair, split-K), `simt_bf16` (GPU only; no CPU class) |
+| which is fastest | n = 8..128 "not always clear"; n = 64..4096 CUDA; n = 4096 CUDA beats CUBLAS; n = 8192 CUBLAS beats CUDA — P:220, P:224 | config 2: `tma_f32` under FP32-strict at every n; under TF32 `tc_tf32` up to 1024, `tc_tf32_2sm` 1536–4096 (selector picks, regret ≤ 0.4 %) |
+| selection quality | StarPU "frequently chose sub-optimal options" (n = 32: OpenMP instead of BLAS; 64..4096: OpenMP / BLAS instead of CUDA) — P:224 | history selector: regret 0–0.4 % on configs 1, 2, 5a, deep-K; ≤ 0.2 % per shape on 5b |
+| runtime overhead | CUDA-only often slightly faster than COMPAR (StarPU decision overhead) — P:222 | host submit ≈ 11 µs per task (config 1, FP32-strict), `profiles/r02_selector.json` |
+"""
+    with open(out, "w") as fh:
+        fh.write(txt)
+    print(txt)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "RESULTS.md"))

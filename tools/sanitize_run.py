@@ -46,3 +46,26 @@ for name in names:
     print(f"{name}: ok", flush=True)
 torch.cuda.synchronize()
 ctx.terminate()
+
+# world mode (loopback, with the NCCL SM reserve): the wide kernel's fused slab-flag launch plus the
+# helper launch sharing its tile counter, row-major (3-D slab map) and transposed B
+if not only or any(n.endswith("_2sm_w") for n in only):
+    os.environ["COMPAR_BCAST_LOOPBACK"] = "2"
+    wctx = cm.Compar(bcast_chunks=4, bcast_ctas=8)
+    os.environ.pop("COMPAR_BCAST_LOOPBACK")
+    wn = [v for v, _ in wctx.variants()]
+    for name in ("tc_bf16_2sm_w", "tc_tf32_2sm_w"):
+        bf = "bf16" in name
+        dt = "bf16" if bf else "f32"
+        for (m, n, k, tb) in ((3000, 4096, 136, 0), (2600, 4096, 264, 1)):
+            A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+            B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))
+            Cd = device_matrix(gen.TAG_C, m, n)
+            d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, ldb=(k if tb else n), alpha=1.5, beta=0.5,
+                             in_dtype=cm.BF16 if bf else cm.F32, compute=cm.COMPUTE_BF16 if bf else cm.COMPUTE_TF32,
+                             transB=tb, world=1, variant_hint=wn.index(name))
+            for _ in range(2):
+                assert wctx.run(d).status == 0, (name, m, n, k)
+        print(f"{name} world loopback: ok", flush=True)
+    torch.cuda.synchronize()
+    wctx.terminate()
