@@ -82,6 +82,10 @@ typedef enum {
     COMPAR_TGT_TCS_TF32 = 10,   /* built-in (c), split-K CTA-pair form: K cut into 2..8 ranges (a function */
                                 /*   of K only), partials summed in split order; small-M*N / deep-K shapes */
     COMPAR_TGT_TCS_BF16 = 11,   /* built-in (c), split-K CTA-pair form, BF16                              */
+    COMPAR_TGT_TCK_TF32 = 12,   /* built-in (c), cluster split-K form: the 2 CTAs of a cluster split one  */
+                                /*   1-SM tile's K (at ceil(kb/2), a function of K only) and reduce   */
+                                /*   through distributed shared memory; single-wave shapes            */
+    COMPAR_TGT_TCK_BF16 = 13,   /* built-in (c), cluster split-K form, BF16                               */
     /* the "sort" interface */
     COMPAR_TGT_SORT_RADIX = 20,   /* built-in: onesweep LSD radix sort, 4 x 8-bit passes, any n      */
     COMPAR_TGT_SORT_BITONIC = 21  /* built-in: single-CTA shared-memory bitonic network, n <= 16384  */

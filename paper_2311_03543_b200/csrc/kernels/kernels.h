@@ -106,6 +106,17 @@ inline int tc_splitk_splits(int64_t m, int64_t n, int64_t k, bool bf16) {
 }
 cudaError_t launch_tc_gemm_splitk(const GemmLaunch &g, bool bf16);
 
+// tc_*_ck (variant c, cluster split-K, tc_gemm_ck.cu): the two CTAs of a cluster split a tile's
+// ceil(K / BK) k-blocks at h = ceil(kb / 2) — a function of K alone (row panels stay bitwise equal).
+// Eligible from 2 k-blocks on.
+inline int tc_clusterk_half(int64_t k, bool bf16) {
+    const int64_t bk = bf16 ? 64 : 32;
+    const int64_t kb = (k + bk - 1) / bk;
+    return static_cast<int>((kb + 1) / 2);
+}
+inline bool tc_clusterk_ok(int64_t k, bool bf16) { return k > (bf16 ? 64 : 32); }
+cudaError_t launch_tc_gemm_ck(const GemmLaunch &g, bool bf16);
+
 // TMA eligibility (the selector's constraint filter).
 inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {
     return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * elem_bytes) % 16 == 0);

@@ -13,6 +13,7 @@ cudaError_t preload_simt_kernels();
 cudaError_t preload_tc2_kernels();
 cudaError_t preload_tcw_kernels();
 cudaError_t preload_tcm_kernels();
+cudaError_t preload_tck_kernels();
 
 namespace {
 
@@ -60,6 +61,7 @@ cudaError_t preload_kernels() {
     if (e == cudaSuccess) e = preload_tc2_kernels();
     if (e == cudaSuccess) e = preload_tcw_kernels();
     if (e == cudaSuccess) e = preload_tcm_kernels();
+    if (e == cudaSuccess) e = preload_tck_kernels();
     return e;
 }
 

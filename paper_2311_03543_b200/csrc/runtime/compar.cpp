@@ -314,11 +314,13 @@ bool admits(compar_target t, compar_dtype dt, compar_compute cp) {
         case COMPAR_TGT_TC_TF32:
         case COMPAR_TGT_TC2_TF32:
         case COMPAR_TGT_TCW_TF32:
-        case COMPAR_TGT_TCS_TF32: return dt == COMPAR_F32 && cp == COMPAR_COMPUTE_TF32;
+        case COMPAR_TGT_TCS_TF32:
+        case COMPAR_TGT_TCK_TF32: return dt == COMPAR_F32 && cp == COMPAR_COMPUTE_TF32;
         case COMPAR_TGT_TC_BF16:
         case COMPAR_TGT_TC2_BF16:
         case COMPAR_TGT_TCW_BF16:
         case COMPAR_TGT_TCS_BF16:
+        case COMPAR_TGT_TCK_BF16:
         case COMPAR_TGT_SIMT_BF16: return dt == COMPAR_BF16 && cp == COMPAR_COMPUTE_BF16;
         case COMPAR_TGT_SORT_RADIX:
         case COMPAR_TGT_SORT_BITONIC: return false;   // the sort interface's variants
@@ -340,9 +342,11 @@ bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, co
     if ((simt || t == COMPAR_TGT_TMA_F32) && (mrows + 127) / 128 > 65535) return false;
     if (simt) return true;
     const int eb = (t == COMPAR_TGT_TC_BF16 || t == COMPAR_TGT_TC2_BF16 || t == COMPAR_TGT_TCW_BF16 ||
-                    t == COMPAR_TGT_TCS_BF16) ? 2 : 4;
+                    t == COMPAR_TGT_TCS_BF16 || t == COMPAR_TGT_TCK_BF16) ? 2 : 4;
     if ((t == COMPAR_TGT_TCS_TF32 || t == COMPAR_TGT_TCS_BF16) &&
         tc_splitk_splits(mrows, d->n, d->k, t == COMPAR_TGT_TCS_BF16) < 2)
+        return false;
+    if ((t == COMPAR_TGT_TCK_TF32 || t == COMPAR_TGT_TCK_BF16) && !tc_clusterk_ok(d->k, t == COMPAR_TGT_TCK_BF16))
         return false;
     if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;
     if ((d->lda * eb) % 16 != 0 || (d->ldb * eb) % 16 != 0) return false;
@@ -711,6 +715,8 @@ compar_status run_builtin(Ctx *c, compar_target t, const compar_gemm_desc *d, co
         case COMPAR_TGT_TCW_BF16: e = launch_tc_gemm_2sm_wide(g, true); break;
         case COMPAR_TGT_TCS_TF32: e = launch_tc_gemm_splitk(g, false); break;
         case COMPAR_TGT_TCS_BF16: e = launch_tc_gemm_splitk(g, true); break;
+        case COMPAR_TGT_TCK_TF32: e = launch_tc_gemm_ck(g, false); break;
+        case COMPAR_TGT_TCK_BF16: e = launch_tc_gemm_ck(g, true); break;
         case COMPAR_TGT_SIMT_BF16: e = launch_simt_bf16(g); break;
         default: return fail(COMPAR_E_INVALID, "not a built-in target");
     }
@@ -1271,6 +1277,8 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         compar_register_variant(c, "gemm", "simt_bf16", COMPAR_TGT_SIMT_BF16, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_tf32_sk", COMPAR_TGT_TCS_TF32, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_bf16_sk", COMPAR_TGT_TCS_BF16, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "tc_tf32_ck", COMPAR_TGT_TCK_TF32, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "tc_bf16_ck", COMPAR_TGT_TCK_BF16, nullptr, nullptr, &id);
         compar_register_sort_variant(c, "sort_radix", COMPAR_TGT_SORT_RADIX, nullptr, nullptr, &id);
         compar_register_sort_variant(c, "sort_bitonic", COMPAR_TGT_SORT_BITONIC, nullptr, nullptr, &id);
     }
@@ -1350,7 +1358,7 @@ compar_status compar_register_variant(void *ctx, const char *iface, const char *
     if (!name || !*name || std::strlen(name) > 63) return fail(COMPAR_E_INVALID, "bad variant name");
     for (const char *p = name; *p; ++p)
         if (*p == ' ' || *p == '\t' || *p == '\n') return fail(COMPAR_E_INVALID, "variant name has whitespace");
-    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_TCS_BF16) return fail(COMPAR_E_INVALID, "unknown target");
+    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_TCK_BF16) return fail(COMPAR_E_INVALID, "unknown target");
     if (target == COMPAR_TGT_USER && !fn) return fail(COMPAR_E_INVALID, "USER variant needs a launch function");
     if (target != COMPAR_TGT_USER && c->virt) return fail(COMPAR_E_INVALID, "built-in targets need CUDA");
     std::lock_guard<std::mutex> lk(c->mu);
@@ -1467,11 +1475,13 @@ double static_lb_ns(const Ctx *c, compar_target t, const Key &k) {
         case COMPAR_TGT_TC_BF16:
         case COMPAR_TGT_TC2_BF16:
         case COMPAR_TGT_TCW_BF16:
-        case COMPAR_TGT_TCS_BF16: peak = 2.25e15; break;
+        case COMPAR_TGT_TCS_BF16:
+        case COMPAR_TGT_TCK_BF16: peak = 2.25e15; break;
         case COMPAR_TGT_TC_TF32:
         case COMPAR_TGT_TC2_TF32:
         case COMPAR_TGT_TCW_TF32:
-        case COMPAR_TGT_TCS_TF32: peak = 1.125e15; break;
+        case COMPAR_TGT_TCS_TF32:
+        case COMPAR_TGT_TCK_TF32: peak = 1.125e15; break;
         default: return 0.0;
     }
     const double m = static_cast<double>(k.m), n = static_cast<double>(k.n), kk = static_cast<double>(k.k);

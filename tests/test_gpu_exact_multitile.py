@@ -79,11 +79,12 @@ def test_multitile_full_compare(ctx, name, transB):
 
 
 def test_multitile_full_compare_splitk(ctx):
-    """The split-K variants over many (tile, k-range) work items: bitwise too (planes summed in
-    split order, every partial an exact integer)."""
+    """The split-K variants over many (tile, k-range) work items and the cluster split-K variants over
+    many clusters (several waves): bitwise too (partials summed in split order, every partial an
+    exact integer)."""
     m, n, k = 2048, 1536, 4160
     ref = full_ref(m, n, k)
-    for name in ("tc_tf32_sk", "tc_bf16_sk"):
+    for name in ("tc_tf32_sk", "tc_bf16_sk", "tc_tf32_ck", "tc_bf16_ck"):
         got = launch(ctx, name, m, n, k).double().cpu().numpy()
         np.testing.assert_array_equal(got, ref, err_msg=name)
 

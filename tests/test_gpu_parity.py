@@ -35,6 +35,8 @@ VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tc_bf16_2sm_w": (cm.BF16, cm.COMPUTE_BF16, 1e-5),
             "tc_tf32_sk": (cm.F32, cm.COMPUTE_TF32, 5e-3),
             "tc_bf16_sk": (cm.BF16, cm.COMPUTE_BF16, 1e-5),
+            "tc_tf32_ck": (cm.F32, cm.COMPUTE_TF32, 5e-3),
+            "tc_bf16_ck": (cm.BF16, cm.COMPUTE_BF16, 1e-5),
             # FP32 accumulation of exactly-widened BF16 operands: held to the strict-FP32 bound
             "simt_bf16": (cm.BF16, cm.COMPUTE_BF16, 1e-5)}
 
@@ -53,6 +55,8 @@ def sk_splits(m, n, k, bf16):
 def skip_ineligible(name, m, n, k):
     if name.endswith("_sk") and not sk_splits(m, n, k, "bf16" in name):
         pytest.skip(f"{name} needs >= 64 k-blocks (K = {k})")
+    if name.endswith("_ck") and k <= (64 if "bf16" in name else 32):
+        pytest.skip(f"{name} needs >= 2 k-blocks (K = {k})")
 
 
 @pytest.fixture(scope="module")

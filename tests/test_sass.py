@@ -46,8 +46,9 @@ def has(ops, prefix):
 
 
 def test_tcgen05_one_sm_kernels(kernels):
-    for n, ops in family(kernels, "tc_gemm_kernel<").items():
-        assert has(ops, "UTCHMMA") and has(ops, "UTMALDG") and has(ops, "LDTM"), n
+    for tag in ("tc_gemm_kernel<", "tc_gemm_ck_kernel<"):
+        for n, ops in family(kernels, tag).items():
+            assert has(ops, "UTCHMMA") and has(ops, "UTMALDG") and has(ops, "LDTM"), n
 
 
 def test_tcgen05_pair_kernels(kernels):

@@ -16,7 +16,8 @@ sys.path.insert(0, ROOT)
 
 SHAPES = [(1024, "bf16"), (2048, "bf16"), (1024, "f32"), (2048, "f32")]
 CONFIGS = [("tc", "COMPAR_TC1_BN", "256"), ("tc", "COMPAR_TC1_BN", "128"), ("tc", "COMPAR_TC1_BN", "64"),
-           ("tc2", "COMPAR_TC2_BN", "256"), ("tc2", "COMPAR_TC2_BN", "128"), ("w", None, None), ("cublas", None, None)]
+           ("tc2", "COMPAR_TC2_BN", "256"), ("tc2", "COMPAR_TC2_BN", "128"), ("w", None, None), ("ck", None, None),
+           ("cublas", None, None)]
 REPS = 5
 
 
@@ -25,7 +26,8 @@ def labels():
     for s, dt in SHAPES:
         pre = "tc_bf16" if dt == "bf16" else "tc_tf32"
         for fam, env, val in CONFIGS:
-            name = {"tc": pre, "tc2": pre + "_2sm", "w": pre + "_2sm_w", "cublas": "cublas_addmm_f32out"}[fam]
+            name = {"tc": pre, "tc2": pre + "_2sm", "w": pre + "_2sm_w", "ck": pre + "_ck",
+                    "cublas": "cublas_addmm_f32out"}[fam]
             out.append(f"{s}^3_{dt}/{name}{'/' + val if val else ''}")
     return out
 
@@ -60,7 +62,7 @@ def run():
             if env:
                 os.environ.pop(env)
             names = [v for v, _ in ctx.variants()]
-            name = {"tc": pre, "tc2": pre + "_2sm", "w": pre + "_2sm_w"}[fam]
+            name = {"tc": pre, "tc2": pre + "_2sm", "w": pre + "_2sm_w", "ck": pre + "_ck"}[fam]
             d = cm.make_desc(s, s, s, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=0.5,
                              in_dtype=cm.BF16 if dt == "bf16" else cm.F32,
                              compute=cm.COMPUTE_BF16 if dt == "bf16" else cm.COMPUTE_TF32,
