@@ -173,8 +173,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
         }
         if (lane == 0) ptx::tc_commit(tfull);
         __syncwarp();
-    } else {  // ---------------- epilogue warps: the accumulator is complete
-        ptx::mbar_wait(tfull, 0);
+    }
+    // epilogue warps: this thread's C_in values (rows ew + 4 i of the CTA's 64, columns lane * 4 +
+    // 128 j) are fetched while the mainloop runs — issued together, not one dependent round trip
+    // per row in the reduction below
+    constexpr int kCj = (C::BN + 127) / 128;
+    float4 cin[16][kCj];
+    const int ew = warp - 2;
+    if (warp >= 2) {
+        const bool ldc = p.beta != 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+#pragma unroll
+            for (int j = 0; j < kCj; ++j) {
+                cin[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int64_t grow = static_cast<int64_t>(mb) * C::BM + static_cast<int64_t>(rank) * 64 + ew + 4 * i;
+                const int col = lane * 4 + 128 * j;
+                const int64_t gcol = static_cast<int64_t>(nb) * C::BN + col;
+                if (ldc && col < C::BN && grow < p.m && p.cvec && gcol + 4 <= p.n)
+                    cin[i][j] = __ldg(reinterpret_cast<const float4 *>(p.C_in + grow * p.ldc_in + gcol));
+            }
+        }
+        ptx::mbar_wait(tfull, 0);                    // the accumulator is complete
         ptx::tc_fence_after();
     }
     // both CTAs' rings are idle (every MMA read its stage; every load landed): the receive buffers
@@ -205,33 +225,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
     ptx::cluster_sync();                             // both partials of every owned row have landed
     if (warp >= 2) {
         // rows [64 rank, 64 rank + 64) of the tile: 16 per warp, 4 consecutive columns per lane
-        const int ew = warp - 2;
         const bool ldc = p.beta != 0.f;
-        for (int rr = ew; rr < 64; rr += 4) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int rr = ew + 4 * i;
             const int64_t grow = static_cast<int64_t>(mb) * C::BM + static_cast<int64_t>(rank) * 64 + rr;
             if (grow >= p.m) break;
-            const float *cin = p.C_in + grow * p.ldc_in;
             float *cout = p.C_out + grow * p.ldc_out;
-            for (int col = lane * 4; col < C::BN; col += 128) {
+#pragma unroll
+            for (int j = 0; j < kCj; ++j) {
+                const int col = lane * 4 + 128 * j;
                 const int64_t gcol = static_cast<int64_t>(nb) * C::BN + col;
-                if (gcol >= p.n) break;
+                if (col >= C::BN || gcol >= p.n) break;
                 const float4 s0 = ptx::lds128(smem0 + recv_off<C::BN>(0, rr, col >> 2));
                 const float4 s1 = ptx::lds128(smem0 + recv_off<C::BN>(1, rr, col >> 2));
                 float o[4] = {p.alpha * (s0.x + s1.x), p.alpha * (s0.y + s1.y), p.alpha * (s0.z + s1.z),
                               p.alpha * (s0.w + s1.w)};
                 if (p.cvec && gcol + 4 <= p.n) {
                     if (ldc) {
-                        const float4 ci = *reinterpret_cast<const float4 *>(cin + gcol);
-                        o[0] = fmaf(p.beta, ci.x, o[0]);
-                        o[1] = fmaf(p.beta, ci.y, o[1]);
-                        o[2] = fmaf(p.beta, ci.z, o[2]);
-                        o[3] = fmaf(p.beta, ci.w, o[3]);
+                        o[0] = fmaf(p.beta, cin[i][j].x, o[0]);
+                        o[1] = fmaf(p.beta, cin[i][j].y, o[1]);
+                        o[2] = fmaf(p.beta, cin[i][j].z, o[2]);
+                        o[3] = fmaf(p.beta, cin[i][j].w, o[3]);
                     }
                     *reinterpret_cast<float4 *>(cout + gcol) = make_float4(o[0], o[1], o[2], o[3]);
-                } else {
+                } else {                             // ragged / unaligned edge: scalar
+                    const float *cr = p.C_in + grow * p.ldc_in;
                     for (int e = 0; e < 4 && gcol + e < p.n; ++e) {
                         float v = o[e];
-                        if (ldc) v = fmaf(p.beta, cin[gcol + e], v);
+                        if (ldc) v = fmaf(p.beta, cr[gcol + e], v);
                         cout[gcol + e] = v;
                     }
                 }
@@ -278,11 +300,13 @@ cudaError_t launch_tck_t(const GemmLaunch &g) {
 }  // namespace
 
 cudaError_t launch_tc_gemm_ck(const GemmLaunch &g, bool bf16) {
-    // Tile width: the widest of 256 / 128 / 64 whose 2 CTAs per tile still fit one wave (every
-    // element's k split and order are the same for any width: bitwise-identical C).
+    // Tile width: the narrowest of 64 / 128 / 256 whose 2 CTAs per tile fit one wave — most SMs
+    // busy, since a K = 16 MMA costs about the same at any N (profiles/r02_single_wave_trace.md);
+    // 256 when none fits.  Every element's k split and order are the same for any width
+    // (bitwise-identical C).
     const int64_t mb = (g.m + 127) / 128;
-    int bn = 64;
-    for (int w : {256, 128}) {
+    int bn = 256;
+    for (int w : {64, 128}) {
         if (2 * mb * ((g.n + w - 1) / w) <= g.num_sms) {
             bn = w;
             break;
