@@ -28,6 +28,26 @@ namespace {
 
 constexpr int kThreadsK = 192;
 
+#ifdef COMPAR_TRACE
+// Development-only phase stamps of CTA 0 (tools/trace_pair.py run2, -DCOMPAR_TRACE build).
+__device__ unsigned long long g_trace2[16];
+#define TRACE2(i)                                                                             \
+    do {                                                                                      \
+        if (blockIdx.x == 0) g_trace2[i] = clock64();                                        \
+    } while (0)
+#define TRACE2_GT(i)                                                                          \
+    do {                                                                                      \
+        if (blockIdx.x == 0) {                                                                \
+            unsigned long long t;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                           \
+            g_trace2[i] = t;                                                                  \
+        }                                                                                     \
+    } while (0)
+#else
+#define TRACE2(i) ((void)0)
+#define TRACE2_GT(i) ((void)0)
+#endif
+
 template <bool kBF16, bool kTransB, int kBN>
 struct TcKCfg {
     static constexpr int BM = 128, BN = kBN;
@@ -88,6 +108,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::DATA_BYTES + 480);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        TRACE2_GT(10);
+        TRACE2(0);
+    }
     const uint32_t rank = ptx::cluster_ctarank();
     const int tile = static_cast<int>(blockIdx.x >> 1);
     const int mb = tile / p.n_blocks, nb = tile - (tile / p.n_blocks) * p.n_blocks;
@@ -127,6 +151,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TRACE2(1);
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer: this CTA's half of K
@@ -150,6 +175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
         uint32_t phase = 0;
         for (int i = 0; i < nk; ++i) {
             ptx::mbar_wait(full0 + 8 * stage, phase);
+            if (i == 0 && lane == 0) TRACE2(2);
             ptx::tc_fence_after();
             if (lane == 0) {
                 const uint32_t so = stage * C::STAGE_BYTES;
@@ -196,12 +222,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
         }
         ptx::mbar_wait(tfull, 0);                    // the accumulator is complete
         ptx::tc_fence_after();
+        if (warp == 2 && lane == 0) TRACE2(3);
     }
     // both CTAs' rings are idle (every MMA read its stage; every load landed): the receive buffers
     // (aliasing the rings) may be written from either CTA
     ptx::tc_fence_before();
     ptx::cluster_sync();
     ptx::tc_fence_after();
+    if (threadIdx.x == 64) TRACE2(4);
     if (warp >= 2) {
         const int q = warp & 3;                      // TMEM lanes / tile rows [32q, 32q + 32)
         const uint32_t owner = static_cast<uint32_t>(q >> 1);
@@ -221,8 +249,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
             }
         }
     }
+    if (threadIdx.x == 64) TRACE2(5);
     ptx::tc_fence_before();
     ptx::cluster_sync();                             // both partials of every owned row have landed
+    if (threadIdx.x == 64) TRACE2(6);
     if (warp >= 2) {
         // rows [64 rank, 64 rank + 64) of the tile: 16 per warp, 4 consecutive columns per lane
         const bool ldc = p.beta != 0.f;
@@ -260,7 +290,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
             }
         }
     }
+    if (threadIdx.x == 64) TRACE2(7);
     __syncthreads();
+    if (threadIdx.x == 0) {
+        TRACE2(8);
+        TRACE2_GT(11);
+    }
     if (warp == 1) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
@@ -298,6 +333,12 @@ cudaError_t launch_tck_t(const GemmLaunch &g) {
 }
 
 }  // namespace
+
+#ifdef COMPAR_TRACE
+int trace2_read(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_trace2, sizeof(g_trace2)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 cudaError_t launch_tc_gemm_ck(const GemmLaunch &g, bool bf16) {
     // Tile width: the narrowest of 64 / 128 / 256 whose 2 CTAs per tile fit one wave — most SMs
@@ -347,3 +388,7 @@ cudaError_t preload_tck_kernels() {
 }
 
 }  // namespace compar
+
+#ifdef COMPAR_TRACE
+extern "C" int compar_trace2_read(unsigned long long *out) { return compar::trace2_read(out); }
+#endif

@@ -33,7 +33,7 @@ for name in names:
     if name.endswith("_sk"):   # the split-K variant needs >= 64 k-blocks
         shapes = [(77, 136, 4160, 0, 0.5, 1), (300, 264, 8200, 1, 0.0, 3), (129, 520, 4160, 0, -1.0, 2)]
     else:                      # more tiles than CTAs / clusters: the counter-fed tiles after the static first
-        shapes.append((4096, 2304, 64, 0, 0.5, 1))
+        shapes.append((4096, 2304, 136 if name.endswith("_ck") else 64, 0, 0.5, 1))
     for (m, n, k, tb, beta, panels) in shapes:
         A = device_matrix(gen.TAG_A, m, k, dtype=dt)
         B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))

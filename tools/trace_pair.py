@@ -39,7 +39,10 @@ lib = ctypes.CDLL(os.environ["COMPAR_LIB"])
 ctx = cm.Compar()
 names = [v for v, _ in ctx.variants()]
 args = [int(x) for x in sys.argv[2:]] or [256, 128, 64]
-one_sm = sys.argv[1] == "run1"   # the 1-SM kernel (tc_gemm.cu; stamps of CTA 0: 0 entry, 1 init,
+one_sm = sys.argv[1] in ("run1", "run2")   # run2: the cluster split-K kernel (tc_gemm_ck.cu; stamps
+                                           # 1 init, 2 first stage, 3 accumulator complete, 4 after
+                                           # cluster barrier 1, 5 partials sent, 6 after barrier 2,
+                                           # 7 reduced + stored, 8 exit)   # the 1-SM kernel (tc_gemm.cu; stamps of CTA 0: 0 entry, 1 init,
                                   # 2 first TMA, 3 / 4 first / last stage landed, 5 epilogue sees the
                                   # accumulator, 6 tile stored, 8 exit; 10 / 11 globaltimer)
 for i in range(0, len(args), 3):
@@ -50,13 +53,15 @@ for i in range(0, len(args), 3):
             B = device_matrix(gen.TAG_B, k, n, dtype="bf16")
             C = device_matrix(gen.TAG_C, m, n)
             d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=beta, in_dtype=cm.BF16,
-                             compute=cm.COMPUTE_BF16, variant_hint=names.index("tc_bf16"))
+                             compute=cm.COMPUTE_BF16,
+                             variant_hint=names.index("tc_bf16_ck" if sys.argv[1] == "run2" else "tc_bf16"))
             for _ in range(5):
                 rep = ctx.run(d)
             buf = (ctypes.c_ulonglong * 16)()
-            assert lib.compar_trace1_read(buf) == 0
+            assert (lib.compar_trace2_read if sys.argv[1] == "run2" else lib.compar_trace1_read)(buf) == 0
             t = list(buf)
-            st = " ".join(f"{j}:{t[j] - t[0]:6d}" for j in (1, 2, 3, 4, 5, 6, 8))
+            st = " ".join(f"{j}:{t[j] - t[0]:6d}" for j in ((1, 2, 3, 4, 5, 6, 7, 8) if sys.argv[1] == "run2"
+                                                                 else (1, 2, 3, 4, 5, 6, 8)))
             print(f"1sm {m}x{n}x{k} beta={beta}: {st} | wall {(t[11] - t[10]) / 1e3:.2f} us | event {rep.ns / 1e3:.2f} us",
                   flush=True)
         continue
