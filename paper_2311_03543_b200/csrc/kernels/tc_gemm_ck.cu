@@ -235,17 +235,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
         const uint32_t owner = static_cast<uint32_t>(q >> 1);
         const int row = (q & 1) * 32 + lane;         // row inside the owner's 64
         const uint32_t dst = ptx::mapa_rank(smem0, owner);
+        const uint32_t tq = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+        uint32_t r[32], rn[32];
+        ptx::tmem_ld_32x32b_x32(tq, r);
+        ptx::tmem_ld_wait();
 #pragma unroll 1
         for (int c = 0; c < C::BN / 32; ++c) {
-            uint32_t r[32];
-            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
-            ptx::tmem_ld_wait();
+            if (c + 1 < C::BN / 32) ptx::tmem_ld_32x32b_x32(tq + (c + 1) * 32, rn);   // next chunk in flight
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
                 const uint32_t a = dst + recv_off<C::BN>(static_cast<int>(rank), row, c * 8 + g);
                 asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(r[4 * g]),
                              "r"(r[4 * g + 1]), "r"(r[4 * g + 2]), "r"(r[4 * g + 3])
                              : "memory");
+            }
+            if (c + 1 < C::BN / 32) {
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) r[e] = rn[e];
             }
         }
     }
@@ -254,37 +261,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
     ptx::cluster_sync();                             // both partials of every owned row have landed
     if (threadIdx.x == 64) TRACE2(6);
     if (warp >= 2) {
-        // rows [64 rank, 64 rank + 64) of the tile: 16 per warp, 4 consecutive columns per lane
+        // rows [64 rank, 64 rank + 64) of the tile: 16 per warp, 4 consecutive columns per lane; in
+        // groups of kG rows, both partial slots read for the whole group before any store
         const bool ldc = p.beta != 0.f;
+        constexpr int kG = 8 / kCj;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int rr = ew + 4 * i;
-            const int64_t grow = static_cast<int64_t>(mb) * C::BM + static_cast<int64_t>(rank) * 64 + rr;
-            if (grow >= p.m) break;
-            float *cout = p.C_out + grow * p.ldc_out;
+        for (int i0 = 0; i0 < 16; i0 += kG) {
+            float4 s0[kG][kCj], s1[kG][kCj];
 #pragma unroll
-            for (int j = 0; j < kCj; ++j) {
-                const int col = lane * 4 + 128 * j;
-                const int64_t gcol = static_cast<int64_t>(nb) * C::BN + col;
-                if (col >= C::BN || gcol >= p.n) break;
-                const float4 s0 = ptx::lds128(smem0 + recv_off<C::BN>(0, rr, col >> 2));
-                const float4 s1 = ptx::lds128(smem0 + recv_off<C::BN>(1, rr, col >> 2));
-                float o[4] = {p.alpha * (s0.x + s1.x), p.alpha * (s0.y + s1.y), p.alpha * (s0.z + s1.z),
-                              p.alpha * (s0.w + s1.w)};
-                if (p.cvec && gcol + 4 <= p.n) {
-                    if (ldc) {
-                        o[0] = fmaf(p.beta, cin[i][j].x, o[0]);
-                        o[1] = fmaf(p.beta, cin[i][j].y, o[1]);
-                        o[2] = fmaf(p.beta, cin[i][j].z, o[2]);
-                        o[3] = fmaf(p.beta, cin[i][j].w, o[3]);
+            for (int i = 0; i < kG; ++i) {
+#pragma unroll
+                for (int j = 0; j < kCj; ++j) {
+                    const int col = lane * 4 + 128 * j;
+                    if (col < C::BN) {
+                        s0[i][j] = ptx::lds128(smem0 + recv_off<C::BN>(0, ew + 4 * (i0 + i), col >> 2));
+                        s1[i][j] = ptx::lds128(smem0 + recv_off<C::BN>(1, ew + 4 * (i0 + i), col >> 2));
                     }
-                    *reinterpret_cast<float4 *>(cout + gcol) = make_float4(o[0], o[1], o[2], o[3]);
-                } else {                             // ragged / unaligned edge: scalar
-                    const float *cr = p.C_in + grow * p.ldc_in;
-                    for (int e = 0; e < 4 && gcol + e < p.n; ++e) {
-                        float v = o[e];
-                        if (ldc) v = fmaf(p.beta, cr[gcol + e], v);
-                        cout[gcol + e] = v;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kG; ++i) {
+                const int rr = ew + 4 * (i0 + i);
+                const int64_t grow = static_cast<int64_t>(mb) * C::BM + static_cast<int64_t>(rank) * 64 + rr;
+                float *cout = p.C_out + grow * p.ldc_out;
+#pragma unroll
+                for (int j = 0; j < kCj; ++j) {
+                    const int col = lane * 4 + 128 * j;
+                    const int64_t gcol = static_cast<int64_t>(nb) * C::BN + col;
+                    if (col >= C::BN || grow >= p.m || gcol >= p.n) continue;
+                    const float4 cij = cin[i0 + i][j];
+                    float o[4] = {p.alpha * (s0[i][j].x + s1[i][j].x), p.alpha * (s0[i][j].y + s1[i][j].y),
+                                  p.alpha * (s0[i][j].z + s1[i][j].z), p.alpha * (s0[i][j].w + s1[i][j].w)};
+                    if (p.cvec && gcol + 4 <= p.n) {
+                        if (ldc) {
+                            o[0] = fmaf(p.beta, cij.x, o[0]);
+                            o[1] = fmaf(p.beta, cij.y, o[1]);
+                            o[2] = fmaf(p.beta, cij.z, o[2]);
+                            o[3] = fmaf(p.beta, cij.w, o[3]);
+                        }
+                        *reinterpret_cast<float4 *>(cout + gcol) = make_float4(o[0], o[1], o[2], o[3]);
+                    } else {                         // ragged / unaligned edge: scalar
+                        const float *cr = p.C_in + grow * p.ldc_in;
+                        for (int e = 0; e < 4 && gcol + e < p.n; ++e) {
+                            float v = o[e];
+                            if (ldc) v = fmaf(p.beta, cr[gcol + e], v);
+                            cout[gcol + e] = v;
+                        }
                     }
                 }
             }
