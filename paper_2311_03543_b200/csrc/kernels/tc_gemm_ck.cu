@@ -217,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK, 1)
                 const int col = lane * 4 + 128 * j;
                 const int64_t gcol = static_cast<int64_t>(nb) * C::BN + col;
                 if (ldc && col < C::BN && grow < p.m && p.cvec && gcol + 4 <= p.n)
-                    cin[i][j] = __ldg(reinterpret_cast<const float4 *>(p.C_in + grow * p.ldc_in + gcol));
+                    cin[i][j] = ptx::ldg128_now(p.C_in + grow * p.ldc_in + gcol);
             }
         }
         ptx::mbar_wait(tfull, 0);                    // the accumulator is complete
