@@ -31,30 +31,61 @@ bool History::best_mean(const std::vector<int> &ids, const Key &k, unsigned __in
     return found;
 }
 
-bool History::pruned(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb, size_t i) {
-    if (prune_pct <= 0) return false;
-    unsigned __int128 bs = 0;
+namespace {
+// The records of one decision's eligible variants, looked up once (the submit path is the paper's
+// "decision overhead": one map lookup per variant instead of one per test).
+struct KeyView {
+    std::vector<Record *> r;
+    bool have_best = false;
+    unsigned __int128 bs = 0;   // best mean as the exact fraction bs / bc
     int64_t bc = 0;
-    if (!best_mean(ids, k, &bs, &bc)) return false;
-    const Record &r = rec(ids[i], k);
-    // measured: mean_i > P/100 * best  <=>  100 * sum_i * bc > P * bs * count_i
-    if (r.count > 0 && 100 * r.sum_ns * static_cast<unsigned __int128>(bc) >
-                           static_cast<unsigned __int128>(prune_pct) * bs * static_cast<unsigned __int128>(r.count))
+};
+
+void view(History &h, const std::vector<int> &ids, const Key &k, KeyView &v) {
+    v.r.resize(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) v.r[i] = &h.rec(ids[i], k);
+    for (const Record *r : v.r) {
+        if (r->count == 0) continue;
+        if (!v.have_best || r->sum_ns * static_cast<unsigned __int128>(v.bc) <
+                                v.bs * static_cast<unsigned __int128>(r->count)) {
+            v.bs = r->sum_ns;
+            v.bc = r->count;
+            v.have_best = true;
+        }
+    }
+}
+
+// R32 on a prepared view.
+bool pruned_in(const KeyView &v, int prune_pct, const std::vector<double> *lb, size_t i) {
+    if (prune_pct <= 0 || !v.have_best) return false;
+    const Record &r = *v.r[i];
+    if (r.count > 0 && 100 * r.sum_ns * static_cast<unsigned __int128>(v.bc) >
+                           static_cast<unsigned __int128>(prune_pct) * v.bs * static_cast<unsigned __int128>(r.count))
         return true;
-    // static: lb_i > P/100 * best  <=>  lb_i * 100 * bc > P * bs   (double, same order as the oracle)
     const double l = lb ? (*lb)[i] : 0.0;
-    return l > 0.0 && l * 100.0 * static_cast<double>(bc) > static_cast<double>(prune_pct) * static_cast<double>(bs);
+    return l > 0.0 && l * 100.0 * static_cast<double>(v.bc) > static_cast<double>(prune_pct) * static_cast<double>(v.bs);
+}
+}  // namespace
+
+bool History::pruned(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb, size_t i) {
+    KeyView v;
+    view(*this, ids, k, v);
+    return pruned_in(v, prune_pct, lb, i);
 }
 
 bool History::calibrating(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb) {
     const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
+    KeyView v;
+    view(*this, ids, k, v);
     for (size_t i = 0; i < ids.size(); ++i)
-        if (rec(ids[i], k).seen < need && !pruned(ids, k, lb, i)) return true;
+        if (v.r[i]->seen < need && !pruned_in(v, prune_pct, lb, i)) return true;
     return false;
 }
 
 int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const std::vector<double> *lb) {
     const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
+    KeyView v;
+    view(*this, ids, k, v);
     // Calibration.  Interleaved: least-seen eligible variant, first in registry order on ties.
     // Blocked: the variant of smallest lower bound (ties: eligibility order) that has not completed
     // its W + K executions.  Pruned variants (R32) are done calibrating.
@@ -62,8 +93,8 @@ int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const
     int64_t best_seen = 0;
     double best_lb = 0.0;
     for (size_t i = 0; i < ids.size(); ++i) {
-        const int64_t s = rec(ids[i], k).seen;
-        if (s >= need || pruned(ids, k, lb, i)) continue;
+        const int64_t s = v.r[i]->seen;
+        if (s >= need || pruned_in(v, prune_pct, lb, i)) continue;
         const double l = lb ? (*lb)[i] : 0.0;
         if (calib_blocked) {
             if (best < 0 || l < best_lb) {
@@ -83,13 +114,13 @@ int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const
     // Model: argmin of sum/count compared as sum_a * count_b < sum_b * count_a (exact).
     best = -1;
     for (size_t i = 0; i < ids.size(); ++i) {
-        const Record &r = rec(ids[i], k);
+        const Record &r = *v.r[i];
         if (r.count == 0) continue;
         if (best < 0) {
             best = static_cast<int>(i);
             continue;
         }
-        const Record &b = rec(ids[best], k);
+        const Record &b = *v.r[best];
         // 128-bit products: sums < 2^96 in practice, counts < 2^31.
         if (r.sum_ns * static_cast<unsigned __int128>(b.count) < b.sum_ns * static_cast<unsigned __int128>(r.count))
             best = static_cast<int>(i);
