@@ -69,6 +69,7 @@ class SelectorOracle:
     calib_k: int = 3           # K_cal
     eager: bool = False
     blocked: bool = False      # calibration order (R19); False = SPEC S:369 interleaving
+    explore_pct: int = 150     # DESIGN.md R37 predict-mode exploration threshold (percent)
     prune_pct: int = 300       # DESIGN.md R32 calibration pruning threshold (percent, the runtime default); 0 = SPEC
     hist: dict = field(default_factory=dict)   # (v, key) -> Record
 
@@ -246,6 +247,12 @@ class SelectorOracle:
                 best = (v, est[t][0], est[t][1])
         if best is None:
             return None
+        if not best[2] and self.explore_pct > 0:
+            # R37: the best estimate is a measured mean; a variant known only by its prediction,
+            # predicted within explore_pct/100 of it, is measured (W + 1 runs) before it is trusted
+            for t, v in enumerate(eligible):
+                if est[t] is not None and est[t][1] and est[t][0] * 100.0 <= float(self.explore_pct) * best[1]:
+                    return v, (MODE_WARMUP if self.rec(v, key).seen < self.calib_warmup else MODE_CALIB)
         return best[0], (MODE_PREDICT if best[2] else MODE_MODEL)
 
     # ---- R32 static lower bound of a built-in GEMM variant (mirrors the runtime's class peaks,

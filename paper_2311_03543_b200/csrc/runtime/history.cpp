@@ -267,6 +267,16 @@ int History::decide_predict(const std::vector<int> &ids, const Key &k, Mode *mod
         if (best < 0 || est[i] < est[best]) best = static_cast<int>(i);
     }
     if (best < 0) return -1;
+    if (!pred[best] && explore_pct > 0) {
+        // R37: the best estimate is a measured mean; a variant known only by its prediction,
+        // predicted within explore_pct/100 of it, is measured (W + 1 runs) before it is trusted.
+        for (size_t i = 0; i < ids.size(); ++i)
+            if (known[i] && pred[i] && est[i] * 100.0 <= static_cast<double>(explore_pct) * est[best]) {
+                const Record *r = find(ids[i], k);
+                *mode = (r ? r->seen : 0) < calib_warmup ? kWarmup : kCalib;
+                return static_cast<int>(i);
+            }
+    }
     *mode = pred[best] ? kPredict : kModel;
     return best;
 }

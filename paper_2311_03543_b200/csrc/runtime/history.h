@@ -56,6 +56,7 @@ public:
     int calib_k = 3;
     bool calib_blocked = true;
     int prune_pct = 300;   // 0: no pruning (SPEC S:363-371 behaviour)
+    int explore_pct = 150; // predict mode (R37): measure a predicted variant within this % of the measured best
 
     // Records belong to variant NAMES (so a loaded perf model applies to whichever registry index
     // that name gets); names are interned to small ids for the hot path.
@@ -93,6 +94,8 @@ public:
     // Decision of the "predict" scheduler: measured mean where (v, key) has samples, prediction
     // otherwise; returns -1 (caller falls back to calibration) if some variant has neither.
     // A variant with neither whose lower bound exceeds prune_pct/100 x the best estimate is skipped.
+    // R37: when the best estimate is measured, the first variant (eligibility order) known only by
+    // a prediction within explore_pct/100 of it is returned instead, as a warm-up / calibration run.
     int decide_predict(const std::vector<int> &ids, const Key &k, Mode *mode,
                        const std::vector<double> *lb = nullptr) const;
     // Positions (into ids) of the variants with neither a sample for k nor a prediction (and not

@@ -267,10 +267,11 @@ def test_failed_variant_marks_task_failed_without_retry():
 
 def test_predict_scheduler_matches_oracle():
     """NEXT-2 through the C ABI (sched = predict): after training on four sizes, unseen sizes are
-    decided from the fitted models without calibration; every decision equals the oracle's."""
-    cost = [lambda m, n, k: 40_000 + 800.0 * 2 * m * n * k * 1e-9,
+    decided from the fitted models without calibration, a close prediction is explored (R37);
+    every decision equals the oracle's."""
+    cost = [lambda m, n, k: (40_000 + 800.0 * 2 * m * n * k * 1e-9) * (1.2 if m == 5000 else 1.0),
             lambda m, n, k: 4_000 + 2_500.0 * 2 * m * n * k * 1e-9,
-            lambda m, n, k: 20_000 + 1_200.0 * 2 * m * n * k * 1e-9]
+            lambda m, n, k: (20_000 + 1_200.0 * 2 * m * n * k * 1e-9) * (0.8 if m == 5000 else 1.0)]
     ctx, _ = vctx(cost, sched=cm.SCHED_PREDICT)
     orc = so.SelectorOracle(3, blocked=True)      # runtime default calibration order (R19)
 
@@ -292,6 +293,12 @@ def test_predict_scheduler_matches_oracle():
             step(s)
     modes = [step(s)[1] for s in (300, 3000, 1000, 7000, 300)]
     assert modes[:4] == [cm.MODE_PREDICT] * 4
+    # R37: at 5000 variant 0 (predicted best) measures 1.2x its prediction; variant 2, predicted
+    # slower but within 1.5x of that measurement, is explored (warm-up + timed run); it runs at 0.8x
+    # its prediction there and wins on its mean
+    trace = [step(5000) for _ in range(6)]
+    assert trace == [(0, cm.MODE_PREDICT), (0, cm.MODE_PREDICT), (2, cm.MODE_WARMUP), (2, cm.MODE_CALIB),
+                     (2, cm.MODE_MODEL), (2, cm.MODE_MODEL)]
     ctx.terminate()
 
 

@@ -161,6 +161,42 @@ def test_predict_calibrates_only_unknown_variants():
     assert sel.decide_predict(key, [0, 1, 2]) == (2, so.MODE_MODEL)   # its measured 1 us beats both predictions
 
 
+def test_predict_explores_close_predictions():
+    """R37 pin: when the best estimate of a key is a measured mean, a variant known only by its
+    prediction and predicted within explore_pct/100 of it is measured (one warm-up, one timed run)
+    before the measured variant is trusted; one predicted beyond that factor is never run."""
+    gf = lambda s: 2 * s ** 3 * 1e-9
+    fit = [lambda s: 10_000 + 1000.0 * gf(s), lambda s: 10_000 + 1100.0 * gf(s), lambda s: 10_000 + 2500.0 * gf(s)]
+
+    def trained(explore):
+        sel = so.SelectorOracle(3)
+        sel.explore_pct = explore
+        for s in (256, 512, 1024, 2048):
+            for _ in range(12):
+                v, mode = sel.decide(_key(s), [0, 1, 2])
+                warm = sel.commit(v, _key(s), mode)
+                sel.harvest(v, _key(s), mode, warm, round(fit[v](s)))
+        return sel
+
+    key = _key(3000)
+    actual = [round(fit[0](3000)), 40_000, round(fit[2](3000))]   # variant 1 beats its own prediction here
+    for explore, expect in ((150, [(1, so.MODE_WARMUP), (1, so.MODE_CALIB), (1, so.MODE_MODEL)]),
+                            (0, [(0, so.MODE_MODEL)] * 3)):
+        sel = trained(explore)
+        for _ in range(4):                                  # variant 0 measured at the key
+            v, mode = sel.decide(key, [0])
+            warm = sel.commit(v, key, mode)
+            sel.harvest(v, key, mode, warm, actual[v])
+        assert sel.predict(1, key) <= 1.5 * actual[0] < sel.predict(2, key)
+        trace = []
+        for _ in range(3):
+            v, mode = sel.decide_predict(key, [0, 1, 2])
+            trace.append((v, mode))
+            warm = sel.commit(v, key, mode)
+            sel.harvest(v, key, mode, warm, actual[v])
+        assert trace == expect
+
+
 @pytest.mark.parametrize("m,p,expect", [
     (32768, 8, [0, 4096, 8192, 12288, 16384, 20480, 24576, 28672, 32768]),
     (32768, 2, [0, 16384, 32768]),
