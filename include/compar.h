@@ -84,7 +84,8 @@ typedef enum {
     COMPAR_TGT_TCS_BF16 = 11,   /* built-in (c), split-K CTA-pair form, BF16                              */
     COMPAR_TGT_TCK_TF32 = 12,   /* built-in (c), cluster split-K form: the 2 CTAs of a cluster split one  */
                                 /*   1-SM tile's K (at ceil(kb/2), a function of K only) and reduce   */
-                                /*   through distributed shared memory; single-wave shapes            */
+                                /*   through distributed shared memory; single-wave shapes only       */
+                                /*   (ceil(m/128) * ceil(n/256) <= SMs, K > one k-block)              */
     COMPAR_TGT_TCK_BF16 = 13,   /* built-in (c), cluster split-K form, BF16                               */
     /* the "sort" interface */
     COMPAR_TGT_SORT_RADIX = 20,   /* built-in: onesweep LSD radix sort, 4 x 8-bit passes, any n      */

@@ -108,13 +108,16 @@ cudaError_t launch_tc_gemm_splitk(const GemmLaunch &g, bool bf16);
 
 // tc_*_ck (variant c, cluster split-K, tc_gemm_ck.cu): the two CTAs of a cluster split a tile's
 // ceil(K / BK) k-blocks at h = ceil(kb / 2) — a function of K alone (row panels stay bitwise equal).
-// Eligible from 2 k-blocks on.
+// Eligible from 2 k-blocks on, and only where the 128 x 256 tiles of the (panel) shape fit one wave
+// of clusters (tiles <= SMs): a single-wave form, not calibrated on multi-wave shapes it cannot win.
 inline int tc_clusterk_half(int64_t k, bool bf16) {
     const int64_t bk = bf16 ? 64 : 32;
     const int64_t kb = (k + bk - 1) / bk;
     return static_cast<int>((kb + 1) / 2);
 }
-inline bool tc_clusterk_ok(int64_t k, bool bf16) { return k > (bf16 ? 64 : 32); }
+inline bool tc_clusterk_ok(int64_t m, int64_t n, int64_t k, bool bf16, int sms) {
+    return k > (bf16 ? 64 : 32) && ((m + 127) / 128) * ((n + 255) / 256) <= sms;
+}
 cudaError_t launch_tc_gemm_ck(const GemmLaunch &g, bool bf16);
 
 // TMA eligibility (the selector's constraint filter).

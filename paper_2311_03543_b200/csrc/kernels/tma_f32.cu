@@ -132,17 +132,20 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + TY * i, k4));
             if (kTransB) {
+                // column j's 4 k values as one float4; columns paired for FFMA2 (each element's
+                // k order unchanged: x, y, z, w)
+                float4 b[MJ];
 #pragma unroll
-                for (int j = 0; j < MJ; ++j) {
-                    const float4 b = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + TX * j, k4));
+                for (int j = 0; j < MJ; ++j) b[j] = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + TX * j, k4));
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
-                        acc[i][j] = fmaf(a[i].y, b.y, acc[i][j]);
-                        acc[i][j] = fmaf(a[i].z, b.z, acc[i][j]);
-                        acc[i][j] = fmaf(a[i].w, b.w, acc[i][j]);
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < MJ; j += 2) {
+                        ffma2(acc[i][j], acc[i][j + 1], a[i].x, b[j].x, b[j + 1].x);
+                        ffma2(acc[i][j], acc[i][j + 1], a[i].y, b[j].y, b[j + 1].y);
+                        ffma2(acc[i][j], acc[i][j + 1], a[i].z, b[j].z, b[j + 1].z);
+                        ffma2(acc[i][j], acc[i][j + 1], a[i].w, b[j].w, b[j + 1].w);
                     }
-                }
             } else {
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {

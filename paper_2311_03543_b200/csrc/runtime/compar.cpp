@@ -346,7 +346,7 @@ bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, co
     if ((t == COMPAR_TGT_TCS_TF32 || t == COMPAR_TGT_TCS_BF16) &&
         tc_splitk_splits(mrows, d->n, d->k, t == COMPAR_TGT_TCS_BF16) < 2)
         return false;
-    if ((t == COMPAR_TGT_TCK_TF32 || t == COMPAR_TGT_TCK_BF16) && !tc_clusterk_ok(d->k, t == COMPAR_TGT_TCK_BF16))
+    if ((t == COMPAR_TGT_TCK_TF32 || t == COMPAR_TGT_TCK_BF16) && !tc_clusterk_ok(mrows, d->n, d->k, t == COMPAR_TGT_TCK_BF16, c->num_sms))
         return false;
     if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;
     if ((d->lda * eb) % 16 != 0 || (d->ldb * eb) % 16 != 0) return false;

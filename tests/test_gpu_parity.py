@@ -421,3 +421,20 @@ def test_host_mode_tasks_on_two_streams_do_not_share_staging_early(ctx):
         assert ctx.sync(t).status == 0
     for (Ah, Bh, Ch), (rows, ref) in zip(outs, refs):
         np.testing.assert_array_equal(Ch.numpy()[rows].astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("m,n,k,ok", [(2048, 2048, 2048, True), (1024, 1024, 1024, True), (2048, 1536, 4160, True),
+                                      (128 * 148, 256, 512, True), (128 * 149, 256, 512, False),
+                                      (8192, 8192, 8192, False), (32768, 32768, 32768, False),
+                                      (1024, 1024, 64, False)])
+def test_cluster_splitk_single_wave_eligibility(ctx, m, n, k, ok):
+    """tc_*_ck is a single-wave form: eligible iff K spans >= 2 k-blocks (BF16: > 64) and the 128 x 256
+    tiles fit one wave of clusters (ceil(m/128) * ceil(n/256) <= SMs); selection only, no launch."""
+    buf = torch.empty(64, device="cuda", dtype=torch.float32)
+    d = cm.make_desc(m, n, k, A=buf, B=buf, C_in=buf, C_out=buf, lda=k, ldb=n, ldc_in=n, ldc_out=n, alpha=1.0,
+                     beta=0.5, in_dtype=cm.BF16, compute=cm.COMPUTE_BF16,
+                     stream=torch.cuda.current_stream().cuda_stream)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    if m == 128 * 149 and sms > 148:
+        pytest.skip("boundary case written for 148 SMs")
+    assert (vid(ctx, "tc_bf16_ck") in ctx.eligible(d)) == ok

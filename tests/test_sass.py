@@ -5,7 +5,7 @@ defining instructions (B200_PROFILING.md SASS mnemonics):
   * tcgen05 kernels: UTCHMMA (tcgen05.mma; .2CTA for the CTA-pair forms), UTMALDG (TMA loads),
     LDTM (tcgen05.ld from TMEM); the TMA-epilogue pair / wide kernels also UTMASTG (TMA stores);
     the wide kernel's row-major instantiations the 3-D slab-packed B loads (UTMALDG.3D.2CTA);
-  * FFMA variants: FFMA2 (sm_100 paired FMA; simt_f32 every instantiation, tma_f32 row-major B).
+  * FFMA variants: FFMA2 (sm_100 paired FMA; every simt_f32 and tma_f32 instantiation).
 """
 import os
 import re
@@ -66,7 +66,5 @@ def test_tcgen05_pair_kernels(kernels):
 def test_ffma_kernels_use_ffma2(kernels):
     for n, ops in family(kernels, "simt_f32_kernel<").items():
         assert "FFMA2" in ops, n
-    for n, ops in family(kernels, "tma_f32_kernel<false").items():
+    for n, ops in family(kernels, "tma_f32_kernel<").items():
         assert "FFMA2" in ops and has(ops, "UTMALDG"), n
-    for n, ops in family(kernels, "tma_f32_kernel<true").items():
-        assert has(ops, "UTMALDG"), n
