@@ -52,7 +52,13 @@ struct TmaCfg {
     static constexpr int kConsumers = TX * TY;
     static constexpr int kThreads = kConsumers + 32;
     static constexpr uint32_t A_BYTES = TB * BK * 4, B_BYTES = BK * TB * 4, STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 128;
+    // transB: transposed B stage [BK][TB]; double-buffered for TB = 128 (one CTA per SM), single for
+    // TB = 64 so three CTAs still fit an SM
+    static constexpr uint32_t T_BYTES = BK * TB * 4;
+    static constexpr int kTBufs = TB == 128 ? 2 : 1;
+    static constexpr uint32_t smem(bool transB) {
+        return STAGES * STAGE_BYTES + (transB ? kTBufs * T_BYTES : 0) + 1024 + 128;
+    }
     static constexpr int kMinBlocks = TB == 128 ? 1 : 3;
 };
 
@@ -77,8 +83,11 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     constexpr int BM = TB, BN = TB, TY = Cf::TY, TX = Cf::TX, MJ = Cf::MJ, MJ4 = Cf::MJ4, kConsumers = Cf::kConsumers;
     constexpr uint32_t A_BYTES = Cf::A_BYTES, STAGE_BYTES = Cf::STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    // 1024-byte aligned base as an offset into smem_raw (not a uintptr_t round trip), so the compiler
+    // keeps the shared address space and the micro-tile reads are LDS, not generic loads
+    uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t *tbuf = smem + STAGES * STAGE_BYTES;              // transB: kTBufs x [BK][BN] FP32
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tbuf + (kTransB ? Cf::kTBufs * Cf::T_BYTES : 0));
     const uint32_t full0 = ptx::smem_u32(bars), empty0 = full0 + 8 * STAGES;
     const uint32_t smem0 = ptx::smem_u32(smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -126,42 +135,46 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
         ptx::mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
         const uint8_t *sa = smem + s * STAGE_BYTES;
         const uint8_t *sb = sa + A_BYTES;
+        if (kTransB) {
+            // B^T arrives as [BN rows of n][32 k] (128-byte swizzle); the consumers transpose it into
+            // tbuf[kb % kTBufs] = [32 k][BN] so the inner loop below is the row-major one (B columns
+            // paired in adjacent registers for FFMA2, each element's k order unchanged).  Double
+            // buffering needs one consumer barrier per stage: a warp rewriting buffer (kb+1)&1 has
+            // passed barrier kb, which every warp reaches only after its compute on kb-1; a single
+            // buffer also needs one before it is rewritten.
+            if (Cf::kTBufs == 1 && kb > 0) asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
+            float *t = reinterpret_cast<float *>(tbuf + (kb % Cf::kTBufs) * Cf::T_BYTES);
+#pragma unroll
+            for (int q = 0; q < BN * (BK / 4) / kConsumers; ++q) {
+                const int idx = tid + q * kConsumers, r = idx % BN, c = idx / BN;
+                const float4 v = *reinterpret_cast<const float4 *>(sb + sw128_off(r, c));
+                t[(4 * c + 0) * BN + r] = v.x;
+                t[(4 * c + 1) * BN + r] = v.y;
+                t[(4 * c + 2) * BN + r] = v.z;
+                t[(4 * c + 3) * BN + r] = v.w;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
+            sb = reinterpret_cast<const uint8_t *>(t);
+        }
 #pragma unroll 2
         for (int k4 = 0; k4 < BK / 4; ++k4) {
             float4 a[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + TY * i, k4));
-            if (kTransB) {
-                // column j's 4 k values as one float4; columns paired for FFMA2 (each element's
-                // k order unchanged: x, y, z, w)
-                float4 b[MJ];
 #pragma unroll
-                for (int j = 0; j < MJ; ++j) b[j] = *reinterpret_cast<const float4 *>(sb + sw128_off(tx + TX * j, k4));
+            for (int kk = 0; kk < 4; ++kk) {
+                const float *brow = reinterpret_cast<const float *>(sb + (k4 * 4 + kk) * (BN * 4));
+                float b[MJ];
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int h = 0; h < MJ4; ++h) {
+                    const float4 bh = *reinterpret_cast<const float4 *>(brow + h * (BN / MJ4) + tx * 4);
+                    b[4 * h + 0] = bh.x, b[4 * h + 1] = bh.y, b[4 * h + 2] = bh.z, b[4 * h + 3] = bh.w;
+                }
 #pragma unroll
-                    for (int j = 0; j < MJ; j += 2) {
-                        ffma2(acc[i][j], acc[i][j + 1], a[i].x, b[j].x, b[j + 1].x);
-                        ffma2(acc[i][j], acc[i][j + 1], a[i].y, b[j].y, b[j + 1].y);
-                        ffma2(acc[i][j], acc[i][j + 1], a[i].z, b[j].z, b[j + 1].z);
-                        ffma2(acc[i][j], acc[i][j + 1], a[i].w, b[j].w, b[j + 1].w);
-                    }
-            } else {
+                for (int i = 0; i < 8; ++i) {
+                    const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const float *brow = reinterpret_cast<const float *>(sb + (k4 * 4 + kk) * (BN * 4));
-                    float b[MJ];
-#pragma unroll
-                    for (int h = 0; h < MJ4; ++h) {
-                        const float4 bh = *reinterpret_cast<const float4 *>(brow + h * (BN / MJ4) + tx * 4);
-                        b[4 * h + 0] = bh.x, b[4 * h + 1] = bh.y, b[4 * h + 2] = bh.z, b[4 * h + 3] = bh.w;
-                    }
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
-#pragma unroll
-                        for (int j = 0; j < MJ; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
-                    }
+                    for (int j = 0; j < MJ; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
                 }
             }
         }
@@ -180,23 +193,15 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
         for (int i = 0; i < 8; ++i) {
             const int64_t r = m0 + ty + TY * i;
             const float *cin = p.C_in + r * p.ldc_in;
-            if (kTransB) {
 #pragma unroll
-                for (int j = 0; j < MJ; ++j) {
-                    const int64_t c = n0 + tx + TX * j;
-                    ci[i][j] = r < p.m && c < p.n ? cin[c] : 0.f;
-                }
-            } else {
+            for (int h = 0; h < MJ4; ++h) {
+                const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
+                if (r < p.m && p.cvec && c + 3 < p.n) {
+                    const float4 v = *reinterpret_cast<const float4 *>(cin + c);
+                    ci[i][h * 4 + 0] = v.x, ci[i][h * 4 + 1] = v.y, ci[i][h * 4 + 2] = v.z, ci[i][h * 4 + 3] = v.w;
+                } else {
 #pragma unroll
-                for (int h = 0; h < MJ4; ++h) {
-                    const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
-                    if (r < p.m && p.cvec && c + 3 < p.n) {
-                        const float4 v = *reinterpret_cast<const float4 *>(cin + c);
-                        ci[i][h * 4 + 0] = v.x, ci[i][h * 4 + 1] = v.y, ci[i][h * 4 + 2] = v.z, ci[i][h * 4 + 3] = v.w;
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) ci[i][h * 4 + j] = r < p.m && c + j < p.n ? cin[c + j] : 0.f;
-                    }
+                    for (int j = 0; j < 4; ++j) ci[i][h * 4 + j] = r < p.m && c + j < p.n ? cin[c + j] : 0.f;
                 }
             }
         }
@@ -206,33 +211,21 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
         const int64_t r = m0 + ty + TY * i;
         if (r >= p.m) continue;
         float *crow = p.C_out + r * p.ldc_out;
-        if (kTransB) {
 #pragma unroll
-            for (int j = 0; j < MJ; ++j) {
-                const int64_t c = n0 + tx + TX * j;
-                if (c < p.n) {
-                    float o = p.alpha * acc[i][j];
-                    if (has_cin) o = fmaf(p.beta, ci[i][j], o);
-                    crow[c] = o;
-                }
+        for (int h = 0; h < MJ4; ++h) {
+            const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                o[j] = p.alpha * acc[i][h * 4 + j];
+                if (has_cin) o[j] = fmaf(p.beta, ci[i][h * 4 + j], o[j]);
             }
-        } else {
+            if (p.cvec && c + 3 < p.n) {
+                *reinterpret_cast<float4 *>(crow + c) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
 #pragma unroll
-            for (int h = 0; h < MJ4; ++h) {
-                const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
-                float o[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    o[j] = p.alpha * acc[i][h * 4 + j];
-                    if (has_cin) o[j] = fmaf(p.beta, ci[i][h * 4 + j], o[j]);
-                }
-                if (p.cvec && c + 3 < p.n) {
-                    *reinterpret_cast<float4 *>(crow + c) = make_float4(o[0], o[1], o[2], o[3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (c + j < p.n) crow[c + j] = o[j];
-                }
+                for (int j = 0; j < 4; ++j)
+                    if (c + j < p.n) crow[c + j] = o[j];
             }
         }
     }
@@ -244,7 +237,7 @@ cudaError_t launch_t(const GemmLaunch &g) {
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [] {
-        attr = cudaFuncSetAttribute(tma_f32_kernel<kTransB, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+        attr = cudaFuncSetAttribute(tma_f32_kernel<kTransB, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::smem(kTransB));
     });
     if (attr != cudaSuccess) return attr;
     CUtensorMap ta, tb;
@@ -259,7 +252,7 @@ cudaError_t launch_t(const GemmLaunch &g) {
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     dim3 grid(static_cast<unsigned>((g.n + TB - 1) / TB), static_cast<unsigned>((g.m + TB - 1) / TB));
-    tma_f32_kernel<kTransB, TB><<<grid, Cf::kThreads, Cf::SMEM, g.stream>>>(ta, tb, p);
+    tma_f32_kernel<kTransB, TB><<<grid, Cf::kThreads, Cf::smem(kTransB), g.stream>>>(ta, tb, p);
     return cudaGetLastError();
 }
 
