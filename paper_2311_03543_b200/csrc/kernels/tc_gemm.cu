@@ -39,22 +39,35 @@ struct TcCfg {
     static constexpr int BM = 128, BN = kBN;       // 256, or 128 / 64 for grids that leave SMs idle
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;   // two accumulators
     static constexpr int ELEM = kBF16 ? 2 : 4;
-    static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K
+    static constexpr int BK = 128 / ELEM;          // one 128-byte swizzle row of K (a "k-atom")
     static constexpr int UMMA_K = 32 / ELEM;       // K per tcgen05.mma (16 bf16 / 8 tf32)
-    static constexpr int STAGES = 4;   // (as many as fit 192 KiB measured the same: DESIGN.md §5)
-    static constexpr uint32_t A_BYTES = BM * 128;
-    static constexpr uint32_t B_BYTES = BN * 128;
+    // k-atoms per ring stage.  The MMA thread's wait on a stage's full barrier returns only after
+    // the tcgen05.mma it issued before have drained (~290 cycles + 52 per queued M = 128 MMA,
+    // tools/mma_rate.cu), so with N <= 128 (an MMA every 48-64 cycles) four MMAs per wait leave the
+    // tensor pipe idle half the time; two k-atoms per stage (eight MMAs per wait) halve that.
+    // N = 256 MMAs (128 cycles each) already cover the wait.
+    static constexpr int KA = BN <= 128 ? 2 : 1;
+    static constexpr int BKS = KA * BK;            // K per stage
+    static constexpr int STAGES = BN == 128 ? 3 : 4;   // <= 192 KiB of ring
+    static constexpr uint32_t A_ATOM_BYTES = BM * 128;
+    static constexpr uint32_t A_BYTES = KA * A_ATOM_BYTES;
+    static constexpr uint32_t B_ATOM_BYTES = BN * 128;   // one k-atom of B (either layout)
+    static constexpr uint32_t B_BYTES = KA * B_ATOM_BYTES;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int B_ATOM_N = 128 / ELEM;    // N elements per 128-byte MN atom
     static constexpr int B_BOXES = kTransB ? 1 : BN / B_ATOM_N;
-    static constexpr uint32_t B_BOX_BYTES = kTransB ? B_BYTES : BK * 128;
+    // K-major B: one BN x 128 B box per k-atom; MN-major B: BN / B_ATOM_N boxes of BKS k-rows x 128 B
+    static constexpr uint32_t B_BOX_BYTES = kTransB ? B_ATOM_BYTES : BKS * 128;
     // MN-major B: BF16 uses the canonical SWIZZLE_128B atom (8 K-rows x 128 B, SBO 1024);
     // 32-bit TF32 requires the 32-byte-granule SWIZZLE_128B_BASE32B atom (4 K-rows x 128 B,
     // descriptor layout type 1, SBO 512) loaded by TMA with SWIZZLE_128B_ATOM_32B.
     static constexpr bool B_BASE32 = !kBF16 && !kTransB;
     static constexpr uint32_t B_SBO = B_BASE32 ? 512 : 1024;
     static constexpr uint32_t B_LAYOUT = B_BASE32 ? 1 : 2;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 512;
+    // epilogue staging: per epilogue warp one 32 x 32 FP32 chunk, rows padded to 36 words
+    static constexpr uint32_t EPI_LD = 36;
+    static constexpr uint32_t EPI_BYTES = 4 * 32 * EPI_LD * 4;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 512 + EPI_BYTES + 1024;
     // Instruction descriptor: D=F32 [4,6), A/B format [7,10)/[10,13) (1 BF16, 2 TF32),
     // a_major=K [15], b_major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
@@ -111,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
     using C = TcCfg<kBF16, kTransB, kBN>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);   // shared-space 1 KiB base
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
     const uint32_t full0 = ptx::smem_u32(bars);
     const uint32_t empty0 = full0 + 8 * C::STAGES;
@@ -135,13 +148,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sb = sa + C::A_BYTES;
         const uint32_t fb = full0 + 8 * stage;
         ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
-        ptx::tma_load_2d(sa, &tmA, fb, kb * C::BK, mb * C::BM);
+#pragma unroll
+        for (int a = 0; a < C::KA; ++a)
+            ptx::tma_load_2d(sa + a * C::A_ATOM_BYTES, &tmA, fb, kb * C::BKS + a * C::BK, mb * C::BM);
         if (kTransB) {
-            ptx::tma_load_2d(sb, &tmB, fb, kb * C::BK, nb * C::BN);
+#pragma unroll
+            for (int a = 0; a < C::KA; ++a)
+                ptx::tma_load_2d(sb + a * C::B_ATOM_BYTES, &tmB, fb, kb * C::BKS + a * C::BK, nb * C::BN);
         } else {
 #pragma unroll
             for (int b = 0; b < C::B_BOXES; ++b)
-                ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N, kb * C::BK);
+                ptx::tma_load_2d(sb + b * C::B_BOX_BYTES, &tmB, fb, nb * C::BN + b * C::B_ATOM_N, kb * C::BKS);
         }
     };
     int early = 0;   // k-blocks of the first tile issued before the block-wide barrier
@@ -249,9 +266,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t so = stage * C::STAGE_BYTES;
                     const uint64_t as = ptx::desc_adv(adesc0, so), bs = ptx::desc_adv(bdesc0, so);
 #pragma unroll
-                    for (int j = 0; j < C::BK / C::UMMA_K; ++j) {
-                        const uint64_t adesc = ptx::desc_adv(as, j * 32);
-                        const uint64_t bdesc = ptx::desc_adv(bs, kTransB ? j * 32 : j * C::UMMA_K * 128);
+                    for (int j = 0; j < C::BKS / C::UMMA_K; ++j) {
+                        constexpr int J = C::BK / C::UMMA_K;   // MMAs per k-atom
+                        const uint64_t adesc = ptx::desc_adv(as, (j / J) * C::A_ATOM_BYTES + (j % J) * 32);
+                        const uint64_t bdesc = ptx::desc_adv(bs, kTransB ? (j / J) * C::B_ATOM_BYTES + (j % J) * 32
+                                                                         : j * C::UMMA_K * 128);
                         if (kBF16)
                             ptx::mma_bf16(d_tmem, adesc, bdesc, C::IDESC, (kb | j) != 0);
                         else
@@ -277,64 +296,79 @@ __global__ void __launch_bounds__(kThreads, 1)
             tile_coords(t, p.m_blocks, p.n_blocks, p.group_m, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
-            const int64_t row = static_cast<int64_t>(mb) * C::BM + q * 32 + lane;
-            const bool row_ok = row < p.m;
-            float *crow = p.C_out + row * p.ldc_out;
-            const float *cin = p.C_in + row * p.ldc_in;
+            // Each 32 x 32 chunk goes TMEM -> registers (thread = row) -> padded shared staging ->
+            // registers (lanes 8j..8j+7 = one row's 128 bytes) -> coalesced float4 C_in loads and
+            // C_out stores (4 full rows per instruction instead of 32 partial ones).  C_in chunks
+            // are fetched two ahead, chunks 0 and 1 before the accumulator is ready.
+            const int64_t row_base = static_cast<int64_t>(mb) * C::BM + q * 32;
             const int64_t colb = static_cast<int64_t>(nb) * C::BN;
-            // C_in one 32-column chunk ahead in registers: chunk 0 is loaded before the accumulator
-            // is ready, so its latency hides under the mainloop (small grids are otherwise bound by
-            // the serial C_in round trips of the epilogue)
-            const bool pre = p.beta != 0.f && p.cvec && row_ok;
-            auto vec_chunk = [&](int c) { return pre && colb + c * 32 + 32 <= p.n; };
-            float4 cur[8], nxt[8];
-            if (vec_chunk(0)) {
+            const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;   // coalesced layout
+            const bool beta_on = p.beta != 0.f;
+            auto fast_chunk = [&](int c) { return p.cvec && colb + c * 32 + 32 <= p.n; };
+            auto load_cin = [&](int c, float4 (&dst)[8]) {
+                if (!beta_on || !fast_chunk(c)) return;
 #pragma unroll
-                for (int v = 0; v < 8; ++v) cur[v] = *reinterpret_cast<const float4 *>(cin + colb + 4 * v);
-            }
+                for (int i = 0; i < 8; ++i) {
+                    const int64_t r = row_base + i * 4 + sub_r;
+                    if (r < p.m)
+                        dst[i] = *reinterpret_cast<const float4 *>(p.C_in + r * p.ldc_in + colb + c * 32 + sub_c);
+                }
+            };
+            float4 cin0[8], cin1[8];
+            load_cin(0, cin0);
+            if (C::BN / 32 > 1) load_cin(1, cin1);
+            float *stage_f = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + 512) + q * 32 * C::EPI_LD;
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             if (local == 0 && warp == 2 && lane == 0) TRACE1(5);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < C::BN / 32; ++c) {
                 const int64_t col0 = colb + c * 32;
-                if (c + 1 < C::BN / 32 && vec_chunk(c + 1)) {
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) nxt[v] = *reinterpret_cast<const float4 *>(cin + col0 + 32 + 4 * v);
-                }
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN + c * 32, r);
                 ptx::tmem_ld_wait();
-                if (row_ok && col0 < p.n) {
-                    if (p.cvec && col0 + 32 <= p.n) {
+                if (fast_chunk(c)) {
+                    float *mine = stage_f + lane * C::EPI_LD;
 #pragma unroll
-                        for (int v = 0; v < 8; ++v) {
-                            float4 o;
-                            o.x = p.alpha * __uint_as_float(r[4 * v + 0]);
-                            o.y = p.alpha * __uint_as_float(r[4 * v + 1]);
-                            o.z = p.alpha * __uint_as_float(r[4 * v + 2]);
-                            o.w = p.alpha * __uint_as_float(r[4 * v + 3]);
-                            if (pre) {
-                                o.x = fmaf(p.beta, cur[v].x, o.x);
-                                o.y = fmaf(p.beta, cur[v].y, o.y);
-                                o.z = fmaf(p.beta, cur[v].z, o.z);
-                                o.w = fmaf(p.beta, cur[v].w, o.w);
-                            }
-                            *reinterpret_cast<float4 *>(crow + col0 + 4 * v) = o;
+                    for (int v = 0; v < 8; ++v)
+                        *reinterpret_cast<float4 *>(mine + 4 * v) =
+                            make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                        __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int64_t rr = row_base + i * 4 + sub_r;
+                        const float4 a = *reinterpret_cast<const float4 *>(stage_f + (i * 4 + sub_r) * C::EPI_LD + sub_c);
+                        float4 o;
+                        o.x = p.alpha * a.x, o.y = p.alpha * a.y, o.z = p.alpha * a.z, o.w = p.alpha * a.w;
+                        if (beta_on) {
+                            const float4 ci = cin0[i];
+                            o.x = fmaf(p.beta, ci.x, o.x);
+                            o.y = fmaf(p.beta, ci.y, o.y);
+                            o.z = fmaf(p.beta, ci.z, o.z);
+                            o.w = fmaf(p.beta, ci.w, o.w);
                         }
-                    } else {
+                        if (rr < p.m) *reinterpret_cast<float4 *>(p.C_out + rr * p.ldc_out + col0 + sub_c) = o;
+                    }
+                    __syncwarp();   // staging reused by the next chunk
+                } else {
+                    const int64_t row = row_base + lane;
+                    if (row < p.m && col0 < p.n) {
+                        float *crow = p.C_out + row * p.ldc_out;
+                        const float *cin = p.C_in + row * p.ldc_in;
 #pragma unroll
                         for (int e = 0; e < 32; ++e) {
                             if (col0 + e < p.n) {
                                 float o = p.alpha * __uint_as_float(r[e]);
-                                if (p.beta != 0.f) o = fmaf(p.beta, cin[col0 + e], o);
+                                if (beta_on) o = fmaf(p.beta, cin[col0 + e], o);
                                 crow[col0 + e] = o;
                             }
                         }
                     }
                 }
 #pragma unroll
-                for (int v = 0; v < 8; ++v) cur[v] = nxt[v];
+                for (int i = 0; i < 8; ++i) cin0[i] = cin1[i];
+                if (c + 2 < C::BN / 32) load_cin(c + 2, cin1);
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -364,7 +398,7 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
     CUtensorMap ta, tb;
     if (!get_tmap_2d(&ta, g.A, C::ELEM, g.m, g.k, g.lda, C::BM, C::BK, Swz::B128)) return cudaErrorInvalidValue;
     bool ok = kTransB ? get_tmap_2d(&tb, g.B, C::ELEM, g.n, g.k, g.ldb, C::BN, C::BK, Swz::B128)
-                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BK, C::B_ATOM_N,
+                      : get_tmap_2d(&tb, g.B, C::ELEM, g.k, g.n, g.ldb, C::BKS, C::B_ATOM_N,
                                     C::B_BASE32 ? Swz::B128_32B : Swz::B128);
     if (!ok) return cudaErrorInvalidValue;
     TcParams p;
@@ -373,7 +407,7 @@ cudaError_t launch_tc_t(const GemmLaunch &g) {
     p.C_in = g.C_in, p.ldc_in = g.ldc_in, p.C_out = g.C_out, p.ldc_out = g.ldc_out;
     p.m_blocks = static_cast<int>((g.m + C::BM - 1) / C::BM);
     p.n_blocks = static_cast<int>((g.n + C::BN - 1) / C::BN);
-    p.num_kb = static_cast<int>((g.k + C::BK - 1) / C::BK);
+    p.num_kb = static_cast<int>((g.k + C::BKS - 1) / C::BKS);   // ring stages (KA k-atoms each)
     p.cvec = ((g.ldc_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_out) & 15) == 0) &&
              (g.beta == 0.f || (((g.ldc_in & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.C_in) & 15) == 0)));
     p.sched = sched_workspace(g.stream);
