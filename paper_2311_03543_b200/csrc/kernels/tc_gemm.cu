@@ -44,11 +44,20 @@ struct TcCfg {
     // k-atoms per ring stage.  The MMA thread's wait on a stage's full barrier returns only after
     // the tcgen05.mma it issued before have drained (~290 cycles + 52 per queued M = 128 MMA,
     // tools/mma_rate.cu), so with N <= 128 (an MMA every 48-64 cycles) four MMAs per wait leave the
-    // tensor pipe idle half the time; two k-atoms per stage (eight MMAs per wait) halve that.
-    // N = 256 MMAs (128 cycles each) already cover the wait.
-    static constexpr int KA = BN <= 128 ? 2 : 1;
+    // tensor pipe idle half the time.  Measured (tools/trace_pair.py run1): N = 64
+    // takes four k-atoms x 2 stages (16 MMAs per wait; 1024^2 x 4096: 17.2 -> 13.8 us vs 2 x 4),
+    // N = 128 two x 3 (3 x 2 was slower); N = 256 MMAs (128 cycles each) already cover the wait.
+#ifndef COMPAR_KA64          // (experiment knobs: k-atoms / stages of the N = 64 / 128 forms)
+#define COMPAR_KA64 4
+#define COMPAR_ST64 2
+#endif
+#ifndef COMPAR_KA128
+#define COMPAR_KA128 2
+#define COMPAR_ST128 3
+#endif
+    static constexpr int KA = BN == 64 ? COMPAR_KA64 : BN == 128 ? COMPAR_KA128 : 1;
     static constexpr int BKS = KA * BK;            // K per stage
-    static constexpr int STAGES = BN == 128 ? 3 : 4;   // <= 192 KiB of ring
+    static constexpr int STAGES = BN == 64 ? COMPAR_ST64 : BN == 128 ? COMPAR_ST128 : 4;   // <= 192 KiB of ring
     static constexpr uint32_t A_ATOM_BYTES = BM * 128;
     static constexpr uint32_t A_BYTES = KA * A_ATOM_BYTES;
     static constexpr uint32_t B_ATOM_BYTES = BN * 128;   // one k-atom of B (either layout)
@@ -92,6 +101,15 @@ struct TcParams {
 // Development-only phase stamps (tools/trace_pair.py builds a separate library with -DCOMPAR_TRACE):
 // clock64 at fixed points of CTA 0, globaltimer at entry / exit.
 __device__ unsigned long long g_trace1[16];
+__device__ unsigned long long g_trace1_cta[2 * 160];   // globaltimer at entry / exit of CTAs 0..159
+#define TRACE1_CTA(i)                                                                         \
+    do {                                                                                      \
+        if (blockIdx.x < 160) {                                                               \
+            unsigned long long t;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                           \
+            g_trace1_cta[2 * blockIdx.x + (i)] = t;                                           \
+        }                                                                                     \
+    } while (0)
 #define TRACE1(i)                                                                             \
     do {                                                                                      \
         if (blockIdx.x == 0) g_trace1[i] = clock64();                                        \
@@ -107,6 +125,7 @@ __device__ unsigned long long g_trace1[16];
 #else
 #define TRACE1(i) ((void)0)
 #define TRACE1_GT(i) ((void)0)
+#define TRACE1_CTA(i) ((void)0)
 #endif
 
 __device__ __forceinline__ void tile_coords(int t, int m_blocks, int n_blocks, int group, int &mb, int &nb) {
@@ -140,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         TRACE1_GT(10);
         TRACE1(0);
+        TRACE1_CTA(0);
     }
     const int num_tiles = p.m_blocks * p.n_blocks;
     // One k-block of tile (mb, nb) into ring stage `stage` (producer thread only).
@@ -380,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         TRACE1(8);
         TRACE1_GT(11);
+        TRACE1_CTA(1);
     }
     if (warp == 1) ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
@@ -453,6 +474,9 @@ cudaError_t launch_tc_gemm(const GemmLaunch &g, bool bf16) {
 int trace1_read(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_trace1, sizeof(g_trace1)) == cudaSuccess ? 0 : -1;
 }
+int trace1_cta_read(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_trace1_cta, sizeof(g_trace1_cta)) == cudaSuccess ? 0 : -1;
+}
 #endif
 
 cudaError_t preload_tc_kernels() {
@@ -480,4 +504,5 @@ cudaError_t preload_tc_kernels() {
 
 #ifdef COMPAR_TRACE
 extern "C" int compar_trace1_read(unsigned long long *out) { return compar::trace1_read(out); }
+extern "C" int compar_trace1_cta_read(unsigned long long *out) { return compar::trace1_cta_read(out); }
 #endif

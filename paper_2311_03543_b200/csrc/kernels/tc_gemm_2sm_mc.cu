@@ -92,6 +92,15 @@ struct TcMParams {
 // Development-only phase stamps (tools/trace_pair.py builds a separate library with -DCOMPAR_TRACE):
 // clock64 at fixed points of CTAs 0 and 1, globaltimer at entry / exit.
 __device__ unsigned long long g_trace[2][16];
+__device__ unsigned long long g_trace_cta[2 * 160];   // globaltimer at entry / exit of CTAs 0..159
+#define TRACE_CTA(i)                                                                          \
+    do {                                                                                      \
+        if (blockIdx.x < 160) {                                                               \
+            unsigned long long t;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                           \
+            g_trace_cta[2 * blockIdx.x + (i)] = t;                                            \
+        }                                                                                     \
+    } while (0)
 #define TRACE(i)                                                                              \
     do {                                                                                      \
         if (blockIdx.x < 2) g_trace[blockIdx.x][i] = clock64();                               \
@@ -107,6 +116,7 @@ __device__ unsigned long long g_trace[2][16];
 #else
 #define TRACE(i) ((void)0)
 #define TRACE_GT(i) ((void)0)
+#define TRACE_CTA(i) ((void)0)
 #endif
 
 enum { kFull = 0, kSplit = 1 };
@@ -150,6 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
     if (threadIdx.x == 0) {
         TRACE_GT(10);
         TRACE(0);
+        TRACE_CTA(0);
     }
     const uint32_t rank = ptx::cluster_ctarank();   // 0 (MMA leader) or 1
     const bool leader = rank == 0;
@@ -460,6 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
     if (threadIdx.x == 0) {
         TRACE(8);
         TRACE_GT(11);
+        TRACE_CTA(1);
     }
     if (warp == 1) {
         ptx::tc_fence_after();
@@ -470,6 +482,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
 #ifdef COMPAR_TRACE
 int trace_read(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : -1;
+}
+int trace_cta_read(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_trace_cta, sizeof(g_trace_cta)) == cudaSuccess ? 0 : -1;
 }
 #endif
 
@@ -630,4 +645,5 @@ cudaError_t preload_tcm_kernels() {
 
 #ifdef COMPAR_TRACE
 extern "C" int compar_trace_read(unsigned long long *out) { return compar::trace_read(out); }
+extern "C" int compar_trace_cta_read(unsigned long long *out) { return compar::trace_cta_read(out); }
 #endif

@@ -152,13 +152,14 @@ def main(out_path):
     # crossovers: smallest size from which variant X's median beats Y's (within the 1.5x grid)
     cross = {}
     for mode, rows in c2.items():
-        vs = rows[0]["eligible"]
+        vs = sorted({v for r in rows for v in r["eligible"]})
         for x in vs:
             for y in vs:
                 if x == y:
                     continue
-                wins = [r["shape"][0] for r in rows if r["median_ns"][x] < r["median_ns"][y]]
-                loses = [r["shape"][0] for r in rows if r["median_ns"][x] >= r["median_ns"][y]]
+                both = [r for r in rows if x in r["median_ns"] and y in r["median_ns"]]   # (tc_*_ck: single-wave shapes only)
+                wins = [r["shape"][0] for r in both if r["median_ns"][x] < r["median_ns"][y]]
+                loses = [r["shape"][0] for r in both if r["median_ns"][x] >= r["median_ns"][y]]
                 if wins and loses and min(wins) > min(loses):
                     cross[f"{mode}: {x} beats {y} from"] = min(wins)
     c2["crossovers"] = cross

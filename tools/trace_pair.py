@@ -64,6 +64,14 @@ for i in range(0, len(args), 3):
                                                                  else (1, 2, 3, 4, 5, 6, 8)))
             print(f"1sm {m}x{n}x{k} beta={beta}: {st} | wall {(t[11] - t[10]) / 1e3:.2f} us | event {rep.ns / 1e3:.2f} us",
                   flush=True)
+            if sys.argv[1] == "run1":   # entry / exit spread over the CTAs (globaltimer, ns)
+                cb = (ctypes.c_ulonglong * 320)()
+                assert lib.compar_trace1_cta_read(cb) == 0
+                ent = [cb[2 * i] for i in range(160) if cb[2 * i] and cb[2 * i + 1] >= cb[2 * i]]
+                ext = [cb[2 * i + 1] for i in range(160) if cb[2 * i] and cb[2 * i + 1] >= cb[2 * i]]
+                e0 = min(ent)
+                print(f"    ctas {len(ent)}: entry spread {(max(ent) - e0) / 1e3:.2f} us, exit first "
+                      f"{(min(ext) - e0) / 1e3:.2f} last {(max(ext) - e0) / 1e3:.2f} us", flush=True)
         continue
     for beta in (0.5, 0.0):
         A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
@@ -80,4 +88,11 @@ for i in range(0, len(args), 3):
             st = " ".join(f"{j}:{t[j] - t[0]:6d}" for j in list(range(10)) + [12, 13, 14, 15])
             print(f"{m}x{n}x{k} beta={beta} cta{cta}: {st} | wall {(t[11] - t[10]) / 1e3:.2f} us | event {rep.ns / 1e3:.2f} us",
                   flush=True)
+        cb = (ctypes.c_ulonglong * 320)()
+        assert lib.compar_trace_cta_read(cb) == 0
+        ent = [cb[2 * i] for i in range(160) if cb[2 * i] and cb[2 * i + 1] >= cb[2 * i]]
+        ext = [cb[2 * i + 1] for i in range(160) if cb[2 * i] and cb[2 * i + 1] >= cb[2 * i]]
+        e0 = min(ent)
+        print(f"    ctas {len(ent)}: entry spread {(max(ent) - e0) / 1e3:.2f} us, exit first "
+              f"{(min(ext) - e0) / 1e3:.2f} last {(max(ext) - e0) / 1e3:.2f} us", flush=True)
 ctx.terminate()
