@@ -93,6 +93,17 @@ struct TcMParams {
 // clock64 at fixed points of CTAs 0 and 1, globaltimer at entry / exit.
 __device__ unsigned long long g_trace[2][16];
 __device__ unsigned long long g_trace_cta[2 * 160];   // globaltimer at entry / exit of CTAs 0..159
+// per-item globaltimer stamps of CTAs 0..159, items 0..7: [0] first TMA of the item issued (warp 0),
+// [1] accumulator committed (MMA warp, leader), [2] last C_out store issued (epilogue warp 2)
+__device__ unsigned long long g_trace_item[160 * 8 * 3];
+#define TRACE_ITEM(j, w)                                                                      \
+    do {                                                                                      \
+        if (blockIdx.x < 160 && (j) < 8) {                                                    \
+            unsigned long long t;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                           \
+            g_trace_item[(blockIdx.x * 8 + (j)) * 3 + (w)] = t;                               \
+        }                                                                                     \
+    } while (0)
 #define TRACE_CTA(i)                                                                          \
     do {                                                                                      \
         if (blockIdx.x < 160) {                                                               \
@@ -117,6 +128,7 @@ __device__ unsigned long long g_trace_cta[2 * 160];   // globaltimer at entry / 
 #define TRACE(i) ((void)0)
 #define TRACE_GT(i) ((void)0)
 #define TRACE_CTA(i) ((void)0)
+#define TRACE_ITEM(j, w) ((void)0)
 #endif
 
 enum { kFull = 0, kSplit = 1 };
@@ -276,6 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                         ptx::tma_load_2d_2sm(sb + b * C::B_BOX_BYTES, &tmB, fb, c0, c1);
                     }
                     if (kstep == 0 && me == 0) TRACE(2);
+                    if (kb == it.kb0 && me == 0) TRACE_ITEM(i, 0);
                 }
             }
             if (rank == 0 && me == 0) {  // last cluster out re-arms the counters for the next launch on this stream
@@ -329,6 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 }
                 if (lane == 0) ptx::tc_commit_2sm_mc(tfull0 + 8 * acc, 0x3);
                 if (local == 0 && lane == 0) TRACE(4);
+                if (lane == 0) TRACE_ITEM(local, 1);
                 __syncwarp();
             }
         }
@@ -461,6 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 __syncwarp();
             }
             if (local == 0 && warp == 2 && lane == 0) TRACE(6);
+            if (warp == 2 && lane == 0) TRACE_ITEM(local, 2);
         }
         if (lane == 0) ptx::bulk_wait<0>();
         if (warp == 2 && lane == 0) TRACE(7);
@@ -485,6 +500,14 @@ int trace_read(unsigned long long *out) {
 }
 int trace_cta_read(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_trace_cta, sizeof(g_trace_cta)) == cudaSuccess ? 0 : -1;
+}
+int trace_item_read(unsigned long long *out, int clear) {
+    if (cudaMemcpyFromSymbol(out, g_trace_item, sizeof(g_trace_item)) != cudaSuccess) return -1;
+    if (clear) {
+        static unsigned long long z[160 * 8 * 3];
+        if (cudaMemcpyToSymbol(g_trace_item, z, sizeof(z)) != cudaSuccess) return -1;
+    }
+    return 0;
 }
 #endif
 
@@ -646,4 +669,5 @@ cudaError_t preload_tcm_kernels() {
 #ifdef COMPAR_TRACE
 extern "C" int compar_trace_read(unsigned long long *out) { return compar::trace_read(out); }
 extern "C" int compar_trace_cta_read(unsigned long long *out) { return compar::trace_cta_read(out); }
+extern "C" int compar_trace_item_read(unsigned long long *out, int clear) { return compar::trace_item_read(out, clear); }
 #endif

@@ -113,6 +113,10 @@ def test_predict_scheduler_real_kernels_match_oracle():
     finally:
         ctx.terminate()
     # the generalisation did its job: shapes first seen after the fit decided without calibrating
-    # every variant (PREDICT decisions exist), and the stream ends in model / predict mode
+    # every variant (PREDICT decisions exist), and the stream settles into model / predict mode.
+    # (R37 exploration — one warm-up + one timed run of a variant predicted within 1.5x of the
+    # measured best — may still fall on any single late task, so the tail is judged as a whole.)
     assert cm.MODE_PREDICT in modes
-    assert modes[-1] in (cm.MODE_MODEL, cm.MODE_PREDICT)
+    tail = modes[-30:]
+    settled = sum(md in (cm.MODE_MODEL, cm.MODE_PREDICT) for md in tail)
+    assert settled >= 0.7 * len(tail), modes
