@@ -693,6 +693,15 @@ def main():
                             "variants_in_timed_region": used,
                             "eligible": [variant_names[v] for v in ctx.eligible(desc)]},
                "clocks": clocks, "e2e": e2e, "north_star_targets": targets, "cublas_same_op": yard}
+        # tensor utilisation from FLOP per SM-cycle at the clock sampled under load (ncu's
+        # tensor-pipe-active counter under-reports the CTA-pair kernels): a BF16 tcgen05 M=128 N=256
+        # K=16 MMA per SM retires 2*128*256*16 FLOP in 128 cycles = 8192 FLOP / SM-cycle
+        sm_mhz = (clocks or {}).get("sm_mhz")
+        if sm_mhz:
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            per = achieved * 1e12 / (sms * sm_mhz * 1e6)
+            out["roofline"]["per_sm_cycle"] = {"flop_per_sm_cycle": per, "peak_flop_per_sm_cycle": 8192,
+                                               "frac": per / 8192, "sms": sms, "sm_mhz": sm_mhz}
     if world > 1:
         dist.barrier()
     ctx.terminate()
