@@ -131,6 +131,26 @@ def main(out):
             best = min(ours)
             sw_rows.append(f"| {key.replace('^3', '³').replace('_f32', ' TF32').replace('_bf16', ' BF16')} | "
                            f"{f(best[0], 2)} µs ({best[1].split('/', 1)[1]}) | {f(cub, 2)} µs |")
+    # selector quality and host overhead for the paper-context table
+    regs = []
+    for key in ("config1", "config5a", "deepk"):
+        regs += [x.get("regret", 0.0) for x in (sel.get(key) or []) if isinstance(x, dict)]
+    regs.append((sel.get("config2") or {}).get("max_regret", 0.0))
+    reg_single = max(regs) if regs else None
+    b5 = sel.get("config5b") or {}
+    reg_5b_h = max((v["regret"] for v in (b5.get("history") or {}).get("per_shape", {}).values()), default=None)
+    reg_5b_p = max((v["regret"] for v in (b5.get("predict") or {}).get("per_shape", {}).values()), default=None)
+    overhead = "host submit ≈ 11 µs per task through the Python binding (config 1), `profiles/r02_selector.json`"
+    ho = os.path.join(ROOT, "profiles", "r02_host_overhead.jsonl")
+    if os.path.exists(ho):
+        recs = {r["mode"]: r for r in (json.loads(ln) for ln in open(ho) if ln.strip().startswith("{"))}
+        if "gpu" in recs and "virtual" in recs:
+            g, v = recs["gpu"], recs["virtual"]
+            overhead = (f"native C caller (`tools/host_overhead_c.cpp`, `profiles/r02_host_overhead.jsonl`): "
+                        f"selection + bookkeeping {v['select_us'] + v['submit_us'] + v['sync_us']:.2f} µs per task "
+                        f"(virtual clock); 64³ GPU task: submit {g['submit_us']:.1f} µs (events + launch), "
+                        f"sync {g['sync_us']:.1f} µs incl. the {g['kernel_us']:.1f} µs kernel; through the Python "
+                        f"binding ≈ 11 µs per submit")
     txt = f"""# RESULTS — COMPAR GEMM hot path on B200 (BASELINE.md §5 format)
 
 Generated by `tools/results_table.py` from committed measurement files only; every row names its
@@ -147,7 +167,7 @@ bound; integer inputs bitwise) — all `-m gpu` parity suites pass.
 
 ## Single-wave tensor-core shapes (kernel-only, builder-run r02, `profiles/r02_single_wave_ncu.json`)
 
-""" + "\n".join(sw_rows) + """
+""" + "\n".join(sw_rows) + f"""
 
 (Where the time goes and what was changed: `profiles/r02_single_wave_trace.md`.)
 
@@ -162,9 +182,9 @@ findings, quoted with their hardware:
 | machine | Xeon E5-2620 v4 (8 cores, 68.3 GB/s) + Titan Xp (GP102, 3840 cores, 1.41–1.58 GHz, 547.6 GB/s, ≈ 12.1 TFLOP/s FP32 derived) — P:153-157, Table 1 | one B200 (148 SMs, 1965 MHz max, ≈ 6.5 TB/s measured, 1672 TFLOP/s BF16 measured burst) |
 | precision / workload | FP32 `float` arrays, square n = 8..8192, mean of 10 repetitions — P:78, P:201-205, P:166 | FP32 / TF32 / BF16 (C FP32), the BASELINE configs, medians of ≥ 10 |
 | variants | BLAS, OpenMP, CUDA, CUBLAS — P:201-205, Table 2 | `simt_f32`, `tma_f32`, `tc_*` (1-SM, pair, wide pair, split-K), `simt_bf16` (GPU only; no CPU class) |
-| which is fastest | n = 8..128 "not always clear"; n = 64..4096 CUDA; n = 4096 CUDA beats CUBLAS; n = 8192 CUBLAS beats CUDA — P:220, P:224 | config 2: `tma_f32` under FP32-strict at every n; under TF32 `tc_tf32` up to 1024, `tc_tf32_2sm` 1536–4096 (selector picks, regret ≤ 0.4 %) |
-| selection quality | StarPU "frequently chose sub-optimal options" (n = 32: OpenMP instead of BLAS; 64..4096: OpenMP / BLAS instead of CUDA) — P:224 | history selector: regret 0–0.4 % on configs 1, 2, 5a, deep-K; ≤ 0.2 % per shape on 5b |
-| runtime overhead | CUDA-only often slightly faster than COMPAR (StarPU decision overhead) — P:222 | host submit ≈ 11 µs per task (config 1, FP32-strict), `profiles/r02_selector.json` |
+| which is fastest | n = 8..128 "not always clear"; n = 64..4096 CUDA; n = 4096 CUDA beats CUBLAS; n = 8192 CUBLAS beats CUDA — P:220, P:224 | config 2: `tma_f32` under FP32-strict at every n; under TF32 `tc_tf32` up to 1024, `tc_tf32_2sm` 1536–4096 (selector picks, regret ≤ {f(100 * reg_single, 1)} %) |
+| selection quality | StarPU "frequently chose sub-optimal options" (n = 32: OpenMP instead of BLAS; 64..4096: OpenMP / BLAS instead of CUDA) — P:224 | history selector: regret ≤ {f(100 * reg_single, 1)} % on configs 1, 2, 5a, deep-K; ≤ {f(100 * reg_5b_h, 1)} % per shape on 5b (predict scheduler ≤ {f(100 * reg_5b_p, 1)} %) |
+| runtime overhead | CUDA-only often slightly faster than COMPAR (StarPU decision overhead) — P:222 | {overhead} |
 """
     with open(out, "w") as fh:
         fh.write(txt)
