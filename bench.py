@@ -341,11 +341,14 @@ def alu_peak_tflops(peaks):
 # (key, m, n, k, storage, compute class) of the BASELINE.json north-star targets timed after the
 # headline: config 3 in BF16 (target >= 70 % of the burst BF16 peak), config 5a (HBM-bound), and
 # the paper's own arithmetic with FP32 storage ("float arrays", P:202 SGEMM): TF32 tensor
-# cores at the headline 32768^3 shape and strict FP32 (FFMA variants only) at 8192^3.
+# cores at the headline 32768^3 shape, strict FP32 (FFMA variants only) at 8192^3, and FP32 accuracy
+# on tensor cores (class F32_SPLIT, R38: three TF32 products per product) at both.
 TARGETS = (("config3_8192cube_bf16", 8192, 8192, 8192, "bf16", "bf16"),
            ("config5a_65536x256x4096_bf16", 65536, 256, 4096, "bf16", "bf16"),
            ("config4_32768cube_tf32_fp32_storage", 32768, 32768, 32768, "f32", "tf32"),
-           ("config3_8192cube_f32_strict", 8192, 8192, 8192, "f32", "f32"))
+           ("config3_8192cube_f32_strict", 8192, 8192, 8192, "f32", "f32"),
+           ("config3_8192cube_f32_split", 8192, 8192, 8192, "f32", "f32x3"),
+           ("config4_32768cube_f32_split", 32768, 32768, 32768, "f32", "f32x3"))
 
 
 def north_star_targets(ctx, cm, peaks, R=10):
@@ -368,7 +371,8 @@ def north_star_targets(ctx, cm, peaks, R=10):
         A = device_matrix(gen.TAG_A, m, k, dtype=sdt)
         B = device_matrix(gen.TAG_B, k, n, dtype=sdt)
         C = device_matrix(gen.TAG_C, m, n)
-        compute = {"bf16": cm.COMPUTE_BF16, "tf32": cm.COMPUTE_TF32, "f32": cm.COMPUTE_F32_STRICT}[cls]
+        compute = {"bf16": cm.COMPUTE_BF16, "tf32": cm.COMPUTE_TF32, "f32": cm.COMPUTE_F32_STRICT,
+                   "f32x3": cm.COMPUTE_F32_SPLIT}[cls]
         in_dtype = cm.BF16 if sdt == "bf16" else cm.F32
 
         def mk(hint=-1):
@@ -404,12 +408,15 @@ def north_star_targets(ctx, cm, peaks, R=10):
         eb = 2 if sdt == "bf16" else 4
         nbytes = eb * (m * k + k * n) + 4 * m * n * 2
         tflops = flops / t_sel / 1e3
-        peak = {"bf16": peaks["bf16_tflops"], "tf32": peaks["bf16_tflops"] / 2.0, "f32": alu}[cls]
+        peak = {"bf16": peaks["bf16_tflops"], "tf32": peaks["bf16_tflops"] / 2.0, "f32": alu,
+                "f32x3": peaks["bf16_tflops"] / 6.0}[cls]
         out[key] = {"variant": names[chosen], "ms": t_sel / 1e6, "tflops": tflops,
                     "peak_tflops": peak, "frac_of_peak": tflops / peak,
                     "peak_kind": {"bf16": "measured burst BF16 (MEASURED_PEAKS.bf16_tflops)",
                                   "tf32": "half the measured burst BF16 peak (nominal TF32 = BF16 / 2)",
-                                  "f32": "FFMA ceiling: SMs x 128 x 2 x sm_max_mhz"}[cls],
+                                  "f32": "FFMA ceiling: SMs x 128 x 2 x sm_max_mhz",
+                                  "f32x3": "a third of half the measured burst BF16 peak (three TF32 "
+                                           "products per FP32 product)"}[cls],
                     "hbm_gbs": nbytes / t_sel, "frac_of_hbm_peak": nbytes / t_sel / peaks["hbm_gbs"],
                     "best_variant": best, "regret": med[names[chosen]] / med[best] - 1.0,
                     "median_ns_per_variant": med, "pruned_unlaunched": pruned, "calibration_runs": calib,
@@ -418,8 +425,9 @@ def north_star_targets(ctx, cm, peaks, R=10):
             out[key]["frac_of_bf16_burst_peak"] = tflops / peaks["bf16_tflops"]
         if cls == "tf32":
             out[key]["frac_of_tf32_sustained"] = tflops / (peaks.get("bf16_tflops_sustained", peak * 2) / 2.0)
-        if cls == "f32":
+        if cls in ("f32", "f32x3"):
             out[key]["fp32_alu_peak_tflops"] = alu
+            out[key]["over_fp32_alu_peak"] = tflops / alu
         del A, B, C
         torch.cuda.empty_cache()
     out["selector_regret_max"] = max(v["regret"] for v in out.values() if isinstance(v, dict))

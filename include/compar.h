@@ -61,10 +61,20 @@ typedef enum { COMPAR_F32 = 0, COMPAR_BF16 = 1 } compar_dtype;             /* st
  *   F32_STRICT: FP32 FFMA only  -> eligible targets SIMT_F32, TMA_F32
  *   TF32:       FP32 storage, TF32 tensor cores allowed -> SIMT_F32, TMA_F32, TC_TF32
  *   BF16:       BF16 storage (in_dtype must be BF16)    -> TC_BF16 (+ pair forms), SIMT_BF16
+ *   F32_SPLIT:  FP32 storage, FP32 accuracy for finite inputs (every element inside the FP32
+ *               dot-product error bound, R38) -> SIMT_F32, TMA_F32, TCX_F32 (three
+ *               TF32 tensor-core products per FP32 product).  Unlike F32_STRICT it does not
+ *               promise IEEE FFMA semantics: a non-finite A / B entry may turn an FP32 +-inf
+ *               result into NaN (the hi*lo cross terms multiply it by zero).
  * The tcgen05 and TMA targets further require the TMA alignment rule (16-byte aligned bases and
  * row pitches); SIMT_F32 / SIMT_BF16 accept any shape and alignment, so every valid descriptor
  * has at least one eligible built-in.                                                        */
-typedef enum { COMPAR_COMPUTE_F32_STRICT = 0, COMPAR_COMPUTE_TF32 = 1, COMPAR_COMPUTE_BF16 = 2 } compar_compute;
+typedef enum {
+    COMPAR_COMPUTE_F32_STRICT = 0,
+    COMPAR_COMPUTE_TF32 = 1,
+    COMPAR_COMPUTE_BF16 = 2,
+    COMPAR_COMPUTE_F32_SPLIT = 3
+} compar_compute;
 
 /* Target of a variant (the paper's `target` clause).  USER variants are
  * caller-supplied launch functions, eligible for every dtype/compute. */
@@ -87,6 +97,11 @@ typedef enum {
                                 /*   through distributed shared memory; single-wave shapes only       */
                                 /*   (ceil(m/128) * ceil(n/256) <= SMs, K > one k-block)              */
     COMPAR_TGT_TCK_BF16 = 13,   /* built-in (c), cluster split-K form, BF16                               */
+    COMPAR_TGT_TCX_F32 = 14,    /* built-in (c), FP32-accuracy form (class F32_SPLIT): A, B split into  */
+                                /*   TF32 hi + lo in a library workspace (12 (mk + kn) bytes), one TF32 */
+                                /*   tcgen05 GEMM over 3K (hi*hi + hi*lo + lo*hi) in 1024-k chunks      */
+                                /*   combined by round-to-nearest epilogues; K >= 64, TMA alignment,  */
+                                /*   not in world-panel or host-memory tasks                           */
     /* the "sort" interface */
     COMPAR_TGT_SORT_RADIX = 20,   /* built-in: onesweep LSD radix sort, 4 x 8-bit passes, any n      */
     COMPAR_TGT_SORT_BITONIC = 21  /* built-in: single-CTA shared-memory bitonic network, n <= 16384  */

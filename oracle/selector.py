@@ -28,8 +28,9 @@ from dataclasses import dataclass, field
 # precision classes / targets (mirror include/compar.h values; restated, not imported)
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER = 0, 1, 2, 3, 4
 TGT_SIMT_BF16 = 9
+TGT_TCX_F32 = 14
 F32, BF16 = 0, 1
-COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
+COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16, COMPUTE_F32_SPLIT = 0, 1, 2, 3
 MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
 
 
@@ -45,6 +46,8 @@ def admits(target: int, in_dtype: int, compute: int) -> bool:
         return target in (TGT_SIMT_F32, TGT_TMA_F32)
     if compute == COMPUTE_TF32:
         return target in (TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32)
+    if compute == COMPUTE_F32_SPLIT:   # FP32 accuracy: the FFMA variants and the split TF32 form (R38)
+        return target in (TGT_SIMT_F32, TGT_TMA_F32, TGT_TCX_F32)
     return False
 
 
@@ -259,10 +262,12 @@ class SelectorOracle:
     # restated): FLOPs at the nominal peak of its class, compulsory bytes at nominal 8 TB/s.
     @staticmethod
     def static_lb_ns(cls, key, sms=148):
-        """cls: 'ffma' | 'bf16' | 'tf32' | None (USER: no bound)."""
+        """cls: 'ffma' | 'bf16' | 'tf32' | 'f32x3' | None (USER: no bound).  'f32x3' (R38) runs three
+        TF32 products per FP32 product: a third of the TF32 peak."""
         if cls is None:
             return 0.0
-        peak = {"ffma": float(sms) * 128.0 * 2.0 * 1.965e9, "bf16": 2.25e15, "tf32": 1.125e15}[cls]
+        peak = {"ffma": float(sms) * 128.0 * 2.0 * 1.965e9, "bf16": 2.25e15, "tf32": 1.125e15,
+                "f32x3": 1.125e15 / 3.0}[cls]
         m, n, k, dtype, _c, _t, beta0 = key
         m, n, k = float(m), float(n), float(k)
         flops = 2.0 * m * n * k

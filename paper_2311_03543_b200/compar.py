@@ -19,18 +19,20 @@ OK, E_INVALID, E_STATE, E_DUPLICATE, E_NO_VARIANT, E_CUDA, E_NCCL, E_TASK_FAILED
 STATUS_NAMES = ["OK", "E_INVALID", "E_STATE", "E_DUPLICATE", "E_NO_VARIANT", "E_CUDA", "E_NCCL", "E_TASK_FAILED",
                 "E_UNKNOWN_TASK", "E_IO", "E_FORMAT", "E_OOM"]
 F32, BF16 = 0, 1
-COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16 = 0, 1, 2
+COMPUTE_F32_STRICT, COMPUTE_TF32, COMPUTE_BF16, COMPUTE_F32_SPLIT = 0, 1, 2, 3
 TGT_SIMT_F32, TGT_TMA_F32, TGT_TC_TF32, TGT_TC_BF16, TGT_USER, TGT_TC2_TF32, TGT_TC2_BF16, TGT_TCW_TF32, TGT_TCW_BF16 = \
     0, 1, 2, 3, 4, 5, 6, 7, 8
 TGT_SIMT_BF16 = 9
 TGT_TCS_TF32, TGT_TCS_BF16 = 10, 11
 TGT_TCK_TF32, TGT_TCK_BF16 = 12, 13
+TGT_TCX_F32 = 14
 TGT_SORT_RADIX, TGT_SORT_BITONIC = 20, 21
 KEY_U32, KEY_I32, KEY_F32 = 0, 1, 2
 # built-in targets by precision class (the §8(b) eligibility table; include/compar.h)
 TARGETS_STRICT = (TGT_SIMT_F32, TGT_TMA_F32)
 TARGETS_TF32 = TARGETS_STRICT + (TGT_TC_TF32, TGT_TC2_TF32, TGT_TCW_TF32, TGT_TCS_TF32, TGT_TCK_TF32)
 TARGETS_BF16 = (TGT_TC_BF16, TGT_TC2_BF16, TGT_TCW_BF16, TGT_SIMT_BF16, TGT_TCS_BF16, TGT_TCK_BF16)
+TARGETS_F32_SPLIT = TARGETS_STRICT + (TGT_TCX_F32,)
 MODE_WARMUP, MODE_CALIB, MODE_MODEL, MODE_EAGER, MODE_HINT, MODE_NOOP, MODE_PREDICT = 0, 1, 2, 3, 4, 5, 6
 SCHED_HISTORY, SCHED_EAGER, SCHED_PREDICT = 0, 1, 2
 CALIB_INTERLEAVED, CALIB_BLOCKED = 0, 1

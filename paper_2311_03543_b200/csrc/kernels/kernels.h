@@ -120,6 +120,13 @@ inline bool tc_clusterk_ok(int64_t m, int64_t n, int64_t k, bool bf16, int sms) 
 }
 cudaError_t launch_tc_gemm_ck(const GemmLaunch &g, bool bf16);
 
+// tc_f32x3 (variant c, FP32-accuracy form, tc_f32x3.cu): operands split into TF32 hi + lo in a
+// per-stream workspace of tc_f32x3_workspace_bytes(), then one TF32 tcgen05 GEMM over 3K in
+// chunks of 1024 original k.  Eligible from K >= tc_f32x3_min_k.
+constexpr int64_t tc_f32x3_min_k = 64;
+size_t tc_f32x3_workspace_bytes(int64_t m, int64_t n, int64_t k, int transB);
+cudaError_t launch_tc_gemm_f32x3(const GemmLaunch &g);
+
 // TMA eligibility (the selector's constraint filter).
 inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {
     return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * elem_bytes) % 16 == 0);

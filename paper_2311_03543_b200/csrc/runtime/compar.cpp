@@ -275,7 +275,7 @@ compar_status validate(Ctx *c, const compar_gemm_desc *d) {
     if (!d) return fail(COMPAR_E_INVALID, "desc is NULL");
     if (d->m < 0 || d->n < 0 || d->k < 0) return fail(COMPAR_E_INVALID, "negative dimension");
     if (d->in_dtype != COMPAR_F32 && d->in_dtype != COMPAR_BF16) return fail(COMPAR_E_INVALID, "bad in_dtype");
-    if (d->compute < COMPAR_COMPUTE_F32_STRICT || d->compute > COMPAR_COMPUTE_BF16)
+    if (d->compute < COMPAR_COMPUTE_F32_STRICT || d->compute > COMPAR_COMPUTE_F32_SPLIT)
         return fail(COMPAR_E_INVALID, "bad compute");
     if ((d->in_dtype == COMPAR_BF16) != (d->compute == COMPAR_COMPUTE_BF16))
         return fail(COMPAR_E_INVALID, "BF16 storage requires COMPUTE_BF16 and vice versa");
@@ -316,6 +316,7 @@ bool admits(compar_target t, compar_dtype dt, compar_compute cp) {
         case COMPAR_TGT_TCW_TF32:
         case COMPAR_TGT_TCS_TF32:
         case COMPAR_TGT_TCK_TF32: return dt == COMPAR_F32 && cp == COMPAR_COMPUTE_TF32;
+        case COMPAR_TGT_TCX_F32: return dt == COMPAR_F32 && cp == COMPAR_COMPUTE_F32_SPLIT;
         case COMPAR_TGT_TC_BF16:
         case COMPAR_TGT_TC2_BF16:
         case COMPAR_TGT_TCW_BF16:
@@ -347,6 +348,13 @@ bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, co
         tc_splitk_splits(mrows, d->n, d->k, t == COMPAR_TGT_TCS_BF16) < 2)
         return false;
     if ((t == COMPAR_TGT_TCK_TF32 || t == COMPAR_TGT_TCK_BF16) && !tc_clusterk_ok(mrows, d->n, d->k, t == COMPAR_TGT_TCK_BF16, c->num_sms))
+        return false;
+    // FP32-accuracy split form (R38): the per-product split error is below the FP32 bound's c*K*u
+    // from K >= 64; its workspace holds both operands whole, so not for row-panel (world) or
+    // host-memory (chunked) tasks, and at most 32 GiB
+    if (t == COMPAR_TGT_TCX_F32 &&
+        (d->k < tc_f32x3_min_k || d->world == COMPAR_WORLD_PANELS || d->mem == COMPAR_MEM_HOST ||
+         tc_f32x3_workspace_bytes(mrows, d->n, d->k, d->transB) > (size_t(32) << 30)))
         return false;
     if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;
     if ((d->lda * eb) % 16 != 0 || (d->ldb * eb) % 16 != 0) return false;
@@ -717,6 +725,7 @@ compar_status run_builtin(Ctx *c, compar_target t, const compar_gemm_desc *d, co
         case COMPAR_TGT_TCS_BF16: e = launch_tc_gemm_splitk(g, true); break;
         case COMPAR_TGT_TCK_TF32: e = launch_tc_gemm_ck(g, false); break;
         case COMPAR_TGT_TCK_BF16: e = launch_tc_gemm_ck(g, true); break;
+        case COMPAR_TGT_TCX_F32: e = launch_tc_gemm_f32x3(g); break;
         case COMPAR_TGT_SIMT_BF16: e = launch_simt_bf16(g); break;
         default: return fail(COMPAR_E_INVALID, "not a built-in target");
     }
@@ -1279,6 +1288,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         compar_register_variant(c, "gemm", "tc_bf16_sk", COMPAR_TGT_TCS_BF16, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_tf32_ck", COMPAR_TGT_TCK_TF32, nullptr, nullptr, &id);
         compar_register_variant(c, "gemm", "tc_bf16_ck", COMPAR_TGT_TCK_BF16, nullptr, nullptr, &id);
+        compar_register_variant(c, "gemm", "tc_f32x3", COMPAR_TGT_TCX_F32, nullptr, nullptr, &id);
         compar_register_sort_variant(c, "sort_radix", COMPAR_TGT_SORT_RADIX, nullptr, nullptr, &id);
         compar_register_sort_variant(c, "sort_bitonic", COMPAR_TGT_SORT_BITONIC, nullptr, nullptr, &id);
     }
@@ -1358,7 +1368,7 @@ compar_status compar_register_variant(void *ctx, const char *iface, const char *
     if (!name || !*name || std::strlen(name) > 63) return fail(COMPAR_E_INVALID, "bad variant name");
     for (const char *p = name; *p; ++p)
         if (*p == ' ' || *p == '\t' || *p == '\n') return fail(COMPAR_E_INVALID, "variant name has whitespace");
-    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_TCK_BF16) return fail(COMPAR_E_INVALID, "unknown target");
+    if (target < COMPAR_TGT_SIMT_F32 || target > COMPAR_TGT_TCX_F32) return fail(COMPAR_E_INVALID, "unknown target");
     if (target == COMPAR_TGT_USER && !fn) return fail(COMPAR_E_INVALID, "USER variant needs a launch function");
     if (target != COMPAR_TGT_USER && c->virt) return fail(COMPAR_E_INVALID, "built-in targets need CUDA");
     std::lock_guard<std::mutex> lk(c->mu);
@@ -1482,6 +1492,7 @@ double static_lb_ns(const Ctx *c, compar_target t, const Key &k) {
         case COMPAR_TGT_TCW_TF32:
         case COMPAR_TGT_TCS_TF32:
         case COMPAR_TGT_TCK_TF32: peak = 1.125e15; break;
+        case COMPAR_TGT_TCX_F32: peak = 1.125e15 / 3.0; break;   // three TF32 products per FP32 product
         default: return 0.0;
     }
     const double m = static_cast<double>(k.m), n = static_cast<double>(k.n), kk = static_cast<double>(k.k);

@@ -38,7 +38,9 @@ VARIANTS = {"simt_f32": (cm.F32, cm.COMPUTE_F32_STRICT, 1e-5),
             "tc_tf32_ck": (cm.F32, cm.COMPUTE_TF32, 5e-3),
             "tc_bf16_ck": (cm.BF16, cm.COMPUTE_BF16, 1e-5),
             # FP32 accumulation of exactly-widened BF16 operands: held to the strict-FP32 bound
-            "simt_bf16": (cm.BF16, cm.COMPUTE_BF16, 1e-5)}
+            "simt_bf16": (cm.BF16, cm.COMPUTE_BF16, 1e-5),
+            # FP32 accuracy from three TF32 products per product (R38): the strict-FP32 bounds
+            "tc_f32x3": (cm.F32, cm.COMPUTE_F32_SPLIT, 1e-5)}
 
 SHAPES = [(1, 1, 1), (7, 13, 5), (64, 64, 64), (65, 127, 129), (129, 257, 70), (128, 256, 64),
           (300, 520, 1000), (1000, 777, 333), (257, 1, 100), (1, 300, 4097)]
@@ -57,6 +59,8 @@ def skip_ineligible(name, m, n, k):
         pytest.skip(f"{name} needs >= 64 k-blocks (K = {k})")
     if name.endswith("_ck") and k <= (64 if "bf16" in name else 32):
         pytest.skip(f"{name} needs >= 2 k-blocks (K = {k})")
+    if name == "tc_f32x3" and k < 64:
+        pytest.skip("tc_f32x3 needs K >= 64 (DESIGN.md R38)")
 
 
 @pytest.fixture(scope="module")
@@ -111,8 +115,9 @@ class Case:
 
     def check(self):
         A, B, C0, alpha, beta, dt, tf32 = self._args
+        # (tc_f32x3 claims FP32 accuracy: no widening of the norm tolerance for tensor-core accumulation)
         return assert_parity(self.got, self.ref, A, B, C0, alpha, beta, dt, tf32, self.tol, self.name,
-                             tc=self.name.startswith("tc_"))
+                             tc=self.name.startswith("tc_") and self.name != "tc_f32x3")
 
 
 @pytest.mark.parametrize("name", list(VARIANTS))

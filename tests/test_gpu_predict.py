@@ -53,6 +53,8 @@ def lb_class(name):
         return "tf32"
     if name.startswith("tc_bf16"):
         return "bf16"
+    if name == "tc_f32x3":
+        return "f32x3"
     return "ffma" if name in ("simt_f32", "tma_f32", "simt_bf16") else None
 
 

@@ -110,6 +110,11 @@ def test_admits_table():
     assert el(bf16, so.COMPUTE_BF16) == [3]
     assert so.admits(so.TGT_SIMT_BF16, bf16, so.COMPUTE_BF16) and not so.admits(so.TGT_SIMT_BF16, f32, so.COMPUTE_TF32)
     assert el(bf16, so.COMPUTE_TF32) == []
+    # F32_SPLIT (R38): FP32 accuracy -> the FFMA variants and the TF32-split form, never plain TF32
+    assert el(f32, so.COMPUTE_F32_SPLIT) == [0, 1]
+    assert so.admits(so.TGT_TCX_F32, f32, so.COMPUTE_F32_SPLIT)
+    assert not any(so.admits(so.TGT_TCX_F32, f32, c) for c in (so.COMPUTE_F32_STRICT, so.COMPUTE_TF32))
+    assert not so.admits(so.TGT_TCX_F32, bf16, so.COMPUTE_F32_SPLIT)
     assert so.tma_ok(4, [0, 256], [64, 8]) and not so.tma_ok(4, [4], [64]) and not so.tma_ok(2, [0], [9])
 
 
