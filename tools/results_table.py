@@ -70,8 +70,10 @@ def main(out):
             if not isinstance(t, dict):
                 continue
             shape = {"config3_8192cube_bf16": "8192³", "config5a_65536x256x4096_bf16": "65536×256×4096",
-                     "config4_32768cube_tf32_fp32_storage": "32768³", "config3_8192cube_f32_strict": "8192³"}.get(key, key)
-            prec = "BF16" if "bf16" in key else ("TF32 (FP32 storage)" if "tf32" in key else "FP32 strict")
+                     "config4_32768cube_tf32_fp32_storage": "32768³", "config3_8192cube_f32_strict": "8192³",
+                     "config3_8192cube_f32_split": "8192³", "config4_32768cube_f32_split": "32768³"}.get(key, key)
+            prec = ("BF16" if "bf16" in key else "TF32 (FP32 storage)" if "tf32" in key else
+                    "FP32 accuracy (F32_SPLIT, 3×TF32)" if "split" in key else "FP32 strict")
             cfg = key.split("_")[0].replace("config", "")
             hb = f"{f(t.get('frac_of_hbm_peak', 0) * 100)} %" if "5a" in key else "—"
             row(cfg, shape, t["variant"], prec, 1, f"{f(t['ms'] * 1e3, 1)} µs" if t["ms"] < 1 else f"{f(t['ms'], 2)} ms",
@@ -85,15 +87,19 @@ def main(out):
         row("1", "64³", c["chosen"], "FP32 strict" if c["compute"] == 0 else "TF32", 1,
             f"{f(c['median_ns'][c['chosen']] / 1e3, 1)} µs", "—", "—", "launch-bound", "—", "1e-5 / tol.",
             f(c["regret"] * 100, 1) + " %", "—", "—", "—", "builder-run r02 (`profiles/r02_selector.json`)")
-    for mode in ("F32_STRICT", "TF32"):
+    for mode in ("F32_STRICT", "TF32", "F32_SPLIT"):
         for r in (sel.get("config2") or {}).get(mode, []):
             s = r["shape"][0]
             t = r["median_ns"][r["chosen"]]
             tfl = 2.0 * s ** 3 / t / 1e3
-            peak = 74.45 if mode == "F32_STRICT" else bf16 / 2
-            row("2", f"{s}³", r["chosen"], "FP32 strict" if mode == "F32_STRICT" else "TF32", 1, f"{f(t / 1e3, 1)} µs",
-                f(tfl), f(tfl / peak * 100), "FFMA ceiling" if mode == "F32_STRICT" else "BF16 burst / 2", "—",
-                "1e-5 / 5e-3", f(r["regret"] * 100, 1) + " %", "—", "—", "—", "builder-run r02 (selector sweep)")
+            ffma = mode == "F32_STRICT" or (mode == "F32_SPLIT" and r["chosen"] != "tc_f32x3")
+            peak = 74.45 if ffma else (bf16 / 2 if mode == "TF32" else bf16 / 6)
+            prec = {"F32_STRICT": "FP32 strict", "TF32": "TF32", "F32_SPLIT": "FP32 accuracy (F32_SPLIT)"}[mode]
+            kind = "FFMA ceiling" if ffma else ("BF16 burst / 2" if mode == "TF32" else "BF16 burst / 6")
+            row("2", f"{s}³", r["chosen"], prec, 1, f"{f(t / 1e3, 1)} µs",
+                f(tfl), f(tfl / peak * 100), kind, "—",
+                "5e-3" if mode == "TF32" else "1e-5", f(r["regret"] * 100, 1) + " %", "—", "—", "—",
+                "builder-run r02 (selector sweep)")
     for r in sel.get("config5a", []):
         m, n, k = r["shape"]
         t = r["median_ns"][r["chosen"]]

@@ -1,7 +1,7 @@
 """Selector evaluation on real cudaEvent timings (BASELINE configs 1, 2, 5).
 
 * config 1: 64^3 FP32 — calibration trace, chosen variant, host submit overhead;
-* config 2: square sweep 256..4096 FP32 (F32_STRICT and TF32) — regret at every size and the
+* config 2: square sweep 256..4096 FP32 (F32_STRICT, TF32 and F32_SPLIT) — regret at every size and the
   variant crossover points;
 * config 5a: tall-skinny 65536x256x4096 (BF16, TF32) — regret;
 * config 5b: mixed stream of 200 tasks (shapes drawn with numpy PCG64 seed 7), FP32 under TF32,
@@ -31,6 +31,7 @@ from paper_2311_03543_b200 import compar as cm  # noqa: E402
 R = 10
 TF32_T = set(cm.TARGETS_TF32)
 STRICT_T = set(cm.TARGETS_STRICT)
+SPLIT_T = set(cm.TARGETS_F32_SPLIT)
 BF16_T = set(cm.TARGETS_BF16)
 
 
@@ -142,11 +143,12 @@ def main(out_path):
 
     # ---- config 2: square sweep
     sizes = [256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096]
-    c2 = {"F32_STRICT": [], "TF32": []}
+    c2 = {"F32_STRICT": [], "TF32": [], "F32_SPLIT": []}
     for s in sizes:
         prob = Problem(s, s, s)
         c2["F32_STRICT"].append(regret_case(ctx, names, prob, cm.COMPUTE_F32_STRICT, STRICT_T))
         c2["TF32"].append(regret_case(ctx, names, prob, cm.COMPUTE_TF32, TF32_T))
+        c2["F32_SPLIT"].append(regret_case(ctx, names, prob, cm.COMPUTE_F32_SPLIT, SPLIT_T))
         del prob
         torch.cuda.empty_cache()
     # crossovers: smallest size from which variant X's median beats Y's (within the 1.5x grid)
@@ -163,7 +165,7 @@ def main(out_path):
                 if wins and loses and min(wins) > min(loses):
                     cross[f"{mode}: {x} beats {y} from"] = min(wins)
     c2["crossovers"] = cross
-    c2["max_regret"] = max(r["regret"] for rows in (c2["F32_STRICT"], c2["TF32"]) for r in rows)
+    c2["max_regret"] = max(r["regret"] for rows in (c2["F32_STRICT"], c2["TF32"], c2["F32_SPLIT"]) for r in rows)
     res["config2"] = c2
 
     # ---- config 5a: tall-skinny
