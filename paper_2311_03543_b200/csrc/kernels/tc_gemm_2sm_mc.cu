@@ -38,10 +38,7 @@ constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;
 constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
 constexpr int kRingM = 4;
 
-// kSW: the single-wave instantiation (every CTA pair owns at most one 256-wide tile, beta != 0):
-// 3 stages instead of 5, and the smem this frees holds all four C_in chunks of each epilogue warp,
-// fetched by TMA while the mainloop runs — the tile's exposed epilogue then only writes C.
-template <bool kBF16, bool kTransB, int kBN, bool kSW = false>
+template <bool kBF16, bool kTransB, int kBN>
 struct TcMCfg {
     static constexpr int BM = 128;              // A rows per CTA (UMMA_M = 256 per pair)
     static constexpr int BN = kBN;              // UMMA_N (256, or 128 for grids that leave pairs idle);
@@ -51,9 +48,8 @@ struct TcMCfg {
     static constexpr int ELEM = kBF16 ? 2 : 4;
     static constexpr int BK = 128 / ELEM;
     static constexpr int UMMA_K = 32 / ELEM;
-    // 256-wide tiles: 5 stages so the 8 epilogue warps' staging (64 KiB) fits beside the ring;
-    // single-wave: 3 stages beside 128 KiB of staging
-    static constexpr int STAGES = kBN == 256 ? (kSW ? 3 : 5) : 6;
+    // 256-wide tiles: 5 stages so the 8 epilogue warps' staging (64 KiB) fits beside the ring
+    static constexpr int STAGES = kBN == 256 ? 5 : 6;
     static constexpr uint32_t A_BYTES = BM * 128;
     static constexpr uint32_t B_BYTES = BN_CTA * 128;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -68,7 +64,7 @@ struct TcMCfg {
     // C_in / C_out staging chunks (32 x 32 FP32) per epilogue warp: a warp handles BN/64 chunks —
     // both of a 128-wide tile are loaded before its accumulator is ready; the 256-wide tile's four
     // cycle through two buffers
-    static constexpr int EPI_BUFS = kSW ? 4 : 2;
+    static constexpr int EPI_BUFS = 2;
     static constexpr uint32_t EPI_BYTES = kEpiWarpsM * EPI_BUFS * 4096;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
@@ -150,12 +146,12 @@ __device__ __forceinline__ void tile_coords_m(int t, int m_blocks, int n_blocks,
     nb = r / gm;
 }
 
-template <bool kBF16, bool kTransB, int kBN, bool kSW>
+template <bool kBF16, bool kTransB, int kBN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
     tc_gemm_2sm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmCo, const __grid_constant__ CUtensorMap tmCi,
                           TcMParams p) {
-    using C = TcMCfg<kBF16, kTransB, kBN, kSW>;
+    using C = TcMCfg<kBF16, kTransB, kBN>;
     constexpr int kCluster = 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -554,15 +550,15 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
     }
 }
 
-template <bool kBF16, bool kTransB, int kBN = 256, bool kSW = false>
+template <bool kBF16, bool kTransB, int kBN = 256>
 cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
-    using C = TcMCfg<kBF16, kTransB, kBN, kSW>;
+    using C = TcMCfg<kBF16, kTransB, kBN>;
     constexpr int kCluster = 2;
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kSW>,
+        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (attr_err != cudaSuccess) return;
         cudaLaunchConfig_t cfg = {};
@@ -571,7 +567,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         at.val.clusterDim.x = kCluster, at.val.clusterDim.y = 1, at.val.clusterDim.z = 1;
         cfg.gridDim = dim3(kCluster * 64), cfg.blockDim = dim3(kThreadsM), cfg.dynamicSmemBytes = C::SMEM;
         cfg.attrs = &at, cfg.numAttrs = 1;
-        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kSW>, &cfg);
+        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN>, &cfg);
     });
     if (attr_err != cudaSuccess) return attr_err;
     if (max_clusters <= 0) return cudaErrorInvalidConfiguration;
@@ -614,7 +610,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
     if (clusters < 1) clusters = 1;
     if (items < clusters) clusters = items;
     p.nprod = kn.tc2_producers == 1 ? 1 : 2;
-    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kSW><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
+    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     if (p.splits > 1) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -640,13 +636,6 @@ cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16) {
         if (bf16) return g.transB ? launch_tcm_t<true, true, 128>(g) : launch_tcm_t<true, false, 128>(g);
         return g.transB ? launch_tcm_t<false, true, 128>(g) : launch_tcm_t<false, false, 128>(g);
     }
-    // single wave of 256-wide tiles with beta != 0: the instantiation that prefetches all of C_in
-    // during the mainloop (COMPAR_TC2_SW=0 disables; same k order per element, bitwise-same C)
-    const int pairs = g.num_sms / 2;
-    if (knobs_of(g).tc2_sw && g.beta != 0.f && tiles256 <= pairs) {
-        if (bf16) return g.transB ? launch_tcm_t<true, true, 256, true>(g) : launch_tcm_t<true, false, 256, true>(g);
-        return g.transB ? launch_tcm_t<false, true, 256, true>(g) : launch_tcm_t<false, false, 256, true>(g);
-    }
     if (bf16) return g.transB ? launch_tcm_t<true, true>(g) : launch_tcm_t<true, false>(g);
     return g.transB ? launch_tcm_t<false, true>(g) : launch_tcm_t<false, false>(g);
 }
@@ -662,7 +651,7 @@ cudaError_t preload_tcm_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess;
 #define COMPAR_PRELOAD_TCM(B, T, N) \
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, N, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, N>);
     COMPAR_PRELOAD_TCM(true, false, 256)
     COMPAR_PRELOAD_TCM(true, true, 256)
     COMPAR_PRELOAD_TCM(false, false, 256)
@@ -672,10 +661,6 @@ cudaError_t preload_tcm_kernels() {
     COMPAR_PRELOAD_TCM(false, false, 128)
     COMPAR_PRELOAD_TCM(false, true, 128)
 #undef COMPAR_PRELOAD_TCM
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, false, 256, true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, true, 256, true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, false, 256, true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, true, 256, true>);
     return e;
 }
 

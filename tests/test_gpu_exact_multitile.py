@@ -123,39 +123,3 @@ def test_full_size_exact_sampled(ctx, name, shape):
     np.testing.assert_array_equal(got2, ref2)
     del Cd
     torch.cuda.empty_cache()
-
-
-# ---- the pair kernel's single-wave instantiation (tc_gemm_2sm_mc.cu kSW: 37..74 pair tiles of
-# 256 x 256 with beta != 0 -> 3 stages and all of C_in prefetched during the mainloop) ----
-
-@pytest.mark.parametrize("name", ["tc_bf16_2sm", "tc_tf32_2sm"])
-@pytest.mark.parametrize("shape", [(2048, 2048, 1000), (1800, 2000, 777)], ids=lambda s: "x".join(map(str, s)))
-def test_single_wave_instantiation_exact(ctx, name, shape):
-    """64 pair tiles (the second shape ragged in every dimension): bitwise against the oracle."""
-    m, n, k = shape
-    got = launch(ctx, name, m, n, k).double().cpu().numpy()
-    np.testing.assert_array_equal(got, full_ref(m, n, k))
-
-
-@pytest.mark.parametrize("transB", [0, 1])
-def test_single_wave_instantiation_bitwise_vs_default(monkeypatch, transB):
-    """Real-valued BF16 inputs: the single-wave instantiation keeps every element's k order, so C
-    is bitwise the 5-stage instantiation's (COMPAR_TC2_SW=0, read at context init)."""
-    m, n, k = 2048, 2048, 2048
-    A = device_matrix(gen.TAG_A, m, k, dtype="bf16")
-    B = device_matrix(gen.TAG_B, k, n, dtype="bf16", transposed=bool(transB))
-    C0 = device_matrix(gen.TAG_C, m, n)
-    outs = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("COMPAR_TC2_SW", flag)
-        c = cm.Compar()
-        try:
-            Cd = C0.clone()
-            d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, ldb=k if transB else n, alpha=1.5, beta=0.5,
-                             in_dtype=cm.BF16, compute=cm.COMPUTE_BF16, transB=transB,
-                             variant_hint=vid(c, "tc_bf16_2sm"), stream=torch.cuda.current_stream().cuda_stream)
-            assert c.run(d).status == 0
-            outs.append(Cd)
-        finally:
-            c.terminate()
-    assert torch.equal(outs[0], outs[1])
