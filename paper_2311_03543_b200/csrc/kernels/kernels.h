@@ -16,6 +16,8 @@ struct Knobs {
     int tc2_group = 0;       // COMPAR_TCM_GROUP: pair raster band (cluster tiles)
     int tc2_rowstore_group = 0;   // COMPAR_TC_GROUP: raster band of the row-store pair kernel
     int tc2_producers = 2;   // COMPAR_TC2_PRODUCERS: TMA producer warps per CTA in the pair kernel (1 or 2)
+    int even_waves = 1;      // COMPAR_EVEN_WAVES=0: the pair kernel on every CTA pair even when its
+                             // last wave of tiles is partial
     int tcw_group = 0;       // COMPAR_TCW_GROUP: wide-pair raster band (pair rows)
     int tcw_delay = 24;      // COMPAR_TCW_DELAY: wide-pair epilogue-overlap delay in k-steps
     int tma_tile = 0;        // COMPAR_TMA_TILE: tma_f32 tile 128 / 64

@@ -609,6 +609,14 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
     int clusters = g.num_sms / kCluster < max_clusters ? g.num_sms / kCluster : max_clusters;
     if (clusters < 1) clusters = 1;
     if (items < clusters) clusters = items;
+    // even waves: the fewest clusters that still need the same number of item waves, so no wave
+    // is partial (config 5a: 256 tiles on 64 pairs = 4 full waves instead of 3.46 waves on 74,
+    // whose last 0.46 wave ran MMA-bound on 68 SMs while the rest idled); the makespan in tiles
+    // per cluster is unchanged and each tile gets more of the HBM / L2 bandwidth
+    if (kn.even_waves) {
+        const int waves = (items + clusters - 1) / clusters;
+        clusters = (items + waves - 1) / waves;
+    }
     p.nprod = kn.tc2_producers == 1 ? 1 : 2;
     tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     if (p.splits > 1) {
