@@ -38,7 +38,12 @@ constexpr int kThreadsM = 96 + 32 * kEpiWarpsM;
 constexpr int kGroupM4 = 4;  // 512-row cluster tiles per raster band (COMPAR_TCM_GROUP overrides)
 constexpr int kRingM = 4;
 
-template <bool kBF16, bool kTransB, int kBN>
+// kDeep (multi-wave launches of 256-wide tiles, where each tile's epilogue overlaps the next tile's
+// mainloop): 6 stages and one C staging buffer per epilogue warp instead of 5 and 2 — more A bytes in
+// flight per SM for the HBM-bound shapes (config 5a 128.4 -> 126.3 us, 8192^3 742 -> 738 us); the
+// single-wave launch keeps the second buffer, whose C_in prefetch its exposed epilogue needs
+// (2048^3: 33.3 vs 34.8 us with one).
+template <bool kBF16, bool kTransB, int kBN, bool kDeep = false>
 struct TcMCfg {
     static constexpr int BM = 128;              // A rows per CTA (UMMA_M = 256 per pair)
     static constexpr int BN = kBN;              // UMMA_N (256, or 128 for grids that leave pairs idle);
@@ -49,7 +54,8 @@ struct TcMCfg {
     static constexpr int BK = 128 / ELEM;
     static constexpr int UMMA_K = 32 / ELEM;
     // 256-wide tiles: 5 stages so the 8 epilogue warps' staging (64 KiB) fits beside the ring
-    static constexpr int STAGES = kBN == 256 ? 5 : 6;
+    // (kDeep: 6 stages beside 32 KiB)
+    static constexpr int STAGES = kBN == 256 && !kDeep ? 5 : 6;
     static constexpr uint32_t A_BYTES = BM * 128;
     static constexpr uint32_t B_BYTES = BN_CTA * 128;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -64,7 +70,7 @@ struct TcMCfg {
     // C_in / C_out staging chunks (32 x 32 FP32) per epilogue warp: a warp handles BN/64 chunks —
     // both of a 128-wide tile are loaded before its accumulator is ready; the 256-wide tile's four
     // cycle through two buffers
-    static constexpr int EPI_BUFS = 2;
+    static constexpr int EPI_BUFS = kDeep ? 1 : 2;
     static constexpr uint32_t EPI_BYTES = kEpiWarpsM * EPI_BUFS * 4096;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
@@ -146,12 +152,12 @@ __device__ __forceinline__ void tile_coords_m(int t, int m_blocks, int n_blocks,
     nb = r / gm;
 }
 
-template <bool kBF16, bool kTransB, int kBN>
+template <bool kBF16, bool kTransB, int kBN, bool kDeep>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
     tc_gemm_2sm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmCo, const __grid_constant__ CUtensorMap tmCi,
                           TcMParams p) {
-    using C = TcMCfg<kBF16, kTransB, kBN>;
+    using C = TcMCfg<kBF16, kTransB, kBN, kDeep>;
     constexpr int kCluster = 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -550,15 +556,15 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
     }
 }
 
-template <bool kBF16, bool kTransB, int kBN = 256>
+template <bool kBF16, bool kTransB, int kBN = 256, bool kDeep = false>
 cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
-    using C = TcMCfg<kBF16, kTransB, kBN>;
+    using C = TcMCfg<kBF16, kTransB, kBN, kDeep>;
     constexpr int kCluster = 2;
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN>,
+        attr_err = cudaFuncSetAttribute(tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kDeep>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (attr_err != cudaSuccess) return;
         cudaLaunchConfig_t cfg = {};
@@ -567,7 +573,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         at.val.clusterDim.x = kCluster, at.val.clusterDim.y = 1, at.val.clusterDim.z = 1;
         cfg.gridDim = dim3(kCluster * 64), cfg.blockDim = dim3(kThreadsM), cfg.dynamicSmemBytes = C::SMEM;
         cfg.attrs = &at, cfg.numAttrs = 1;
-        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN>, &cfg);
+        attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kDeep>, &cfg);
     });
     if (attr_err != cudaSuccess) return attr_err;
     if (max_clusters <= 0) return cudaErrorInvalidConfiguration;
@@ -618,7 +624,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         clusters = (items + waves - 1) / waves;
     }
     p.nprod = kn.tc2_producers == 1 ? 1 : 2;
-    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
+    tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kDeep><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     if (p.splits > 1) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -644,6 +650,10 @@ cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16) {
         if (bf16) return g.transB ? launch_tcm_t<true, true, 128>(g) : launch_tcm_t<true, false, 128>(g);
         return g.transB ? launch_tcm_t<false, true, 128>(g) : launch_tcm_t<false, false, 128>(g);
     }
+    if (2 * tiles256 > g.num_sms) {   // more 256-wide tiles than CTA pairs: the deep-ring form
+        if (bf16) return g.transB ? launch_tcm_t<true, true, 256, true>(g) : launch_tcm_t<true, false, 256, true>(g);
+        return g.transB ? launch_tcm_t<false, true, 256, true>(g) : launch_tcm_t<false, false, 256, true>(g);
+    }
     if (bf16) return g.transB ? launch_tcm_t<true, true>(g) : launch_tcm_t<true, false>(g);
     return g.transB ? launch_tcm_t<false, true>(g) : launch_tcm_t<false, false>(g);
 }
@@ -659,7 +669,7 @@ cudaError_t preload_tcm_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess;
 #define COMPAR_PRELOAD_TCM(B, T, N) \
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, N>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<B, T, N, false>);
     COMPAR_PRELOAD_TCM(true, false, 256)
     COMPAR_PRELOAD_TCM(true, true, 256)
     COMPAR_PRELOAD_TCM(false, false, 256)
@@ -669,6 +679,10 @@ cudaError_t preload_tcm_kernels() {
     COMPAR_PRELOAD_TCM(false, false, 128)
     COMPAR_PRELOAD_TCM(false, true, 128)
 #undef COMPAR_PRELOAD_TCM
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, false, 256, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<true, true, 256, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, false, 256, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, tc_gemm_2sm_mc_kernel<false, true, 256, true>);
     return e;
 }
 
