@@ -650,7 +650,7 @@ cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16) {
         if (bf16) return g.transB ? launch_tcm_t<true, true, 128>(g) : launch_tcm_t<true, false, 128>(g);
         return g.transB ? launch_tcm_t<false, true, 128>(g) : launch_tcm_t<false, false, 128>(g);
     }
-    if (2 * tiles256 > g.num_sms) {   // more 256-wide tiles than CTA pairs: the deep-ring form
+    if (knobs_of(g).tc2_deep && 2 * tiles256 > g.num_sms) {   // more 256-wide tiles than pairs: deep ring
         if (bf16) return g.transB ? launch_tcm_t<true, true, 256, true>(g) : launch_tcm_t<true, false, 256, true>(g);
         return g.transB ? launch_tcm_t<false, true, 256, true>(g) : launch_tcm_t<false, false, 256, true>(g);
     }
