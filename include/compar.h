@@ -159,7 +159,7 @@ typedef struct {
                                    bound (FLOPs at its class's nominal peak, compulsory bytes at
                                    nominal HBM bandwidth), exceeds calib_prune/100 x the key's best
                                    mean; blocked calibration visits variants by increasing lower
-                                   bound.  0: off.  <0: COMPAR_CALIB_PRUNE or 300 */
+                                   bound.  0: off.  <0: COMPAR_CALIB_PRUNE or 150 */
     int bcast_ctas;             /* world mode, NCCL broadcast: the communicator's maxCTAs (NCCL
                                    config), and the SMs a GEMM overlapping a broadcast leaves free.
                                    <0: COMPAR_BCAST_CTAS or 4                                        */

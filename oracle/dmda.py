@@ -35,7 +35,7 @@ class DmdaOracle:
     nranks: int = 1
     lanes: int = 1
     blocked: bool = True
-    prune_pct: int = 300       # the runtime's default (R32)
+    prune_pct: int = 150       # the runtime's default (R32)
     sel: SelectorOracle = None
     ready: list = field(default_factory=list)
     live: list = field(default_factory=list)      # (task, w, end, span, write)

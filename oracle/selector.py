@@ -73,7 +73,7 @@ class SelectorOracle:
     eager: bool = False
     blocked: bool = False      # calibration order (R19); False = SPEC S:369 interleaving
     explore_pct: int = 150     # DESIGN.md R37 predict-mode exploration threshold (percent)
-    prune_pct: int = 300       # DESIGN.md R32 calibration pruning threshold (percent, the runtime default); 0 = SPEC
+    prune_pct: int = 150       # DESIGN.md R32 calibration pruning threshold (percent, the runtime default); 0 = SPEC
     hist: dict = field(default_factory=dict)   # (v, key) -> Record
 
     def rec(self, v: int, key) -> Record:

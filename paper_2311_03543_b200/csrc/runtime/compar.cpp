@@ -1193,7 +1193,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
     if (cfg.calib_order != COMPAR_CALIB_INTERLEAVED && cfg.calib_order != COMPAR_CALIB_BLOCKED)
         return fail(COMPAR_E_INVALID, "calib_order must be INTERLEAVED (0) or BLOCKED (1)");
     if (cfg.builtins < 0) cfg.builtins = 1;
-    if (cfg.calib_prune < 0) cfg.calib_prune = env_int("COMPAR_CALIB_PRUNE", 300);
+    if (cfg.calib_prune < 0) cfg.calib_prune = env_int("COMPAR_CALIB_PRUNE", 150);
     if (cfg.calib_prune != 0 && cfg.calib_prune < 100)
         return fail(COMPAR_E_INVALID, "calib_prune must be 0 (off) or >= 100 (percent of the best mean)");
     if (cfg.bcast_ctas < 0) cfg.bcast_ctas = env_int("COMPAR_BCAST_CTAS", 4);

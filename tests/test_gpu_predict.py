@@ -97,7 +97,7 @@ def test_predict_scheduler_real_kernels_match_oracle():
             d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=1.5, beta=0.0, compute=cm.COMPUTE_TF32,
                              stream=st)
             ctx.perf_save(path)
-            orc = so.SelectorOracle(len(names), blocked=True, prune_pct=300)
+            orc = so.SelectorOracle(len(names), blocked=True, prune_pct=150)
             orc.hist = load_dump(path, names)
             elig = ctx.eligible(d)
             key = (m, n, k, so.F32, so.COMPUTE_TF32, 0, 1)

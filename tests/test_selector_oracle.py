@@ -30,8 +30,9 @@ def test_spec_s369_alternation():
 
 
 def test_config1_calibration_plan():
-    """3 variants x (1 warm-up + 3 timed) = 12 calibration runs in order 0,1,2,... then model."""
-    sel = so.SelectorOracle(3)
+    """3 variants x (1 warm-up + 3 timed) = 12 calibration runs in order 0,1,2,... then model
+    (the SPEC S:369 plan: calibration pruning off, R32)."""
+    sel = so.SelectorOracle(3, prune_pct=0)
     trace = run_stream(sel, "k", [0, 1, 2], lambda v: [30, 10, 20][v], 13)
     assert [v for v, _ in trace[:12]] == [0, 1, 2] * 4
     assert [m for _, m in trace[:3]] == [so.MODE_WARMUP] * 3
