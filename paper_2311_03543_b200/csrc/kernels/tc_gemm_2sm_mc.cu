@@ -72,7 +72,10 @@ struct TcMCfg {
     // cycle through two buffers
     static constexpr int EPI_BUFS = kDeep ? 1 : 2;
     static constexpr uint32_t EPI_BYTES = kEpiWarpsM * EPI_BUFS * 4096;
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
+    // chunks per epilogue warp beyond its staging buffers: on a CTA pair's last tile they are staged
+    // in the drained ring (LAST_BUFS per warp, one mbarrier each)
+    static constexpr int LAST_BUFS = kBN / 64 > EPI_BUFS ? kBN / 64 - EPI_BUFS : 0;
     static constexpr uint32_t IDESC = (1u << 4) | ((kBF16 ? 1u : 2u) << 7) | ((kBF16 ? 1u : 2u) << 10) |
                                       ((kTransB ? 0u : 1u) << 16) | ((uint32_t(BN) >> 3) << 17) |
                                       ((uint32_t(2 * BM) >> 4) << 24);
@@ -172,7 +175,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
     const uint32_t rempty0 = rfull0 + 8 * kRingM;
     const uint32_t cbar0 = rempty0 + 8 * kRingM;
     const uint32_t ring0 = cbar0 + 8 * C::EPI_BUFS * kEpiWarpsM;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 480);
+    const uint32_t lbar0 = ring0 + 4 * kRingM;   // [warp][LAST_BUFS] C_in chunks of the last tile
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES + 1016);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -203,6 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
             ptx::mbar_init(rempty0 + 8 * r, kConsumers);
         }
         for (int b = 0; b < C::EPI_BUFS * kEpiWarpsM; ++b) ptx::mbar_init(cbar0 + 8 * b, 1);
+        for (int b = 0; b < C::LAST_BUFS * kEpiWarpsM; ++b) ptx::mbar_init(lbar0 + 8 * b, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm<C::TMEM_COLS>(ptx::smem_u32(tmem_slot));
@@ -360,6 +365,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
         // staging chunk b of this warp and its C_in barrier (computed: no local-memory arrays)
         auto buf = [&](int b) -> uint32_t { return epi0 + static_cast<uint32_t>(NB * ew + b) * 4096; };
         auto cbar = [&](int b) -> uint32_t { return cbar0 + 8 * static_cast<uint32_t>(NB * ew + b); };
+        // the last tile's extra C_in chunks: 4 KiB slots of the drained stage ring, and their barriers
+        auto lbuf = [&](int x) -> uint32_t { return smem0 + static_cast<uint32_t>(C::LAST_BUFS * ew + x) * 4096; };
+        auto lbar = [&](int x) -> uint32_t { return lbar0 + 8 * static_cast<uint32_t>(C::LAST_BUFS * ew + x); };
         uint32_t loads_odd = 0;   // bit b: an odd number of C_in loads issued into chunk b
         const uint32_t tempty_leader = ptx::mapa_rank(tempty0, 0);
         const bool ldc = p.beta != 0.f;
@@ -413,6 +421,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
             __syncwarp();
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             if (local == 0 && warp == 2 && lane == 0) TRACE(5);
+            // The pair's last tile: once its accumulator is complete the MMAs have drained the
+            // stage ring, and no later item will refill it, so the chunks beyond this warp's staging
+            // buffers are all loaded into ring memory now, in parallel (not one after another as
+            // staging buffers free up) — the last tile's epilogue is exposed.  "Last" is known when
+            // the producer has already published the next ring value as the end marker; a warp
+            // that does not see it yet takes the ordinary path (decisions are per warp and safe).
+            bool last = false;
+            if (C::LAST_BUFS > 0 && ldc) {
+                if (lane == 0) {
+                    const int slot = local % kRingM;
+                    if (ptx::mbar_try_wait_cluster(rfull0 + 8 * slot, (local / kRingM) & 1))
+                        last = static_cast<int>(ptx::ld_shared_u32(ring0 + 4 * slot)) >= num_items;
+                    if (last) {
+                        for (int x = 0; x < C::LAST_BUFS; ++x) {
+                            ptx::mbar_arrive_expect_tx(lbar(x), 4096);
+                            ptx::tma_load_2d(lbuf(x), &tmCi, lbar(x), col_base + static_cast<int32_t>(tcol(NB + x)),
+                                             row_base);
+                        }
+                    }
+                }
+                last = __shfl_sync(0xffffffffu, last, 0);
+            }
             ptx::tc_fence_after();
             const uint32_t tm = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::BN;
             // accumulator chunk j+1 is read from TMEM while chunk j is being finished
@@ -425,7 +455,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 if (jj + 1 < kChunks) ptx::tmem_ld_32x32b_x32(tm + tcol(jj + 1), rn);
                 const bool tr = local == 0 && warp == 2 && lane == 0 && jj == 1;   // (trace stamps only)
                 if (tr) TRACE(12);
-                if (ldc) {
+                const bool lx = last && jj >= NB;          // chunk staged in the drained ring
+                const uint32_t cb = lx ? lbuf(jj - NB) : buf(b);
+                if (lx) {
+                    ptx::mbar_wait(lbar(jj - NB), 0);      // used once per launch: phase 0
+                } else if (ldc) {
                     ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
                 } else if (jj >= NB) {
                     if (lane == 0) ptx::bulk_wait_read<NB - 1>();
@@ -436,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 float4 ci[8];
                 if (ldc) {
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) ci[g] = ptx::lds128(buf(b) + swz + ((g ^ (lane & 7)) << 4));
+                    for (int g = 0; g < 8; ++g) ci[g] = ptx::lds128(cb + swz + ((g ^ (lane & 7)) << 4));
                 }
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
@@ -451,23 +485,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                         o.z = fmaf(p.beta, ci[g].z, o.z);
                         o.w = fmaf(p.beta, ci[g].w, o.w);
                     }
-                    ptx::sts128(buf(b) + swz + ((g ^ (lane & 7)) << 4), o);
+                    ptx::sts128(cb + swz + ((g ^ (lane & 7)) << 4), o);
                 }
                 if (tr) TRACE(9);
                 ptx::fence_proxy_async_smem();
                 if (tr) TRACE(14);
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tmCo, buf(b), col_base + static_cast<int32_t>(tcol(jj)), row_base);
+                    ptx::tma_store_2d(&tmCo, cb, col_base + static_cast<int32_t>(tcol(jj)), row_base);
                     ptx::bulk_commit();
                     if (tr) TRACE(15);
-                    if (ldc && jj + NB < kChunks) {
+                    if (ldc && !last && jj + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);
                         ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + static_cast<int32_t>(tcol(jj + NB)), row_base);
                     }
                 }
-                if (ldc && jj + NB < kChunks) loads_odd ^= 1u << b;
+                if (ldc && !last && jj + NB < kChunks) loads_odd ^= 1u << b;
                 if (jj + 1 < kChunks) {
                     ptx::tmem_ld_wait();
 #pragma unroll
