@@ -123,3 +123,35 @@ def test_full_size_exact_sampled(ctx, name, shape):
     np.testing.assert_array_equal(got2, ref2)
     del Cd
     torch.cuda.empty_cache()
+
+
+# ---- pair-kernel schedule forms (tc_gemm_2sm_mc.cu): single-wave (5 stages, two staging buffers),
+# deep ring (multi-wave: 6 stages, one buffer), even waves (fewest pairs with as many waves), and the
+# last tile's C_in chunks staged in the drained ring — all bitwise against the oracle ----
+
+@pytest.mark.parametrize("name", ["tc_bf16_2sm", "tc_tf32_2sm"])
+@pytest.mark.parametrize("shape", [(2048, 2048, 1000), (1800, 2000, 776), (9000, 2304, 520)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_pair_schedule_forms_exact(ctx, name, shape):
+    """64 pair tiles (single wave), the same ragged, and 36 x 9 = 324 tiles (deep ring, even waves:
+    5 waves on 65 pairs, last tile staged in the ring)."""
+    m, n, k = shape
+    got = launch(ctx, name, m, n, k).double().cpu().numpy()
+    np.testing.assert_array_equal(got, full_ref(m, n, k))
+
+
+@pytest.mark.parametrize("name", ["tc_bf16_2sm", "tc_tf32_2sm"])
+def test_pair_deep_ring_beta0_exact(ctx, name):
+    """beta = 0 on the deep-ring form (C_in never read, stores drain through one staging buffer)."""
+    m, n, k = 9000, 2304, 520
+    bf = "bf16" in name
+    dt = "bf16" if bf else "f32"
+    A = device_matrix(gen.TAG_A, m, k, I, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, I, dtype=dt)
+    Cd = torch.full((m, n), float("nan"), device="cuda")
+    d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, alpha=ALPHA, beta=0.0,
+                     in_dtype=cm.BF16 if bf else cm.F32, compute=cm.COMPUTE_BF16 if bf else cm.COMPUTE_TF32,
+                     variant_hint=vid(ctx, name), stream=torch.cuda.current_stream().cuda_stream)
+    assert ctx.run(d).status == 0
+    ref = og.gemm(gen.matrix(gen.TAG_A, m, k, I, "f32"), gen.matrix(gen.TAG_B, k, n, I, "f32"), alpha=ALPHA)
+    np.testing.assert_array_equal(Cd.double().cpu().numpy(), ref)
