@@ -16,6 +16,7 @@ struct Knobs {
     int tc2_group = 0;       // COMPAR_TCM_GROUP: pair raster band (cluster tiles)
     int tc2_rowstore_group = 0;   // COMPAR_TC_GROUP: raster band of the row-store pair kernel
     int tc2_producers = 2;   // COMPAR_TC2_PRODUCERS: TMA producer warps per CTA in the pair kernel (1 or 2)
+    int tc2_tmem_cin = 1;    // COMPAR_TC2_TMEM_CIN=0: single-wave pair launches read C_in from shared memory
     int tc2_deep = 1;        // COMPAR_TC2_DEEP=0: no deep-ring (6-stage) pair instantiation for multi-wave grids
     int even_waves = 1;      // COMPAR_EVEN_WAVES=0: the pair kernel on every CTA pair even when its
                              // last wave of tiles is partial

@@ -30,6 +30,7 @@ Knobs read_knobs() {
     k.tc2_producers = get("COMPAR_TC2_PRODUCERS", 2) == 1 ? 1 : 2;
     k.even_waves = get("COMPAR_EVEN_WAVES", 1) != 0;
     k.tc2_deep = get("COMPAR_TC2_DEEP", 1) != 0;
+    k.tc2_tmem_cin = get("COMPAR_TC2_TMEM_CIN", 1) != 0;
     k.tcw_group = get("COMPAR_TCW_GROUP", 0);
     k.tcw_delay = get("COMPAR_TCW_DELAY", 24);
     if (k.tcw_delay < 0) k.tcw_delay = 0;

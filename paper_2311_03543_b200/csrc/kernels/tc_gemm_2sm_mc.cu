@@ -95,6 +95,9 @@ struct TcMParams {
     int splits, ksplit;
     float *spart;          // [splits][m padded to 256][n padded to 256] raw FP32 partials
     int64_t spart_ld, spart_plane;
+    // single wave (every pair owns at most one tile) with beta != 0: the idle second accumulator's
+    // TMEM columns hold the tile's C_in, staged while the mainloop runs
+    int tmem_cin;
 };
 
 #ifdef COMPAR_TRACE
@@ -419,6 +422,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
             }
             if (ldc) loads_odd ^= (1u << NB) - 1;
             __syncwarp();
+            // Single wave: this warp's C_in chunks go through its staging buffers into TMEM columns
+            // [BN, 2 BN) (the second accumulator, which no later tile uses) before the accumulator is
+            // ready — the tile's exposed epilogue then reads C_in from TMEM and only writes C.
+            const bool tcin = p.tmem_cin && ldc && local == 0;
+            const uint32_t tm_cin = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + C::BN;
+            if (tcin) {
+#pragma unroll 1
+                for (int j = 0; j < kChunks; ++j) {
+                    const int b = j % NB;
+                    if (j >= NB) {   // buffer b's previous chunk was read by the lanes: reload it
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::mbar_arrive_expect_tx(cbar(b), 4096);
+                            ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + static_cast<int32_t>(tcol(j)), row_base);
+                        }
+                        loads_odd ^= 1u << b;
+                    }
+                    ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
+                    uint32_t v[32];
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        const float4 c4 = ptx::lds128(buf(b) + swz + ((g ^ (lane & 7)) << 4));
+                        v[4 * g + 0] = __float_as_uint(c4.x);
+                        v[4 * g + 1] = __float_as_uint(c4.y);
+                        v[4 * g + 2] = __float_as_uint(c4.z);
+                        v[4 * g + 3] = __float_as_uint(c4.w);
+                    }
+                    ptx::tmem_st_32x32b_x32(tm_cin + tcol(j), v);
+                }
+                ptx::tmem_st_wait();
+                __syncwarp();
+            }
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             if (local == 0 && warp == 2 && lane == 0) TRACE(5);
             // The pair's last tile: once its accumulator is complete the MMAs have drained the
@@ -428,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
             // the producer has already published the next ring value as the end marker; a warp
             // that does not see it yet takes the ordinary path (decisions are per warp and safe).
             bool last = false;
-            if (C::LAST_BUFS > 0 && ldc) {
+            if (C::LAST_BUFS > 0 && ldc && !tcin) {
                 if (lane == 0) {
                     const int slot = local % kRingM;
                     if (ptx::mbar_try_wait_cluster(rfull0 + 8 * slot, (local / kRingM) & 1))
@@ -455,9 +491,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 if (jj + 1 < kChunks) ptx::tmem_ld_32x32b_x32(tm + tcol(jj + 1), rn);
                 const bool tr = local == 0 && warp == 2 && lane == 0 && jj == 1;   // (trace stamps only)
                 if (tr) TRACE(12);
-                const bool lx = last && jj >= NB;          // chunk staged in the drained ring
+                // chunk staged in the drained ring (the last tile's C_in beyond the staging buffers; with
+                // tcin — a single wave, so the only tile is the last — the output of those chunks)
+                const bool lx = (last || tcin) && jj >= NB && C::LAST_BUFS > 0;
                 const uint32_t cb = lx ? lbuf(jj - NB) : buf(b);
-                if (lx) {
+                float4 ci[8];
+                if (tcin) {                                // C_in from TMEM; buf(b) only stages the output
+                    uint32_t cr[32];
+                    ptx::tmem_ld_32x32b_x32(tm_cin + tcol(jj), cr);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        ci[g] = make_float4(__uint_as_float(cr[4 * g]), __uint_as_float(cr[4 * g + 1]),
+                                            __uint_as_float(cr[4 * g + 2]), __uint_as_float(cr[4 * g + 3]));
+                } else if (lx) {
                     ptx::mbar_wait(lbar(jj - NB), 0);      // used once per launch: phase 0
                 } else if (ldc) {
                     ptx::mbar_wait(cbar(b), ((loads_odd >> b) & 1) ^ 1);
@@ -467,8 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                 }
                 if (tr) TRACE(13);
                 // all eight C_in vectors first, then the eight results (no load waits behind a store)
-                float4 ci[8];
-                if (ldc) {
+                if (ldc && !tcin) {
 #pragma unroll
                     for (int g = 0; g < 8; ++g) ci[g] = ptx::lds128(cb + swz + ((g ^ (lane & 7)) << 4));
                 }
@@ -495,13 +541,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsM, 1)
                     ptx::tma_store_2d(&tmCo, cb, col_base + static_cast<int32_t>(tcol(jj)), row_base);
                     ptx::bulk_commit();
                     if (tr) TRACE(15);
-                    if (ldc && !last && jj + NB < kChunks) {
+                    if (ldc && !last && !tcin && jj + NB < kChunks) {
                         ptx::bulk_wait_read<0>();
                         ptx::mbar_arrive_expect_tx(cbar(b), 4096);
                         ptx::tma_load_2d(buf(b), &tmCi, cbar(b), col_base + static_cast<int32_t>(tcol(jj + NB)), row_base);
                     }
                 }
-                if (ldc && !last && jj + NB < kChunks) loads_odd ^= 1u << b;
+                if (ldc && !last && !tcin && jj + NB < kChunks) loads_odd ^= 1u << b;
                 if (jj + 1 < kChunks) {
                     ptx::tmem_ld_wait();
 #pragma unroll
@@ -636,6 +682,7 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
     if (!p.sched) return cudaErrorMemoryAllocation;
     const int tiles = p.m_blocks * p.n_blocks;
     p.splits = 1, p.ksplit = p.num_kb, p.spart = nullptr, p.spart_ld = 0, p.spart_plane = 0;
+    p.tmem_cin = 0;
     if (splits > 1) {
         p.splits = splits;
         p.ksplit = (p.num_kb + splits - 1) / splits;
@@ -658,6 +705,8 @@ cudaError_t launch_tcm_t(const GemmLaunch &g, int splits = 1) {
         clusters = (items + waves - 1) / waves;
     }
     p.nprod = kn.tc2_producers == 1 ? 1 : 2;
+    // single wave of 256-wide tiles with beta != 0: C_in staged in the second accumulator's TMEM
+    p.tmem_cin = kn.tc2_tmem_cin && kBN == 256 && p.splits == 1 && g.beta != 0.f && items <= clusters;
     tc_gemm_2sm_mc_kernel<kBF16, kTransB, kBN, kDeep><<<kCluster * clusters, kThreadsM, C::SMEM, g.stream>>>(ta, tb, tco, tci, p);
     if (p.splits > 1) {
         cudaError_t e = cudaGetLastError();
