@@ -35,6 +35,8 @@ for name in names:
         shapes = [(77, 136, 4160, 0, 0.5, 1), (300, 264, 8200, 1, 0.0, 3), (129, 520, 4160, 0, -1.0, 2)]
     else:                      # more tiles than CTAs / clusters: the counter-fed tiles after the static first
         shapes.append((4096, 2304, 136 if name.endswith("_ck") else 64, 0, 0.5, 1))
+    if name.endswith("_2sm"):  # 64 pair tiles of 256 x 256: the single-wave form (C_in staged in TMEM)
+        shapes.append((2048, 2048, 136, 0, 0.5, 1))
     if name == "tc_f32x3":     # several accumulation chunks, ragged last chunk, both B layouts
         shapes += [(300, 264, 2100, 1, 0.5, 1), (129, 520, 1030, 0, 0.0, 1)]
     for (m, n, k, tb, beta, panels) in shapes:
