@@ -37,7 +37,8 @@ if __name__ == "__main__":
     A = device_matrix(gen.TAG_A, m, k, dtype=dt, ld=lda)
     B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb), ld=ldb)
     Cd = device_matrix(gen.TAG_C, m, n, ld=ldc)
-    compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else cm.COMPUTE_F32_STRICT)
+    compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else
+                                          cm.COMPUTE_F32_SPLIT if name == "tc_f32x3" else cm.COMPUTE_F32_STRICT)
     d = cm.make_desc(m, n, k, A=A.data_ptr(), B=B.data_ptr(), C_in=Cd.data_ptr(), C_out=Cd.data_ptr(), lda=lda,
                      ldb=ldb, ldc_in=ldc, ldc_out=ldc, alpha=1.5, beta=a.beta, in_dtype=cm.BF16 if bf else cm.F32,
                      compute=compute, transB=tb, variant_hint=names.index(name))
