@@ -20,7 +20,7 @@ for name in names:
     if only and name not in only:
         continue
     if name.startswith("sort_"):
-        for n in ([2, 1000, 16384] if name == "sort_bitonic" else [2, 1000, 16384, 70001]):
+        for n in ([2, 1000, 16384] if name == "sort_bitonic" else [2, 1000, 16384, 70001, (1 << 24) + 12345]):
             x = torch.randn(n, device="cuda")
             r = ctx.sort(x, variant_hint=names.index(name))
             assert r.status == 0 and bool((x[1:] >= x[:-1]).all()), (name, n)
