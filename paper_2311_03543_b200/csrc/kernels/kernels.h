@@ -130,6 +130,10 @@ cudaError_t launch_tc_gemm_ck(const GemmLaunch &g, bool bf16);
 constexpr int64_t tc_f32x3_min_k = 64;
 size_t tc_f32x3_workspace_bytes(int64_t m, int64_t n, int64_t k, int transB);
 cudaError_t launch_tc_gemm_f32x3(const GemmLaunch &g);
+// The per-stream split-K planes and tc_f32x3 operand workspaces (up to GiBs) are released when the
+// last runtime context terminates (compar_terminate).
+void release_f32x3_workspaces();
+void release_split_workspaces();
 
 // TMA eligibility (the selector's constraint filter).
 inline bool tma_compatible(const void *p, int64_t ld, int elem_bytes) {

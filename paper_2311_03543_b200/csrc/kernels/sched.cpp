@@ -51,10 +51,23 @@ int *sched_workspace(cudaStream_t s) {
     return p;
 }
 
+namespace {
+std::mutex g_split_mu;
+std::map<cudaStream_t, SplitWorkspace> g_split;
+}  // namespace
+
+void release_split_workspaces() {
+    std::lock_guard<std::mutex> lk(g_split_mu);
+    for (auto &kv : g_split) {
+        if (kv.second.part) cudaFree(kv.second.part);
+        if (kv.second.count) cudaFree(kv.second.count);
+    }
+    g_split.clear();
+}
+
 SplitWorkspace *split_workspace(cudaStream_t s, size_t part_bytes, size_t count_words) {
-    static std::mutex mu;
-    static std::map<cudaStream_t, SplitWorkspace> slots;
-    std::lock_guard<std::mutex> lk(mu);
+    std::lock_guard<std::mutex> lk(g_split_mu);
+    auto &slots = g_split;
     SplitWorkspace &w = slots[s];
     if (w.part_bytes < part_bytes) {
         if (w.part) cudaFree(w.part);

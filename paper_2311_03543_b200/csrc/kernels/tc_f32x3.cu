@@ -145,10 +145,12 @@ struct X3Workspace {
     size_t bytes = 0;
 };
 
+std::mutex g_x3_mu;
+std::map<cudaStream_t, X3Workspace> g_x3;
+
 float *x3_workspace(cudaStream_t s, size_t bytes) {
-    static std::mutex mu;
-    static std::map<cudaStream_t, X3Workspace> slots;
-    std::lock_guard<std::mutex> lk(mu);
+    std::lock_guard<std::mutex> lk(g_x3_mu);
+    auto &slots = g_x3;
     X3Workspace &w = slots[s];
     if (w.bytes < bytes) {
         if (w.buf) {
@@ -172,6 +174,13 @@ unsigned grid_for(int64_t work, int num_sms) {
 }
 
 }  // namespace
+
+void release_f32x3_workspaces() {
+    std::lock_guard<std::mutex> lk(g_x3_mu);
+    for (auto &kv : g_x3)
+        if (kv.second.buf) cudaFree(kv.second.buf);   // (cudaFree waits for the device)
+    g_x3.clear();
+}
 
 size_t tc_f32x3_workspace_bytes(int64_t m, int64_t n, int64_t k, int transB) {
     const int64_t k3 = 3 * round4(k);

@@ -1317,12 +1317,18 @@ compar_status compar_terminate(void *ctx) {
         c->done.clear();
     }
     if (!c->perf_path.empty()) st = compar_perf_save(c, c->perf_path.c_str());
+    bool last_ctx = false;
     {
         std::lock_guard<std::mutex> lk(g_live_mu);
         g_live.erase(c);
+        last_ctx = g_live.empty();
     }
     if (!c->virt) {
         cudaStreamSynchronize(c->stream);
+        if (last_ctx) {   // no context can have work in flight: drop the large kernel workspaces
+            release_f32x3_workspaces();
+            release_split_workspaces();
+        }
         for (auto &b : c->staging)
             if (b) cudaFree(b);
         if (c->breplica) cudaFree(c->breplica);

@@ -142,3 +142,33 @@ def test_f32x3_panels_bitwise(ctx):
         outs.append(Cd.cpu())
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+def test_f32x3_workspace_released_at_last_terminate(tmp_path):
+    """The per-stream operand workspace (12 (mk + kn) bytes: 3.2 GB at 8192^3) is freed when the
+    last context terminates (a separate process, so no other test's context is alive)."""
+    import subprocess
+    import sys
+    script = tmp_path / "ws.py"
+    script.write_text(
+        "import sys, torch\n"
+        f"sys.path.insert(0, {str(__import__('os').path.dirname(__import__('os').path.dirname(__file__)))!r})\n"
+        "import gen\n"
+        "from gen.device import device_matrix\n"
+        "from paper_2311_03543_b200 import compar as cm\n"
+        "m = n = k = 8192\n"
+        "A, B, C = device_matrix(gen.TAG_A, m, k), device_matrix(gen.TAG_B, k, n), device_matrix(gen.TAG_C, m, n)\n"
+        "ctx = cm.Compar()\n"
+        "names = [v for v, _ in ctx.variants()]\n"
+        "d = cm.make_desc(m, n, k, A=A, B=B, C_in=C, C_out=C, alpha=1.0, beta=0.5, compute=cm.COMPUTE_F32_SPLIT,\n"
+        "                 variant_hint=names.index('tc_f32x3'), stream=torch.cuda.current_stream().cuda_stream)\n"
+        "assert ctx.run(d).status == 0\n"
+        "torch.cuda.synchronize()\n"
+        "f0 = torch.cuda.mem_get_info()[0]\n"
+        "ctx.terminate()\n"
+        "f1 = torch.cuda.mem_get_info()[0]\n"
+        "print(f1 - f0)\n")
+    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    freed = int(out.stdout.strip().splitlines()[-1])
+    assert freed >= 12 * (8192 * 8192 * 2) * 0.95, freed
