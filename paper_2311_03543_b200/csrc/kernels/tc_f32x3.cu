@@ -208,7 +208,7 @@ cudaError_t launch_tc_gemm_f32x3(const GemmLaunch &g) {
                                                                                              n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // the product GEMM: one launch of the CTA-pair TF32 kernel per chunk of 3 * kChunkK tensor-core
+    // the product GEMM: one launch of a tcgen05 TF32 kernel per chunk of 3 * kChunkK tensor-core
     // k; the first applies the caller's beta * C_in, later ones accumulate into C_out (beta = 1, a
     // round-to-nearest FMA per element).  One kernel over the whole 3K with the chunks switched
     // in-kernel (C kept in L2 between a tile's chunks) measured slower at every size (8192^3 5.15
@@ -216,6 +216,11 @@ cudaError_t launch_tc_gemm_f32x3(const GemmLaunch &g) {
     // tiles in flight), so the chunks are separate launches.  The tile-width choice keeps every
     // element's k order, so row panels stay bitwise equal.  Only the last chunk can be short
     // (3 * round4(kc) k).
+    // Small grids (at most 16 pair tiles) take the 1-SM kernel, the rest the CTA-pair kernel: the
+    // un-split tcgen05 forms sum every element's k in the same MMA steps, so their results are bitwise
+    // identical (tests/test_gpu_parity.py::test_unsplit_tcgen05_forms_bitwise_identical) and the
+    // choice may depend on the panel's M without breaking the row-panel invariance.
+    const bool pair = ((m + 255) / 256) * ((n + 255) / 256) > 16;
     for (int64_t c0 = 0; c0 < k; c0 += kChunkK) {
         GemmLaunch gc = g;
         const int64_t kcp = round4(k - c0 < kChunkK ? k - c0 : kChunkK);
@@ -229,7 +234,7 @@ cudaError_t launch_tc_gemm_f32x3(const GemmLaunch &g) {
             gc.C_in = g.C_out;
             gc.ldc_in = g.ldc_out;
         }
-        e = launch_tc_gemm_2sm(gc, false);
+        e = pair ? launch_tc_gemm_2sm(gc, false) : launch_tc_gemm(gc, false);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

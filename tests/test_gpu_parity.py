@@ -443,3 +443,30 @@ def test_cluster_splitk_single_wave_eligibility(ctx, m, n, k, ok):
     if m == 128 * 149 and sms > 148:
         pytest.skip("boundary case written for 148 SMs")
     assert (vid(ctx, "tc_bf16_ck") in ctx.eligible(d)) == ok
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("transB", [0, 1])
+@pytest.mark.parametrize("shape,beta", [((1024, 1024, 3072), 0.5), ((2048, 1536, 1000), 0.0), ((300, 520, 1000), -1.0)],
+                         ids=lambda x: "x".join(map(str, x)) if isinstance(x, tuple) else str(x))
+def test_unsplit_tcgen05_forms_bitwise_identical(ctx, dt, transB, shape, beta):
+    """The 1-SM, CTA-pair and wide-pair forms sum every element's k in the same K = 16 (BF16) / 8
+    (TF32) MMA steps into an FP32 TMEM accumulator, so their C is bitwise identical on real-valued
+    inputs (only the split-K forms, which sum K ranges separately, differ) — what lets a launcher
+    (tc_f32x3, the world pipeline) pick among them by shape without changing any result."""
+    m, n, k = shape
+    bf = dt == "bf16"
+    A = device_matrix(gen.TAG_A, m, k, dtype=dt)
+    B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(transB))
+    C0 = device_matrix(gen.TAG_C, m, n)
+    outs = {}
+    for name in (("tc_bf16", "tc_bf16_2sm", "tc_bf16_2sm_w") if bf else ("tc_tf32", "tc_tf32_2sm", "tc_tf32_2sm_w")):
+        Cd = C0.clone()
+        d = cm.make_desc(m, n, k, A=A, B=B, C_in=Cd, C_out=Cd, ldb=k if transB else n, alpha=1.5, beta=beta,
+                         in_dtype=cm.BF16 if bf else cm.F32, compute=cm.COMPUTE_BF16 if bf else cm.COMPUTE_TF32,
+                         transB=transB, variant_hint=vid(ctx, name), stream=torch.cuda.current_stream().cuda_stream)
+        assert ctx.run(d).status == 0
+        outs[name] = Cd
+    ref = next(iter(outs.values()))
+    for name, o in outs.items():
+        assert torch.equal(o, ref), name
