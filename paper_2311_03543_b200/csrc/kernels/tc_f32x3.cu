@@ -70,73 +70,91 @@ __device__ __forceinline__ void seg_pos(int64_t k, int64_t K, int64_t &p0, int64
 }
 
 // K runs along columns (A, and B when transB): Y[r][segments of k] for X[r][k], k < round4(K)
-// (zero beyond K).  lo_first = 0: (hi, lo, hi) — the A side; 1: (lo, hi, hi) — the B side.
-__global__ void __launch_bounds__(256) split_cols_kernel(const float *__restrict__ X, int64_t ldx,
-                                                         float *__restrict__ Y, int64_t ldy, int64_t rows,
-                                                         int64_t K, int lo_first) {
+// (zero beyond K), four k per work item i.  lo_first = 0: (hi, lo, hi) — the A side; 1: (lo, hi,
+// hi) — the B side.
+__device__ __forceinline__ void split_cols_item(int64_t i, const float *__restrict__ X, int64_t ldx,
+                                                float *__restrict__ Y, int64_t ldy, int64_t K, int lo_first) {
     const int64_t q = (K + 3) / 4;
-    const int64_t total = rows * q;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = i / q, k0 = (i - r * q) * 4;
-        const float *x = X + r * ldx + k0;
-        float v[4];
-        if (k0 + 4 <= K) {
-            const float4 t = __ldcs(reinterpret_cast<const float4 *>(x));
-            v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
-        } else {
-            for (int e = 0; e < 4; ++e) v[e] = k0 + e < K ? x[e] : 0.f;
-        }
-        float h[4], l[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) split2(v[e], h[e], l[e]);
-        int64_t p0, kcp;
-        seg_pos(k0, K, p0, kcp);
-        float *y = Y + r * ldy + p0;
-        const float4 hv = make_float4(h[0], h[1], h[2], h[3]), lv = make_float4(l[0], l[1], l[2], l[3]);
-        __stcg(reinterpret_cast<float4 *>(y), lo_first ? lv : hv);
-        __stcg(reinterpret_cast<float4 *>(y + kcp), lo_first ? hv : lv);
-        __stcg(reinterpret_cast<float4 *>(y + 2 * kcp), hv);
+    const int64_t r = i / q, k0 = (i - r * q) * 4;
+    const float *x = X + r * ldx + k0;
+    float v[4];
+    if (k0 + 4 <= K) {
+        const float4 t = __ldcs(reinterpret_cast<const float4 *>(x));
+        v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+    } else {
+        for (int e = 0; e < 4; ++e) v[e] = k0 + e < K ? x[e] : 0.f;
     }
+    float h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) split2(v[e], h[e], l[e]);
+    int64_t p0, kcp;
+    seg_pos(k0, K, p0, kcp);
+    float *y = Y + r * ldy + p0;
+    const float4 hv = make_float4(h[0], h[1], h[2], h[3]), lv = make_float4(l[0], l[1], l[2], l[3]);
+    __stcg(reinterpret_cast<float4 *>(y), lo_first ? lv : hv);
+    __stcg(reinterpret_cast<float4 *>(y + kcp), lo_first ? hv : lv);
+    __stcg(reinterpret_cast<float4 *>(y + 2 * kcp), hv);
 }
 
 // K runs along rows (row-major B, K x N): rows of Y at the (lo, hi, hi) segment positions of k,
-// for k < round4(K) (zero rows beyond K).
-__global__ void __launch_bounds__(256) split_rows_kernel(const float *__restrict__ X, int64_t ldx,
-                                                         float *__restrict__ Y, int64_t ldy, int64_t K,
-                                                         int64_t cols) {
-    const int64_t kr = (K + 3) / 4 * 4;
+// for k < round4(K) (zero rows beyond K), four columns per work item i.
+__device__ __forceinline__ void split_rows_item(int64_t i, const float *__restrict__ X, int64_t ldx,
+                                                float *__restrict__ Y, int64_t ldy, int64_t K, int64_t cols) {
     const int64_t q = (cols + 3) / 4;
-    const int64_t total = kr * q;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t k = i / q, c0 = (i - k * q) * 4;
-        int64_t p0, kcp;
-        seg_pos(k, K, p0, kcp);
-        float *y0 = Y + p0 * ldy + c0;
-        float *y1 = y0 + kcp * ldy;
-        float *y2 = y0 + 2 * kcp * ldy;
-        if (c0 + 4 <= cols) {
-            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (k < K) t = __ldcs(reinterpret_cast<const float4 *>(X + k * ldx + c0));
-            float h[4], l[4];
-            split2(t.x, h[0], l[0]);
-            split2(t.y, h[1], l[1]);
-            split2(t.z, h[2], l[2]);
-            split2(t.w, h[3], l[3]);
-            const float4 hv = make_float4(h[0], h[1], h[2], h[3]), lv = make_float4(l[0], l[1], l[2], l[3]);
-            __stcg(reinterpret_cast<float4 *>(y0), lv);
-            __stcg(reinterpret_cast<float4 *>(y1), hv);
-            __stcg(reinterpret_cast<float4 *>(y2), hv);
-        } else {
-            for (int64_t c = c0; c < cols; ++c) {
-                float hh, ll;
-                split2(k < K ? X[k * ldx + c] : 0.f, hh, ll);
-                y0[c - c0] = ll;
-                y1[c - c0] = hh;
-                y2[c - c0] = hh;
-            }
+    const int64_t k = i / q, c0 = (i - k * q) * 4;
+    int64_t p0, kcp;
+    seg_pos(k, K, p0, kcp);
+    float *y0 = Y + p0 * ldy + c0;
+    float *y1 = y0 + kcp * ldy;
+    float *y2 = y0 + 2 * kcp * ldy;
+    if (c0 + 4 <= cols) {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < K) t = __ldcs(reinterpret_cast<const float4 *>(X + k * ldx + c0));
+        float h[4], l[4];
+        split2(t.x, h[0], l[0]);
+        split2(t.y, h[1], l[1]);
+        split2(t.z, h[2], l[2]);
+        split2(t.w, h[3], l[3]);
+        const float4 hv = make_float4(h[0], h[1], h[2], h[3]), lv = make_float4(l[0], l[1], l[2], l[3]);
+        __stcg(reinterpret_cast<float4 *>(y0), lv);
+        __stcg(reinterpret_cast<float4 *>(y1), hv);
+        __stcg(reinterpret_cast<float4 *>(y2), hv);
+    } else {
+        for (int64_t c = c0; c < cols; ++c) {
+            float hh, ll;
+            split2(k < K ? X[k * ldx + c] : 0.f, hh, ll);
+            y0[c - c0] = ll;
+            y1[c - c0] = hh;
+            y2[c - c0] = hh;
         }
+    }
+}
+
+// Both operands in ONE launch (a launch is ~4 us of fixed cost at the sizes where this matters):
+// work items [0, a_items) split A, the rest split B (columns when transB, rows otherwise).
+struct SplitArgs {
+    const float *A;
+    int64_t lda;
+    float *A3;
+    int64_t lda3;
+    const float *B;
+    int64_t ldb;
+    float *B3;
+    int64_t ldb3;
+    int64_t m, n, k;
+    int transB;
+    int64_t a_items, items;
+};
+
+__global__ void __launch_bounds__(256) split_ab_kernel(const SplitArgs a) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.items;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < a.a_items)
+            split_cols_item(i, a.A, a.lda, a.A3, a.lda3, a.k, 0);
+        else if (a.transB)
+            split_cols_item(i - a.a_items, a.B, a.ldb, a.B3, a.ldb3, a.k, 1);
+        else
+            split_rows_item(i - a.a_items, a.B, a.ldb, a.B3, a.ldb3, a.k, a.n);
     }
 }
 
@@ -198,14 +216,13 @@ cudaError_t launch_tc_gemm_f32x3(const GemmLaunch &g) {
     if (!ws) return cudaErrorMemoryAllocation;
     float *A3 = ws;
     float *B3 = ws + m * lda3;
-    const float *A = static_cast<const float *>(g.A);
-    const float *B = static_cast<const float *>(g.B);
-    split_cols_kernel<<<grid_for(m * ((k + 3) / 4), g.num_sms), 256, 0, g.stream>>>(A, g.lda, A3, lda3, m, k, 0);
-    if (g.transB)
-        split_cols_kernel<<<grid_for(n * ((k + 3) / 4), g.num_sms), 256, 0, g.stream>>>(B, g.ldb, B3, ldb3, n, k, 1);
-    else
-        split_rows_kernel<<<grid_for(round4(k) * ((n + 3) / 4), g.num_sms), 256, 0, g.stream>>>(B, g.ldb, B3, ldb3, k,
-                                                                                             n);
+    SplitArgs sa;
+    sa.A = static_cast<const float *>(g.A), sa.lda = g.lda, sa.A3 = A3, sa.lda3 = lda3;
+    sa.B = static_cast<const float *>(g.B), sa.ldb = g.ldb, sa.B3 = B3, sa.ldb3 = ldb3;
+    sa.m = m, sa.n = n, sa.k = k, sa.transB = g.transB;
+    sa.a_items = m * ((k + 3) / 4);
+    sa.items = sa.a_items + (g.transB ? n * ((k + 3) / 4) : round4(k) * ((n + 3) / 4));
+    split_ab_kernel<<<grid_for(sa.items, g.num_sms), 256, 0, g.stream>>>(sa);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // the product GEMM: one launch of a tcgen05 TF32 kernel per chunk of 3 * kChunkK tensor-core
