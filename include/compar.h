@@ -101,7 +101,7 @@ typedef enum {
                                 /*   TF32 hi + lo in a library workspace (12 (mk + kn) bytes), one TF32 */
                                 /*   tcgen05 GEMM over 3K (hi*hi + hi*lo + lo*hi) in 1024-k chunks      */
                                 /*   combined by round-to-nearest epilogues; K >= 64, TMA alignment,  */
-                                /*   not in world-panel or host-memory tasks                           */
+                                /*   not in host-memory tasks                                          */
     /* the "sort" interface */
     COMPAR_TGT_SORT_RADIX = 20,   /* built-in: onesweep LSD radix sort, 4 x 8-bit passes, any n      */
     COMPAR_TGT_SORT_BITONIC = 21  /* built-in: single-CTA shared-memory bitonic network, n <= 16384  */

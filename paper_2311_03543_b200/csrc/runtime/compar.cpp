@@ -350,10 +350,12 @@ bool constraints_ok(const Ctx *c, compar_target t, const compar_gemm_desc *d, co
     if ((t == COMPAR_TGT_TCK_TF32 || t == COMPAR_TGT_TCK_BF16) && !tc_clusterk_ok(mrows, d->n, d->k, t == COMPAR_TGT_TCK_BF16, c->num_sms))
         return false;
     // FP32-accuracy split form (R38): the per-product split error is below the FP32 bound's c*K*u
-    // from K >= 64; its workspace holds both operands whole, so not for row-panel (world) or
-    // host-memory (chunked) tasks, and at most 32 GiB
+    // from K >= 64; its workspace holds the launch's operands whole, so not for host-memory tasks
+    // (whose row chunks would re-split B every chunk), and at most 32 GiB.  Row-panel (world) tasks
+    // launch it once per B slab: each launch re-splits the rank's A panel (HBM-bound, small beside
+    // the slab's GEMM) and the slab
     if (t == COMPAR_TGT_TCX_F32 &&
-        (d->k < tc_f32x3_min_k || d->world == COMPAR_WORLD_PANELS || d->mem == COMPAR_MEM_HOST ||
+        (d->k < tc_f32x3_min_k || d->mem == COMPAR_MEM_HOST ||
          tc_f32x3_workspace_bytes(mrows, d->n, d->k, d->transB) > (size_t(32) << 30)))
         return false;
     if (d->m > INT32_MAX || d->n > INT32_MAX || d->k > INT32_MAX) return false;

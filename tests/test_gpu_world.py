@@ -44,7 +44,9 @@ CASES = [("tc_bf16", 1000, 1000, 704, 0), ("tc_bf16", 1000, 1000, 704, 1), ("tc_
          # the wide pair kernel: N a multiple of 512 -> one fused launch waiting per slab on device flags
          ("tc_bf16_2sm_w", 1000, 2048, 704, 0), ("tc_bf16_2sm_w", 777, 3072, 304, 1),
          ("tc_tf32_2sm_w", 600, 1536, 260, 0), ("tc_tf32_2sm_w", 520, 1024, 512, 1),
-         ("tc_bf16_2sm_w", 640, 1000, 512, 0)]          # (N not a multiple of 512: per-slab launches)
+         ("tc_bf16_2sm_w", 640, 1000, 512, 0),          # (N not a multiple of 512: per-slab launches)
+         # FP32 accuracy (R38): one launch per slab, each re-splitting the panel's A and the slab
+         ("tc_f32x3", 600, 1280, 1100, 0), ("tc_f32x3", 520, 1536, 2100, 1)]
 
 
 @pytest.mark.parametrize("chunks", [1, 3, 4])
@@ -54,7 +56,8 @@ def test_loopback_slab_pipeline_bitwise(loop_ctx, chunks, name, m, n, k, tb):
     names = [v for v, _ in ctx.variants()]
     bf = "bf16" in name
     dt = "bf16" if bf else "f32"
-    compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else cm.COMPUTE_F32_STRICT)
+    compute = cm.COMPUTE_BF16 if bf else (cm.COMPUTE_TF32 if "tf32" in name else
+                                          cm.COMPUTE_F32_SPLIT if name == "tc_f32x3" else cm.COMPUTE_F32_STRICT)
     A = device_matrix(gen.TAG_A, m, k, dtype=dt)
     B = device_matrix(gen.TAG_B, k, n, dtype=dt, transposed=bool(tb))
     C0 = device_matrix(gen.TAG_C, m, n)
@@ -75,7 +78,8 @@ def test_loopback_slab_pipeline_bitwise(loop_ctx, chunks, name, m, n, k, tb):
         Ah, Bh, Ch = gen.matrix(gen.TAG_A, m, k, dtype=dt), gen.matrix(gen.TAG_B, k, n, dtype=dt), gen.matrix(gen.TAG_C, m, n)
         ref = og.gemm(Ah, Bh, Ch, alpha=1.5, beta=0.5, dtype=dt)
         tf32 = name.startswith("tc_tf32")
-        assert_parity(got, ref, Ah, Bh, Ch, 1.5, 0.5, dt, tf32, 5e-3 if tf32 else 1e-5, name, tc=name.startswith("tc_"))
+        assert_parity(got, ref, Ah, Bh, Ch, 1.5, 0.5, dt, tf32, 5e-3 if tf32 else 1e-5, name,
+                      tc=name.startswith("tc_") and name != "tc_f32x3")
 
 
 @pytest.mark.parametrize("name,m,n,k,tb", [("tc_bf16_2sm_w", 4096, 4096, 1024, 0), ("tc_tf32_2sm_w", 3072, 4096, 520, 1),
