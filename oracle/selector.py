@@ -23,6 +23,7 @@ n=4096 -> v1), tie -> lowest index, permutation invariance, save/load replay.
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 # precision classes / targets (mirror include/compar.h values; restated, not imported)
@@ -73,6 +74,7 @@ class SelectorOracle:
     eager: bool = False
     blocked: bool = False      # calibration order (R19); False = SPEC S:369 interleaving
     explore_pct: int = 150     # DESIGN.md R37 predict-mode exploration threshold (percent)
+    long_warm_ms: int = 200    # DESIGN.md R39: warm-up time for variants whose lower bound is >= 10 ms
     prune_pct: int = 150       # DESIGN.md R32 calibration pruning threshold (percent, the runtime default); 0 = SPEC
     hist: dict = field(default_factory=dict)   # (v, key) -> Record
 
@@ -104,9 +106,18 @@ class SelectorOracle:
         lv = lb[t] if lb else 0.0
         return lv > 0.0 and lv * 100.0 * float(bc) > float(self.prune_pct) * float(bs)
 
+    def warm_count(self, lb_ns=0.0):
+        """R39, written from the rule: a variant whose static lower bound is at least 10 ms gets
+        ceil(long_warm_ms / lb) warm-up executions (at least W, at most 6) — enough to run ~200 ms
+        before its timed samples; every other variant gets W."""
+        if self.long_warm_ms <= 0 or lb_ns < 10e6:
+            return self.calib_warmup
+        w = math.ceil(self.long_warm_ms * 1e6 / lb_ns)
+        return min(6, max(self.calib_warmup, w))
+
     def calibrating(self, key, eligible, lb=None):
-        need = self.calib_warmup + self.calib_k
-        return any(self.rec(v, key).seen < need and not self.pruned(key, eligible, t, lb)
+        return any(self.rec(v, key).seen < self.warm_count(lb[t] if lb else 0.0) + self.calib_k
+                   and not self.pruned(key, eligible, t, lb)
                    for t, v in enumerate(eligible))
 
     def decide(self, key, eligible, lb=None):
@@ -119,9 +130,10 @@ class SelectorOracle:
             raise LookupError("E_NO_VARIANT")
         if self.eager:
             return eligible[0], MODE_EAGER
-        need = self.calib_warmup + self.calib_k
+        warm = [self.warm_count(lb[t] if lb else 0.0) for t in range(len(eligible))]
         seen = [self.rec(v, key).seen for v in eligible]
-        cand = [t for t in range(len(eligible)) if seen[t] < need and not self.pruned(key, eligible, t, lb)]
+        cand = [t for t in range(len(eligible))
+                if seen[t] < warm[t] + self.calib_k and not self.pruned(key, eligible, t, lb)]
         if cand:                                               # step 4: calibration
             if self.blocked:   # R19 / R32: finish one variant's W + K executions before the next,
                 # visiting variants by increasing lower bound (ties: eligibility order)
@@ -129,7 +141,7 @@ class SelectorOracle:
             else:
                 best = min(cand, key=lambda t: (seen[t], eligible[t]))
             v = eligible[best]
-            return v, (MODE_WARMUP if seen[best] < self.calib_warmup else MODE_CALIB)
+            return v, (MODE_WARMUP if seen[best] < warm[best] else MODE_CALIB)
         best_v = None                                           # step 5: model
         for v in eligible:
             r = self.rec(v, key)
@@ -146,12 +158,13 @@ class SelectorOracle:
             best_v = eligible[0]
         return best_v, MODE_MODEL
 
-    def commit(self, v: int, key, mode: int) -> bool:
-        """Account a submitted execution; returns True if it is a warm-up."""
+    def commit(self, v: int, key, mode: int, lb_ns: float = 0.0) -> bool:
+        """Account a submitted execution (lb_ns: the variant's static lower bound, R39); returns
+        True if it is a warm-up."""
         if mode in (MODE_EAGER, MODE_HINT, MODE_NOOP):  # MODE_PREDICT executions are accounted
             return False
         r = self.rec(v, key)
-        warm = r.seen < self.calib_warmup
+        warm = r.seen < self.warm_count(lb_ns)
         r.seen += 1
         return warm
 
@@ -255,7 +268,8 @@ class SelectorOracle:
             # predicted within explore_pct/100 of it, is measured (W + 1 runs) before it is trusted
             for t, v in enumerate(eligible):
                 if est[t] is not None and est[t][1] and est[t][0] * 100.0 <= float(self.explore_pct) * best[1]:
-                    return v, (MODE_WARMUP if self.rec(v, key).seen < self.calib_warmup else MODE_CALIB)
+                    return v, (MODE_WARMUP if self.rec(v, key).seen < self.warm_count(lb[t] if lb else 0.0)
+                               else MODE_CALIB)
         return best[0], (MODE_PREDICT if best[2] else MODE_MODEL)
 
     # ---- R32 static lower bound of a built-in GEMM variant (mirrors the runtime's class peaks,

@@ -1554,7 +1554,7 @@ compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector
         if (ppos >= 0) {
             *variant = idx[ppos];
             *mode = pm;
-            if (commit) *warm = c->hist.commit(names[ppos], plan.key);
+            if (commit) *warm = c->hist.commit(names[ppos], plan.key, c->hist.warm_count(lb[ppos]));
             return COMPAR_OK;
         }
         // Only the variants with neither a sample nor a model are calibrated for this key (a
@@ -1573,7 +1573,7 @@ compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector
             const int pos = c->hist.decide(unames, plan.key, &m, &ulb);
             *variant = uidx[pos];
             *mode = m;
-            if (commit) *warm = c->hist.commit(unames[pos], plan.key);
+            if (commit) *warm = c->hist.commit(unames[pos], plan.key, c->hist.warm_count(ulb[pos]));
             return COMPAR_OK;
         }
     }
@@ -1585,7 +1585,7 @@ compar_status choose_core(Ctx *c, const std::vector<int> &idx, const std::vector
     const int pos = c->hist.decide(names, plan.key, &m, &lb);
     *variant = idx[pos];
     *mode = m;
-    if (commit) *warm = c->hist.commit(names[pos], plan.key);
+    if (commit) *warm = c->hist.commit(names[pos], plan.key, c->hist.warm_count(lb[pos]));
     return COMPAR_OK;
 }
 
@@ -1732,7 +1732,9 @@ compar_status compar_gemm_submit(void *ctx, const compar_gemm_desc *d, uint64_t 
         t.lane = w % c->placer.lanes();
         t.remote = t.owner != c->rank;
         c->placer.commit(t.id, w, end, acc);
-        if (t.history) t.warm = c->hist.commit(c->variants[t.variant].hid, plan.key);
+        if (t.history)
+            t.warm = c->hist.commit(c->variants[t.variant].hid, plan.key,
+                                    c->hist.warm_count(static_lb_ns(c, c->variants[t.variant].target, plan.key)));
         // lanes > 1: model-mode executions overlap other lanes, so their times are not samples
         if (c->placer.lanes() > 1 && (t.mode == kModel || t.mode == kPredict)) t.history = false;
     }

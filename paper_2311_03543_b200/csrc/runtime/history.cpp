@@ -73,17 +73,23 @@ bool History::pruned(const std::vector<int> &ids, const Key &k, const std::vecto
     return pruned_in(v, prune_pct, lb, i);
 }
 
+int History::warm_count(double lb_ns) const {
+    if (long_warm_ms <= 0 || lb_ns < 10e6) return calib_warmup;
+    const int w = static_cast<int>(std::ceil(static_cast<double>(long_warm_ms) * 1e6 / lb_ns));
+    return w > 6 ? 6 : (w < calib_warmup ? calib_warmup : w);
+}
+
 bool History::calibrating(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb) {
-    const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
     KeyView v;
     view(*this, ids, k, v);
-    for (size_t i = 0; i < ids.size(); ++i)
+    for (size_t i = 0; i < ids.size(); ++i) {
+        const int64_t need = static_cast<int64_t>(warm_count(lb ? (*lb)[i] : 0.0)) + calib_k;
         if (v.r[i]->seen < need && !pruned_in(v, prune_pct, lb, i)) return true;
+    }
     return false;
 }
 
 int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const std::vector<double> *lb) {
-    const int64_t need = static_cast<int64_t>(calib_warmup) + calib_k;
     KeyView v;
     view(*this, ids, k, v);
     // Calibration.  Interleaved: least-seen eligible variant, first in registry order on ties.
@@ -94,8 +100,9 @@ int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const
     double best_lb = 0.0;
     for (size_t i = 0; i < ids.size(); ++i) {
         const int64_t s = v.r[i]->seen;
-        if (s >= need || pruned_in(v, prune_pct, lb, i)) continue;
         const double l = lb ? (*lb)[i] : 0.0;
+        const int64_t need = static_cast<int64_t>(warm_count(l)) + calib_k;   // W + K (R39: W per variant)
+        if (s >= need || pruned_in(v, prune_pct, lb, i)) continue;
         if (calib_blocked) {
             if (best < 0 || l < best_lb) {
                 best = static_cast<int>(i);
@@ -108,7 +115,7 @@ int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const
         }
     }
     if (best >= 0) {
-        *mode = best_seen < calib_warmup ? kWarmup : kCalib;
+        *mode = best_seen < warm_count(lb ? (*lb)[best] : 0.0) ? kWarmup : kCalib;
         return best;
     }
     // Model: argmin of sum/count compared as sum_a * count_b < sum_b * count_a (exact).
@@ -129,9 +136,9 @@ int History::decide(const std::vector<int> &ids, const Key &k, Mode *mode, const
     return best < 0 ? 0 : best;
 }
 
-bool History::commit(int id, const Key &k) {
+bool History::commit(int id, const Key &k, int warm_n) {
     Record &r = rec(id, k);
-    const bool warm = r.seen < calib_warmup;
+    const bool warm = r.seen < warm_n;
     ++r.seen;
     return warm;
 }
@@ -273,7 +280,7 @@ int History::decide_predict(const std::vector<int> &ids, const Key &k, Mode *mod
         for (size_t i = 0; i < ids.size(); ++i)
             if (known[i] && pred[i] && est[i] * 100.0 <= static_cast<double>(explore_pct) * est[best]) {
                 const Record *r = find(ids[i], k);
-                *mode = (r ? r->seen : 0) < calib_warmup ? kWarmup : kCalib;
+                *mode = (r ? r->seen : 0) < warm_count(lb ? (*lb)[i] : 0.0) ? kWarmup : kCalib;
                 return static_cast<int>(i);
             }
     }

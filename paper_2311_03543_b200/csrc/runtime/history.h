@@ -57,6 +57,12 @@ public:
     bool calib_blocked = true;
     int prune_pct = 300;   // 0: no pruning (SPEC S:363-371 behaviour)
     int explore_pct = 150; // predict mode (R37): measure a predicted variant within this % of the measured best
+    int long_warm_ms = 200; // R39: variants whose static lower bound is >= 10 ms warm up for ~this long (0: off)
+
+    // R39: warm-up executions of a variant whose static lower bound is lb_ns: W, or for long kernels
+    // (lb >= 10 ms) enough to run ~long_warm_ms first (at most 6) — their timed samples then see the
+    // power-capped steady state the model-mode runs will see, not the boost of a cool GPU.
+    int warm_count(double lb_ns) const;
 
     // Records belong to variant NAMES (so a loaded perf model applies to whichever registry index
     // that name gets); names are interned to small ids for the hot path.
@@ -75,8 +81,8 @@ public:
     int decide(const std::vector<int> &ids, const Key &k, Mode *mode, const std::vector<double> *lb = nullptr);
     // R32: is position i of ids pruned from calibration for k?
     bool pruned(const std::vector<int> &ids, const Key &k, const std::vector<double> *lb, size_t i);
-    // Account an assigned execution; returns true if it is a warm-up.
-    bool commit(int id, const Key &k);
+    // Account an assigned execution (warm: its variant's warm_count); returns true if it is a warm-up.
+    bool commit(int id, const Key &k, int warm);
     void harvest(int id, const Key &k, int64_t ns);
 
     const std::map<std::pair<int, Key>, Record> &table() const { return table_; }

@@ -284,3 +284,31 @@ def test_static_lower_bound_closed_form():
     nbytes = 2 * (65536 * 4096 + 4096 * 256) + 4 * 65536 * 256 * 2
     assert so.SelectorOracle.static_lb_ns("bf16", ts) == pytest.approx(nbytes / 8e12 * 1e9)
     assert so.SelectorOracle.static_lb_ns(None, ts) == 0.0
+
+
+def test_long_kernel_warmup_rule():
+    """R39 closed forms: W for variants whose static lower bound is below 10 ms; from 10 ms,
+    ceil(200 ms / lb) warm-ups, at least W and at most 6; off with long_warm_ms = 0."""
+    sel = so.SelectorOracle(3, blocked=True)
+    assert [sel.warm_count(x) for x in (0.0, 9.99e6, 10e6, 31.3e6, 62.5e6, 188e6, 250e6)] == [1, 1, 6, 6, 4, 2, 1]
+    assert so.SelectorOracle(3, long_warm_ms=0).warm_count(50e6) == 1
+    assert so.SelectorOracle(3, calib_warmup=3).warm_count(150e6) == 3      # never below W
+
+
+def test_long_kernel_calibration_plan():
+    """Blocked calibration of three long variants (lb 31 ms, 31 ms, 62.5 ms): 6 + 3, 6 + 3, then
+    4 + 3 executions, warm-ups dropped, then model mode on the smallest timed mean."""
+    sel = so.SelectorOracle(3, blocked=True, prune_pct=0)
+    lb = [31e6, 31e6, 62.5e6]
+    cost = [52_000_000, 50_000_000, 100_000_000]
+    trace = []
+    for _ in range(26):
+        v, mode = sel.decide("k", [0, 1, 2], lb)
+        warm = sel.commit(v, "k", mode, lb[v])
+        sel.harvest(v, "k", mode, warm, cost[v])
+        trace.append((v, mode))
+    assert [v for v, _ in trace[:25]] == [0] * 9 + [1] * 9 + [2] * 7
+    assert [m for _, m in trace[:9]] == [so.MODE_WARMUP] * 6 + [so.MODE_CALIB] * 3
+    assert [m for _, m in trace[18:25]] == [so.MODE_WARMUP] * 4 + [so.MODE_CALIB] * 3
+    assert trace[25] == (1, so.MODE_MODEL)
+    assert sel.rec(0, "k").count == 3 and sel.rec(2, "k").count == 3
