@@ -147,6 +147,7 @@ struct Ctx {
     // host-memory pipeline
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     int host_chunks = 32;   // row chunks of the host-memory pipeline (32768-row bench: 8 -> 32 chunks, e2e 178 -> 170 ms)
+    int host_tail_split = 1;   // COMPAR_HOST_TAIL_SPLIT=0: uniform chunks to the end
     // task-parallel world
     Placer placer;
     bool placer_ready = false;
@@ -1083,7 +1084,16 @@ compar_status host_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStre
     const int64_t M = d->m, K = d->k, N = d->n;
     const int64_t per = (M + c->host_chunks - 1) / c->host_chunks;
     const int64_t rows = std::max<int64_t>(256, (per + 255) / 256 * 256);
-    const int nchunk = static_cast<int>((M + rows - 1) / rows);
+    // chunk boundaries: uniform chunks of `rows`, the last one cut into halving pieces (>= 256 rows)
+    // so the exposed tail — the last chunk's GEMM and its copy back — is a fraction of a chunk
+    std::vector<int64_t> bounds{0};
+    while (bounds.back() < M) {
+        const int64_t left = M - bounds.back();
+        int64_t step = std::min(rows, left);
+        if (left <= rows && c->host_tail_split) step = std::max<int64_t>(256, (left / 2 + 255) / 256 * 256);
+        bounds.push_back(std::min(M, bounds.back() + step));
+    }
+    const int nchunk = static_cast<int>(bounds.size()) - 1;
     cudaEvent_t ready = get_event(c);
     t.extra.push_back(ready);
     cudaEventRecord(ready, st);
@@ -1097,7 +1107,7 @@ compar_status host_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStre
     cudaEventRecord(pr.start, st);
     compar_status r = COMPAR_OK;
     for (int i = 0; i < nchunk && r == COMPAR_OK; ++i) {
-        const int64_t r0 = i * rows, ri = std::min(rows, M - r0);
+        const int64_t r0 = bounds[i], ri = bounds[i + 1] - bounds[i];
         const size_t a_off = static_cast<size_t>(r0) * d->lda * eb;
         const size_t a_len = static_cast<size_t>(ri - 1) * d->lda * eb + static_cast<size_t>(K) * eb;
         cudaMemcpyAsync(static_cast<char *>(const_cast<void *>(A)) + a_off, static_cast<const char *>(d->A) + a_off,
@@ -1270,6 +1280,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         if (sms_cap >= 2 && sms_cap < c->num_sms) c->num_sms = sms_cap;
         c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", cfg.bcast_ctas);
         c->host_chunks = env_int("COMPAR_HOST_CHUNKS", 32);
+        c->host_tail_split = env_int("COMPAR_HOST_TAIL_SPLIT", 1);
     }
     {
         std::lock_guard<std::mutex> lk(g_live_mu);
