@@ -84,6 +84,10 @@ cudaError_t launch_tc_gemm_2sm_wide(const GemmLaunch &g, bool bf16);  // variant
 cudaError_t launch_tc_gemm_pairs(const GemmLaunch &g, bool bf16);
 cudaError_t launch_scale(const GemmLaunch &g);               // k == 0 or alpha == 0: C_out = beta*C_in
 cudaError_t launch_spin(cudaStream_t s, int64_t ns);         // synthetic-cost fixture
+// Device rows -> mapped pinned host memory (dst: the host buffer's device alias) by `ctas` CTAs: a
+// rate-limited D2H that leaves the H2D direction more of the PCIe link than a copy engine does.
+cudaError_t launch_rows_to_host(float *dst, int64_t ld_dst, const float *src, int64_t ld_src, int64_t rows,
+                                int64_t cols, int ctas, cudaStream_t s);
 cudaError_t preload_kernels();                               // force module load (no lazy loading in calibration)
 int *sched_workspace(cudaStream_t s);                        // {next, done} tile counters for persistent kernels
 // Split-K partial planes of the tc_*_sk variant (grown on demand, per stream).

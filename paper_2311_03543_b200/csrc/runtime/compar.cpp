@@ -148,6 +148,7 @@ struct Ctx {
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     int host_chunks = 32;   // row chunks of the host-memory pipeline (32768-row bench: 8 -> 32 chunks, e2e 178 -> 170 ms)
     int host_tail_split = 1;   // COMPAR_HOST_TAIL_SPLIT=0: uniform chunks to the end
+    int d2h_kernel_ctas = 4;   // COMPAR_D2H_KERNEL_CTAS: CTAs of the mapped-memory D2H copy (0: copy engine)
     // task-parallel world
     Placer placer;
     bool placer_ready = false;
@@ -1094,6 +1095,15 @@ compar_status host_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStre
         bounds.push_back(std::min(M, bounds.back() + step));
     }
     const int nchunk = static_cast<int>(bounds.size()) - 1;
+    // the host C buffer's device alias when it is mapped pinned memory (else nullptr: copy engine)
+    float *cout_host_dev = nullptr;
+    {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, d->C_out) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+            cout_host_dev = static_cast<float *>(pa.devicePointer);
+        else
+            cudaGetLastError();   // (clear a lookup error on pageable memory)
+    }
     cudaEvent_t ready = get_event(c);
     t.extra.push_back(ready);
     cudaEventRecord(ready, st);
@@ -1135,9 +1145,19 @@ compar_status host_pipeline(Ctx *c, const compar_gemm_desc *d, Task &t, cudaStre
         cudaEventRecord(span.second, st);
         pr.sub.push_back(span);
         cudaStreamWaitEvent(c->d2h_stream, span.second, 0);
-        // 2-D copy: only the n valid columns of each row go back (the ld gap on the host is untouched)
-        cudaMemcpy2DAsync(d->C_out + r0 * d->ldc_out, d->ldc_out * 4, Cout + r0 * d->ldc_out, d->ldc_out * 4, N * 4, ri,
-                          cudaMemcpyDeviceToHost, c->d2h_stream);
+        // 2-D copy: only the n valid columns of each row go back (the ld gap on the host is untouched).
+        // Into mapped pinned memory the copy is a kernel of a few CTAs: a copy engine runs D2H at
+        // full rate and takes the H2D direction down to ~52 GB/s while it does; a 4-CTA kernel moves
+        // ~47 GB/s and leaves H2D ~53.4 (tools/pcie_mix.cu) — H2D is this pipeline's bound
+        if (cout_host_dev && c->d2h_kernel_ctas > 0) {
+            const compar_status ks = launch_rows_to_host(cout_host_dev + r0 * d->ldc_out, d->ldc_out, Cout + r0 * d->ldc_out,
+                                                         d->ldc_out, ri, N, c->d2h_kernel_ctas, c->d2h_stream) == cudaSuccess
+                                         ? COMPAR_OK : COMPAR_E_TASK_FAILED;
+            if (ks != COMPAR_OK) r = ks;
+        } else {
+            cudaMemcpy2DAsync(d->C_out + r0 * d->ldc_out, d->ldc_out * 4, Cout + r0 * d->ldc_out, d->ldc_out * 4, N * 4,
+                              ri, cudaMemcpyDeviceToHost, c->d2h_stream);
+        }
         c->stats.bytes_d2h += static_cast<int64_t>(ri * N * 4);
     }
     cudaEventRecord(pr.stop, st);
@@ -1281,6 +1301,7 @@ compar_status compar_init(const compar_config *cfg_in, void **ctx) {
         c->bcast_reserve_sms = env_int("COMPAR_BCAST_RESERVE_SMS", cfg.bcast_ctas);
         c->host_chunks = env_int("COMPAR_HOST_CHUNKS", 32);
         c->host_tail_split = env_int("COMPAR_HOST_TAIL_SPLIT", 1);
+        c->d2h_kernel_ctas = env_int("COMPAR_D2H_KERNEL_CTAS", 4);
     }
     {
         std::lock_guard<std::mutex> lk(g_live_mu);
