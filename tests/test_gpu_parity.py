@@ -470,3 +470,26 @@ def test_unsplit_tcgen05_forms_bitwise_identical(ctx, dt, transB, shape, beta):
     ref = next(iter(outs.values()))
     for name, o in outs.items():
         assert torch.equal(o, ref), name
+
+
+def test_host_pipeline_pageable_cout_uses_copy_engine(ctx):
+    """mem = HOST with a PAGEABLE C_out (no device alias): the pipeline copies C back with the copy
+    engine instead of the mapped-memory copy kernel; the result equals the device path bitwise."""
+    m, n, k = 1536, 777, 384
+    A = gen.matrix(gen.TAG_A, m, k, dtype="bf16")
+    B = gen.matrix(gen.TAG_B, k, n, dtype="bf16")
+    C0 = gen.matrix(gen.TAG_C, m, n)
+    Ah = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Bh = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Cin = torch.from_numpy(C0.copy()).pin_memory()
+    Cout = torch.zeros((m, n), dtype=torch.float32)          # pageable
+    assert not Cout.is_pinned()
+    d = cm.make_desc(m, n, k, A=Ah, B=Bh, C_in=Cin, C_out=Cout, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
+                     compute=cm.COMPUTE_BF16, mem=cm.MEM_HOST, variant_hint=vid(ctx, "tc_bf16_2sm"))
+    assert ctx.run(d).status == 0
+    Ad, Bd, Cd = Ah.cuda(), Bh.cuda(), Cin.cuda()
+    d2 = cm.make_desc(m, n, k, A=Ad, B=Bd, C_in=Cd, C_out=Cd, alpha=1.5, beta=0.5, in_dtype=cm.BF16,
+                      compute=cm.COMPUTE_BF16, variant_hint=vid(ctx, "tc_bf16_2sm"),
+                      stream=torch.cuda.current_stream().cuda_stream)
+    assert ctx.run(d2).status == 0
+    assert torch.equal(Cout, Cd.cpu())
