@@ -189,8 +189,10 @@ typedef struct {
                                    the library stages them through its own device buffers: B
                                    first, then A / C_in row chunks up and C_out chunks down on two
                                    copy streams while the GEMM runs on the previous chunk; only the
-                                   n valid columns of each C_out row are written on the host.  The
-                                   task's end event follows the last D2H copy.                   */
+                                   n valid columns of each C_out row are written on the host (by a
+                                   4-CTA copy kernel when C_out is mapped pinned memory, which
+                                   leaves the H2D direction more of the link; else by the copy
+                                   engine).  The task's end event follows the last D2H copy.     */
     void *stream;               /* cudaStream_t to order the task on; NULL: the CUDA legacy default
                                    stream (ordered after the caller's default-stream work)        */
     int panels;                 /* loopback row panels on this device (1..COMPAR_MAX_PANELS);
