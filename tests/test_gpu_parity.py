@@ -54,13 +54,40 @@ def sk_splits(m, n, k, bf16):
     return s if s >= 2 and tiles * s * 256 * 256 * 4 <= (1 << 30) else 0
 
 
-def skip_ineligible(name, m, n, k):
+def ineligible_reason(name, m, n, k):
+    """The eligibility rules of the K-split variants and tc_f32x3 (kernels.h, R38),
+    restated: a case they exclude is checked as a refusal instead of a product."""
     if name.endswith("_sk") and not sk_splits(m, n, k, "bf16" in name):
-        pytest.skip(f"{name} needs >= 64 k-blocks (K = {k})")
+        return f"{name} needs >= 64 k-blocks (K = {k})"
     if name.endswith("_ck") and k <= (64 if "bf16" in name else 32):
-        pytest.skip(f"{name} needs >= 2 k-blocks (K = {k})")
+        return f"{name} needs >= 2 k-blocks (K = {k})"
     if name == "tc_f32x3" and k < 64:
-        pytest.skip("tc_f32x3 needs K >= 64 (DESIGN.md R38)")
+        return "tc_f32x3 needs K >= 64 (DESIGN.md R38)"
+    return None
+
+
+def assert_refused(ctx, d, name):
+    """An ineligible variant is outside E (§8(c) step 1) and a task hinted to it is refused
+    (E_INVALID "not eligible") before anything launches: never run on a shape it does not support."""
+    v = vid(ctx, name)
+    assert v not in ctx.eligible(d)
+    d.variant_hint = v
+    with pytest.raises(cm.ComparError) as ei:
+        ctx.run(d)
+    assert ei.value.status == cm.E_INVALID and "not eligible" in str(ei.value), ei.value
+    return Refused(name)
+
+
+class Refused:
+    """run_case's result for a refused (ineligible) case: no C was produced, so there is nothing
+    to compare — the refusal itself was the check."""
+
+    def __init__(self, name):
+        self.name = name
+        self.got = self.ref = np.zeros((0,))
+
+    def check(self):
+        return None
 
 
 @pytest.fixture(scope="module")
@@ -75,7 +102,7 @@ def vid(ctx, name):
 
 
 def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, seed=11, ldc_pad=4):
-    skip_ineligible(name, m, n, k)
+    refused = ineligible_reason(name, m, n, k)
     dtype_id, compute, tol = VARIANTS[name]
     dt = "bf16" if dtype_id == cm.BF16 else "f32"
     A = gen.matrix(gen.TAG_A, m, k, dist, dt, seed=seed)
@@ -94,6 +121,8 @@ def run_case(ctx, name, m, n, k, dist=gen.DIST_U, beta=0.5, transB=0, pad=8, see
     d = cm.make_desc(m, n, k, A=Ad, B=Bd, C_in=Cd, C_out=Cd, lda=lda, ldb=ldb, ldc_in=ldc, ldc_out=ldc,
                      alpha=alpha, beta=beta, in_dtype=dtype_id, compute=compute, transB=transB,
                      stream=torch.cuda.current_stream().cuda_stream, variant_hint=vid(ctx, name))
+    if refused:
+        return assert_refused(ctx, d, name)
     rep = ctx.run(d)
     assert rep.status == 0 and rep.variant == vid(ctx, name)
     got = to_host_f64(Cd[:, :n])
