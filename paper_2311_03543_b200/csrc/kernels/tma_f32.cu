@@ -156,27 +156,55 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
             asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
             sb = reinterpret_cast<const uint8_t *>(t);
         }
-#pragma unroll 2
-        for (int k4 = 0; k4 < BK / 4; ++k4) {
-            float4 a[8];
+        // Fragments one step ahead (double-buffered registers): the A float4s of k-quad k4 + 1 and
+        // the B row of k + 1 are read from shared memory before the FFMA2s of k, so an LDS latency
+        // is exposed once per stage, not once per k-quad.  Each element's k order is unchanged.
+        auto load_a = [&](float4(&a)[8], int k4) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4 *>(sa + sw128_off(ty + TY * i, k4));
+        };
+        auto load_b = [&](float(&b)[MJ], int kq) {
+            const float *brow = reinterpret_cast<const float *>(sb + kq * (BN * 4));
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const float *brow = reinterpret_cast<const float *>(sb + (k4 * 4 + kk) * (BN * 4));
-                float b[MJ];
-#pragma unroll
-                for (int h = 0; h < MJ4; ++h) {
-                    const float4 bh = *reinterpret_cast<const float4 *>(brow + h * (BN / MJ4) + tx * 4);
-                    b[4 * h + 0] = bh.x, b[4 * h + 1] = bh.y, b[4 * h + 2] = bh.z, b[4 * h + 3] = bh.w;
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
-#pragma unroll
-                    for (int j = 0; j < MJ; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
-                }
+            for (int h = 0; h < MJ4; ++h) {
+                const float4 bh = *reinterpret_cast<const float4 *>(brow + h * (BN / MJ4) + tx * 4);
+                b[4 * h + 0] = bh.x, b[4 * h + 1] = bh.y, b[4 * h + 2] = bh.z, b[4 * h + 3] = bh.w;
             }
+        };
+        auto fma_k = [&](const float4(&a)[8], int kk, const float(&b)[MJ]) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+#pragma unroll
+                for (int j = 0; j < MJ; j += 2) ffma2(acc[i][j], acc[i][j + 1], av, b[j], b[j + 1]);
+            }
+        };
+        float4 a0[8], a1[8];
+        float b0[MJ], b1[MJ];
+        load_a(a0, 0);
+        load_b(b0, 0);
+#pragma unroll 1
+        for (int k8 = 0; k8 < BK / 8; ++k8) {
+            const int q = 8 * k8;               // first k of this pair of k-quads
+            const bool more = k8 + 1 < BK / 8;
+            load_a(a1, 2 * k8 + 1);
+            load_b(b1, q + 1);
+            fma_k(a0, 0, b0);
+            load_b(b0, q + 2);
+            fma_k(a0, 1, b1);
+            load_b(b1, q + 3);
+            fma_k(a0, 2, b0);
+            load_b(b0, q + 4);
+            fma_k(a0, 3, b1);
+            if (more) load_a(a0, 2 * k8 + 2);
+            load_b(b1, q + 5);
+            fma_k(a1, 0, b0);
+            load_b(b0, q + 6);
+            fma_k(a1, 1, b1);
+            load_b(b1, q + 7);
+            fma_k(a1, 2, b0);
+            if (more) load_b(b0, q + 8);
+            fma_k(a1, 3, b1);
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(empty0 + 8 * s);
