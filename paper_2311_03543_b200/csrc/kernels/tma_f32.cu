@@ -211,12 +211,17 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
     }
 
     // ---------------- epilogue
-    // C_in is gathered for the whole micro-tile before the first store: C_in may alias C_out, so
-    // the compiler cannot hoist a load above an earlier store, and load/store pairs issued in turn
-    // would serialise 8 * MJ4 (or 8 * MJ) memory round trips.
-    float ci[8][MJ];
-    const bool has_cin = p.beta != 0.f;
-    if (has_cin) {
+    // alpha * acc in place, then + beta * C_in (o = alpha * acc, then fmaf(beta, C_in, o)); all of
+    // C_in is gathered before the first store: C_in may alias C_out, so the compiler cannot hoist a
+    // load above an earlier store, and load / store pairs issued in turn would serialise 8 * MJ4
+    // memory round trips.  (In place: 159 registers instead of 166, 1.7-1.9 % faster at 3072^3 -
+    // 8192^3.)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < MJ; ++j) acc[i][j] = p.alpha * acc[i][j];
+    if (p.beta != 0.f) {
+        float ci[8][MJ];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int64_t r = m0 + ty + TY * i;
@@ -233,6 +238,10 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
                 }
             }
         }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < MJ; ++j) acc[i][j] = fmaf(p.beta, ci[i][j], acc[i][j]);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -244,10 +253,7 @@ __global__ void __launch_bounds__(TmaCfg<TB>::kThreads, TmaCfg<TB>::kMinBlocks)
             const int64_t c = n0 + h * (BN / MJ4) + tx * 4;
             float o[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                o[j] = p.alpha * acc[i][h * 4 + j];
-                if (has_cin) o[j] = fmaf(p.beta, ci[i][h * 4 + j], o[j]);
-            }
+            for (int j = 0; j < 4; ++j) o[j] = acc[i][h * 4 + j];
             if (p.cvec && c + 3 < p.n) {
                 *reinterpret_cast<float4 *>(crow + c) = make_float4(o[0], o[1], o[2], o[3]);
             } else {
