@@ -1,18 +1,17 @@
 #!/bin/bash
 # One GPU checkpoint of the round's evidence (run on the gpurun box from the repo root):
-# full -m gpu suite, bench line, native host-overhead probe, sanitizers, ncu of the headline kernel
+# full -m gpu suite, bench line, native host-overhead probe, ncu of the headline kernel
 # and the bench launch list, single-wave kernel times.  Outputs under gpurun_out/ck_<tag>/.
 TAG=${1:-r02}
 O=gpurun_out/ck_$TAG
-mkdir -p $O/san
+mkdir -p $O
+# (compute-sanitizer runs were dropped: the GPU pool closed compute-sanitizer late in round 2; the
+# committed sanitizer logs under profiles/sanitizer/ are from the earlier checkpoints)
 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 --timeout 900 > $O/pytest.log 2>&1; echo "pytest_rc=$?" >> $O/pytest.log
 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench_rc=$?"
 g++ -O2 -I include -I /usr/local/cuda/include tools/host_overhead_c.cpp -L paper_2311_03543_b200 -lcompar \
     -L /usr/local/cuda/lib64 -lcudart -Wl,-rpath,$PWD/paper_2311_03543_b200 -o /tmp/host_overhead_c && \
     { /tmp/host_overhead_c virtual; /tmp/host_overhead_c gpu; } > $O/host_overhead.jsonl 2>&1
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > $O/san/memcheck_all.txt 2>&1
-timeout 900 compute-sanitizer --tool synccheck python tools/sanitize_run.py tc_bf16 tc_tf32 tc_bf16_2sm tc_tf32_2sm tc_bf16_2sm_w tc_tf32_2sm_w tc_bf16_sk tc_bf16_ck tc_tf32_ck tc_f32x3 > $O/san/synccheck_tc.txt 2>&1
-timeout 900 compute-sanitizer --tool racecheck python tools/sanitize_run.py tc_bf16 tc_bf16_ck simt_f32 tma_f32 > $O/san/racecheck_1sm_ffma.txt 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tc_gemm_2sm_wide -c 1 -o $O/tc_bf16_2sm_w_32768 \
     python tools/prof_run.py tc_bf16_2sm_w 32768 32768 32768 1 > $O/ncu_full.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv \
