@@ -78,6 +78,20 @@ def test_multitile_full_compare(ctx, name, transB):
     np.testing.assert_array_equal(got, full_ref(m, n, k))
 
 
+@pytest.mark.parametrize("transB", [0, 1])
+@pytest.mark.parametrize("shape", [(4096, 5120, 1000), (1000, 1200, 776)], ids=["128-tiles", "64-tiles"])
+@pytest.mark.parametrize("name", ["tma_f32", "simt_f32"])
+def test_ffma_multiwave_full_compare(ctx, name, shape, transB):
+    """The FFMA variants over several waves of CTAs, bitwise: 4096 x 5120 x 1000 runs tma_f32's
+    128-tiles (1280 tiles, 8.6 waves; 32 k-blocks with a ragged last one, so the 4-stage ring wraps
+    and the register fragments read one k ahead cross every stage boundary), 1000 x 1200 x 776 its
+    64-tiles (a grid of <= 3/4 of the SMs in 128-tiles; K = 776 keeps the rows 16-byte aligned, as
+    TMA requires)."""
+    m, n, k = shape
+    got = launch(ctx, name, m, n, k, transB).double().cpu().numpy()
+    np.testing.assert_array_equal(got, full_ref(m, n, k))
+
+
 def test_multitile_full_compare_splitk(ctx):
     """The split-K variants over many (tile, k-range) work items and the cluster split-K variants over
     many clusters (several waves): bitwise too (partials summed in split order, every partial an
